@@ -1,0 +1,154 @@
+/*
+ * lmx.h -- C ABI of the B200-native local max matching engine (liblmx.so).
+ *
+ * This is the drop-in boundary for the reference's matching entry point.
+ * The reference is pure Python with no FFI, so each entry
+ * point below names the reference function whose contract it takes over;
+ * INTEGRATION.md shows the ctypes binding the reference would add.
+ *
+ *   lmx_local_max      <- locmax.matchers.local_max_seq(g, seed, rerandomize)
+ *                         (/root/reference/pkg/src/locmax/matchers.py:61-122),
+ *                         one-shot: host Graph arrays in, host Matching + trace out
+ *   lmx_load_graph     <- the read-only Graph arrays local_max_seq consumes
+ *                         (graph.py:20-34; only num_vertices, edge_u, edge_v,
+ *                         edge_weight are read, matchers.py:80-92)
+ *   lmx_match          <- local_max_seq's round loop (matchers.py:87-119) plus
+ *                         matching_from_edge_ids (graph.py:195-203) and the
+ *                         RoundStats trace (matchers.py:21-25,117)
+ *   lmx_build_graph    <- locmax.graph.build_graph (graph.py:59-119) numbering
+ *                         contract, on the device, for inputs too large for the
+ *                         reference's Python dict loop
+ *   lmx_gen_rmat       <- (new generator, SURVEY.md §8d C3/N★/C5; the reference
+ *                         has none)
+ *
+ * Conventions: plain pointers and sizes; int status return (LMX_OK = 0);
+ * the message of the last failure is available from lmx_last_error(ctx) or,
+ * for the one-shot call, in the caller's err buffer.  Inputs are never
+ * mutated (graph.py:117-118 ownership rule); outputs are caller-allocated.
+ * Device pointers are CUDA device addresses valid in the ctx's device.
+ */
+#ifndef LMX_H
+#define LMX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMX_ABI_VERSION 1
+
+/* status codes */
+#define LMX_OK 0
+#define LMX_EINVAL 1   /* domain error (bad ids, NaN/inf/negative weight): ValueError */
+#define LMX_ECUDA 2    /* CUDA runtime / launch failure: RuntimeError */
+#define LMX_ENOMEM 3   /* device allocation failed: MemoryError */
+#define LMX_ELIMIT 4   /* instance exceeds the 32-bit vertex / edge id range */
+#define LMX_ESTATE 5   /* call out of order (no graph loaded, ...) */
+
+/* where a pointer lives */
+#define LMX_HOST 0
+#define LMX_DEVICE 1
+
+typedef struct lmx_ctx lmx_ctx;
+
+/* matchers.py:21-25 RoundStats */
+typedef struct {
+    int64_t edges_before;
+    int64_t edges_matched;
+    int64_t edges_removed;
+} lmx_round_stats;
+
+/* Per-call timing of the last lmx_match / lmx_load_graph (CUDA events). */
+typedef struct {
+    double setup_ms;        /* lmx_load_graph: H2D + slot-record build (K0) */
+    double rounds_ms;       /* lmx_match: first round kernel .. last match kernel */
+    double output_ms;       /* lmx_match: matched-id sort + output copies */
+    int64_t round_launches; /* kernels launched by the round loop */
+    int64_t slot_reads;     /* slots read by the round kernels (for roofline) */
+} lmx_timing;
+
+int lmx_abi_version(void);
+
+/* Create / destroy an engine bound to one CUDA device. */
+int lmx_create(int device, lmx_ctx **out);
+void lmx_destroy(lmx_ctx *ctx);
+const char *lmx_last_error(const lmx_ctx *ctx);
+
+/* Run all work on this stream (a cudaStream_t passed as void*); NULL = the
+ * context's own non-blocking stream. */
+int lmx_set_stream(lmx_ctx *ctx, void *cuda_stream);
+
+/*
+ * Load (replace) the graph: n vertices, m edges in the reference's edge-array
+ * form (edge ids are positions 0..m-1).  Validation follows graph.py:80-88:
+ * ids in [0, n), no self loops, weights finite and >= 0 (-0.0 allowed).
+ * Builds the per-vertex slot records on the device (K0).
+ */
+int lmx_load_graph(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u,
+                   const int64_t *edge_v, const double *edge_weight, int where);
+
+/*
+ * Local max maximal matching of the loaded graph (matchers.py:61-122).
+ * seed_masked = the Python seed & (2^64-1) (tiebreak.py:49).
+ * mate_out: int64[n] (-1 = unmatched); matched_ids_out: int64[>= n/2],
+ * ascending original edge ids; rounds_out: lmx_round_stats[max_rounds].
+ * Outputs live where `out_where` says.  The loaded graph stays intact, so
+ * lmx_match may be called repeatedly (e.g. different seeds).
+ */
+int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate_out,
+              int64_t *matched_ids_out, int64_t *n_matched_out, lmx_round_stats *rounds_out,
+              int max_rounds, int *n_rounds_out, int out_where);
+
+int lmx_last_timing(const lmx_ctx *ctx, lmx_timing *out);
+
+/* Copy the RoundStats trace of the last lmx_match (up to cap entries);
+ * returns the number of rounds, or -1 on a bad ctx. */
+int lmx_last_rounds(lmx_ctx *ctx, lmx_round_stats *out, int cap);
+
+/* One-shot host-buffer entry point: the local_max_seq drop-in for an FFI
+ * binding.  err may be NULL. */
+int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u,
+                  const int64_t *edge_v, const double *edge_weight, uint64_t seed_masked,
+                  int rerandomize, int64_t *mate_out, int64_t *matched_ids_out,
+                  int64_t *n_matched_out, lmx_round_stats *rounds_out, int max_rounds,
+                  int *n_rounds_out, char *err, size_t errlen);
+
+/*
+ * build_graph (graph.py:59-119) on the device.  Raw triples (u, v, w),
+ * count k, already validated for range/weight domain by the caller or by
+ * this call (returns LMX_EINVAL naming the first bad position).  Drops
+ * self-loops; collapses parallel pairs to the heaviest occurrence (earliest on
+ * ties) keeping that occurrence's orientation; numbers edges by first
+ * occurrence of the pair.  num_vertices < 0 => max id + 1 over non-loop
+ * edges.  The result becomes the context's loaded graph; lmx_graph_size and
+ * lmx_graph_export read it back.
+ */
+int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
+                    const double *w, int64_t num_vertices, int where);
+
+/* Synthetic RMAT (Graph500 a,b,c; d = 1-a-b-c) with edge_factor * 2^scale raw
+ * edges, U[0,1) weights from a counter-based hash of (seed, raw index), optional
+ * bijective vertex relabelling, then build_graph semantics.  Loads the result. */
+int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                 uint64_t seed, int permute);
+
+/* Raw RMAT triples only (no build), for oracle parity of the generator. */
+int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                     uint64_t seed, int permute, int64_t *u_out, int64_t *v_out,
+                     double *w_out, int out_where);
+
+int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out);
+
+/* Copy the loaded graph's edge arrays out (graph.py Graph.edge_u/v/weight). */
+int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edge_weight,
+                     int out_where);
+
+/* Device memory in use by the context (bytes). */
+int64_t lmx_device_bytes(const lmx_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMX_H */

@@ -1,0 +1,453 @@
+"""CPU oracle for the local max matching path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this module, and only
+as the checker / the timed CPU baseline.  The product package
+(``paper_1302_4587_b200``) never imports it.
+
+Contents
+--------
+* ``c_local_max``     -- ctypes front end of ``lmx_oracle.c`` (restates
+  ``matchers.py:61-122``); fast enough for every config up to RMAT-24.
+* ``numpy_local_max`` -- a numpy restatement of ``local_max_seq`` that uses
+  the same whole-array numpy operations as the reference
+  (``np.maximum.at`` scatter-max stages, ``matchers.py:87-119``), so timing it
+  times the reference's algorithm at the reference's speed (1 core).
+* ``mix64`` / ``round_seed`` / ``edge_salts`` / ``weight_bits`` -- numpy
+  restatements of ``tiebreak.py:28-59,105-113``.
+* ``gen_random`` / ``gen_rgg`` / ``with_unit_weights`` / ``build_graph_loop``
+  -- restatements of ``generate.py:48-143,146-197,219-222`` and
+  ``graph.py:59-119`` used to regenerate the reference's instances in tests
+  (the reference itself is absent on the GPU box).
+
+Parity pin: ``tests/test_oracle_golden.py`` checks all of the above against
+``tests/golden/*.npz``, produced from the unmodified reference by
+``tests/golden/make_golden.py``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "liblmx_oracle.so")
+_UINT64_MASK = (1 << 64) - 1
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_MIX_A = np.uint64(0xBF58476D1CE4E5B9)
+_MIX_B = np.uint64(0x94D049BB133111EB)
+
+
+def build() -> str:
+    """Compile lmx_oracle.c with plain gcc (oracle/Makefile)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH) or (
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "lmx_oracle.c"))
+        ):
+            build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        lib.lmxo_mix64.restype = ctypes.c_uint64
+        lib.lmxo_mix64.argtypes = [ctypes.c_uint64]
+        lib.lmxo_round_seed.restype = ctypes.c_uint64
+        lib.lmxo_round_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
+        lib.lmxo_local_max.restype = ctypes.c_int
+        p = ctypes.c_void_p
+        lib.lmxo_local_max.argtypes = [
+            ctypes.c_int64, ctypes.c_int64, p, p, p, ctypes.c_uint64, ctypes.c_int,
+            p, p, p, p, ctypes.c_int,
+        ]
+        lib.lmxo_edge_salts.restype = None
+        lib.lmxo_edge_salts.argtypes = [ctypes.c_uint64, p, ctypes.c_int64, p]
+        _lib = lib
+    return _lib
+
+
+# ---------------------------------------------------------------- tiebreak.py
+
+def mix64(values: np.ndarray) -> np.ndarray:
+    """tiebreak.py:28-37."""
+    with np.errstate(over="ignore"):
+        x = np.asarray(values, dtype=np.uint64) + _GOLDEN
+        x ^= x >> np.uint64(30)
+        x *= _MIX_A
+        x ^= x >> np.uint64(27)
+        x *= _MIX_B
+        x ^= x >> np.uint64(31)
+    return x
+
+
+def round_seed(seed: int, round_index: int, rerandomize: bool = True) -> int:
+    """tiebreak.py:40-52."""
+    if round_index < 0:
+        raise ValueError("round_index must be nonnegative")
+    r = round_index if rerandomize else 0
+    base = np.array([seed & _UINT64_MASK], dtype=np.uint64)
+    return int(mix64(mix64(base) ^ np.uint64(r))[0])
+
+
+def edge_salts(round_seed_value: int, edge_ids) -> np.ndarray:
+    """tiebreak.py:55-59."""
+    ids = np.asarray(edge_ids, dtype=np.uint64)
+    return mix64(ids ^ np.uint64(round_seed_value & _UINT64_MASK))
+
+
+def weight_bits(weights) -> np.ndarray:
+    """tiebreak.py:105-113."""
+    w = np.asarray(weights, dtype=np.float64) + 0.0
+    return w.view(np.uint64)
+
+
+# ---------------------------------------------------------------- results
+
+@dataclass
+class OracleResult:
+    mate: np.ndarray          # int64[n], -1 unmatched
+    matched_ids: np.ndarray   # int64, ascending
+    rounds: list              # [(edges_before, edges_matched, edges_removed)]
+
+
+def c_local_max(n: int, edge_u, edge_v, edge_weight, seed: int,
+                rerandomize: bool = True) -> OracleResult:
+    """lmx_oracle.c restatement of matchers.py:61-122."""
+    lib = _load()
+    eu = np.ascontiguousarray(edge_u, dtype=np.int64)
+    ev = np.ascontiguousarray(edge_v, dtype=np.int64)
+    w = np.ascontiguousarray(edge_weight, dtype=np.float64)
+    m = int(eu.size)
+    mate = np.empty(max(n, 1), dtype=np.int64)
+    ids = np.empty(max(n // 2 + 1, 1), dtype=np.int64)
+    nm = np.zeros(1, dtype=np.int64)
+    max_rounds = 4096
+    rounds = np.zeros(3 * max_rounds, dtype=np.int64)
+    r = lib.lmxo_local_max(
+        n, m, eu.ctypes.data, ev.ctypes.data, w.ctypes.data,
+        seed & _UINT64_MASK, 1 if rerandomize else 0,
+        mate.ctypes.data, ids.ctypes.data, nm.ctypes.data, rounds.ctypes.data, max_rounds,
+    )
+    if r < 0:
+        raise RuntimeError(f"oracle failed with status {r}")
+    rr = rounds[: 3 * r].reshape(r, 3)
+    return OracleResult(mate[:n].copy(), ids[: int(nm[0])].copy(),
+                        [tuple(int(x) for x in row) for row in rr])
+
+
+def c_mix64(v: int) -> int:
+    return int(_load().lmxo_mix64(v & _UINT64_MASK))
+
+
+def c_round_seed(seed: int, r: int, rerandomize: bool = True) -> int:
+    return int(_load().lmxo_round_seed(seed & _UINT64_MASK, r, 1 if rerandomize else 0))
+
+
+def c_edge_salts(rs: int, ids) -> np.ndarray:
+    a = np.ascontiguousarray(ids, dtype=np.uint64)
+    out = np.empty_like(a)
+    _load().lmxo_edge_salts(rs & _UINT64_MASK, a.ctypes.data, a.size, out.ctypes.data)
+    return out
+
+
+def numpy_local_max(n: int, edge_u, edge_v, edge_weight, seed: int,
+                    rerandomize: bool = True) -> OracleResult:
+    """numpy restatement of local_max_seq (matchers.py:61-122), same ops."""
+    edge_u = np.asarray(edge_u, dtype=np.int64)
+    edge_v = np.asarray(edge_v, dtype=np.int64)
+    edge_weight = np.asarray(edge_weight, dtype=np.float64)
+    m = edge_u.size
+    cand_w = np.zeros(n, dtype=np.uint64)
+    cand_s = np.zeros(n, dtype=np.uint64)
+    cand_id = np.full(n, -1, dtype=np.int64)
+    vertex_matched = np.zeros(n, dtype=bool)
+    live = np.arange(m, dtype=np.int64)
+    parts = []
+    rounds = []
+    r = 0
+    while live.size:
+        rs = round_seed(seed, r, rerandomize)
+        wbits = weight_bits(edge_weight[live])
+        salts = edge_salts(rs, live)
+        us = edge_u[live]
+        vs = edge_v[live]
+        np.maximum.at(cand_w, us, wbits)
+        np.maximum.at(cand_w, vs, wbits)
+        tie_u = cand_w[us] == wbits
+        tie_v = cand_w[vs] == wbits
+        np.maximum.at(cand_s, us[tie_u], salts[tie_u])
+        np.maximum.at(cand_s, vs[tie_v], salts[tie_v])
+        tie_u &= cand_s[us] == salts
+        tie_v &= cand_s[vs] == salts
+        np.maximum.at(cand_id, us[tie_u], live[tie_u])
+        np.maximum.at(cand_id, vs[tie_v], live[tie_v])
+        won = (cand_id[us] == live) & (cand_id[vs] == live)
+        new_edges = live[won]
+        parts.append(new_edges)
+        vertex_matched[us[won]] = True
+        vertex_matched[vs[won]] = True
+        alive = ~(vertex_matched[us] | vertex_matched[vs])
+        for ends in (us[alive], vs[alive]):
+            cand_w[ends] = 0
+            cand_s[ends] = 0
+            cand_id[ends] = -1
+        survivors = live[alive]
+        rounds.append((int(live.size), int(new_edges.size), int(live.size - survivors.size)))
+        live = survivors
+        r += 1
+    matched = np.sort(np.concatenate(parts)) if parts else np.empty(0, dtype=np.int64)
+    mate = np.full(n, -1, dtype=np.int64)
+    if matched.size:
+        mate[edge_u[matched]] = edge_v[matched]
+        mate[edge_v[matched]] = edge_u[matched]
+    return OracleResult(mate, matched, rounds)
+
+
+# ---------------------------------------------------------------- generators
+
+def build_graph_loop(edge_list, num_vertices=None):
+    """graph.py:59-119 numbering contract, as (n, edge_u, edge_v, edge_weight)."""
+    kept = {}
+    us, vs, ws = [], [], []
+    max_id = -1
+    for pos, (u, v, w) in enumerate(edge_list):
+        ui, vi = int(u), int(v)
+        if ui < 0 or vi < 0:
+            raise ValueError(f"edge {pos}: negative vertex id ({ui}, {vi})")
+        if num_vertices is not None and (ui >= num_vertices or vi >= num_vertices):
+            raise ValueError(f"edge {pos}: vertex id out of range")
+        wf = float(w)
+        if math.isnan(wf) or math.isinf(wf) or wf < 0.0:
+            raise ValueError(f"edge {pos}: weight must be finite and >= 0, got {w!r}")
+        if ui == vi:
+            continue
+        max_id = max(max_id, ui, vi)
+        pair = (ui, vi) if ui < vi else (vi, ui)
+        at = kept.get(pair)
+        if at is None:
+            kept[pair] = len(us)
+            us.append(ui)
+            vs.append(vi)
+            ws.append(wf)
+        elif wf > ws[at]:
+            us[at], vs[at], ws[at] = ui, vi, wf
+    n = num_vertices if num_vertices is not None else max_id + 1
+    return (n, np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64),
+            np.asarray(ws, dtype=np.float64))
+
+
+def gen_random_edges(n: int, alpha: int, seed: int):
+    """generate.py:48-89 (sparse branch): raw (u, v, w) arrays before build."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    m = alpha * n
+    capacity = n * (n - 1) // 2
+    if m > capacity:
+        raise ValueError("density infeasible")
+    rng = np.random.default_rng(seed)
+    if 2 * m > capacity:
+        lo, hi = np.triu_indices(n, k=1)
+        pick = rng.choice(capacity, size=m, replace=False)
+        chosen = lo[pick] * n + hi[pick]
+        weights = rng.random(m)
+        return chosen // n, chosen % n, weights
+    chosen = np.empty(0, dtype=np.int64)
+    while chosen.size < m:
+        need = m - chosen.size
+        batch = need + need // 8 + 16
+        a = rng.integers(0, n, size=batch, dtype=np.int64)
+        b = rng.integers(0, n, size=batch, dtype=np.int64)
+        ok = a != b
+        lo = np.minimum(a[ok], b[ok])
+        hi = np.maximum(a[ok], b[ok])
+        packed = lo * n + hi
+        _, first = np.unique(packed, return_index=True)
+        packed = packed[np.sort(first)]
+        packed = packed[~np.isin(packed, chosen)]
+        chosen = np.concatenate([chosen, packed[:need]])
+    weights = rng.random(m)
+    return chosen // n, chosen % n, weights
+
+
+def gen_random(n: int, alpha: int, seed: int, unit: bool = False):
+    """generate.py:48-89 (+ with_unit_weights, :219-222).  The raw pairs are
+    distinct and lo < hi, so build_graph keeps them in order unchanged."""
+    u, v, w = gen_random_edges(n, alpha, seed)
+    if unit:
+        w = np.ones_like(w)
+    return n, u.astype(np.int64), v.astype(np.int64), w.astype(np.float64)
+
+
+def _morton_order(points: np.ndarray) -> np.ndarray:
+    """generate.py:97-110."""
+    q = np.clip((points * 65536.0).astype(np.uint32), 0, 65535).astype(np.uint64)
+
+    def spread(b):
+        b = (b | (b << np.uint64(16))) & np.uint64(0x0000FFFF0000FFFF)
+        b = (b | (b << np.uint64(8))) & np.uint64(0x00FF00FF00FF00FF)
+        b = (b | (b << np.uint64(4))) & np.uint64(0x0F0F0F0F0F0F0F0F)
+        b = (b | (b << np.uint64(2))) & np.uint64(0x3333333333333333)
+        b = (b | (b << np.uint64(1))) & np.uint64(0x5555555555555555)
+        return b
+
+    key = spread(q[:, 0]) | (spread(q[:, 1]) << np.uint64(1))
+    return np.argsort(key, kind="stable")
+
+
+def _radius_edges_grid(points: np.ndarray, radius: float):
+    """generate.py:146-197 (same cell sweep order, so same edge order)."""
+    n = points.shape[0]
+    side = max(1, int(math.floor(1.0 / radius)))
+    cx = np.minimum((points[:, 0] / (1.0 / side)).astype(np.int64), side - 1)
+    cy = np.minimum((points[:, 1] / (1.0 / side)).astype(np.int64), side - 1)
+    cell = cx * side + cy
+    order = np.lexsort((np.arange(n), cell))
+    sorted_cell = cell[order]
+    uniq, starts = np.unique(sorted_cell, return_index=True)
+    starts = np.concatenate([starts, [n]])
+    cell_slice = {int(c): (int(starts[i]), int(starts[i + 1])) for i, c in enumerate(uniq)}
+    us, vs, ds = [], [], []
+    r2 = radius * radius
+    for i, c in enumerate(uniq):
+        px, py = int(c) // side, int(c) % side
+        own = order[starts[i]:starts[i + 1]]
+        parts = []
+        for dx in (-1, 0, 1):
+            qx = px + dx
+            if not 0 <= qx < side:
+                continue
+            for dy in (-1, 0, 1):
+                qy = py + dy
+                if not 0 <= qy < side:
+                    continue
+                sl = cell_slice.get(qx * side + qy)
+                if sl is not None:
+                    parts.append(order[sl[0]:sl[1]])
+        cand = np.concatenate(parts)
+        diff = points[own][:, None, :] - points[cand][None, :, :]
+        d2 = np.einsum("ijk,ijk->ij", diff, diff)
+        pi, qi = np.nonzero((d2 < r2) & (own[:, None] < cand[None, :]))
+        if pi.size:
+            us.append(own[pi])
+            vs.append(cand[qi])
+            ds.append(np.sqrt(d2[pi, qi]))
+    if not us:
+        e = np.empty(0, dtype=np.int64)
+        return e, e.copy(), np.empty(0, dtype=np.float64)
+    return np.concatenate(us), np.concatenate(vs), np.concatenate(ds)
+
+
+def gen_rgg(x: int, seed: int, weight_mode: str = "euclidean"):
+    """generate.py:113-143.  Raw pairs are distinct with u < v, so the
+    build_graph numbering is the identity on the raw order."""
+    n = 1 << x
+    rng = np.random.default_rng(seed)
+    points = rng.random((n, 2))
+    points = points[_morton_order(points)]
+    radius = 0.55 * math.sqrt(math.log(n) / n)
+    eu, ev, dist = _radius_edges_grid(points, radius)
+    w = dist if weight_mode == "euclidean" else rng.random(eu.size)
+    return n, eu.astype(np.int64), ev.astype(np.int64), np.asarray(w, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- RMAT (new generator)
+
+_RMAT_TAG0 = 0x524D41545F4C5654
+_RMAT_TAG1 = 0x524D41545F574754
+_RMAT_TAG2 = 0x524D41545F504552
+
+
+def _mix64_int(x: int) -> int:
+    return int(mix64(np.array([x & _UINT64_MASK], dtype=np.uint64))[0])
+
+
+def rmat_perm(x: np.ndarray, scale: int, s2: int) -> np.ndarray:
+    """Restatement of csrc/lmx_build.cu:rmat_perm (bijection on `scale` bits)."""
+    mask = np.uint64((1 << scale) - 1)
+    h = scale // 2 + 1
+    h2 = scale - h if scale - h > 0 else 1
+    with np.errstate(over="ignore"):
+        y = x.astype(np.uint64)
+        y = (y * np.uint64(0x9E3779B97F4A7C15)) & mask
+        y ^= y >> np.uint64(h)
+        y = (y * np.uint64(0xBF58476D1CE4E5B9)) & mask
+        y ^= y >> np.uint64(h2)
+        y ^= np.uint64(s2) & mask
+    return y
+
+
+def rmat_raw(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+             seed: int = 1, permute: bool = True):
+    """CPU restatement of the device RMAT generator (csrc/lmx_build.cu header)."""
+    k = edge_factor << scale
+    A = int(np.rint(a * 65536.0))
+    B = int(np.rint(b * 65536.0))
+    C = int(np.rint(c * 65536.0))
+    AB, ABC = A + B, A + B + C
+    s0 = _mix64_int((seed & _UINT64_MASK) ^ _RMAT_TAG0)
+    s1 = _mix64_int((seed & _UINT64_MASK) ^ _RMAT_TAG1)
+    s2 = _mix64_int((seed & _UINT64_MASK) ^ _RMAT_TAG2)
+    i = np.arange(k, dtype=np.uint64)
+    u = np.zeros(k, dtype=np.uint64)
+    v = np.zeros(k, dtype=np.uint64)
+    h = None
+    with np.errstate(over="ignore"):
+        for lvl in range(scale):
+            if lvl % 4 == 0:
+                h = mix64(np.uint64(s0) ^ (i * np.uint64(16) + np.uint64(lvl // 4)))
+            x = (h >> np.uint64(16 * (lvl % 4))) & np.uint64(0xFFFF)
+            bit = np.uint64(1 << (scale - 1 - lvl))
+            ub = x >= np.uint64(AB)                                   # quadrants (1,0), (1,1)
+            vb = ((x >= np.uint64(A)) & (x < np.uint64(AB))) | (x >= np.uint64(ABC))
+            u |= np.where(ub, bit, np.uint64(0))
+            v |= np.where(vb, bit, np.uint64(0))
+        if permute:
+            u = rmat_perm(u, scale, s2)
+            v = rmat_perm(v, scale, s2)
+        w = (mix64(np.uint64(s1) ^ i) >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return u.astype(np.int64), v.astype(np.int64), w
+
+
+def build_graph_vec(u, v, w, num_vertices=None):
+    """Vectorised numpy restatement of graph.py:59-119 (pinned against
+    build_graph_loop / the reference in tests); used for RMAT-size oracles."""
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    w = np.asarray(w, dtype=np.float64)
+    pos = np.arange(u.size, dtype=np.int64)
+    keep = u != v
+    u, v, w, pos = u[keep], v[keep], w[keep], pos[keep]
+    n = num_vertices if num_vertices is not None else (int(max(u.max(), v.max())) + 1 if u.size else 0)
+    if u.size == 0:
+        e = np.empty(0, dtype=np.int64)
+        return n, e, e.copy(), np.empty(0, dtype=np.float64)
+    lo = np.minimum(u, v)
+    hi = np.maximum(u, v)
+    key = lo * np.int64(max(n, 1)) + hi
+    order = np.lexsort((pos, key))
+    ks = key[order]
+    head = np.ones(ks.size, dtype=bool)
+    head[1:] = ks[1:] != ks[:-1]
+    starts = np.nonzero(head)[0]
+    run = np.cumsum(head) - 1
+    ws = w[order]
+    runmax = np.maximum.reduceat(ws, starts)
+    is_max = ws == runmax[run]
+    big = np.iinfo(np.int64).max
+    cand = np.where(is_max, order, big)          # order is ascending inside a run
+    kept = np.minimum.reduceat(cand, starts)
+    first = order[starts]
+    eo = np.argsort(first, kind="stable")
+    kept = kept[eo]
+    return n, u[kept], v[kept], w[kept]

@@ -1,0 +1,484 @@
+// lmx_build.cu -- device graph builders.
+//
+// lmx_build_graph: the build_graph numbering contract (graph.py:59-119) for
+// raw triple lists too large for the reference's Python dict loop:
+//   * reject negative / out-of-range ids and NaN / inf / negative weights,
+//     naming the first bad input position (graph.py:80-88);
+//   * drop self-loops (graph.py:89-91);
+//   * collapse parallel pairs: keep the first occurrence of the maximum
+//     weight (strict '>' double comparison, graph.py:99-100) with that
+//     occurrence's orientation and weight bits;
+//   * edge ids follow the first occurrence of each pair (graph.py:94-98);
+//   * n = num_vertices, or max id over non-loop triples + 1 (graph.py:103).
+// Implementation: stable LSD radix sort of (pair key, position), one thread
+// per equal-key run, a prefix sum over first-occurrence flags for the ids.
+//
+// lmx_gen_rmat: RMAT (Chakrabarti et al.; Graph500 a,b,c,d) raw triples from a
+// counter-based hash, so the CPU oracle (oracle/oracle.py:rmat_raw) generates
+// the identical list:
+//   s_q  = mix64(seed ^ 0x524D4154...)            (stream keys, q = 0, 1, 2)
+//   level bits: h = mix64(s_0 ^ (i * 16 + l / 4)), x = (h >> 16 * (l % 4)) & 0xFFFF
+//     quadrant (0,0) if x < A, (0,1) if x < A+B, (1,0) if x < A+B+C, else (1,1)
+//     with A = round(a * 65536) etc.; bit (scale-1-l) of u / v
+//   weight: (mix64(s_1 ^ i) >> 11) * 2^-53  in [0, 1)
+//   permute: x -> bijection on scale bits (odd multiplies mod 2^scale, xor
+//     shifts, xor with s_2), applied to both endpoints.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "lmx_internal.cuh"
+
+using namespace lmx;
+
+namespace lmx {
+
+constexpr uint64_t kRmatTag0 = 0x524D41545F4C5654ULL;   // "RMAT_LVT"
+constexpr uint64_t kRmatTag1 = 0x524D41545F574754ULL;   // "RMAT_WGT"
+constexpr uint64_t kRmatTag2 = 0x524D41545F504552ULL;   // "RMAT_PER"
+
+struct RmatParams {
+    int scale;
+    uint32_t A, AB, ABC;   // cumulative 16-bit thresholds
+    uint64_t s0, s1, s2;
+    int permute;
+};
+
+__host__ __device__ __forceinline__ uint32_t rmat_perm(uint32_t x, const RmatParams &p) {
+    const uint64_t mask = (p.scale >= 64) ? ~0ULL : ((1ULL << p.scale) - 1);
+    const int h = p.scale / 2 + 1;
+    uint64_t y = x;
+    y = (y * 0x9E3779B97F4A7C15ULL) & mask;
+    y ^= y >> h;
+    y = (y * 0xBF58476D1CE4E5B9ULL) & mask;
+    y ^= y >> (p.scale - h > 0 ? p.scale - h : 1);
+    y ^= p.s2 & mask;
+    return (uint32_t)y;
+}
+
+__global__ void k_rmat_raw(RmatParams p, unsigned long long k, uint32_t *u, uint32_t *v, double *w) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        uint32_t a = 0, b = 0;
+        uint64_t h = 0;
+        for (int l = 0; l < p.scale; ++l) {
+            if ((l & 3) == 0) h = mix64(p.s0 ^ (i * 16ULL + (unsigned long long)(l >> 2)));
+            const uint32_t x = (uint32_t)((h >> (16 * (l & 3))) & 0xFFFFu);
+            const uint32_t bit = 1u << (p.scale - 1 - l);
+            if (x < p.A) {
+            } else if (x < p.AB) {
+                b |= bit;
+            } else if (x < p.ABC) {
+                a |= bit;
+            } else {
+                a |= bit;
+                b |= bit;
+            }
+        }
+        if (p.permute) {
+            a = rmat_perm(a, p);
+            b = rmat_perm(b, p);
+        }
+        u[i] = a;
+        v[i] = b;
+        w[i] = (double)(mix64(p.s1 ^ i) >> 11) * (1.0 / 9007199254740992.0);
+    }
+}
+
+// Validation of raw int64 triples (graph.py:80-88); narrows ids to u32.
+__global__ void k_raw_convert(const long long *u, const long long *v, const double *w, unsigned long long k,
+                              long long nlimit, unsigned long long base, uint32_t *uo, uint32_t *vo,
+                              double *wo, unsigned long long *bad, unsigned long long *maxid) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long mx = 0;
+    bool any = false;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        const long long a = u[i], b = v[i];
+        const double x = w[i];
+        bool ok = a >= 0 && b >= 0 && a < 0xFFFFFFFFLL && b < 0xFFFFFFFFLL && isfinite(x) && !(x < 0.0);
+        if (nlimit >= 0) ok = ok && a < nlimit && b < nlimit;
+        if (!ok) atomicMin(bad, base + i);
+        uo[base + i] = (uint32_t)a;
+        vo[base + i] = (uint32_t)b;
+        wo[base + i] = x;
+        if (ok && a != b) {
+            const unsigned long long t = (unsigned long long)(a > b ? a : b);
+            mx = t > mx ? t : mx;
+            any = true;
+        }
+    }
+    if (any) atomicMax(maxid, mx + 1);
+}
+
+__global__ void k_max_id(const uint32_t *u, const uint32_t *v, unsigned long long k, unsigned long long *maxid) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long mx = 0;
+    bool any = false;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        if (u[i] != v[i]) {
+            const unsigned long long t = u[i] > v[i] ? u[i] : v[i];
+            mx = t > mx ? t : mx;
+            any = true;
+        }
+    }
+    if (any) atomicMax(maxid, mx + 1);
+}
+
+__global__ void k_pair_keys(const uint32_t *u, const uint32_t *v, unsigned long long k, int bits,
+                            unsigned long long *key, uint32_t *idx) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long all = (bits >= 32) ? 0xFFFFFFFFULL : ((1ULL << bits) - 1);
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        const unsigned long long a = u[i], b = v[i];
+        const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+        key[i] = (a == b) ? ((all << bits) | all) : ((lo << bits) | hi);   // loops -> one sentinel run
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// One thread per run head: keep the first occurrence of the max weight.
+__global__ void k_runs(const unsigned long long *key, const uint32_t *idx, unsigned long long k,
+                       unsigned long long sentinel, const uint32_t *u, const uint32_t *v, const double *w,
+                       uint32_t *first_flag, uint32_t *kept) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        const unsigned long long kk = key[i];
+        if (kk == sentinel) continue;
+        if (i > 0 && key[i - 1] == kk) continue;
+        uint32_t best = idx[i];
+        double bw = w[best];
+        for (unsigned long long j = i + 1; j < k && key[j] == kk; ++j) {
+            const uint32_t c = idx[j];
+            const double cw = w[c];
+            if (cw > bw) {   // graph.py:99 strict '>' keeps the earliest of equal weights
+                bw = cw;
+                best = c;
+            }
+        }
+        first_flag[idx[i]] = 1u;   // idx ascending inside a run: idx[i] is the first occurrence
+        kept[i] = best;
+    }
+}
+
+__global__ void k_emit(const unsigned long long *key, const uint32_t *idx, unsigned long long k,
+                       unsigned long long sentinel, const uint32_t *kept, const uint32_t *eid_of_pos,
+                       const uint32_t *u, const uint32_t *v, const double *w, uint32_t *eu, uint32_t *ev,
+                       double *ew) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        const unsigned long long kk = key[i];
+        if (kk == sentinel) continue;
+        if (i > 0 && key[i - 1] == kk) continue;
+        const uint32_t e = eid_of_pos[idx[i]];
+        const uint32_t c = kept[i];
+        eu[e] = u[c];
+        ev[e] = v[c];
+        ew[e] = w[c];
+    }
+}
+
+__global__ void k_export(const uint32_t *eu, const uint32_t *ev, unsigned long long m, long long *u,
+                         long long *v) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += stride) {
+        u[i] = eu[i];
+        v[i] = ev[i];
+    }
+}
+
+}  // namespace lmx
+
+static int bgrid(lmx_ctx *ctx, unsigned long long work) {
+    unsigned long long b = (work + kBlock - 1) / kBlock;
+    const unsigned long long cap = (unsigned long long)ctx->num_sms * 16;
+    return (int)std::max<unsigned long long>(1, std::min(b, cap));
+}
+
+static int bits_for(unsigned long long n) {
+    int b = 1;
+    while (b < 32 && (1ULL << b) < n) ++b;
+    return b;
+}
+
+// Dedupe/number raw triples ru/rv/rw (device, k entries) into ctx->eu/ev/w; frees the raw arrays.
+static int build_from_raw(lmx_ctx *ctx, uint32_t *ru, uint32_t *rv, double *rw, unsigned long long k,
+                          long long n) {
+    cudaStream_t st = ctx->stream;
+    const int bits = bits_for((unsigned long long)std::max<long long>(n, 2));
+    const unsigned long long all = (bits >= 32) ? 0xFFFFFFFFULL : ((1ULL << bits) - 1);
+    const unsigned long long sentinel = (all << bits) | all;
+    unsigned long long *key = nullptr, *key2 = nullptr;
+    uint32_t *idx = nullptr, *idx2 = nullptr, *flag = nullptr, *kept = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    const size_t kk = std::max<unsigned long long>(k, 1);
+    int rc = LMX_OK;
+    unsigned long long m = 0;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&key, kk * 8, "build keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&key2, kk * 8, "build keys2")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&idx, kk * 4, "build idx")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&idx2, kk * 4, "build idx2")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&flag, (kk + 1) * 4, "build flags")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&kept, kk * 4, "build kept")) != LMX_OK) break;
+        k_pair_keys<<<bgrid(ctx, k), kBlock, 0, st>>>(ru, rv, k, bits, key, idx);
+        size_t t1 = 0, t2 = 0;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, key, key2, idx, idx2, (long long)k, 0,
+                                                        2 * bits, st);
+        if (e == cudaSuccess)
+            e = cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, flag, (long long)(k + 1), st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build sizing"); break; }
+        tmp_bytes = std::max(t1, t2);
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "build tmp")) != LMX_OK) break;
+        e = cub::DeviceRadixSort::SortPairs(tmp, t1, key, key2, idx, idx2, (long long)k, 0, 2 * bits, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, (kk + 1) * 4, st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build sort"); break; }
+        k_runs<<<bgrid(ctx, k), kBlock, 0, st>>>(key2, idx2, k, sentinel, ru, rv, rw, flag, kept);
+        e = cub::DeviceScan::ExclusiveSum(tmp, t2, flag, flag, (long long)(k + 1), st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&m, flag + k, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build runs"); break; }
+        m &= 0xFFFFFFFFULL;
+        lmx_free_graph(ctx);
+        ctx->n = n;
+        ctx->m = (int64_t)m;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->eu, std::max<size_t>(m, 1) * 4, "edge_u")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->ev, std::max<size_t>(m, 1) * 4, "edge_v")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->w, std::max<size_t>(m, 1) * 8, "edge_weight")) != LMX_OK) break;
+        k_emit<<<bgrid(ctx, k), kBlock, 0, st>>>(key2, idx2, k, sentinel, kept, flag, ru, rv, rw, ctx->eu,
+                                                ctx->ev, ctx->w);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build emit"); break; }
+    } while (0);
+    cudaStreamSynchronize(st);
+    // dev_bytes accounting of these temporaries is not tracked after lmx_free_graph; just free
+    if (key) cudaFree(key);
+    if (key2) cudaFree(key2);
+    if (idx) cudaFree(idx);
+    if (idx2) cudaFree(idx2);
+    if (flag) cudaFree(flag);
+    if (kept) cudaFree(kept);
+    if (tmp) cudaFree(tmp);
+    cudaFree(ru);
+    cudaFree(rv);
+    cudaFree(rw);
+    if (rc != LMX_OK) return rc;
+    return lmx_setup_slots(ctx);
+}
+
+static RmatParams rmat_params(int scale, double a, double b, double c, uint64_t seed, int permute) {
+    RmatParams p;
+    p.scale = scale;
+    const double A = std::nearbyint(a * 65536.0), B = std::nearbyint(b * 65536.0), C = std::nearbyint(c * 65536.0);
+    p.A = (uint32_t)A;
+    p.AB = (uint32_t)(A + B);
+    p.ABC = (uint32_t)(A + B + C);
+    p.s0 = mix64(seed ^ kRmatTag0);
+    p.s1 = mix64(seed ^ kRmatTag1);
+    p.s2 = mix64(seed ^ kRmatTag2);
+    p.permute = permute;
+    return p;
+}
+
+static int rmat_check(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c) {
+    if (scale < 1 || scale > 31) return lmx_fail(ctx, LMX_EINVAL, "scale must be in [1, 31]");
+    if (edge_factor < 1) return lmx_fail(ctx, LMX_EINVAL, "edge_factor must be >= 1");
+    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0))
+        return lmx_fail(ctx, LMX_EINVAL, "RMAT probabilities must be >= 0 with a+b+c <= 1");
+    const unsigned long long k = (unsigned long long)edge_factor << scale;
+    if (k >= 0xFFFFFFFFULL) return lmx_fail(ctx, LMX_ELIMIT, "raw edge count exceeds 32-bit positions");
+    return LMX_OK;
+}
+
+extern "C" {
+
+int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                     int permute, int64_t *u_out, int64_t *v_out, double *w_out, int out_where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    LMX_TRY(rmat_check(ctx, scale, edge_factor, a, b, c));
+    const unsigned long long k = (unsigned long long)edge_factor << scale;
+    const RmatParams p = rmat_params(scale, a, b, c, seed, permute);
+    uint32_t *ru = nullptr, *rv = nullptr;
+    double *rw = nullptr;
+    long long *lu = nullptr, *lv = nullptr;
+    LMX_CUDA(ctx, cudaMalloc(&ru, k * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rv, k * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rw, k * 8));
+    LMX_CUDA(ctx, cudaMalloc(&lu, k * 8));
+    LMX_CUDA(ctx, cudaMalloc(&lv, k * 8));
+    k_rmat_raw<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(p, k, ru, rv, rw);
+    k_export<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(ru, rv, k, lu, lv);
+    const cudaMemcpyKind kind = out_where == LMX_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaError_t e = cudaMemcpyAsync(u_out, lu, k * 8, kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(v_out, lv, k * 8, kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(w_out, rw, k * 8, kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(ru);
+    cudaFree(rv);
+    cudaFree(rw);
+    cudaFree(lu);
+    cudaFree(lv);
+    LMX_CUDA(ctx, e);
+    return LMX_OK;
+}
+
+int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                 int permute) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    LMX_TRY(rmat_check(ctx, scale, edge_factor, a, b, c));
+    const unsigned long long k = (unsigned long long)edge_factor << scale;
+    const RmatParams p = rmat_params(scale, a, b, c, seed, permute);
+    lmx_free_graph(ctx);
+    uint32_t *ru = nullptr, *rv = nullptr;
+    double *rw = nullptr;
+    LMX_CUDA(ctx, cudaMalloc(&ru, k * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rv, k * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rw, k * 8));
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    k_rmat_raw<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(p, k, ru, rv, rw);
+    LMX_CUDA(ctx, cudaGetLastError());
+    LMX_TRY(build_from_raw(ctx, ru, rv, rw, k, 1LL << scale));
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->timing.setup_ms = ms;
+    return LMX_OK;
+}
+
+int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v, const double *w,
+                    int64_t num_vertices, int where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (k < 0) return lmx_fail(ctx, LMX_EINVAL, "negative triple count");
+    if (k >= (int64_t)0xFFFFFFFFLL) return lmx_fail(ctx, LMX_ELIMIT, "triple count exceeds 32-bit positions");
+    if (num_vertices >= (int64_t)0xFFFFFFFFLL) return lmx_fail(ctx, LMX_ELIMIT, "n exceeds 32-bit ids");
+    lmx_free_graph(ctx);
+    cudaStream_t st = ctx->stream;
+    const unsigned long long kk = (unsigned long long)k;
+    uint32_t *ru = nullptr, *rv = nullptr;
+    double *rw = nullptr;
+    unsigned long long *flags = nullptr;   // [0] first bad, [1] max id + 1
+    LMX_CUDA(ctx, cudaMalloc(&ru, std::max<size_t>(kk, 1) * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rv, std::max<size_t>(kk, 1) * 4));
+    LMX_CUDA(ctx, cudaMalloc(&rw, std::max<size_t>(kk, 1) * 8));
+    LMX_CUDA(ctx, cudaMalloc(&flags, 16));
+    unsigned long long init[2] = {~0ULL, 0ULL};
+    LMX_CUDA(ctx, cudaMemcpyAsync(flags, init, 16, cudaMemcpyHostToDevice, st));
+    cudaError_t e = cudaSuccess;
+    if (kk > 0) {
+        if (where == LMX_DEVICE) {
+            k_raw_convert<<<bgrid(ctx, kk), kBlock, 0, st>>>((const long long *)u, (const long long *)v, w, kk,
+                                                             num_vertices, 0, ru, rv, rw, flags, flags + 1);
+            e = cudaGetLastError();
+        } else {
+            const unsigned long long chunk = 1ULL << 24;
+            const size_t cb = std::min<unsigned long long>(chunk, kk);
+            long long *su = nullptr, *sv = nullptr;
+            double *sw = nullptr;
+            LMX_CUDA(ctx, cudaMalloc(&su, cb * 8));
+            LMX_CUDA(ctx, cudaMalloc(&sv, cb * 8));
+            LMX_CUDA(ctx, cudaMalloc(&sw, cb * 8));
+            for (unsigned long long off = 0; off < kk && e == cudaSuccess; off += chunk) {
+                const unsigned long long c = std::min(chunk, kk - off);
+                e = cudaMemcpyAsync(su, u + off, c * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(sv, v + off, c * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(sw, w + off, c * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) {
+                    k_raw_convert<<<bgrid(ctx, c), kBlock, 0, st>>>(su, sv, sw, c, num_vertices, off, ru, rv, rw,
+                                                                   flags, flags + 1);
+                    e = cudaGetLastError();
+                }
+            }
+            cudaStreamSynchronize(st);
+            cudaFree(su);
+            cudaFree(sv);
+            cudaFree(sw);
+        }
+    }
+    unsigned long long got[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(got, flags, 16, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(flags);
+    if (e != cudaSuccess) {
+        cudaFree(ru);
+        cudaFree(rv);
+        cudaFree(rw);
+        return lmx_cuda_check(ctx, e, "build_graph input");
+    }
+    if (got[0] != ~0ULL) {
+        cudaFree(ru);
+        cudaFree(rv);
+        cudaFree(rw);
+        const unsigned long long pos = got[0];
+        int64_t a = 0, b = 0;
+        double x = 0;
+        if (where == LMX_HOST) {
+            a = u[pos];
+            b = v[pos];
+            x = w[pos];
+        } else {
+            cudaMemcpy(&a, u + pos, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(&b, v + pos, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(&x, w + pos, 8, cudaMemcpyDeviceToHost);
+        }
+        char buf[256];
+        if (a < 0 || b < 0)
+            snprintf(buf, sizeof buf, "edge %llu: negative vertex id (%lld, %lld)", pos, (long long)a, (long long)b);
+        else if (num_vertices >= 0 && (a >= num_vertices || b >= num_vertices))
+            snprintf(buf, sizeof buf, "edge %llu: vertex id out of range for n=%lld: (%lld, %lld)", pos,
+                     (long long)num_vertices, (long long)a, (long long)b);
+        else if (std::isnan(x) || std::isinf(x) || x < 0)
+            snprintf(buf, sizeof buf, "edge %llu: weight must be finite and >= 0, got %.17g", pos, x);
+        else
+            snprintf(buf, sizeof buf, "edge %llu: vertex id exceeds 32-bit range", pos);
+        return lmx_fail(ctx, LMX_EINVAL, buf);
+    }
+    const long long n = num_vertices >= 0 ? num_vertices : (long long)got[1];
+    return build_from_raw(ctx, ru, rv, rw, kk, n);
+}
+
+int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edge_weight, int out_where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    const unsigned long long m = (unsigned long long)ctx->m;
+    if (m == 0) return LMX_OK;
+    long long *lu = nullptr, *lv = nullptr;
+    if (out_where == LMX_DEVICE) {
+        lu = (long long *)edge_u;
+        lv = (long long *)edge_v;
+    } else {
+        LMX_CUDA(ctx, cudaMalloc(&lu, m * 8));
+        LMX_CUDA(ctx, cudaMalloc(&lv, m * 8));
+    }
+    k_export<<<bgrid(ctx, m), kBlock, 0, ctx->stream>>>(ctx->eu, ctx->ev, m, lu, lv);
+    cudaError_t e = cudaGetLastError();
+    const cudaMemcpyKind kind = out_where == LMX_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (e == cudaSuccess && out_where != LMX_DEVICE) {
+        e = cudaMemcpyAsync(edge_u, lu, m * 8, kind, ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(edge_v, lv, m * 8, kind, ctx->stream);
+    }
+    if (e == cudaSuccess && edge_weight) e = cudaMemcpyAsync(edge_weight, ctx->w, m * 8, kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (out_where != LMX_DEVICE) {
+        cudaFree(lu);
+        cudaFree(lv);
+    }
+    LMX_CUDA(ctx, e);
+    return LMX_OK;
+}
+
+}  // extern "C"

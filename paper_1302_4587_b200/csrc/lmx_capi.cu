@@ -1,0 +1,175 @@
+// lmx_capi.cu -- the extern "C" boundary declared in include/lmx.h.
+#include <cstring>
+#include <vector>
+
+#include "lmx_internal.cuh"
+
+namespace {
+thread_local std::string g_create_err;
+}  // namespace
+
+extern "C" {
+
+int lmx_abi_version(void) { return LMX_ABI_VERSION; }
+
+int lmx_create(int device, lmx_ctx **out) {
+    if (!out) return LMX_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        g_create_err = std::string("no CUDA device available: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return LMX_ECUDA;
+    }
+    if (device < 0 || device >= count) {
+        g_create_err = "device index out of range";
+        return LMX_EINVAL;
+    }
+    lmx_ctx *ctx = new lmx_ctx();
+    ctx->device = device;
+    int rc = LMX_OK;
+    do {
+        if ((e = cudaSetDevice(device)) != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "cudaSetDevice"); break; }
+        cudaDeviceProp prop;
+        if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "props"); break; }
+        if (prop.major != 10) {
+            rc = lmx_fail(ctx, LMX_ECUDA, std::string("liblmx is built for sm_100a (B200); device is ") + prop.name);
+            break;
+        }
+        ctx->num_sms = prop.multiProcessorCount;
+        if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            rc = lmx_cuda_check(ctx, e, "stream");
+            break;
+        }
+        ctx->own_stream = true;
+        if ((e = cudaEventCreate(&ctx->ev0)) != cudaSuccess || (e = cudaEventCreate(&ctx->ev1)) != cudaSuccess ||
+            (e = cudaEventCreate(&ctx->ev2)) != cudaSuccess) {
+            rc = lmx_cuda_check(ctx, e, "events");
+            break;
+        }
+        rc = lmx_configure_grids(ctx);
+    } while (0);
+    if (rc != LMX_OK) {
+        g_create_err = ctx->err;
+        lmx_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return LMX_OK;
+}
+
+void lmx_destroy(lmx_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    lmx_free_graph(ctx);
+    if (ctx->ctr) cudaFree(ctx->ctr);
+    if (ctx->ctr_host) cudaFreeHost(ctx->ctr_host);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *lmx_last_error(const lmx_ctx *ctx) {
+    if (!ctx) return g_create_err.c_str();
+    return ctx->err.c_str();
+}
+
+int lmx_set_stream(lmx_ctx *ctx, void *cuda_stream) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+        ctx->own_stream = false;
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return lmx_cuda_check(ctx, e, "stream");
+        ctx->own_stream = true;
+    }
+    return LMX_OK;
+}
+
+int lmx_load_graph(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
+                   const double *edge_weight, int where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    int rc = lmx_load_edges(ctx, n, m, edge_u, edge_v, edge_weight, where);
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->timing.setup_ms = ms;
+    return LMX_OK;
+}
+
+int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate_out,
+              int64_t *matched_ids_out, int64_t *n_matched_out, lmx_round_stats *rounds_out,
+              int max_rounds, int *n_rounds_out, int out_where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded (call lmx_load_graph first)");
+    std::vector<lmx_round_stats> &stats = ctx->rounds;
+    unsigned long long nm = 0;
+    LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
+    LMX_TRY(lmx_emit_outputs(ctx, nm, mate_out, matched_ids_out, out_where));
+    if (n_matched_out) *n_matched_out = (int64_t)nm;
+    if (n_rounds_out) *n_rounds_out = (int)stats.size();
+    if (rounds_out)
+        for (int i = 0; i < (int)stats.size() && i < max_rounds; ++i) rounds_out[i] = stats[i];
+    if (rounds_out && (int)stats.size() > max_rounds)
+        return lmx_fail(ctx, LMX_ELIMIT, "rounds_out too small; fetch with lmx_last_rounds");
+    return LMX_OK;
+}
+
+int lmx_last_rounds(lmx_ctx *ctx, lmx_round_stats *out, int cap) {
+    if (!ctx) return -1;
+    std::vector<lmx_round_stats> &stats = ctx->rounds;
+    for (int i = 0; i < (int)stats.size() && i < cap; ++i) out[i] = stats[i];
+    return (int)stats.size();
+}
+
+int lmx_last_timing(const lmx_ctx *ctx, lmx_timing *out) {
+    if (!ctx || !out) return LMX_EINVAL;
+    *out = ctx->timing;
+    return LMX_OK;
+}
+
+int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
+                  const double *edge_weight, uint64_t seed_masked, int rerandomize, int64_t *mate_out,
+                  int64_t *matched_ids_out, int64_t *n_matched_out, lmx_round_stats *rounds_out,
+                  int max_rounds, int *n_rounds_out, char *err, size_t errlen) {
+    lmx_ctx *ctx = nullptr;
+    int rc = lmx_create(device, &ctx);
+    if (rc == LMX_OK) rc = lmx_load_graph(ctx, n, m, edge_u, edge_v, edge_weight, LMX_HOST);
+    if (rc == LMX_OK)
+        rc = lmx_match(ctx, seed_masked, rerandomize, mate_out, matched_ids_out, n_matched_out, rounds_out,
+                       max_rounds, n_rounds_out, LMX_HOST);
+    if (rc != LMX_OK && err && errlen) {
+        const char *msg = lmx_last_error(ctx);
+        std::strncpy(err, msg, errlen - 1);
+        err[errlen - 1] = 0;
+    }
+    lmx_destroy(ctx);
+    return rc;
+}
+
+int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out) {
+    if (!ctx) return LMX_EINVAL;
+    if (n_out) *n_out = ctx->n;
+    if (m_out) *m_out = ctx->m;
+    return LMX_OK;
+}
+
+int64_t lmx_device_bytes(const lmx_ctx *ctx) { return ctx ? ctx->dev_bytes : 0; }
+
+}  // extern "C"
+

@@ -1,0 +1,402 @@
+// lmx_setup.cu -- K0: device slot records from the reference's edge arrays.
+//
+// The reference keeps a CSR incidence layout (graph.py:108-115: slots sorted
+// by (vertex, edge id), offsets = cumsum of degrees).  local_max_seq itself
+// only reads edge_u / edge_v / edge_weight (matchers.py:80-92), so the device
+// layout is rebuilt here from those arrays:
+//   1. validate + narrow to u32  (graph.py:80-88 domain rules)
+//   2. degree histogram, exclusive scan -> vbeg (u64 offsets)
+//   3. scatter {nbr, eid} slot records (order inside a segment is free: the
+//      key order is total)
+//   4. weight order: if all canonical weight bits are equal, no weight key;
+//      else dense rank of the canonical bits (tiebreak.py:105-113, -0.0 -> 0)
+//      as a u32 key per slot.  The rank preserves the reference's uint64
+//      comparison exactly, so argmax results are bit-identical.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "lmx_internal.cuh"
+
+using namespace lmx;
+
+int lmx_fail(lmx_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int lmx_cuda_check(lmx_ctx *ctx, cudaError_t e, const char *what) {
+    std::string m = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                    ") in " + what;
+    if (e == cudaErrorMemoryAllocation) return lmx_fail(ctx, LMX_ENOMEM, m);
+    return lmx_fail(ctx, LMX_ECUDA, m);
+}
+
+int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what) {
+    if (*p) return LMX_OK;
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return lmx_fail(ctx, e == cudaErrorMemoryAllocation ? LMX_ENOMEM : LMX_ECUDA,
+                        std::string("cudaMalloc(") + std::to_string(bytes) + " B) failed for " + what +
+                            ": " + cudaGetErrorString(e));
+    }
+    ctx->dev_bytes += (int64_t)bytes;
+    return LMX_OK;
+}
+
+void lmx_free(lmx_ctx *ctx, void **p, size_t bytes) {
+    if (*p) {
+        cudaFree(*p);
+        ctx->dev_bytes -= (int64_t)bytes;
+        *p = nullptr;
+    }
+}
+
+void lmx_free_graph(lmx_ctx *ctx) {
+    void **ptrs[] = {(void **)&ctx->eu,     (void **)&ctx->ev,     (void **)&ctx->w,
+                     (void **)&ctx->vbeg,   (void **)&ctx->ids0,   (void **)&ctx->ids1,
+                     (void **)&ctx->wk0,    (void **)&ctx->wk1,    (void **)&ctx->deg0,
+                     (void **)&ctx->vdeg,   (void **)&ctx->cand,   (void **)&ctx->matched,
+                     (void **)&ctx->L[0],   (void **)&ctx->L[1],   (void **)&ctx->H[0],
+                     (void **)&ctx->H[1],   (void **)&ctx->hubs0,  (void **)&ctx->mids,
+                     (void **)&ctx->mids_sorted, (void **)&ctx->mcount, (void **)&ctx->mate,
+                     (void **)&ctx->sort_tmp};
+    for (void **p : ptrs) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    ctx->dev_bytes = 0;
+    ctx->n = ctx->m = 0;
+    ctx->has_wk = false;
+    ctx->n_hubs0 = 0;
+    ctx->sort_tmp_bytes = 0;
+}
+
+namespace lmx {
+
+__device__ __forceinline__ unsigned long long canon_bits(double w) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(w);
+    return (b << 1) == 0 ? 0ULL : b;   // -0.0 -> +0.0 (tiebreak.py:112)
+}
+
+// graph.py:80-88: ids in range, weights finite and >= 0; plus no self loops
+// (a built Graph has none, graph.py:89-91).  Records the first bad position.
+__global__ void k_convert(const long long *u, const long long *v, const double *w,
+                          unsigned long long k, long long n, unsigned long long base, uint32_t *eu,
+                          uint32_t *ev, double *wout, unsigned long long *bad) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += stride) {
+        const long long a = u[i], b = v[i];
+        const double x = w[i];
+        const bool ok = a >= 0 && b >= 0 && a < n && b < n && a != b && isfinite(x) && !(x < 0.0);
+        if (!ok) atomicMin(bad, base + i);
+        eu[base + i] = (uint32_t)a;
+        ev[base + i] = (uint32_t)b;
+        wout[base + i] = x;
+    }
+}
+
+__global__ void k_degrees(const uint32_t *eu, const uint32_t *ev, unsigned long long m, uint32_t *deg) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += stride) {
+        atomicAdd(deg + eu[e], 1u);
+        atomicAdd(deg + ev[e], 1u);
+    }
+}
+
+__global__ void k_widen_deg(const uint32_t *deg, unsigned long long *out, unsigned long long n) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+         i += stride)
+        out[i] = i < n ? deg[i] : 0ULL;
+}
+
+__global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long long m,
+                          const unsigned long long *vbeg, uint32_t *fill, uint2 *ids) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += stride) {
+        const uint32_t a = eu[e], b = ev[e];
+        const unsigned long long pa = vbeg[a] + atomicAdd(fill + a, 1u);
+        const unsigned long long pb = vbeg[b] + atomicAdd(fill + b, 1u);
+        ids[pa] = make_uint2(b, (uint32_t)e);
+        ids[pb] = make_uint2(a, (uint32_t)e);
+    }
+}
+
+__global__ void k_minmax_bits(const double *w, unsigned long long m, unsigned long long *mm) {
+    unsigned long long lo = ~0ULL, hi = 0;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += stride) {
+        const unsigned long long b = canon_bits(w[e]);
+        lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, off);
+        const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+
+__global__ void k_keys(const double *w, unsigned long long m, unsigned long long *keys, uint32_t *vals) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += stride) {
+        keys[e] = canon_bits(w[e]);
+        vals[e] = (uint32_t)e;
+    }
+}
+
+__global__ void k_heads(const unsigned long long *sorted, unsigned long long m, uint32_t *flag) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += stride)
+        flag[i] = (i > 0 && sorted[i] != sorted[i - 1]) ? 1u : 0u;
+}
+
+__global__ void k_rank_scatter(const uint32_t *rank, const uint32_t *vals, unsigned long long m,
+                               uint32_t *wk_edge) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += stride)
+        wk_edge[vals[i]] = rank[i];
+}
+
+__global__ void k_slot_wk(const uint2 *ids, unsigned long long slots, const uint32_t *wk_edge,
+                          uint32_t *wk) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
+         i += stride)
+        wk[i] = wk_edge[ids[i].y];
+}
+
+struct IsHub {
+    const uint32_t *deg;
+    __device__ bool operator()(uint32_t v) const { return deg[v] >= kHubMin; }
+};
+
+}  // namespace lmx
+
+static int grid_for(lmx_ctx *ctx, unsigned long long work) {
+    unsigned long long b = (work + kBlock - 1) / kBlock;
+    const unsigned long long cap = (unsigned long long)ctx->num_sms * 16;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+// Build vbeg / ids0 / wk0 / deg0 / hubs0 from ctx->eu, ev, w (K0).
+int lmx_setup_slots(lmx_ctx *ctx) {
+    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
+    const unsigned long long slots = 2 * m;
+    cudaStream_t st = ctx->stream;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4, "deg0"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (n + 1) * 8, "vbeg"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
+    LMX_TRY(lmx_alloc_match_state(ctx));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->deg0, 0, std::max<size_t>(n, 1) * 4, st));
+    if (m) {
+        k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(ctx->deg0, ctx->vbeg, n);
+    LMX_CUDA(ctx, cudaGetLastError());
+    {
+        size_t tmp = 0;
+        LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->vbeg, ctx->vbeg,
+                                                    (long long)(n + 1), st));
+        void *t = nullptr;
+        LMX_TRY(lmx_alloc(ctx, &t, tmp, "scan tmp"));
+        cudaError_t e = cub::DeviceScan::ExclusiveSum(t, tmp, ctx->vbeg, ctx->vbeg, (long long)(n + 1), st);
+        cudaStreamSynchronize(st);
+        lmx_free(ctx, &t, tmp);
+        LMX_CUDA(ctx, e);
+    }
+    if (m) {
+        // fill counters reuse vdeg
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, n * 4, st));
+        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, ctx->vdeg,
+                                                      ctx->ids0);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    // weight key
+    ctx->has_wk = false;
+    if (m) {
+        unsigned long long *mm = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&mm, 16, "minmax"));
+        unsigned long long init[2] = {~0ULL, 0ULL};
+        LMX_CUDA(ctx, cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
+        k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
+        LMX_CUDA(ctx, cudaGetLastError());
+        unsigned long long got[2];
+        LMX_CUDA(ctx, cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        lmx_free(ctx, (void **)&mm, 16);
+        ctx->has_wk = got[0] != got[1];
+    }
+    if (ctx->has_wk) {
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0"));
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1"));
+        unsigned long long *keys = nullptr, *keys2 = nullptr;
+        uint32_t *vals = nullptr, *vals2 = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        int rc = LMX_OK;
+        do {
+            if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
+            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
+            size_t t1 = 0, t2 = 0;
+            cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, vals, vals2,
+                                                            (long long)m, 0, 64, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "SortPairs size"); break; }
+            e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "scan size"); break; }
+            tmp_bytes = std::max(t1, t2);
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
+            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "SortPairs"); break; }
+            // keys2 sorted, vals2 = eids; heads -> vals (reuse), inclusive sum -> dense rank
+            k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
+            e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank scan"); break; }
+            // wk_edge lives in keys (reuse as u32 array of m)
+            uint32_t *wk_edge = (uint32_t *)keys;
+            k_rank_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, vals2, m, wk_edge);
+            k_slot_wk<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, wk_edge, ctx->wk0);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank kernels"); break; }
+            e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank sync"); break; }
+        } while (0);
+        cudaStreamSynchronize(st);
+        lmx_free(ctx, (void **)&keys, m * 8);
+        lmx_free(ctx, (void **)&keys2, m * 8);
+        lmx_free(ctx, (void **)&vals, m * 4);
+        lmx_free(ctx, (void **)&vals2, m * 4);
+        lmx_free(ctx, &tmp, tmp_bytes);
+        if (rc != LMX_OK) return rc;
+    }
+    // hub list for round 0 (deterministic order: ascending vertex id)
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hubs0, std::max<size_t>(n, 1) * 4, "hubs0"));
+    {
+        unsigned long long *cnt = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8, "hub count"));
+        cub::CountingInputIterator<uint32_t> it(0);
+        IsHub pred{ctx->deg0};
+        size_t tmp = 0;
+        LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->hubs0, cnt, (long long)n, pred, st));
+        void *t = nullptr;
+        LMX_TRY(lmx_alloc(ctx, &t, tmp, "select tmp"));
+        cudaError_t e = cub::DeviceSelect::If(t, tmp, it, ctx->hubs0, cnt, (long long)n, pred, st);
+        unsigned long long h = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        lmx_free(ctx, &t, tmp);
+        lmx_free(ctx, (void **)&cnt, 8);
+        LMX_CUDA(ctx, e);
+        ctx->n_hubs0 = (unsigned int)h;
+    }
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    return LMX_OK;
+}
+
+// lmx_load_graph: validate + narrow the edge arrays, then K0.
+int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
+                   const double *edge_weight, int where) {
+    if (n < 0 || m < 0) return lmx_fail(ctx, LMX_EINVAL, "negative n or m");
+    if (n >= (int64_t)0xFFFFFFFFLL) return lmx_fail(ctx, LMX_ELIMIT, "n exceeds the 32-bit vertex id range");
+    if (m >= (int64_t)0xFFFFFFFFLL) return lmx_fail(ctx, LMX_ELIMIT, "m exceeds the 32-bit edge id range");
+    if (m > 0 && (!edge_u || !edge_v || !edge_weight))
+        return lmx_fail(ctx, LMX_EINVAL, "null edge array");
+    lmx_free_graph(ctx);
+    ctx->n = n;
+    ctx->m = m;
+    cudaStream_t st = ctx->stream;
+    const size_t mm = std::max<int64_t>(m, 1);
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->eu, mm * 4, "edge_u"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ev, mm * 4, "edge_v"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->w, mm * 8, "edge_weight"));
+    unsigned long long *bad = nullptr;
+    LMX_TRY(lmx_alloc(ctx, (void **)&bad, 8, "bad"));
+    LMX_CUDA(ctx, cudaMemsetAsync(bad, 0xFF, 8, st));
+    if (m > 0) {
+        if (where == LMX_DEVICE) {
+            k_convert<<<grid_for(ctx, m), kBlock, 0, st>>>((const long long *)edge_u, (const long long *)edge_v,
+                                                          edge_weight, (unsigned long long)m, n, 0, ctx->eu,
+                                                          ctx->ev, ctx->w, bad);
+            LMX_CUDA(ctx, cudaGetLastError());
+        } else {
+            // chunked H2D through two staging buffers of int64 ids
+            const unsigned long long chunk = 1ULL << 24;
+            long long *su = nullptr, *sv = nullptr;
+            double *sw = nullptr;
+            const size_t cb = std::min<unsigned long long>(chunk, (unsigned long long)m);
+            LMX_TRY(lmx_alloc(ctx, (void **)&su, cb * 8, "stage u"));
+            LMX_TRY(lmx_alloc(ctx, (void **)&sv, cb * 8, "stage v"));
+            LMX_TRY(lmx_alloc(ctx, (void **)&sw, cb * 8, "stage w"));
+            cudaError_t e = cudaSuccess;
+            for (unsigned long long off = 0; off < (unsigned long long)m && e == cudaSuccess; off += chunk) {
+                const unsigned long long k = std::min<unsigned long long>(chunk, (unsigned long long)m - off);
+                e = cudaMemcpyAsync(su, edge_u + off, k * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(sv, edge_v + off, k * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(sw, edge_weight + off, k * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) {
+                    k_convert<<<grid_for(ctx, k), kBlock, 0, st>>>(su, sv, sw, k, n, off, ctx->eu, ctx->ev,
+                                                                  ctx->w, bad);
+                    e = cudaGetLastError();
+                }
+            }
+            cudaStreamSynchronize(st);
+            lmx_free(ctx, (void **)&su, cb * 8);
+            lmx_free(ctx, (void **)&sv, cb * 8);
+            lmx_free(ctx, (void **)&sw, cb * 8);
+            LMX_CUDA(ctx, e);
+        }
+    }
+    unsigned long long badpos = 0;
+    LMX_CUDA(ctx, cudaMemcpyAsync(&badpos, bad, 8, cudaMemcpyDeviceToHost, st));
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    lmx_free(ctx, (void **)&bad, 8);
+    if (badpos != ~0ULL) {
+        int64_t u = 0, v = 0;
+        double w = 0;
+        if (where == LMX_HOST) {
+            u = edge_u[badpos];
+            v = edge_v[badpos];
+            w = edge_weight[badpos];
+        } else {
+            cudaMemcpy(&u, edge_u + badpos, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(&v, edge_v + badpos, 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(&w, edge_weight + badpos, 8, cudaMemcpyDeviceToHost);
+        }
+        lmx_free_graph(ctx);
+        char buf[256];
+        if (u < 0 || v < 0 || u >= n || v >= n)
+            snprintf(buf, sizeof buf, "edge %llu: vertex id out of range for n=%lld: (%lld, %lld)",
+                     (unsigned long long)badpos, (long long)n, (long long)u, (long long)v);
+        else if (u == v)
+            snprintf(buf, sizeof buf, "edge %llu: self-loop (%lld, %lld) in a built graph",
+                     (unsigned long long)badpos, (long long)u, (long long)v);
+        else
+            snprintf(buf, sizeof buf, "edge %llu: weight must be finite and >= 0, got %.17g",
+                     (unsigned long long)badpos, w);
+        return lmx_fail(ctx, LMX_EINVAL, buf);
+    }
+    return lmx_setup_slots(ctx);
+}

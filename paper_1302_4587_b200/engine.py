@@ -1,0 +1,299 @@
+"""ctypes front end of liblmx.so (include/lmx.h) and the drop-in entry points.
+
+``local_max_b200(g, seed, rerandomize=True)`` has the signature and result
+contract of ``locmax.matchers.local_max_seq`` (matchers.py:61-122): same
+``Matching`` (edge set + mate table) and the same ``RoundStats`` trace, bit
+for bit, computed by the sm_100a kernels in ``csrc/``.  There is no CPU
+fallback: if the shared library or a B200 is missing, the call raises.
+
+``run_matcher`` mirrors ``locmax.bench.run_matcher`` (bench.py:119-142) with
+the extra engine ``"b200"``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import time
+
+import numpy as np
+
+from .graph import Graph, Matching, PhaseTrace, RoundStats
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblmx.so")
+_UINT64_MASK = (1 << 64) - 1
+
+LMX_OK, LMX_EINVAL, LMX_ECUDA, LMX_ENOMEM, LMX_ELIMIT, LMX_ESTATE = range(6)
+LMX_HOST, LMX_DEVICE = 0, 1
+
+EXPORTED_SYMBOLS = (
+    "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
+    "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_local_max",
+    "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
+    "lmx_graph_export", "lmx_device_bytes",
+)
+
+
+class LmxRoundStats(ctypes.Structure):
+    _fields_ = [("edges_before", ctypes.c_int64), ("edges_matched", ctypes.c_int64),
+                ("edges_removed", ctypes.c_int64)]
+
+
+class LmxTiming(ctypes.Structure):
+    _fields_ = [("setup_ms", ctypes.c_double), ("rounds_ms", ctypes.c_double),
+                ("output_ms", ctypes.c_double), ("round_launches", ctypes.c_int64),
+                ("slot_reads", ctypes.c_int64)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load liblmx.so; raises RuntimeError (never falls back) if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"liblmx.so not found at {path}; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (or `make -C paper_1302_4587_b200/csrc`)")
+        lib = ctypes.CDLL(path)
+        p, i64, u64, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+        sig = {
+            "lmx_abi_version": (c_int, []),
+            "lmx_create": (c_int, [c_int, ctypes.POINTER(p)]),
+            "lmx_destroy": (None, [p]),
+            "lmx_last_error": (ctypes.c_char_p, [p]),
+            "lmx_set_stream": (c_int, [p, p]),
+            "lmx_load_graph": (c_int, [p, i64, i64, p, p, p, c_int]),
+            "lmx_match": (c_int, [p, u64, c_int, p, p, p, p, c_int, p, c_int]),
+            "lmx_last_timing": (c_int, [p, ctypes.POINTER(LmxTiming)]),
+            "lmx_last_rounds": (c_int, [p, p, c_int]),
+            "lmx_local_max": (c_int, [c_int, i64, i64, p, p, p, u64, c_int, p, p, p, p, c_int, p,
+                                      ctypes.c_char_p, ctypes.c_size_t]),
+            "lmx_build_graph": (c_int, [p, i64, p, p, p, i64, c_int]),
+            "lmx_gen_rmat": (c_int, [p, c_int, c_int, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, u64, c_int]),
+            "lmx_gen_rmat_raw": (c_int, [p, c_int, c_int, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, u64, c_int, p, p, p, c_int]),
+            "lmx_graph_size": (c_int, [p, p, p]),
+            "lmx_graph_export": (c_int, [p, p, p, p, c_int]),
+            "lmx_device_bytes": (i64, [p]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.lmx_abi_version() != 1:
+            raise RuntimeError("liblmx.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def _raise(code: int, msg: str):
+    if code == LMX_EINVAL:
+        raise ValueError(msg)
+    if code == LMX_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array or a torch tensor (CUDA or CPU)."""
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+class Engine:
+    """One liblmx context bound to a CUDA device (a B200)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self._lib.lmx_create(device, ctypes.byref(h))
+        if rc != LMX_OK:
+            _raise(rc, "lmx_create failed: " + self._lib.lmx_last_error(None).decode())
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lmx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc: int, what: str):
+        if rc != LMX_OK:
+            _raise(rc, f"{what}: " + self._lib.lmx_last_error(self._h).decode())
+
+    def set_stream(self, stream_handle: int | None):
+        """Run on a given cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+        self._check(self._lib.lmx_set_stream(self._h, stream_handle or None), "lmx_set_stream")
+
+    # -- graph loading -------------------------------------------------------
+    def load_graph(self, g) -> None:
+        """Load a reference-shaped graph from host numpy arrays (K0 on the device)."""
+        eu = np.ascontiguousarray(g.edge_u, dtype=np.int64)
+        ev = np.ascontiguousarray(g.edge_v, dtype=np.int64)
+        w = np.ascontiguousarray(g.edge_weight, dtype=np.float64)
+        self._check(self._lib.lmx_load_graph(self._h, int(g.num_vertices), int(eu.size),
+                                             eu.ctypes.data, ev.ctypes.data, w.ctypes.data, LMX_HOST),
+                    "lmx_load_graph")
+
+    def load_graph_device(self, n: int, edge_u, edge_v, edge_weight) -> None:
+        """Load from device tensors (int64/int64/float64 CUDA tensors)."""
+        self._check(self._lib.lmx_load_graph(self._h, int(n), int(edge_u.numel()), _ptr(edge_u),
+                                             _ptr(edge_v), _ptr(edge_weight), LMX_DEVICE),
+                    "lmx_load_graph")
+
+    def build_graph(self, u, v, w, num_vertices: int | None = None) -> None:
+        """build_graph (graph.py:59-119) of raw triples on the device."""
+        u = np.ascontiguousarray(u, dtype=np.int64)
+        v = np.ascontiguousarray(v, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        nv = -1 if num_vertices is None else int(num_vertices)
+        self._check(self._lib.lmx_build_graph(self._h, int(u.size), u.ctypes.data, v.ctypes.data,
+                                              w.ctypes.data, nv, LMX_HOST), "lmx_build_graph")
+
+    def gen_rmat(self, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+                 c: float = 0.19, seed: int = 1, permute: bool = True) -> None:
+        self._check(self._lib.lmx_gen_rmat(self._h, scale, edge_factor, a, b, c, seed & _UINT64_MASK,
+                                           int(permute)), "lmx_gen_rmat")
+
+    def gen_rmat_raw(self, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+                     c: float = 0.19, seed: int = 1, permute: bool = True):
+        k = edge_factor << scale
+        u = np.empty(k, dtype=np.int64)
+        v = np.empty(k, dtype=np.int64)
+        w = np.empty(k, dtype=np.float64)
+        self._check(self._lib.lmx_gen_rmat_raw(self._h, scale, edge_factor, a, b, c, seed & _UINT64_MASK,
+                                               int(permute), u.ctypes.data, v.ctypes.data, w.ctypes.data,
+                                               LMX_HOST), "lmx_gen_rmat_raw")
+        return u, v, w
+
+    def graph_size(self) -> tuple[int, int]:
+        n = ctypes.c_int64()
+        m = ctypes.c_int64()
+        self._check(self._lib.lmx_graph_size(self._h, ctypes.byref(n), ctypes.byref(m)), "lmx_graph_size")
+        return int(n.value), int(m.value)
+
+    def export_graph(self) -> Graph:
+        n, m = self.graph_size()
+        eu = np.empty(m, dtype=np.int64)
+        ev = np.empty(m, dtype=np.int64)
+        w = np.empty(m, dtype=np.float64)
+        self._check(self._lib.lmx_graph_export(self._h, eu.ctypes.data, ev.ctypes.data, w.ctypes.data,
+                                               LMX_HOST), "lmx_graph_export")
+        return Graph(n, eu, ev, w)
+
+    def device_bytes(self) -> int:
+        return int(self._lib.lmx_device_bytes(self._h))
+
+    # -- matching ------------------------------------------------------------
+    def match_raw(self, seed: int, rerandomize: bool = True):
+        """Run the round loop; returns (mate int64[n], sorted ids int64, [RoundStats])."""
+        n, _ = self.graph_size()
+        mate = np.empty(max(n, 1), dtype=np.int64)
+        ids = np.empty(max(n // 2 + 1, 1), dtype=np.int64)
+        nm = ctypes.c_int64()
+        nr = ctypes.c_int()
+        self._check(self._lib.lmx_match(self._h, seed & _UINT64_MASK, int(bool(rerandomize)),
+                                        mate.ctypes.data, ids.ctypes.data, ctypes.byref(nm), None, 0,
+                                        ctypes.byref(nr), LMX_HOST), "lmx_match")
+        rounds = self.last_rounds()
+        return mate[:n], ids[: nm.value].copy(), rounds
+
+    def match_device(self, seed: int, mate_out, ids_out, rerandomize: bool = True) -> int:
+        """Device outputs (CUDA tensors int64[n] and int64[>= n/2]); returns #matched edges."""
+        nm = ctypes.c_int64()
+        nr = ctypes.c_int()
+        self._check(self._lib.lmx_match(self._h, seed & _UINT64_MASK, int(bool(rerandomize)),
+                                        _ptr(mate_out), _ptr(ids_out), ctypes.byref(nm), None, 0,
+                                        ctypes.byref(nr), LMX_DEVICE), "lmx_match")
+        return int(nm.value)
+
+    def last_rounds(self) -> list:
+        k = self._lib.lmx_last_rounds(self._h, None, 0)
+        buf = (LmxRoundStats * max(k, 1))()
+        self._lib.lmx_last_rounds(self._h, buf, k)
+        return [RoundStats(int(b.edges_before), int(b.edges_matched), int(b.edges_removed))
+                for b in buf[:k]]
+
+    def last_timing(self) -> dict:
+        t = LmxTiming()
+        self._check(self._lib.lmx_last_timing(self._h, ctypes.byref(t)), "lmx_last_timing")
+        return {"setup_ms": t.setup_ms, "rounds_ms": t.rounds_ms, "output_ms": t.output_ms,
+                "round_launches": int(t.round_launches), "slot_reads": int(t.slot_reads)}
+
+    def match(self, g, seed: int, rerandomize: bool = True) -> tuple[Matching, PhaseTrace]:
+        """local_max_seq contract on a graph already loaded with load_graph(g)."""
+        t0 = time.perf_counter()
+        mate, ids, rounds = self.match_raw(seed, rerandomize)
+        trace = PhaseTrace(rounds=rounds)
+        trace.device_millis = self.last_timing()["rounds_ms"]
+        trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+        return Matching(ids, mate), trace
+
+
+_default_engines: dict[int, Engine] = {}
+
+
+def default_engine(device: int = 0) -> Engine:
+    eng = _default_engines.get(device)
+    if eng is None:
+        eng = Engine(device)
+        _default_engines[device] = eng
+    return eng
+
+
+def local_max_b200(g, seed: int, rerandomize: bool = True, device: int = 0) -> tuple[Matching, PhaseTrace]:
+    """Drop-in for ``locmax.local_max_seq(g, seed, rerandomize)`` (matchers.py:61-122).
+
+    ``wall_millis`` covers the whole call (upload, device loop, readback) like
+    the reference's; ``device_millis`` is the device round loop alone.
+    """
+    t0 = time.perf_counter()
+    eng = default_engine(device)
+    eng.load_graph(g)
+    matching, trace = eng.match(g, seed, rerandomize)
+    trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+    return matching, trace
+
+
+def run_matcher(g, algorithm: str, seed: int, engine: str = "b200", p: int = 4,
+                rerandomize: bool = True):
+    """bench.py:119-142 dispatch with the B200 engines added.
+
+    ``engine="b200"`` runs :func:`local_max_b200`; ``"b200-dist"`` runs the
+    1D-partitioned multi-GPU engine over ``p`` ranks (see ``dist.py``).  Other
+    engines / algorithms are the reference's and are delegated to ``locmax``
+    when it is importable.
+    """
+    if algorithm == "localmax" and engine == "b200":
+        return local_max_b200(g, seed, rerandomize)
+    if algorithm == "localmax" and engine == "b200-dist":
+        from .dist import local_max_dist
+        return local_max_dist(g, p, seed, rerandomize)
+    if engine in ("b200", "b200-dist"):
+        raise ValueError(f"algorithm {algorithm!r} only runs on the seq engine")
+    try:
+        from locmax.bench import run_matcher as ref_run_matcher
+    except ImportError as exc:
+        raise ValueError(f"unknown engine {engine!r} (the reference locmax package is not importable)") from exc
+    return ref_run_matcher(g, algorithm, seed, engine, p, rerandomize)
