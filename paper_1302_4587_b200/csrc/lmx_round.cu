@@ -427,6 +427,8 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
             if (i < total) {
                 v = (i < nH) ? a.H[i] : (a.L ? a.L[i - nH] : (uint32_t)(i - nH));
                 d = a.vdeg[v];
+                // round 0 lists hubs twice (hub list + identity range): skip the second
+                if (!a.L && i >= nH && d >= kHubMin) d = 0;
             }
             uint32_t kd = 3;   // 0 = L_next, 1 = H_next, 2 = matched (emit eid), 3 = none
             uint32_t e = 0;
@@ -561,6 +563,7 @@ static int ensure_ctr(lmx_ctx *ctx, int need) {
         LMX_CUDA(ctx, cudaMemcpyAsync(nc, ctx->ctr, sizeof(RoundCtr) * (size_t)ctx->ctr_cap,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        std::copy(ctx->ctr_host, ctx->ctr_host + ctx->ctr_cap, nh);
         cudaFree(ctx->ctr);
         cudaFreeHost(ctx->ctr_host);
     }
