@@ -67,7 +67,13 @@ typedef struct {
     double output_ms;       /* lmx_match: matched-id sort + output copies */
     int64_t round_launches; /* kernels launched by the round loop */
     int64_t slot_reads;     /* slots read by the round kernels (for roofline) */
+    double round_kernel_ms; /* sum of round-kernel durations (LMX_OPT_KERNEL_TIMING) */
+    double match_kernel_ms; /* sum of match-kernel durations (LMX_OPT_KERNEL_TIMING) */
+    int64_t rounds_executed;/* rounds enqueued, incl. empty speculative ones */
 } lmx_timing;
+
+/* options for lmx_set_option */
+#define LMX_OPT_KERNEL_TIMING 1 /* record a CUDA event after every round/match kernel */
 
 int lmx_abi_version(void);
 
@@ -102,6 +108,7 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
               int max_rounds, int *n_rounds_out, int out_where);
 
 int lmx_last_timing(const lmx_ctx *ctx, lmx_timing *out);
+int lmx_set_option(lmx_ctx *ctx, int option, int64_t value);
 
 /* Copy the RoundStats trace of the last lmx_match (up to cap entries);
  * returns the number of rounds, or -1 on a bad ctx. */

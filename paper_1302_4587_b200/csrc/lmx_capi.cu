@@ -69,6 +69,7 @@ void lmx_destroy(lmx_ctx *ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    for (cudaEvent_t e : ctx->tl_events) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -135,6 +136,15 @@ int lmx_last_rounds(lmx_ctx *ctx, lmx_round_stats *out, int cap) {
     std::vector<lmx_round_stats> &stats = ctx->rounds;
     for (int i = 0; i < (int)stats.size() && i < cap; ++i) out[i] = stats[i];
     return (int)stats.size();
+}
+
+int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
+    if (!ctx) return LMX_EINVAL;
+    if (option == LMX_OPT_KERNEL_TIMING) {
+        ctx->kernel_timing = value != 0;
+        return LMX_OK;
+    }
+    return lmx_fail(ctx, LMX_EINVAL, "unknown option");
 }
 
 int lmx_last_timing(const lmx_ctx *ctx, lmx_timing *out) {

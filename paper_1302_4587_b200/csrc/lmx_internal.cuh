@@ -105,6 +105,8 @@ struct lmx_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     lmx_timing timing{};
     std::vector<lmx_round_stats> rounds;   // trace of the last lmx_match
+    bool kernel_timing = false;
+    std::vector<cudaEvent_t> tl_events;    // per-kernel timeline (kernel_timing)
 };
 
 // helpers shared by the translation units

@@ -591,12 +591,27 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice,
                                   ctx->stream));
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    // optional per-kernel timeline: tl[0] after init, then (after round r, after match r)
+    int tl_used = 0;
+    auto tl_mark = [&](void) -> int {
+        if (!ctx->kernel_timing) return LMX_OK;
+        if (tl_used >= (int)ctx->tl_events.size()) {
+            cudaEvent_t e;
+            LMX_CUDA(ctx, cudaEventCreate(&e));
+            ctx->tl_events.push_back(e);
+        }
+        LMX_CUDA(ctx, cudaEventRecord(ctx->tl_events[tl_used++], ctx->stream));
+        return LMX_OK;
+    };
+    ctx->timing.round_kernel_ms = 0;
+    ctx->timing.match_kernel_ms = 0;
     if (n > 0) {
         lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg,
                                                                      ctx->mate, ctx->matched);
         LMX_CUDA(ctx, cudaGetLastError());
         ctx->timing.round_launches += 1;
     }
+    LMX_TRY(tl_mark());
     int r = 0;
     int n_rounds = -1;
     int batch = 6;
@@ -623,6 +638,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             else if (mode == 1) launch_round<1>(ctx, a);
             else launch_round<2>(ctx, a);
             LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(tl_mark());
             MatchArgs ma;
             ma.vdeg = ctx->vdeg;
             ma.cand = ctx->cand;
@@ -638,6 +654,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ma.ctr_next = ctx->ctr + r + 1;
             lmx_match_kernel<<<ctx->match_blocks, kBlock, 0, ctx->stream>>>(ma);
             LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(tl_mark());
             ctx->timing.round_launches += 2;
         }
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r0, ctx->ctr + r0, sizeof(RoundCtr) * (size_t)batch,
@@ -651,6 +668,15 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         }
         batch = 4;
     }
+    if (ctx->kernel_timing && tl_used > 1) {
+        for (int i = 1; i < tl_used; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->tl_events[i - 1], ctx->tl_events[i]);
+            if (i & 1) ctx->timing.round_kernel_ms += ms;
+            else ctx->timing.match_kernel_ms += ms;
+        }
+    }
+    ctx->timing.rounds_executed = r;
     if (n_rounds < 0) n_rounds = 0;
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     unsigned long long total_matched_v = 0;
@@ -687,6 +713,7 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
             lmx_widen_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
                 ctx->mids_sorted, (long long *)ids_out, n_matched);
             LMX_CUDA(ctx, cudaGetLastError());
+            ctx->timing.round_launches += 1;
         }
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -32,8 +32,9 @@ EXPORTED_SYMBOLS = (
     "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
-    "lmx_graph_export", "lmx_device_bytes",
+    "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
 )
+LMX_OPT_KERNEL_TIMING = 1
 
 
 class LmxRoundStats(ctypes.Structure):
@@ -44,7 +45,8 @@ class LmxRoundStats(ctypes.Structure):
 class LmxTiming(ctypes.Structure):
     _fields_ = [("setup_ms", ctypes.c_double), ("rounds_ms", ctypes.c_double),
                 ("output_ms", ctypes.c_double), ("round_launches", ctypes.c_int64),
-                ("slot_reads", ctypes.c_int64)]
+                ("slot_reads", ctypes.c_int64), ("round_kernel_ms", ctypes.c_double),
+                ("match_kernel_ms", ctypes.c_double), ("rounds_executed", ctypes.c_int64)]
 
 
 _lib = None
@@ -83,6 +85,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_graph_size": (c_int, [p, p, p]),
             "lmx_graph_export": (c_int, [p, p, p, p, c_int]),
             "lmx_device_bytes": (i64, [p]),
+            "lmx_set_option": (c_int, [p, c_int, i64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -239,7 +242,13 @@ class Engine:
         t = LmxTiming()
         self._check(self._lib.lmx_last_timing(self._h, ctypes.byref(t)), "lmx_last_timing")
         return {"setup_ms": t.setup_ms, "rounds_ms": t.rounds_ms, "output_ms": t.output_ms,
-                "round_launches": int(t.round_launches), "slot_reads": int(t.slot_reads)}
+                "round_launches": int(t.round_launches), "slot_reads": int(t.slot_reads),
+                "round_kernel_ms": t.round_kernel_ms, "match_kernel_ms": t.match_kernel_ms,
+                "rounds_executed": int(t.rounds_executed)}
+
+    def set_kernel_timing(self, on: bool = True) -> None:
+        """Record a CUDA event after every round / match kernel (per-kernel durations)."""
+        self._check(self._lib.lmx_set_option(self._h, LMX_OPT_KERNEL_TIMING, int(on)), "lmx_set_option")
 
     def match(self, g, seed: int, rerandomize: bool = True) -> tuple[Matching, PhaseTrace]:
         """local_max_seq contract on a graph already loaded with load_graph(g)."""
