@@ -74,6 +74,9 @@ typedef struct {
 
 /* options for lmx_set_option */
 #define LMX_OPT_KERNEL_TIMING 1 /* record a CUDA event after every round/match kernel */
+#define LMX_OPT_LAYOUT 2        /* weight-key layout of the next load: -1 auto, 0 uniform
+                                   (only valid if all weights are equal), 1 distinct, 2 general */
+#define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
 
 int lmx_abi_version(void);
 

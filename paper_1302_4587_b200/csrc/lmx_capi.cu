@@ -144,6 +144,12 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
         ctx->kernel_timing = value != 0;
         return LMX_OK;
     }
+    if (option == LMX_OPT_LAYOUT) {
+        if (value < -1 || value > 2) return lmx_fail(ctx, LMX_EINVAL, "layout must be -1, 0, 1 or 2");
+        ctx->force_layout = (int)value;
+        return LMX_OK;
+    }
+    if (option == LMX_QUERY_LAYOUT) return ctx->layout;
     return lmx_fail(ctx, LMX_EINVAL, "unknown option");
 }
 

@@ -1,19 +1,29 @@
 // lmx_internal.cuh -- shared definitions of the B200 local max engine.
 //
 // Device data layout:
-//   vbeg   u64[n+1]   CSR segment starts (graph.py:108-115 offsets, rebuilt
-//                     on the device from the edge arrays)
-//   ids0   uint2[2m]  pristine slot records {nbr, eid} sorted by owner
-//   wk0    u32[2m]    dense rank of the canonical weight bits of the slot's
-//                     edge (tiebreak.py:105-113 order, compressed to 32 bits);
-//                     absent when every weight is equal (unit weights)
-//   ids1/wk1          working copy of the slots: round 1 compacts the
-//                     survivors of ids0 into it, rounds >= 2 compact it in
-//                     place, so ids0 is never written and lmx_match can rerun
-//   vdeg   u32[n]     live degree of each vertex (prefix of its segment)
-//   cand   uint2[n]   {nbr, eid} of the vertex's candidate (max key) edge
-//   matched u32[n/32] bitmap of matched vertices
-//   L/H    u32[n] x2  live vertex lists (ping-pong), H = hubs (deg > HUB_T)
+//   vbeg    u64[n+1]   CSR segment starts (graph.py:108-115 offsets, rebuilt on
+//                      the device from the edge arrays)
+//   ids0    uint2[2m]  pristine slot records {nbr, id} grouped by owner, where
+//                      id is the edge id (layouts UNIFORM, GENERAL) or the
+//                      edge's weight key (layout DISTINCT, see below)
+//   wk0     u32[2m]    GENERAL layout only: dense rank of the canonical weight
+//                      bits (tiebreak.py:105-113 order) of the slot's edge
+//   ids1/wk1           working copy: round 1 compacts the survivors of ids0 into
+//                      it, rounds >= 2 compact it in place, so ids0 is never
+//                      written and lmx_match can rerun on the same graph
+//   vdeg    u32[n]     live degree of each vertex (live prefix of its segment)
+//   cand    uint2[n]   {nbr, id} of the vertex's candidate (max key) edge
+//   matched u32[n/32]  bitmap of matched vertices
+//   lists   u32        per round, 5 degree buckets of live vertices (ping-pong)
+//
+// Weight-key layouts (chosen in K0 from the weight multiset):
+//   UNIFORM  every weight equal: the key is the salt alone, id = edge id
+//   DISTINCT at most a few tied weights: id = x is itself the weight key:
+//            x < D (number of distinct weight values) -> unique weight of
+//            dense rank x; x >= D -> tied edge t = x - D with rank
+//            tie_rank[t] and edge id eid_of_x[x].  8-byte slots, no salt
+//            hashing unless two tied edges meet.  eid_of_x[] maps back.
+//   GENERAL  otherwise: id = edge id plus a u32 weight rank per slot (12 B)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,23 +37,31 @@
 namespace lmx {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr int kBlock = 256;            // threads per block, every kernel
+constexpr int kBlock = 256;   // threads per block, every kernel
 constexpr int kWarps = kBlock / 32;
-constexpr uint32_t kThreadMax = 8;     // thread-per-vertex up to this live degree
-constexpr uint32_t kHubMin = 4097;     // block-per-vertex from this live degree
-constexpr int kLanesItems = 8;         // vertices per lane in a warp chunk
-constexpr uint32_t kWarpChunk = 32 * kLanesItems;
-constexpr int kMaxRounds = 4096;
 
-// Per-round device counters; round r's work lists are sized by ctr[r].nL/nH
-// (written by round r-1's match kernel, or by the init kernel for r = 0).
+// live-degree buckets of the per-round vertex lists and their mappings
+constexpr int kBuckets = 5;
+//   0: d <= 4            thread per vertex
+//   1: 5 <= d <= 32      8-lane group per vertex
+//   2: 33 <= d <= 1024   warp per vertex
+//   3: 1025 <= d < 32768 block per vertex
+//   4: d >= 32768        block per vertex, scheduled first
+__host__ __device__ __forceinline__ int bucket_of(uint32_t d) {
+    return d <= 4 ? 0 : d <= 32 ? 1 : d <= 1024 ? 2 : d < 32768 ? 3 : 4;
+}
+
+enum Layout { kUniform = 0, kDistinct = 1, kGeneral = 2 };
+
+// Per-round device counters.  n[b] sizes round r's bucket lists (written by
+// round r-1's match kernel, or set from the round-0 lists).
 struct RoundCtr {
     unsigned long long live_slots;   // sum of post-filter live degrees (= 2 m_r)
     unsigned long long matched_v;    // vertices matched this round (= 2 * matched edges)
     unsigned long long slot_reads;   // slots read by the round kernel
-    unsigned int nL, nH;             // sizes of this round's lists
-    unsigned int cur_hub, cur_L;     // work cursors of the round kernel
-    unsigned int cur_match, pad;
+    unsigned int n[kBuckets];        // list sizes of this round
+    unsigned int cur[kBuckets];      // work cursors of the round kernel
+    unsigned int pad[2];
 };
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t v) {
@@ -75,26 +93,31 @@ struct lmx_ctx {
 
     // graph
     int64_t n = 0, m = 0;
-    bool has_wk = false;
+    int layout = lmx::kUniform;
     uint32_t *eu = nullptr, *ev = nullptr;   // edge endpoints (u32)
     double *w = nullptr;                     // edge weights
     unsigned long long *vbeg = nullptr;      // n+1
     uint2 *ids0 = nullptr, *ids1 = nullptr;
-    uint32_t *wk0 = nullptr, *wk1 = nullptr;
+    uint32_t *wk0 = nullptr, *wk1 = nullptr; // GENERAL layout
     uint32_t *deg0 = nullptr;                // full degree (u32)
-    unsigned int n_hubs0 = 0;
+    // DISTINCT layout tables
+    uint32_t n_distinct = 0;                 // D
+    uint32_t n_tied = 0;
+    uint32_t *eid_of_x = nullptr;            // [D + n_tied] -> edge id
+    uint32_t *tie_rank = nullptr;            // [n_tied]
+    // round-0 bucket lists (built once per graph, ascending vertex id)
+    uint32_t *bins0 = nullptr;               // kBuckets regions of capacity n
+    unsigned int n_bins0[lmx::kBuckets] = {0, 0, 0, 0, 0};
 
     // match state
     uint32_t *vdeg = nullptr;
     uint2 *cand = nullptr;
     uint32_t *matched = nullptr;
-    uint32_t *L[2] = {nullptr, nullptr};
-    uint32_t *H[2] = {nullptr, nullptr};
-    uint32_t *hubs0 = nullptr;
-    uint32_t *mids = nullptr;                // matched edge ids (u32)
+    uint32_t *lists[2] = {nullptr, nullptr}; // ping-pong, kBuckets regions of capacity n
+    uint32_t *mids = nullptr;                // matched ids (u32)
     uint32_t *mids_sorted = nullptr;
     unsigned long long *mcount = nullptr;    // total matched edges
-    lmx::RoundCtr *ctr = nullptr;            // kMaxRounds + 1
+    lmx::RoundCtr *ctr = nullptr;
     lmx::RoundCtr *ctr_host = nullptr;       // pinned mirror
     int ctr_cap = 0;
     long long *mate = nullptr;               // int64[n]
@@ -104,9 +127,10 @@ struct lmx_ctx {
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     lmx_timing timing{};
-    std::vector<lmx_round_stats> rounds;   // trace of the last lmx_match
+    std::vector<lmx_round_stats> rounds;     // trace of the last lmx_match
     bool kernel_timing = false;
-    std::vector<cudaEvent_t> tl_events;    // per-kernel timeline (kernel_timing)
+    std::vector<cudaEvent_t> tl_events;      // per-kernel timeline (kernel_timing)
+    int force_layout = -1;                   // testing: force a weight-key layout
 };
 
 // helpers shared by the translation units
@@ -115,12 +139,11 @@ int lmx_cuda_check(lmx_ctx *ctx, cudaError_t e, const char *what);
 int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what);
 void lmx_free(lmx_ctx *ctx, void **p, size_t bytes);
 void lmx_free_graph(lmx_ctx *ctx);
-int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/wk0 from eu/ev/w
+int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
                    const double *edge_weight, int where);
-#include <vector>
 int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                    std::vector<lmx_round_stats> &stats, unsigned long long &n_matched);
 int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_out,

@@ -2,25 +2,26 @@
 //
 // One round r of local_max_seq (matchers.py:87-119) is two kernels:
 //
-//   lmx_round_kernel<MODE>  (K3 of round r-1 fused with K1 of round r)
+//   lmx_round_kernel<MODE, LAYOUT>  (K3 of round r-1 fused with K1 of round r)
 //     for every vertex v of this round's live lists: stream v's live slots,
 //     drop those whose neighbour was matched in round r-1 (matchers.py:111),
 //     compact the survivors to the front of v's segment (pram.py:248-272's
 //     compaction, done per segment so no global scan is needed), and take the
-//     lexicographic max of (weight rank, mix64(eid ^ rs_r)) over them
+//     lexicographic max of (weight, mix64(eid ^ rs_r)) over them
 //     (matchers.py:93-103; the edge id never decides because mix64 is a
 //     bijection, so distinct edges have distinct salts).
-//       MODE 0 = round 0: no filter, no writes, identity vertex list
-//       MODE 1 = round 1: filter ids0 -> ids1 (pristine copy stays intact)
+//       MODE 0 = round 0: no filter, no writes
+//       MODE 1 = round 1: filter ids0 -> ids1 (the pristine copy stays intact)
 //       MODE 2 = round >= 2: filter ids1 in place
-//     Work mapping: hubs (live degree >= kHubMin) one block each, grabbed
-//     dynamically first; the rest in warp chunks of 256 vertices, each vertex
-//     thread-per-vertex (degree <= kThreadMax) or warp-per-vertex.
+//     Work mapping by live-degree bucket (lmx_internal.cuh): hubs one block
+//     each (largest bucket first), then warp-, 8-lane-group- and
+//     thread-per-vertex, every unit grabbed dynamically so no warp owns more
+//     than a few thousand slots of work.
 //
 //   lmx_match_kernel  (K2 + K4)
 //     v is matched iff cand[cand[v].nbr] is the same edge (matchers.py:105);
-//     sets the matched bitmap and mate, emits the edge id once, and appends
-//     every unmatched vertex with live edges to the next round's lists.
+//     sets the matched bitmap and mate, emits the edge once, and appends every
+//     unmatched vertex with live edges to the next round's bucket lists.
 //
 // The host enqueues rounds in batches without waiting; kernels of rounds past
 // the end find empty lists and exit, so the loop syncs once per batch.
@@ -34,77 +35,114 @@
 namespace lmx {
 
 struct Best {
-    uint32_t wk;
+    uint32_t hi;    // weight key (rank), 0 for UNIFORM
     uint32_t nbr;   // kNone = no candidate
-    uint32_t eid;
+    uint32_t id;
     uint64_t salt;
 };
 
 __device__ __forceinline__ void best_init(Best &b) {
-    b.wk = 0;
+    b.hi = 0;
     b.nbr = kNone;
-    b.eid = kNone;
+    b.id = kNone;
     b.salt = 0;
-}
-
-// Offer one live slot; the salt is only hashed when the weight rank can win.
-__device__ __forceinline__ void best_offer(Best &b, uint32_t k, uint32_t eid, uint32_t nbr,
-                                           uint64_t rs) {
-    if (b.nbr == kNone || k >= b.wk) {
-        uint64_t s = mix64((uint64_t)eid ^ rs);
-        if (b.nbr == kNone || k > b.wk || s > b.salt) {
-            b.wk = k;
-            b.salt = s;
-            b.nbr = nbr;
-            b.eid = eid;
-        }
-    }
 }
 
 __device__ __forceinline__ void best_merge(Best &b, const Best &o) {
     if (o.nbr == kNone) return;
-    if (b.nbr == kNone || o.wk > b.wk || (o.wk == b.wk && o.salt > b.salt)) b = o;
+    if (b.nbr == kNone || o.hi > b.hi || (o.hi == b.hi && o.salt > b.salt)) b = o;
 }
 
 __device__ __forceinline__ Best best_shfl_xor(const Best &b, int off) {
     Best o;
-    o.wk = __shfl_xor_sync(0xffffffffu, b.wk, off);
+    o.hi = __shfl_xor_sync(0xffffffffu, b.hi, off);
     o.nbr = __shfl_xor_sync(0xffffffffu, b.nbr, off);
-    o.eid = __shfl_xor_sync(0xffffffffu, b.eid, off);
+    o.id = __shfl_xor_sync(0xffffffffu, b.id, off);
     o.salt = __shfl_xor_sync(0xffffffffu, (unsigned long long)b.salt, off);
     return o;
 }
 
-__device__ __forceinline__ void best_warp_reduce(Best &b) {
+template <int G>
+__device__ __forceinline__ void best_group_reduce(Best &b) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) best_merge(b, best_shfl_xor(b, off));
+    for (int off = G / 2; off > 0; off >>= 1) best_merge(b, best_shfl_xor(b, off));
 }
 
 struct RoundArgs {
     const unsigned long long *vbeg;
     uint32_t *vdeg;
     uint2 *cand;
-    const uint2 *src_ids;
-    const uint32_t *src_wk;
-    uint2 *dst_ids;
-    uint32_t *dst_wk;
+    const uint2 *ids0;
+    const uint32_t *wk0;
+    uint2 *ids1;
+    uint32_t *wk1;
     const uint32_t *matched;
-    const uint32_t *L;   // unused in MODE 0 (identity over [0, n))
-    const uint32_t *H;
-    RoundCtr *ctr;       // this round's counters
-    uint64_t rs;         // round seed (tiebreak.py:40-52)
-    uint32_t n;
+    const uint32_t *list[kBuckets];
+    RoundCtr *ctr;             // this round's counters
+    uint64_t rs;               // round seed (tiebreak.py:40-52)
+    uint32_t n_distinct;       // DISTINCT layout: D
+    const uint32_t *tie_rank;  // DISTINCT layout
+    const uint32_t *eid_of_x;  // DISTINCT layout
 };
 
-template <int MODE>
-__device__ __forceinline__ uint2 ld_slot(const uint2 *p) {
-    if (MODE < 2) return __ldcs(p);   // pristine records: streamed, evict-first
-    return *p;                        // in-place working copy
+// Offer one live slot {nbr, id} (+ weight rank k for GENERAL) to the running max.
+template <int L>
+__device__ __forceinline__ void offer(Best &b, uint32_t nbr, uint32_t id, uint32_t k, const RoundArgs &a) {
+    if (L == kUniform) {
+        const uint64_t s = mix64((uint64_t)id ^ a.rs);
+        if (b.nbr == kNone || s > b.salt) {
+            b.salt = s;
+            b.nbr = nbr;
+            b.id = id;
+        }
+    } else if (L == kGeneral) {
+        if (b.nbr == kNone || k >= b.hi) {   // hash only when the weight can win
+            const uint64_t s = mix64((uint64_t)id ^ a.rs);
+            if (b.nbr == kNone || k > b.hi || s > b.salt) {
+                b.hi = k;
+                b.salt = s;
+                b.nbr = nbr;
+                b.id = id;
+            }
+        }
+    } else {   // DISTINCT: id is the weight key x
+        if (id < a.n_distinct) {   // unique weight: rank decides alone
+            if (b.nbr == kNone || id > b.hi) {
+                b.hi = id;
+                b.salt = 0;
+                b.nbr = nbr;
+                b.id = id;
+            }
+        } else {                   // tied weight: rank, then salt of the edge id
+            const uint32_t r = __ldg(a.tie_rank + (id - a.n_distinct));
+            if (b.nbr == kNone || r >= b.hi) {
+                const uint64_t s = mix64((uint64_t)__ldg(a.eid_of_x + id) ^ a.rs);
+                if (b.nbr == kNone || r > b.hi || s > b.salt) {
+                    b.hi = r;
+                    b.salt = s;
+                    b.nbr = nbr;
+                    b.id = id;
+                }
+            }
+        }
+    }
 }
-template <int MODE>
-__device__ __forceinline__ uint32_t ld_wk(const uint32_t *p) {
-    if (MODE < 2) return __ldcs(p);
-    return *p;
+
+template <int MODE, int L>
+__device__ __forceinline__ void load_slot(const RoundArgs &a, unsigned long long p, uint2 &x, uint32_t &k) {
+    if (MODE < 2) {
+        x = __ldcs(a.ids0 + p);   // pristine records: streamed once, evict-first
+        k = (L == kGeneral) ? __ldcs(a.wk0 + p) : 0u;
+    } else {
+        x = a.ids1[p];            // working copy, compacted in place
+        k = (L == kGeneral) ? a.wk1[p] : 0u;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void store_slot(const RoundArgs &a, unsigned long long p, uint2 x, uint32_t k) {
+    a.ids1[p] = x;
+    if (L == kGeneral) a.wk1[p] = k;
 }
 
 __device__ __forceinline__ bool is_matched(const uint32_t *bits, uint32_t v) {
@@ -117,251 +155,230 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// ---- thread per vertex -------------------------------------------------
-template <int MODE, bool WK>
-__device__ __forceinline__ uint32_t thread_vertex(const RoundArgs &a, uint32_t v, uint32_t d,
-                                                  Best &b) {
-    const unsigned long long beg = a.vbeg[v];
-    const uint2 *s = a.src_ids + beg;
-    const uint32_t *sk = WK ? a.src_wk + beg : nullptr;
-    uint2 *o = a.dst_ids + beg;
-    uint32_t *ok = WK ? a.dst_wk + beg : nullptr;
+// ---- G lanes per vertex (G in {1, 8, 32}); every lane of the warp calls it.
+// For G < 32 a single pass covers d <= G * ITEMS; for G == 32 (v, d) are
+// warp-uniform and the loop runs ceil(d / (32 * ITEMS)) passes.
+template <int MODE, int L, int G, int ITEMS>
+__device__ __forceinline__ uint32_t group_vertex(const RoundArgs &a, uint32_t v, uint32_t d, int lane,
+                                                 Best &b) {
+    const int gl = lane & (G - 1);
+    const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const uint32_t lt = lanemask_lt() & gmask;
+    const unsigned long long beg = d ? a.vbeg[v] : 0ULL;
+    const uint32_t span = G * ITEMS;
+    const uint32_t npass = (G == 32) ? (d + span - 1) / span : 1u;
     uint32_t w = 0;
-    for (uint32_t i = 0; i < d; i += 4) {
-        uint2 x[4];
-        uint32_t k[4];
-        bool alive[4];
+    for (uint32_t pass = 0; pass < npass; ++pass) {
+        const uint32_t c = pass * span;
+        uint2 x[ITEMS];
+        uint32_t k[ITEMS];
+        bool alive[ITEMS];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (i + j < d) {
-                x[j] = ld_slot<MODE>(s + i + j);
-                k[j] = WK ? ld_wk<MODE>(sk + i + j) : 0u;
-            } else {
-                x[j] = make_uint2(kNone, kNone);
-                k[j] = 0;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            alive[j] = (i + j < d) && (MODE == 0 || !is_matched(a.matched, x[j].x));
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (alive[j]) {
-                if (MODE == 1 || (MODE == 2 && w != i + j)) {
-                    o[w] = x[j];
-                    if (WK) ok[w] = k[j];
-                }
-                ++w;
-                best_offer(b, k[j], x[j].y, x[j].x, a.rs);
-            }
-        }
-    }
-    return w;
-}
-
-// ---- warp per vertex (v, d warp-uniform) ------------------------------
-template <int MODE, bool WK>
-__device__ __forceinline__ uint32_t warp_vertex(const RoundArgs &a, uint32_t v, uint32_t d,
-                                                Best &b, int lane) {
-    const unsigned long long beg = a.vbeg[v];
-    const uint2 *s = a.src_ids + beg;
-    const uint32_t *sk = WK ? a.src_wk + beg : nullptr;
-    uint2 *o = a.dst_ids + beg;
-    uint32_t *ok = WK ? a.dst_wk + beg : nullptr;
-    const uint32_t lt = lanemask_lt();
-    uint32_t w = 0;
-    for (uint32_t c = 0; c < d; c += 128) {
-        uint2 x[4];
-        uint32_t k[4];
-        bool alive[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t i = c + j * 32 + lane;
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t i = c + j * G + gl;
             if (i < d) {
-                x[j] = ld_slot<MODE>(s + i);
-                k[j] = WK ? ld_wk<MODE>(sk + i) : 0u;
+                load_slot<MODE, L>(a, beg + i, x[j], k[j]);
             } else {
                 x[j] = make_uint2(kNone, kNone);
                 k[j] = 0;
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            alive[j] = (c + j * 32 + lane < d) && (MODE == 0 || !is_matched(a.matched, x[j].x));
-        if (MODE == 2) __syncwarp();   // every read of this chunk precedes its writes
+        for (int j = 0; j < ITEMS; ++j)
+            alive[j] = (c + j * G + gl < d) && (MODE == 0 || !is_matched(a.matched, x[j].x));
+        if (MODE == 2) __syncwarp();   // every read of this pass precedes its writes
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < ITEMS; ++j) {
             if (MODE != 0) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, alive[j]);
+                const uint32_t bal = __ballot_sync(0xffffffffu, alive[j]) & gmask;
                 const uint32_t pos = w + __popc(bal & lt);
-                if (alive[j] && (MODE == 1 || pos != c + j * 32 + lane)) {
-                    o[pos] = x[j];
-                    if (WK) ok[pos] = k[j];
-                }
+                if (alive[j] && (MODE == 1 || pos != c + j * G + gl)) store_slot<L>(a, beg + pos, x[j], k[j]);
                 w += __popc(bal);
             }
-            if (alive[j]) best_offer(b, k[j], x[j].y, x[j].x, a.rs);
+            if (alive[j]) offer<L>(b, x[j].x, x[j].y, k[j], a);
         }
     }
-    if (MODE == 0) w = d;
-    return w;
+    best_group_reduce<G>(b);
+    return MODE == 0 ? d : w;
 }
 
-// ---- block per vertex (hubs) --------------------------------------------
-template <int MODE, bool WK>
-__device__ __forceinline__ uint32_t block_vertex(const RoundArgs &a, uint32_t v, uint32_t d,
-                                                 Best &b, uint32_t (*s_cnt)[kWarps]) {
+// ---- one block per vertex (hubs); 8 slots per thread per pass.
+constexpr int kBlockItems = 8;
+
+template <int MODE, int L>
+__device__ __forceinline__ uint32_t block_vertex(const RoundArgs &a, uint32_t v, uint32_t d, Best &b,
+                                                 uint32_t (*s_cnt)[kWarps]) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned long long beg = a.vbeg[v];
-    const uint2 *s = a.src_ids + beg;
-    const uint32_t *sk = WK ? a.src_wk + beg : nullptr;
-    uint2 *o = a.dst_ids + beg;
-    uint32_t *ok = WK ? a.dst_wk + beg : nullptr;
     const uint32_t lt = lanemask_lt();
     uint32_t w = 0;
-    for (uint32_t c = 0; c < d; c += 4 * kBlock) {
-        uint2 x[4];
-        uint32_t k[4];
-        bool alive[4];
+    for (uint32_t c = 0; c < d; c += kBlockItems * kBlock) {
+        uint2 x[kBlockItems];
+        uint32_t k[kBlockItems];
+        bool alive[kBlockItems];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kBlockItems; ++j) {
             const uint32_t i = c + j * kBlock + tid;
             if (i < d) {
-                x[j] = ld_slot<MODE>(s + i);
-                k[j] = WK ? ld_wk<MODE>(sk + i) : 0u;
+                load_slot<MODE, L>(a, beg + i, x[j], k[j]);
             } else {
                 x[j] = make_uint2(kNone, kNone);
                 k[j] = 0;
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kBlockItems; ++j)
             alive[j] = (c + j * kBlock + tid < d) && (MODE == 0 || !is_matched(a.matched, x[j].x));
         if (MODE != 0) {
-            uint32_t bal[4];
+            uint32_t bal[kBlockItems];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kBlockItems; ++j) {
                 bal[j] = __ballot_sync(0xffffffffu, alive[j]);
                 if (lane == 0) s_cnt[j][warp] = __popc(bal[j]);
             }
             __syncthreads();   // counts visible; also orders all reads before writes
-            uint32_t total = 0, before[4];
+            uint32_t base = w;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t acc = 0;
+            for (int j = 0; j < kBlockItems; ++j) {
+                uint32_t before = 0, cj = 0;
 #pragma unroll
                 for (int q = 0; q < kWarps; ++q) {
                     const uint32_t cq = s_cnt[j][q];
-                    acc += (q < warp) ? cq : 0u;
-                    total += cq;
+                    before += (q < warp) ? cq : 0u;
+                    cj += cq;
                 }
-                before[j] = acc;   // within (j), warps before me
+                const uint32_t pos = base + before + __popc(bal[j] & lt);
+                if (alive[j] && (MODE == 1 || pos != c + j * kBlock + tid)) store_slot<L>(a, beg + pos, x[j], k[j]);
+                base += cj;
             }
-            // prefix over j: survivors of earlier j blocks come first
-            uint32_t jbase = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t cj = 0;
-#pragma unroll
-                for (int q = 0; q < kWarps; ++q) cj += s_cnt[j][q];
-                const uint32_t pos = w + jbase + before[j] + __popc(bal[j] & lt);
-                if (alive[j] && (MODE == 1 || pos != c + j * kBlock + tid)) {
-                    o[pos] = x[j];
-                    if (WK) ok[pos] = k[j];
-                }
-                jbase += cj;
-            }
-            w += total;
+            w = base;
             __syncthreads();   // s_cnt reuse
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (alive[j]) best_offer(b, k[j], x[j].y, x[j].x, a.rs);
+        for (int j = 0; j < kBlockItems; ++j)
+            if (alive[j]) offer<L>(b, x[j].x, x[j].y, k[j], a);
     }
-    if (MODE == 0) w = d;
-    return w;
+    return MODE == 0 ? d : w;
 }
 
-template <int MODE, bool WK>
+__device__ __forceinline__ void put_result(const RoundArgs &a, int mode, uint32_t v, uint32_t w, const Best &b) {
+    if (mode != 0) a.vdeg[v] = w;
+    a.cand[v] = (w > 0) ? make_uint2(b.nbr, b.id) : make_uint2(kNone, kNone);
+}
+
+template <int MODE, int L>
 __global__ void __launch_bounds__(kBlock) lmx_round_kernel(RoundArgs a) {
-    __shared__ uint32_t s_cnt[4][kWarps];
+    __shared__ uint32_t s_cnt[kBlockItems][kWarps];
     __shared__ Best s_best[kWarps];
     __shared__ uint32_t s_item;
     __shared__ unsigned long long s_red[2][kWarps];
 
-    const uint32_t nH = a.ctr->nH;
-    const uint32_t nL = a.ctr->nL;
-    if (nH == 0 && nL == 0) return;
+    uint32_t nb[kBuckets];
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < kBuckets; ++q) {
+        nb[q] = a.ctr->n[q];
+        any |= nb[q];
+    }
+    if (any == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long live = 0, reads = 0;
 
-    // phase 1: hubs, one block each, grabbed dynamically
-    for (;;) {
-        if (tid == 0) s_item = atomicAdd(&a.ctr->cur_hub, 1u);
-        __syncthreads();
-        const uint32_t i = s_item;
-        __syncthreads();
-        if (i >= nH) break;
-        const uint32_t v = a.H[i];
-        const uint32_t d = a.vdeg[v];
-        Best b;
-        best_init(b);
-        const uint32_t w = block_vertex<MODE, WK>(a, v, d, b, s_cnt);
-        best_warp_reduce(b);
-        if (lane == 0) s_best[warp] = b;
-        __syncthreads();
-        if (tid == 0) {
-            Best t = s_best[0];
-            for (int q = 1; q < kWarps; ++q) best_merge(t, s_best[q]);
-            if (MODE != 0) a.vdeg[v] = w;
-            a.cand[v] = (w > 0) ? make_uint2(t.nbr, t.eid) : make_uint2(kNone, kNone);
-            live += w;
-            reads += d;
-        }
-        __syncthreads();
-    }
-
-    // phase 2: warp chunks of the vertex list
-    for (;;) {
-        uint32_t chunk = 0;
-        if (lane == 0) chunk = atomicAdd(&a.ctr->cur_L, 1u);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        const unsigned long long base = (unsigned long long)chunk * kWarpChunk;
-        if (base >= nL) break;
+    // phase 1: buckets 4 then 3, one block per vertex
 #pragma unroll 1
-        for (int jj = 0; jj < kLanesItems; ++jj) {
-            const unsigned long long idx = base + (unsigned long long)jj * 32 + lane;
-            uint32_t v = kNone, d = 0;
-            if (idx < nL) {
-                v = (MODE == 0) ? (uint32_t)idx : a.L[idx];
-                d = a.vdeg[v];
-                if (MODE == 0 && d >= kHubMin) d = 0;   // done in phase 1
-            }
-            if (d > 0 && d <= kThreadMax) {
-                Best b;
-                best_init(b);
-                const uint32_t w = thread_vertex<MODE, WK>(a, v, d, b);
-                if (MODE != 0) a.vdeg[v] = w;
-                a.cand[v] = (w > 0) ? make_uint2(b.nbr, b.eid) : make_uint2(kNone, kNone);
+    for (int q = kBuckets - 1; q >= 3; --q) {
+        for (;;) {
+            if (tid == 0) s_item = atomicAdd(&a.ctr->cur[q], 1u);
+            __syncthreads();
+            const uint32_t i = s_item;
+            __syncthreads();
+            if (i >= nb[q]) break;
+            const uint32_t v = a.list[q][i];
+            const uint32_t d = a.vdeg[v];
+            Best b;
+            best_init(b);
+            const uint32_t w = block_vertex<MODE, L>(a, v, d, b, s_cnt);
+            best_group_reduce<32>(b);
+            if (lane == 0) s_best[warp] = b;
+            __syncthreads();
+            if (tid == 0) {
+                Best t = s_best[0];
+                for (int z = 1; z < kWarps; ++z) best_merge(t, s_best[z]);
+                put_result(a, MODE, v, w, t);
                 live += w;
                 reads += d;
             }
-            uint32_t big = __ballot_sync(0xffffffffu, d > kThreadMax);
-            while (big) {
-                const int src = __ffs(big) - 1;
-                big &= big - 1;
-                const uint32_t vv = __shfl_sync(0xffffffffu, v, src);
-                const uint32_t dd = __shfl_sync(0xffffffffu, d, src);
-                Best b;
-                best_init(b);
-                const uint32_t w = warp_vertex<MODE, WK>(a, vv, dd, b, lane);
-                best_warp_reduce(b);
-                if (lane == src) {
-                    if (MODE != 0) a.vdeg[vv] = w;
-                    a.cand[vv] = (w > 0) ? make_uint2(b.nbr, b.eid) : make_uint2(kNone, kNone);
-                    live += w;
-                    reads += dd;
-                }
+            __syncthreads();
+        }
+    }
+
+    // phase 2: bucket 2, warp per vertex, 4 vertices per grab
+    for (;;) {
+        uint32_t i0 = 0;
+        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[2], 4u);
+        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        if (i0 >= nb[2]) break;
+        const uint32_t iend = min(i0 + 4u, nb[2]);
+        for (uint32_t i = i0; i < iend; ++i) {
+            const uint32_t v = a.list[2][i];
+            const uint32_t d = a.vdeg[v];
+            Best b;
+            best_init(b);
+            const uint32_t w = group_vertex<MODE, L, 32, 4>(a, v, d, lane, b);
+            if (lane == 0) {
+                put_result(a, MODE, v, w, b);
+                live += w;
+                reads += d;
+            }
+        }
+    }
+
+    // phase 3: bucket 1, 8 lanes per vertex, 16 vertices per grab
+    for (;;) {
+        uint32_t i0 = 0;
+        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[1], 16u);
+        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        if (i0 >= nb[1]) break;
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t i = i0 + it * 4 + (lane >> 3);
+            uint32_t v = kNone, d = 0;
+            if (i < nb[1]) {
+                v = a.list[1][i];
+                d = a.vdeg[v];
+            }
+            Best b;
+            best_init(b);
+            const uint32_t w = group_vertex<MODE, L, 8, 4>(a, v, d, lane, b);
+            if ((lane & 7) == 0 && d) {
+                put_result(a, MODE, v, w, b);
+                live += w;
+                reads += d;
+            }
+        }
+    }
+
+    // phase 4: bucket 0, thread per vertex, 128 vertices per grab
+    for (;;) {
+        uint32_t i0 = 0;
+        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[0], 128u);
+        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        if (i0 >= nb[0]) break;
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t i = i0 + it * 32 + lane;
+            uint32_t v = kNone, d = 0;
+            if (i < nb[0]) {
+                v = a.list[0][i];
+                d = a.vdeg[v];
+            }
+            Best b;
+            best_init(b);
+            const uint32_t w = group_vertex<MODE, L, 1, 4>(a, v, d, lane, b);
+            if (d) {
+                put_result(a, MODE, v, w, b);
+                live += w;
+                reads += d;
             }
         }
     }
@@ -393,44 +410,50 @@ struct MatchArgs {
     const uint2 *cand;
     uint32_t *matched;
     long long *mate;
-    const uint32_t *L;      // null = identity (round 0)
-    const uint32_t *H;
-    uint32_t *L_next;
-    uint32_t *H_next;
+    const uint32_t *list[kBuckets];
+    uint32_t *next[kBuckets];
     uint32_t *mids;
     unsigned long long *mcount;
-    RoundCtr *ctr;          // this round
-    RoundCtr *ctr_next;     // next round (list sizes)
+    RoundCtr *ctr;        // this round
+    RoundCtr *ctr_next;   // next round (list sizes)
 };
 
 constexpr int kMatchItems = 4;
+constexpr int kTargets = kBuckets + 1;   // next-round buckets + matched-id output
 
 __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
-    __shared__ uint32_t s_cnt[3][kWarps];
-    __shared__ unsigned long long s_base[3];
-    const uint32_t nH = a.ctr->nH, nL = a.ctr->nL;
-    const unsigned long long total = (unsigned long long)nH + nL;
+    __shared__ uint32_t s_cnt[kTargets][kWarps];
+    __shared__ uint32_t s_base[kTargets];
+    uint32_t nb[kBuckets], pre[kBuckets + 1];
+    pre[0] = 0;
+#pragma unroll
+    for (int q = 0; q < kBuckets; ++q) {
+        nb[q] = a.ctr->n[q];
+        pre[q + 1] = pre[q] + nb[q];
+    }
+    const uint32_t total = pre[kBuckets];
     if (total == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
     unsigned long long matched_v = 0;
-    const unsigned long long tile = (unsigned long long)kBlock * kMatchItems;
-    for (unsigned long long t0 = (unsigned long long)blockIdx.x * tile; t0 < total;
-         t0 += (unsigned long long)gridDim.x * tile) {
+    const uint32_t tile = kBlock * kMatchItems;
+    for (uint32_t t0 = blockIdx.x * tile; t0 < total; t0 += gridDim.x * tile) {
         uint32_t vv[kMatchItems], kind[kMatchItems], eid[kMatchItems];
-        uint32_t bal[kMatchItems][3];
-        uint32_t wc[3] = {0, 0, 0};
+        uint32_t wc[kTargets];
+#pragma unroll
+        for (int q = 0; q < kTargets; ++q) wc[q] = 0;
 #pragma unroll
         for (int j = 0; j < kMatchItems; ++j) {
-            const unsigned long long i = t0 + (unsigned long long)j * kBlock + tid;
+            const uint32_t i = t0 + j * kBlock + tid;
             uint32_t v = kNone, d = 0;
             if (i < total) {
-                v = (i < nH) ? a.H[i] : (a.L ? a.L[i - nH] : (uint32_t)(i - nH));
+                int q = 0;
+#pragma unroll
+                for (int z = 1; z < kBuckets; ++z) q += (i >= pre[z]) ? 1 : 0;
+                v = a.list[q][i - pre[q]];
                 d = a.vdeg[v];
-                // round 0 lists hubs twice (hub list + identity range): skip the second
-                if (!a.L && i >= nH && d >= kHubMin) d = 0;
             }
-            uint32_t kd = 3;   // 0 = L_next, 1 = H_next, 2 = matched (emit eid), 3 = none
+            uint32_t kd = kTargets;   // none
             uint32_t e = 0;
             if (d > 0) {
                 const uint2 c = a.cand[v];
@@ -440,57 +463,53 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                     a.mate[v] = (long long)c.x;
                     ++matched_v;
                     if (v < c.x) {
-                        kd = 2;
+                        kd = kBuckets;
                         e = c.y;
                     }
                 } else {
-                    kd = (d >= kHubMin) ? 1u : 0u;
+                    kd = (uint32_t)bucket_of(d);
                 }
             }
             vv[j] = v;
             kind[j] = kd;
             eid[j] = e;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                bal[j][q] = __ballot_sync(0xffffffffu, kd == (uint32_t)q);
-                wc[q] += __popc(bal[j][q]);
-            }
+            for (int q = 0; q < kTargets; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, kd == (uint32_t)q));
         }
         if (lane == 0) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) s_cnt[q][warp] = wc[q];
+            for (int q = 0; q < kTargets; ++q) s_cnt[q][warp] = wc[q];
         }
         __syncthreads();
-        if (tid < 3) {
+        if (tid < kTargets) {
             uint32_t sum = 0;
             for (int w = 0; w < kWarps; ++w) sum += s_cnt[tid][w];
-            unsigned long long base = 0;
+            uint32_t base = 0;
             if (sum) {
-                if (tid == 0) base = atomicAdd(&a.ctr_next->nL, sum);
-                else if (tid == 1) base = atomicAdd(&a.ctr_next->nH, sum);
-                else base = atomicAdd(a.mcount, (unsigned long long)sum);
+                if (tid < kBuckets) base = atomicAdd(&a.ctr_next->n[tid], sum);
+                else base = (uint32_t)atomicAdd(a.mcount, (unsigned long long)sum);
             }
             s_base[tid] = base;
         }
         __syncthreads();
-        unsigned long long pos[3];
+        uint32_t pos[kTargets];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            unsigned long long p = s_base[q];
+        for (int q = 0; q < kTargets; ++q) {
+            uint32_t p = s_base[q];
             for (int w = 0; w < warp; ++w) p += s_cnt[q][w];
             pos[q] = p;
         }
 #pragma unroll
         for (int j = 0; j < kMatchItems; ++j) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
+            for (int q = 0; q < kTargets; ++q) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, kind[j] == (uint32_t)q);
                 if (kind[j] == (uint32_t)q) {
-                    const unsigned long long p = pos[q] + __popc(bal[j][q] & lt);
-                    if (q == 0) a.L_next[p] = vv[j];
-                    else if (q == 1) a.H_next[p] = vv[j];
+                    const uint32_t p = pos[q] + __popc(bal & lt);
+                    if (q < kBuckets) a.next[q][p] = vv[j];
                     else a.mids[p] = eid[j];
                 }
-                pos[q] += __popc(bal[j][q]);
+                pos[q] += __popc(bal);
             }
         }
         __syncthreads();   // s_cnt / s_base reuse
@@ -511,6 +530,13 @@ __global__ void lmx_init_kernel(uint32_t n, const uint32_t *deg0, uint32_t *vdeg
     }
 }
 
+// DISTINCT layout: matched weight keys -> edge ids (before the sort).
+__global__ void lmx_ids_to_eids(uint32_t *ids, unsigned long long k, const uint32_t *eid_of_x) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride)
+        ids[i] = eid_of_x[ids[i]];
+}
+
 __global__ void lmx_widen_kernel(const uint32_t *src, long long *dst, unsigned long long k) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
@@ -522,12 +548,16 @@ __global__ void lmx_widen_kernel(const uint32_t *src, long long *dst, unsigned l
 
 using namespace lmx;
 
+template <int MODE, int L>
+static void launch_round_l(lmx_ctx *ctx, const RoundArgs &a) {
+    lmx_round_kernel<MODE, L><<<ctx->round_blocks, kBlock, 0, ctx->stream>>>(a);
+}
+
 template <int MODE>
 static void launch_round(lmx_ctx *ctx, const RoundArgs &a) {
-    if (ctx->has_wk)
-        lmx_round_kernel<MODE, true><<<ctx->round_blocks, kBlock, 0, ctx->stream>>>(a);
-    else
-        lmx_round_kernel<MODE, false><<<ctx->round_blocks, kBlock, 0, ctx->stream>>>(a);
+    if (ctx->layout == kUniform) launch_round_l<MODE, kUniform>(ctx, a);
+    else if (ctx->layout == kDistinct) launch_round_l<MODE, kDistinct>(ctx, a);
+    else launch_round_l<MODE, kGeneral>(ctx, a);
 }
 
 int lmx_alloc_match_state(lmx_ctx *ctx) {
@@ -536,16 +566,13 @@ int lmx_alloc_match_state(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, n * 8, "cand"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
-    for (int i = 0; i < 2; ++i) {
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->L[i], n * 4, "L"));
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->H[i], n * 4, "H"));
-    }
+    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], n * 4 * kBuckets, "lists"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 4, "mids"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids_sorted, (n / 2 + 1) * 4, "mids_sorted"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mcount, 8, "mcount"));
     size_t tmp = 0;
     LMX_CUDA(ctx, cub::DeviceRadixSort::SortKeys(nullptr, tmp, ctx->mids, ctx->mids_sorted,
-                                                 (int)(n / 2 + 1)));
+                                                 (long long)(n / 2 + 1)));
     ctx->sort_tmp_bytes = tmp + 256;
     LMX_TRY(lmx_alloc(ctx, &ctx->sort_tmp, ctx->sort_tmp_bytes, "sort_tmp"));
     return LMX_OK;
@@ -578,22 +605,24 @@ static int ensure_ctr(lmx_ctx *ctx, int need) {
 int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                    std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
     const uint32_t n = (uint32_t)ctx->n;
+    const size_t cap = (size_t)std::max<int64_t>(ctx->n, 1);
     stats.clear();
     n_matched = 0;
     ctx->timing.round_launches = 0;
     ctx->timing.slot_reads = 0;
+    ctx->timing.round_kernel_ms = 0;
+    ctx->timing.match_kernel_ms = 0;
     LMX_TRY(ensure_ctr(ctx, 64));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, ctx->stream));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->mcount, 0, 8, ctx->stream));
     ctx->ctr_host[0] = RoundCtr{};
-    ctx->ctr_host[0].nL = n;
-    ctx->ctr_host[0].nH = ctx->n_hubs0;
+    for (int q = 0; q < kBuckets; ++q) ctx->ctr_host[0].n[q] = ctx->n_bins0[q];
     LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice,
                                   ctx->stream));
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     // optional per-kernel timeline: tl[0] after init, then (after round r, after match r)
     int tl_used = 0;
-    auto tl_mark = [&](void) -> int {
+    auto tl_mark = [&]() -> int {
         if (!ctx->kernel_timing) return LMX_OK;
         if (tl_used >= (int)ctx->tl_events.size()) {
             cudaEvent_t e;
@@ -603,11 +632,9 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_CUDA(ctx, cudaEventRecord(ctx->tl_events[tl_used++], ctx->stream));
         return LMX_OK;
     };
-    ctx->timing.round_kernel_ms = 0;
-    ctx->timing.match_kernel_ms = 0;
     if (n > 0) {
-        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg,
-                                                                     ctx->mate, ctx->matched);
+        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg, ctx->mate,
+                                                                     ctx->matched);
         LMX_CUDA(ctx, cudaGetLastError());
         ctx->timing.round_launches += 1;
     }
@@ -620,20 +647,23 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         const int r0 = r;
         for (int b = 0; b < batch; ++b, ++r) {
             const int mode = r == 0 ? 0 : (r == 1 ? 1 : 2);
+            const uint32_t *cur = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+            uint32_t *nxt = ctx->lists[(r + 1) & 1];
             RoundArgs a;
             a.vbeg = ctx->vbeg;
             a.vdeg = ctx->vdeg;
             a.cand = ctx->cand;
-            a.src_ids = mode < 2 ? ctx->ids0 : ctx->ids1;
-            a.src_wk = mode < 2 ? ctx->wk0 : ctx->wk1;
-            a.dst_ids = ctx->ids1;
-            a.dst_wk = ctx->wk1;
+            a.ids0 = ctx->ids0;
+            a.wk0 = ctx->wk0;
+            a.ids1 = ctx->ids1;
+            a.wk1 = ctx->wk1;
             a.matched = ctx->matched;
-            a.L = ctx->L[r & 1];
-            a.H = r == 0 ? ctx->hubs0 : ctx->H[r & 1];
+            for (int q = 0; q < kBuckets; ++q) a.list[q] = cur + (size_t)q * cap;
             a.ctr = ctx->ctr + r;
             a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
-            a.n = n;
+            a.n_distinct = ctx->n_distinct;
+            a.tie_rank = ctx->tie_rank;
+            a.eid_of_x = ctx->eid_of_x;
             if (mode == 0) launch_round<0>(ctx, a);
             else if (mode == 1) launch_round<1>(ctx, a);
             else launch_round<2>(ctx, a);
@@ -644,10 +674,10 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ma.cand = ctx->cand;
             ma.matched = ctx->matched;
             ma.mate = ctx->mate;
-            ma.L = r == 0 ? nullptr : ctx->L[r & 1];
-            ma.H = a.H;
-            ma.L_next = ctx->L[(r + 1) & 1];
-            ma.H_next = ctx->H[(r + 1) & 1];
+            for (int q = 0; q < kBuckets; ++q) {
+                ma.list[q] = cur + (size_t)q * cap;
+                ma.next[q] = nxt + (size_t)q * cap;
+            }
             ma.mids = ctx->mids;
             ma.mcount = ctx->mcount;
             ma.ctr = ctx->ctr + r;
@@ -702,9 +732,14 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
                      int64_t *ids_out, int out_where) {
     const size_t n = (size_t)ctx->n;
     if (n_matched > 0) {
+        if (ctx->layout == kDistinct) {
+            lmx_ids_to_eids<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(ctx->mids, n_matched, ctx->eid_of_x);
+            LMX_CUDA(ctx, cudaGetLastError());
+            ctx->timing.round_launches += 1;
+        }
         size_t tmp = ctx->sort_tmp_bytes;
         LMX_CUDA(ctx, cub::DeviceRadixSort::SortKeys(ctx->sort_tmp, tmp, ctx->mids, ctx->mids_sorted,
-                                                     (int)n_matched, 0, 32, ctx->stream));
+                                                     (long long)n_matched, 0, 32, ctx->stream));
     }
     if (out_where == LMX_DEVICE) {
         if (mate_out && n)
@@ -739,9 +774,14 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
 
 // Persistent grid sizes: every resident block slot of the device.
 int lmx_configure_grids(lmx_ctx *ctx) {
-    int occ = 0;
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<2, true>, kBlock, 0));
-    ctx->round_blocks = ctx->num_sms * std::max(occ, 1);
+    int occ = 0, worst = 64;
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<2, kGeneral>, kBlock, 0));
+    worst = std::min(worst, occ);
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<1, kGeneral>, kBlock, 0));
+    worst = std::min(worst, occ);
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<2, kDistinct>, kBlock, 0));
+    worst = std::min(worst, occ);
+    ctx->round_blocks = ctx->num_sms * std::max(worst, 1);
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_match_kernel, kBlock, 0));
     ctx->match_blocks = ctx->num_sms * std::max(occ, 1);
     return LMX_OK;

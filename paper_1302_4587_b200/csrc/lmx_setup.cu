@@ -56,22 +56,23 @@ void lmx_free(lmx_ctx *ctx, void **p, size_t bytes) {
 }
 
 void lmx_free_graph(lmx_ctx *ctx) {
-    void **ptrs[] = {(void **)&ctx->eu,     (void **)&ctx->ev,     (void **)&ctx->w,
-                     (void **)&ctx->vbeg,   (void **)&ctx->ids0,   (void **)&ctx->ids1,
-                     (void **)&ctx->wk0,    (void **)&ctx->wk1,    (void **)&ctx->deg0,
-                     (void **)&ctx->vdeg,   (void **)&ctx->cand,   (void **)&ctx->matched,
-                     (void **)&ctx->L[0],   (void **)&ctx->L[1],   (void **)&ctx->H[0],
-                     (void **)&ctx->H[1],   (void **)&ctx->hubs0,  (void **)&ctx->mids,
-                     (void **)&ctx->mids_sorted, (void **)&ctx->mcount, (void **)&ctx->mate,
-                     (void **)&ctx->sort_tmp};
+    void **ptrs[] = {(void **)&ctx->eu,       (void **)&ctx->ev,          (void **)&ctx->w,
+                     (void **)&ctx->vbeg,     (void **)&ctx->ids0,        (void **)&ctx->ids1,
+                     (void **)&ctx->wk0,      (void **)&ctx->wk1,         (void **)&ctx->deg0,
+                     (void **)&ctx->vdeg,     (void **)&ctx->cand,        (void **)&ctx->matched,
+                     (void **)&ctx->lists[0], (void **)&ctx->lists[1],    (void **)&ctx->bins0,
+                     (void **)&ctx->mids,     (void **)&ctx->mids_sorted, (void **)&ctx->mcount,
+                     (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
+                     (void **)&ctx->tie_rank};
     for (void **p : ptrs) {
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
     ctx->dev_bytes = 0;
     ctx->n = ctx->m = 0;
-    ctx->has_wk = false;
-    ctx->n_hubs0 = 0;
+    ctx->layout = kUniform;
+    ctx->n_distinct = ctx->n_tied = 0;
+    for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = 0;
     ctx->sort_tmp_bytes = 0;
 }
 
@@ -166,25 +167,51 @@ __global__ void k_heads(const unsigned long long *sorted, unsigned long long m, 
         flag[i] = (i > 0 && sorted[i] != sorted[i - 1]) ? 1u : 0u;
 }
 
-__global__ void k_rank_scatter(const uint32_t *rank, const uint32_t *vals, unsigned long long m,
-                               uint32_t *wk_edge) {
+// tied[i]: the sorted weight at i occurs more than once
+__global__ void k_tied(const unsigned long long *sorted, unsigned long long m, uint32_t *tied) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += stride)
-        wk_edge[vals[i]] = rank[i];
+        tied[i] = ((i > 0 && sorted[i] == sorted[i - 1]) || (i + 1 < m && sorted[i] == sorted[i + 1])) ? 1u : 0u;
 }
 
-__global__ void k_slot_wk(const uint2 *ids, unsigned long long slots, const uint32_t *wk_edge,
-                          uint32_t *wk) {
+// GENERAL: rank per edge.  DISTINCT: weight key x per edge plus the maps back.
+__global__ void k_keys_out(const uint32_t *rank, const uint32_t *tie_idx, const uint32_t *tied,
+                           const uint32_t *eid, unsigned long long m, int distinct, uint32_t D,
+                           uint32_t *key_of_eid, uint32_t *eid_of_x, uint32_t *tie_rank) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += stride) {
+        const uint32_t e = eid[i];
+        if (!distinct) {
+            key_of_eid[e] = rank[i];
+            continue;
+        }
+        uint32_t x;
+        if (tied[i]) {
+            x = D + tie_idx[i];
+            tie_rank[tie_idx[i]] = rank[i];
+        } else {
+            x = rank[i];
+        }
+        key_of_eid[e] = x;
+        eid_of_x[x] = e;
+    }
+}
+
+__global__ void k_slot_key(uint2 *ids, unsigned long long slots, const uint32_t *key_of_eid, uint32_t *wk) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
-         i += stride)
-        wk[i] = wk_edge[ids[i].y];
+         i += stride) {
+        if (wk) wk[i] = key_of_eid[ids[i].y];
+        else ids[i].y = key_of_eid[ids[i].y];
+    }
 }
 
-struct IsHub {
+struct InBucket {
     const uint32_t *deg;
-    __device__ bool operator()(uint32_t v) const { return deg[v] >= kHubMin; }
+    int q;
+    __device__ bool operator()(uint32_t v) const { return deg[v] > 0 && bucket_of(deg[v]) == q; }
 };
 
 }  // namespace lmx
@@ -232,8 +259,8 @@ int lmx_setup_slots(lmx_ctx *ctx) {
                                                       ctx->ids0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
-    // weight key
-    ctx->has_wk = false;
+    // weight key layout
+    bool uniform = true;
     if (m) {
         unsigned long long *mm = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&mm, 16, "minmax"));
@@ -245,13 +272,12 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         LMX_CUDA(ctx, cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
         lmx_free(ctx, (void **)&mm, 16);
-        ctx->has_wk = got[0] != got[1];
+        uniform = got[0] == got[1];
     }
-    if (ctx->has_wk) {
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0"));
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1"));
+    ctx->layout = kUniform;
+    if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
         unsigned long long *keys = nullptr, *keys2 = nullptr;
-        uint32_t *vals = nullptr, *vals2 = nullptr;
+        uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
         void *tmp = nullptr;
         size_t tmp_bytes = 0;
         int rc = LMX_OK;
@@ -260,57 +286,93 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&tidx, m * 4, "tie idx")) != LMX_OK) break;
             k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
             size_t t1 = 0, t2 = 0;
             cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, vals, vals2,
                                                             (long long)m, 0, 64, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "SortPairs size"); break; }
-            e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "scan size"); break; }
+            if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort sizing"); break; }
             tmp_bytes = std::max(t1, t2);
             if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
             e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "SortPairs"); break; }
-            // keys2 sorted, vals2 = eids; heads -> vals (reuse), inclusive sum -> dense rank
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort"); break; }
+            // dense rank of the weight value (vals reused)
             k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
             e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank scan"); break; }
-            // wk_edge lives in keys (reuse as u32 array of m)
-            uint32_t *wk_edge = (uint32_t *)keys;
-            k_rank_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, vals2, m, wk_edge);
-            k_slot_wk<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, wk_edge, ctx->wk0);
+            // tied flags and tie indices
+            k_tied<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, tied);
+            e = cub::DeviceScan::ExclusiveSum(tmp, t2, tied, tidx, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "tie scan"); break; }
+            uint32_t last_rank = 0, last_tidx = 0, last_tied = 0;
+            e = cudaMemcpyAsync(&last_rank, vals + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tidx, tidx + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tied, tied + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank readback"); break; }
+            const unsigned long long D = (unsigned long long)last_rank + 1;
+            const unsigned long long T = (unsigned long long)last_tidx + last_tied;
+            bool distinct = (T <= m / 16) && (D + T < 0xFFFFFFFFULL);
+            if (ctx->force_layout == kDistinct) distinct = D + T < 0xFFFFFFFFULL;
+            if (ctx->force_layout == kGeneral) distinct = false;
+            ctx->layout = distinct ? kDistinct : kGeneral;
+            ctx->n_distinct = (uint32_t)D;
+            ctx->n_tied = (uint32_t)T;
+            uint32_t *key_of_eid = (uint32_t *)keys;   // reuse (m u32 fits in m u64)
+            if (distinct) {
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->eid_of_x, (D + T) * 4, "eid_of_x")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4,
+                                    "tie_rank")) != LMX_OK)
+                    break;
+            } else {
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1")) != LMX_OK) break;
+            }
+            k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
+                                                           (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
+            k_slot_key<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, key_of_eid,
+                                                               distinct ? nullptr : ctx->wk0);
             e = cudaGetLastError();
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank kernels"); break; }
-            e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank sync"); break; }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
         } while (0);
         cudaStreamSynchronize(st);
         lmx_free(ctx, (void **)&keys, m * 8);
         lmx_free(ctx, (void **)&keys2, m * 8);
         lmx_free(ctx, (void **)&vals, m * 4);
         lmx_free(ctx, (void **)&vals2, m * 4);
+        lmx_free(ctx, (void **)&tied, m * 4);
+        lmx_free(ctx, (void **)&tidx, m * 4);
         lmx_free(ctx, &tmp, tmp_bytes);
         if (rc != LMX_OK) return rc;
     }
-    // hub list for round 0 (deterministic order: ascending vertex id)
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hubs0, std::max<size_t>(n, 1) * 4, "hubs0"));
+    // round-0 bucket lists (stable: ascending vertex id inside each bucket)
+    const size_t cap = std::max<size_t>(n, 1);
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * kBuckets, "bins0"));
     {
         unsigned long long *cnt = nullptr;
-        LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8, "hub count"));
+        LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8 * kBuckets, "bucket counts"));
         cub::CountingInputIterator<uint32_t> it(0);
-        IsHub pred{ctx->deg0};
         size_t tmp = 0;
-        LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->hubs0, cnt, (long long)n, pred, st));
+        LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->bins0, cnt, (long long)n,
+                                            InBucket{ctx->deg0, 0}, st));
         void *t = nullptr;
         LMX_TRY(lmx_alloc(ctx, &t, tmp, "select tmp"));
-        cudaError_t e = cub::DeviceSelect::If(t, tmp, it, ctx->hubs0, cnt, (long long)n, pred, st);
-        unsigned long long h = 0;
-        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaSuccess;
+        for (int q = 0; q < kBuckets && e == cudaSuccess; ++q) {
+            size_t tb = tmp;
+            e = cub::DeviceSelect::If(t, tb, it, ctx->bins0 + (size_t)q * cap, cnt + q, (long long)n,
+                                      InBucket{ctx->deg0, q}, st);
+        }
+        unsigned long long h[kBuckets] = {0, 0, 0, 0, 0};
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, 8 * kBuckets, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         lmx_free(ctx, &t, tmp);
-        lmx_free(ctx, (void **)&cnt, 8);
+        lmx_free(ctx, (void **)&cnt, 8 * kBuckets);
         LMX_CUDA(ctx, e);
-        ctx->n_hubs0 = (unsigned int)h;
+        for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = (unsigned int)h[q];
     }
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     return LMX_OK;

@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
 )
 LMX_OPT_KERNEL_TIMING = 1
+LMX_OPT_LAYOUT = 2
+LMX_QUERY_LAYOUT = 100
 
 
 class LmxRoundStats(ctypes.Structure):
@@ -245,6 +247,16 @@ class Engine:
                 "round_launches": int(t.round_launches), "slot_reads": int(t.slot_reads),
                 "round_kernel_ms": t.round_kernel_ms, "match_kernel_ms": t.match_kernel_ms,
                 "rounds_executed": int(t.rounds_executed)}
+
+    LAYOUTS = {"auto": -1, "uniform": 0, "distinct": 1, "general": 2}
+
+    def set_layout(self, layout: str = "auto") -> None:
+        """Force the weight-key layout used by the next graph load (testing / tuning)."""
+        self._check(self._lib.lmx_set_option(self._h, LMX_OPT_LAYOUT, self.LAYOUTS[layout]), "lmx_set_option")
+
+    def layout(self) -> str:
+        code = self._lib.lmx_set_option(self._h, LMX_QUERY_LAYOUT, 0)
+        return {v: k for k, v in self.LAYOUTS.items()}[code]
 
     def set_kernel_timing(self, on: bool = True) -> None:
         """Record a CUDA event after every round / match kernel (per-kernel durations)."""

@@ -19,9 +19,21 @@ def _graph(n, eu, ev, w):
     return Graph(n, eu, ev, w)
 
 
-def test_small_golden_runs_bit_exact(engine, golden_small):
+LAYOUTS = ["auto", "distinct", "general"]
+
+
+@pytest.fixture(params=LAYOUTS)
+def layout_engine(engine, request):
+    """The engine with a forced weight-key layout (auto / distinct / general)."""
+    engine.set_layout(request.param)
+    yield engine
+    engine.set_layout("auto")
+
+
+def test_small_golden_runs_bit_exact(layout_engine, golden_small):
     """~1600 reference runs on 409 small graphs: ties, -0.0, zero weights,
-    edgeless graphs, both rerandomize settings."""
+    edgeless graphs, both rerandomize settings -- under every weight layout."""
+    engine = layout_engine
     graphs = {gi: (n, built) for gi, n, _, built, _ in small_cases(golden_small)}
     loaded = None
     count = 0
@@ -74,7 +86,8 @@ def test_drop_in_entry_point_c1():
     assert chk.valid and chk.maximal
 
 
-def test_random_graphs_vs_oracle(engine):
+def test_random_graphs_vs_oracle(layout_engine):
+    engine = layout_engine
     rng = np.random.default_rng(7)
     for trial in range(60):
         n = int(rng.integers(2, 3000))
@@ -94,13 +107,15 @@ def test_random_graphs_vs_oracle(engine):
             assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == res.rounds
 
 
-def test_hubs_and_skew_vs_oracle(engine):
-    """Stars and skewed degrees exercise the warp- and block-per-vertex paths
-    (live degree > 8 and > 4096) including multi-chunk hub compaction."""
+def test_hubs_and_skew_vs_oracle(layout_engine):
+    """Stars and skewed degrees exercise every bucket mapping (thread, 8-lane
+    group, warp, block; degrees around each threshold) including multi-pass
+    in-place hub compaction."""
+    engine = layout_engine
     rng = np.random.default_rng(11)
     parts_u, parts_v = [], []
     n = 60000
-    for hub, deg in ((0, 50000), (1, 20000), (2, 9000), (3, 4097), (4, 4096), (5, 300), (6, 33)):
+    for hub, deg in ((0, 50000), (1, 32768), (2, 32767), (3, 1025), (4, 1024), (5, 300), (6, 33)):
         nb = rng.choice(np.arange(7, n), size=deg, replace=False)
         parts_u.append(np.full(deg, hub))
         parts_v.append(nb)
@@ -190,6 +205,16 @@ def test_device_build_graph_errors():
         build_graph([(0, 1, 1.0), (0, 5, 1.0)], num_vertices=3)
     with pytest.raises(ValueError, match="weight"):
         build_graph([(0, 1, float("nan"))])
+
+
+def test_layout_selection(engine):
+    n, eu, ev, w = O.gen_random(1 << 10, 4, 1)
+    engine.load_graph(_graph(n, eu, ev, w))
+    assert engine.layout() == "distinct"
+    engine.load_graph(_graph(n, eu, ev, np.ones_like(w)))
+    assert engine.layout() == "uniform"
+    engine.load_graph(_graph(n, eu, ev, np.floor(w * 3)))
+    assert engine.layout() == "general"
 
 
 def test_rmat_generator_matches_oracle(engine):
