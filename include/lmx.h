@@ -76,7 +76,10 @@ typedef struct {
 #define LMX_OPT_KERNEL_TIMING 1 /* record a CUDA event after every round/match kernel */
 #define LMX_OPT_LAYOUT 2        /* weight-key layout of the next load: -1 auto, 0 uniform
                                    (only valid if all weights are equal), 1 distinct, 2 general */
+#define LMX_OPT_RELABEL 3       /* degree-descending vertex relabelling of the next load:
+                                   -1 auto (skewed degree distributions), 0 off, 1 on */
 #define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
+#define LMX_QUERY_RELABELED 101 /* lmx_set_option returns 1 if the loaded graph is relabelled */
 
 int lmx_abi_version(void);
 

@@ -149,7 +149,13 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
         ctx->force_layout = (int)value;
         return LMX_OK;
     }
+    if (option == LMX_OPT_RELABEL) {
+        if (value < -1 || value > 1) return lmx_fail(ctx, LMX_EINVAL, "relabel must be -1, 0 or 1");
+        ctx->force_relabel = (int)value;
+        return LMX_OK;
+    }
     if (option == LMX_QUERY_LAYOUT) return ctx->layout;
+    if (option == LMX_QUERY_RELABELED) return ctx->relabeled ? 1 : 0;
     return lmx_fail(ctx, LMX_EINVAL, "unknown option");
 }
 

@@ -87,7 +87,7 @@ struct lmx_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int num_sms = 148;
-    int round_blocks = 0;   // persistent grid of the round kernel
+    int round_grid[3][3] = {};   // persistent grid of each round-kernel instance [MODE][LAYOUT]
     int match_blocks = 0;
     std::string err;
 
@@ -131,6 +131,9 @@ struct lmx_ctx {
     bool kernel_timing = false;
     std::vector<cudaEvent_t> tl_events;      // per-kernel timeline (kernel_timing)
     int force_layout = -1;                   // testing: force a weight-key layout
+    int force_relabel = -1;                  // -1 auto (skewed graphs), 0 off, 1 on
+    bool relabeled = false;                  // device vertex ids are degree-sorted
+    uint32_t *oldid = nullptr;               // device id -> caller's vertex id
 };
 
 // helpers shared by the translation units

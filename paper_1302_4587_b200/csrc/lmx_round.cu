@@ -267,7 +267,7 @@ __device__ __forceinline__ void put_result(const RoundArgs &a, int mode, uint32_
 }
 
 template <int MODE, int L>
-__global__ void __launch_bounds__(kBlock) lmx_round_kernel(RoundArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
     __shared__ uint32_t s_cnt[kBlockItems][kWarps];
     __shared__ Best s_best[kWarps];
     __shared__ uint32_t s_item;
@@ -410,6 +410,7 @@ struct MatchArgs {
     const uint2 *cand;
     uint32_t *matched;
     long long *mate;
+    const uint32_t *oldid;   // device id -> caller id (null: identity)
     const uint32_t *list[kBuckets];
     uint32_t *next[kBuckets];
     uint32_t *mids;
@@ -460,7 +461,8 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                 const uint2 cx = a.cand[c.x];
                 if (cx.x == v && cx.y == c.y) {
                     atomicOr(a.matched + (v >> 5), 1u << (v & 31));
-                    a.mate[v] = (long long)c.x;
+                    if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[c.x];
+                    else a.mate[v] = (long long)c.x;
                     ++matched_v;
                     if (v < c.x) {
                         kd = kBuckets;
@@ -550,7 +552,7 @@ using namespace lmx;
 
 template <int MODE, int L>
 static void launch_round_l(lmx_ctx *ctx, const RoundArgs &a) {
-    lmx_round_kernel<MODE, L><<<ctx->round_blocks, kBlock, 0, ctx->stream>>>(a);
+    lmx_round_kernel<MODE, L><<<ctx->round_grid[MODE][L], kBlock, 0, ctx->stream>>>(a);
 }
 
 template <int MODE>
@@ -674,6 +676,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ma.cand = ctx->cand;
             ma.matched = ctx->matched;
             ma.mate = ctx->mate;
+            ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
             for (int q = 0; q < kBuckets; ++q) {
                 ma.list[q] = cur + (size_t)q * cap;
                 ma.next[q] = nxt + (size_t)q * cap;
@@ -772,16 +775,26 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
     return LMX_OK;
 }
 
-// Persistent grid sizes: every resident block slot of the device.
+// Persistent grid sizes: every resident block slot of the device, per instance.
+template <int MODE, int L>
+static int occ_of(lmx_ctx *ctx) {
+    int occ = 0;
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<MODE, L>, kBlock, 0));
+    ctx->round_grid[MODE][L] = ctx->num_sms * std::max(occ, 1);
+    return LMX_OK;
+}
+
 int lmx_configure_grids(lmx_ctx *ctx) {
-    int occ = 0, worst = 64;
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<2, kGeneral>, kBlock, 0));
-    worst = std::min(worst, occ);
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<1, kGeneral>, kBlock, 0));
-    worst = std::min(worst, occ);
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_round_kernel<2, kDistinct>, kBlock, 0));
-    worst = std::min(worst, occ);
-    ctx->round_blocks = ctx->num_sms * std::max(worst, 1);
+    LMX_TRY((occ_of<0, kUniform>(ctx)));
+    LMX_TRY((occ_of<0, kDistinct>(ctx)));
+    LMX_TRY((occ_of<0, kGeneral>(ctx)));
+    LMX_TRY((occ_of<1, kUniform>(ctx)));
+    LMX_TRY((occ_of<1, kDistinct>(ctx)));
+    LMX_TRY((occ_of<1, kGeneral>(ctx)));
+    LMX_TRY((occ_of<2, kUniform>(ctx)));
+    LMX_TRY((occ_of<2, kDistinct>(ctx)));
+    LMX_TRY((occ_of<2, kGeneral>(ctx)));
+    int occ = 0;
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lmx_match_kernel, kBlock, 0));
     ctx->match_blocks = ctx->num_sms * std::max(occ, 1);
     return LMX_OK;

@@ -63,7 +63,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->lists[0], (void **)&ctx->lists[1],    (void **)&ctx->bins0,
                      (void **)&ctx->mids,     (void **)&ctx->mids_sorted, (void **)&ctx->mcount,
                      (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
-                     (void **)&ctx->tie_rank};
+                     (void **)&ctx->tie_rank, (void **)&ctx->oldid};
     for (void **p : ptrs) {
         if (*p) cudaFree(*p);
         *p = nullptr;
@@ -72,6 +72,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->n = ctx->m = 0;
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
+    ctx->relabeled = false;
     for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = 0;
     ctx->sort_tmp_bytes = 0;
 }
@@ -118,15 +119,38 @@ __global__ void k_widen_deg(const uint32_t *deg, unsigned long long *out, unsign
 }
 
 __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long long m,
-                          const unsigned long long *vbeg, uint32_t *fill, uint2 *ids) {
+                          const unsigned long long *vbeg, const uint32_t *newid, uint32_t *fill, uint2 *ids) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += stride) {
-        const uint32_t a = eu[e], b = ev[e];
+        uint32_t a = eu[e], b = ev[e];
+        if (newid) {
+            a = newid[a];
+            b = newid[b];
+        }
         const unsigned long long pa = vbeg[a] + atomicAdd(fill + a, 1u);
         const unsigned long long pb = vbeg[b] + atomicAdd(fill + b, 1u);
         ids[pa] = make_uint2(b, (uint32_t)e);
         ids[pb] = make_uint2(a, (uint32_t)e);
+    }
+}
+
+// relabelling helpers: sort key = ~degree (stable -> descending degree, ascending id)
+__global__ void k_relabel_keys(const uint32_t *deg, unsigned long long n, uint32_t *key, uint32_t *val) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        key[i] = ~deg[i];
+        val[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_relabel_apply(const uint32_t *oldid, const uint32_t *deg_old, unsigned long long n,
+                                uint32_t *newid, uint32_t *deg_new) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t o = oldid[i];
+        newid[o] = (uint32_t)i;
+        deg_new[i] = deg_old[o];
     }
 }
 
@@ -239,6 +263,68 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
+    // degree-descending relabelling of skewed graphs: hubs get
+    // the low ids, so the matched bitmap and candidate lookups that follow
+    // the skew hit a small, cache-resident id range, and equal-bucket
+    // vertices become contiguous in memory.
+    uint32_t *newid = nullptr;
+    ctx->relabeled = false;
+    if (n > 1 && m) {
+        bool relabel = ctx->force_relabel == 1;
+        if (ctx->force_relabel == -1) {
+            uint32_t *mx = nullptr;
+            size_t tmp = 0;
+            LMX_TRY(lmx_alloc(ctx, (void **)&mx, 4, "max degree"));
+            LMX_CUDA(ctx, cub::DeviceReduce::Max(nullptr, tmp, ctx->deg0, mx, (long long)n, st));
+            void *t = nullptr;
+            LMX_TRY(lmx_alloc(ctx, &t, tmp, "reduce tmp"));
+            uint32_t maxdeg = 0;
+            cudaError_t e = cub::DeviceReduce::Max(t, tmp, ctx->deg0, mx, (long long)n, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&maxdeg, mx, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            lmx_free(ctx, &t, tmp);
+            lmx_free(ctx, (void **)&mx, 4);
+            LMX_CUDA(ctx, e);
+            const double avg = 2.0 * (double)m / (double)n;
+            relabel = (double)maxdeg > 64.0 * std::max(avg, 1.0);
+        }
+        if (relabel) {
+            uint32_t *key = nullptr, *key2 = nullptr, *val = nullptr, *dnew = nullptr;
+            void *t = nullptr;
+            size_t tmp = 0;
+            int rc = LMX_OK;
+            do {
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->oldid, n * 4, "oldid")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&newid, n * 4, "newid")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&key, n * 4, "relabel key")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&key2, n * 4, "relabel key2")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&val, n * 4, "relabel val")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&dnew, n * 4, "deg new")) != LMX_OK) break;
+                k_relabel_keys<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->deg0, n, key, val);
+                cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key2, val, ctx->oldid,
+                                                                (long long)n, 0, 32, st);
+                if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel sort size"); break; }
+                if ((rc = lmx_alloc(ctx, &t, tmp, "relabel tmp")) != LMX_OK) break;
+                e = cub::DeviceRadixSort::SortPairs(t, tmp, key, key2, val, ctx->oldid, (long long)n, 0, 32, st);
+                if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel sort"); break; }
+                k_relabel_apply<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->oldid, ctx->deg0, n, newid, dnew);
+                e = cudaMemcpyAsync(ctx->deg0, dnew, n * 4, cudaMemcpyDeviceToDevice, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel"); break; }
+            } while (0);
+            cudaStreamSynchronize(st);
+            lmx_free(ctx, (void **)&key, n * 4);
+            lmx_free(ctx, (void **)&key2, n * 4);
+            lmx_free(ctx, (void **)&val, n * 4);
+            lmx_free(ctx, (void **)&dnew, n * 4);
+            lmx_free(ctx, &t, tmp);
+            if (rc != LMX_OK) {
+                lmx_free(ctx, (void **)&newid, n * 4);
+                return rc;
+            }
+            ctx->relabeled = true;
+        }
+    }
     k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(ctx->deg0, ctx->vbeg, n);
     LMX_CUDA(ctx, cudaGetLastError());
     {
@@ -255,9 +341,13 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     if (m) {
         // fill counters reuse vdeg
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, n * 4, st));
-        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, ctx->vdeg,
+        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, ctx->vdeg,
                                                       ctx->ids0);
         LMX_CUDA(ctx, cudaGetLastError());
+    }
+    if (newid) {
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        lmx_free(ctx, (void **)&newid, n * 4);
     }
     // weight key layout
     bool uniform = true;

@@ -36,7 +36,9 @@ EXPORTED_SYMBOLS = (
 )
 LMX_OPT_KERNEL_TIMING = 1
 LMX_OPT_LAYOUT = 2
+LMX_OPT_RELABEL = 3
 LMX_QUERY_LAYOUT = 100
+LMX_QUERY_RELABELED = 101
 
 
 class LmxRoundStats(ctypes.Structure):
@@ -253,6 +255,14 @@ class Engine:
     def set_layout(self, layout: str = "auto") -> None:
         """Force the weight-key layout used by the next graph load (testing / tuning)."""
         self._check(self._lib.lmx_set_option(self._h, LMX_OPT_LAYOUT, self.LAYOUTS[layout]), "lmx_set_option")
+
+    def set_relabel(self, mode: str = "auto") -> None:
+        """Degree-descending vertex relabelling of the next load: auto / on / off."""
+        val = {"auto": -1, "off": 0, "on": 1}[mode]
+        self._check(self._lib.lmx_set_option(self._h, LMX_OPT_RELABEL, val), "lmx_set_option")
+
+    def relabeled(self) -> bool:
+        return bool(self._lib.lmx_set_option(self._h, LMX_QUERY_RELABELED, 0))
 
     def layout(self) -> str:
         code = self._lib.lmx_set_option(self._h, LMX_QUERY_LAYOUT, 0)

@@ -19,15 +19,17 @@ def _graph(n, eu, ev, w):
     return Graph(n, eu, ev, w)
 
 
-LAYOUTS = ["auto", "distinct", "general"]
+VARIANTS = [("auto", "auto"), ("distinct", "on"), ("general", "off"), ("general", "on")]
 
 
-@pytest.fixture(params=LAYOUTS)
+@pytest.fixture(params=VARIANTS, ids=lambda p: f"{p[0]}-relabel_{p[1]}")
 def layout_engine(engine, request):
-    """The engine with a forced weight-key layout (auto / distinct / general)."""
-    engine.set_layout(request.param)
+    """The engine with a forced weight-key layout and vertex relabelling mode."""
+    engine.set_layout(request.param[0])
+    engine.set_relabel(request.param[1])
     yield engine
     engine.set_layout("auto")
+    engine.set_relabel("auto")
 
 
 def test_small_golden_runs_bit_exact(layout_engine, golden_small):
@@ -215,6 +217,9 @@ def test_layout_selection(engine):
     assert engine.layout() == "uniform"
     engine.load_graph(_graph(n, eu, ev, np.floor(w * 3)))
     assert engine.layout() == "general"
+    assert not engine.relabeled()          # ER degrees are not skewed
+    engine.gen_rmat(14, 16, seed=3)
+    assert engine.relabeled()              # RMAT is
 
 
 def test_rmat_generator_matches_oracle(engine):
