@@ -202,44 +202,63 @@ __device__ __forceinline__ uint32_t group_vertex(const RoundArgs &a, uint32_t v,
     return MODE == 0 ? d : w;
 }
 
-// ---- one block per vertex (hubs); 8 slots per thread per pass.
-constexpr int kBlockItems = 8;
+// ---- vectorised team paths (a warp or a whole block per vertex) ------------
+// The segment [beg, beg + d) is split into an unaligned head slot, 16-byte
+// aligned slot pairs loaded as uint4, and a tail slot.  Survivors are
+// compacted in item order (any order inside a segment is valid: the key order
+// is total); every read of a pass precedes its writes, and writes only land
+// below the slots already read, so in-place compaction is race-free.
+constexpr int kPairs = 4;                 // uint4 pairs per thread per pass
+constexpr int kBlockItems = 2 * kPairs;   // slot items per thread per pass
 
 template <int MODE, int L>
-__device__ __forceinline__ uint32_t block_vertex(const RoundArgs &a, uint32_t v, uint32_t d, Best &b,
-                                                 uint32_t (*s_cnt)[kWarps]) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned long long beg = a.vbeg[v];
-    const uint32_t lt = lanemask_lt();
-    uint32_t w = 0;
-    for (uint32_t c = 0; c < d; c += kBlockItems * kBlock) {
-        uint2 x[kBlockItems];
-        uint32_t k[kBlockItems];
-        bool alive[kBlockItems];
+__device__ __forceinline__ void load_pair(const RoundArgs &a, unsigned long long p, uint2 &x0, uint2 &x1,
+                                          uint32_t &k0, uint32_t &k1) {
+    uint4 q;
+    if (MODE < 2) q = __ldcs(reinterpret_cast<const uint4 *>(a.ids0 + p));
+    else q = *reinterpret_cast<const uint4 *>(a.ids1 + p);
+    x0 = make_uint2(q.x, q.y);
+    x1 = make_uint2(q.z, q.w);
+    if (L == kGeneral) {
+        uint2 kk;
+        if (MODE < 2) kk = __ldcs(reinterpret_cast<const uint2 *>(a.wk0 + p));
+        else kk = *reinterpret_cast<const uint2 *>(a.wk1 + p);
+        k0 = kk.x;
+        k1 = kk.y;
+    } else {
+        k0 = k1 = 0;
+    }
+}
+
+// Compact + offer NI items per thread of a TEAM (32 = warp, kBlock = block).
+// rd[j] is the segment index item j was read from; w is team-uniform.
+template <int MODE, int L, int TEAM, int NI>
+__device__ __forceinline__ void team_commit(const RoundArgs &a, unsigned long long beg, const uint2 *x,
+                                            const uint32_t *k, const bool *alive, const uint32_t *rd,
+                                            uint32_t &w, Best &b, uint32_t (*s_cnt)[kWarps]) {
+    if (MODE != 0) {
+        const uint32_t lt = lanemask_lt();
+        if (TEAM == 32) {
+            if (MODE == 2) __syncwarp();
 #pragma unroll
-        for (int j = 0; j < kBlockItems; ++j) {
-            const uint32_t i = c + j * kBlock + tid;
-            if (i < d) {
-                load_slot<MODE, L>(a, beg + i, x[j], k[j]);
-            } else {
-                x[j] = make_uint2(kNone, kNone);
-                k[j] = 0;
+            for (int j = 0; j < NI; ++j) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, alive[j]);
+                const uint32_t pos = w + __popc(bal & lt);
+                if (alive[j] && (MODE == 1 || pos != rd[j])) store_slot<L>(a, beg + pos, x[j], k[j]);
+                w += __popc(bal);
             }
-        }
+        } else {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            uint32_t bal[NI];
 #pragma unroll
-        for (int j = 0; j < kBlockItems; ++j)
-            alive[j] = (c + j * kBlock + tid < d) && (MODE == 0 || !is_matched(a.matched, x[j].x));
-        if (MODE != 0) {
-            uint32_t bal[kBlockItems];
-#pragma unroll
-            for (int j = 0; j < kBlockItems; ++j) {
+            for (int j = 0; j < NI; ++j) {
                 bal[j] = __ballot_sync(0xffffffffu, alive[j]);
                 if (lane == 0) s_cnt[j][warp] = __popc(bal[j]);
             }
             __syncthreads();   // counts visible; also orders all reads before writes
             uint32_t base = w;
 #pragma unroll
-            for (int j = 0; j < kBlockItems; ++j) {
+            for (int j = 0; j < NI; ++j) {
                 uint32_t before = 0, cj = 0;
 #pragma unroll
                 for (int q = 0; q < kWarps; ++q) {
@@ -248,16 +267,68 @@ __device__ __forceinline__ uint32_t block_vertex(const RoundArgs &a, uint32_t v,
                     cj += cq;
                 }
                 const uint32_t pos = base + before + __popc(bal[j] & lt);
-                if (alive[j] && (MODE == 1 || pos != c + j * kBlock + tid)) store_slot<L>(a, beg + pos, x[j], k[j]);
+                if (alive[j] && (MODE == 1 || pos != rd[j])) store_slot<L>(a, beg + pos, x[j], k[j]);
                 base += cj;
             }
             w = base;
             __syncthreads();   // s_cnt reuse
         }
-#pragma unroll
-        for (int j = 0; j < kBlockItems; ++j)
-            if (alive[j]) offer<L>(b, x[j].x, x[j].y, k[j], a);
     }
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+        if (alive[j]) offer<L>(b, x[j].x, x[j].y, k[j], a);
+}
+
+// One scalar slot (segment index i) handled by thread 0 of the team.
+template <int MODE, int L, int TEAM>
+__device__ __forceinline__ void team_single(const RoundArgs &a, unsigned long long beg, uint32_t i, uint32_t &w,
+                                            Best &b, uint32_t (*s_cnt)[kWarps]) {
+    uint2 x = make_uint2(kNone, kNone);
+    uint32_t k = 0;
+    bool alive = false;
+    if (threadIdx.x % TEAM == 0) {
+        load_slot<MODE, L>(a, beg + i, x, k);
+        alive = MODE == 0 || !is_matched(a.matched, x.x);
+    }
+    team_commit<MODE, L, TEAM, 1>(a, beg, &x, &k, &alive, &i, w, b, s_cnt);
+}
+
+template <int MODE, int L, int TEAM>
+__device__ __forceinline__ uint32_t team_vertex(const RoundArgs &a, uint32_t v, uint32_t d, Best &b,
+                                                uint32_t (*s_cnt)[kWarps]) {
+    const uint32_t t = threadIdx.x % TEAM;
+    const unsigned long long beg = a.vbeg[v];
+    uint32_t w = 0;
+    const uint32_t head = (uint32_t)(beg & 1ULL);
+    if (head) team_single<MODE, L, TEAM>(a, beg, 0, w, b, s_cnt);
+    const uint32_t rem = d - head;
+    const uint32_t npairs = rem >> 1;
+    for (uint32_t c = 0; c < npairs; c += kPairs * TEAM) {
+        uint2 x[kBlockItems];
+        uint32_t k[kBlockItems], rd[kBlockItems];
+        bool alive[kBlockItems];
+#pragma unroll
+        for (int j = 0; j < kPairs; ++j) {
+            const uint32_t p = c + j * TEAM + t;
+            rd[2 * j] = head + 2 * p;
+            rd[2 * j + 1] = head + 2 * p + 1;
+            if (p < npairs) {
+                load_pair<MODE, L>(a, beg + head + 2ULL * p, x[2 * j], x[2 * j + 1], k[2 * j], k[2 * j + 1]);
+            } else {
+                x[2 * j] = x[2 * j + 1] = make_uint2(kNone, kNone);
+                k[2 * j] = k[2 * j + 1] = 0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPairs; ++j) {
+            const bool in = c + j * TEAM + t < npairs;
+            alive[2 * j] = in && (MODE == 0 || !is_matched(a.matched, x[2 * j].x));
+            alive[2 * j + 1] = in && (MODE == 0 || !is_matched(a.matched, x[2 * j + 1].x));
+        }
+        team_commit<MODE, L, TEAM, kBlockItems>(a, beg, x, k, alive, rd, w, b, s_cnt);
+    }
+    if (rem & 1u) team_single<MODE, L, TEAM>(a, beg, d - 1, w, b, s_cnt);
+    best_group_reduce<32>(b);
     return MODE == 0 ? d : w;
 }
 
@@ -285,7 +356,7 @@ __global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
     unsigned long long live = 0, reads = 0;
 
     // phase 1: buckets 4 then 3, one block per vertex
-#pragma unroll 1
+#pragma unroll
     for (int q = kBuckets - 1; q >= 3; --q) {
         for (;;) {
             if (tid == 0) s_item = atomicAdd(&a.ctr->cur[q], 1u);
@@ -297,8 +368,7 @@ __global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
             const uint32_t d = a.vdeg[v];
             Best b;
             best_init(b);
-            const uint32_t w = block_vertex<MODE, L>(a, v, d, b, s_cnt);
-            best_group_reduce<32>(b);
+            const uint32_t w = team_vertex<MODE, L, kBlock>(a, v, d, b, s_cnt);
             if (lane == 0) s_best[warp] = b;
             __syncthreads();
             if (tid == 0) {
@@ -324,7 +394,7 @@ __global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
             const uint32_t d = a.vdeg[v];
             Best b;
             best_init(b);
-            const uint32_t w = group_vertex<MODE, L, 32, 4>(a, v, d, lane, b);
+            const uint32_t w = team_vertex<MODE, L, 32>(a, v, d, b, s_cnt);
             if (lane == 0) {
                 put_result(a, MODE, v, w, b);
                 live += w;
