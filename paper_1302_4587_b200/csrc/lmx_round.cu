@@ -32,6 +32,12 @@
 
 #include "lmx_internal.cuh"
 
+// Tuning (measured on RMAT-26, profiles/): full occupancy beats per-thread
+// memory-level parallelism for this latency-chained workload.
+#ifndef LMX_MINB
+#define LMX_MINB 8
+#endif
+
 namespace lmx {
 
 struct Best {
@@ -71,7 +77,9 @@ __device__ __forceinline__ void best_group_reduce(Best &b) {
 struct RoundArgs {
     const unsigned long long *vbeg;
     uint32_t *vdeg;
-    uint2 *cand;
+    uint32_t *cand_nbr;   // candidate edge of v: neighbour ...
+    uint32_t *cand_id;    // ... and edge id / weight key (split: the match kernel's
+                          // random read of the partner touches only cand_id)
     const uint2 *ids0;
     const uint32_t *wk0;
     uint2 *ids1;
@@ -208,7 +216,10 @@ __device__ __forceinline__ uint32_t group_vertex(const RoundArgs &a, uint32_t v,
 // compacted in item order (any order inside a segment is valid: the key order
 // is total); every read of a pass precedes its writes, and writes only land
 // below the slots already read, so in-place compaction is race-free.
-constexpr int kPairs = 4;                 // uint4 pairs per thread per pass
+#ifndef LMX_PAIRS
+#define LMX_PAIRS 2
+#endif
+constexpr int kPairs = LMX_PAIRS;         // uint4 pairs per thread per pass
 constexpr int kBlockItems = 2 * kPairs;   // slot items per thread per pass
 
 template <int MODE, int L>
@@ -334,11 +345,12 @@ __device__ __forceinline__ uint32_t team_vertex(const RoundArgs &a, uint32_t v, 
 
 __device__ __forceinline__ void put_result(const RoundArgs &a, int mode, uint32_t v, uint32_t w, const Best &b) {
     if (mode != 0) a.vdeg[v] = w;
-    a.cand[v] = (w > 0) ? make_uint2(b.nbr, b.id) : make_uint2(kNone, kNone);
+    a.cand_nbr[v] = (w > 0) ? b.nbr : kNone;
+    a.cand_id[v] = (w > 0) ? b.id : kNone;
 }
 
 template <int MODE, int L>
-__global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
+__global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a) {
     __shared__ uint32_t s_cnt[kBlockItems][kWarps];
     __shared__ Best s_best[kWarps];
     __shared__ uint32_t s_item;
@@ -349,6 +361,9 @@ __global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
 #pragma unroll
     for (int q = 0; q < kBuckets; ++q) {
         nb[q] = a.ctr->n[q];
+#ifdef LMX_ONLY_BUCKET   // profiling experiments only: time one bucket's mapping
+        if (q != LMX_ONLY_BUCKET) nb[q] = 0;
+#endif
         any |= nb[q];
     }
     if (any == 0) return;
@@ -477,12 +492,14 @@ __global__ void __launch_bounds__(kBlock, 4) lmx_round_kernel(RoundArgs a) {
 
 struct MatchArgs {
     const uint32_t *vdeg;
-    const uint2 *cand;
+    const uint32_t *cand_nbr;
+    const uint32_t *cand_id;
     uint32_t *matched;
     long long *mate;
     const uint32_t *oldid;   // device id -> caller id (null: identity)
-    const uint32_t *list[kBuckets];
-    uint32_t *next[kBuckets];
+    const uint32_t *list;    // kBuckets regions of capacity `cap`
+    uint32_t *next;          // kBuckets regions of capacity `cap`
+    unsigned long long cap;
     uint32_t *mids;
     unsigned long long *mcount;
     RoundCtr *ctr;        // this round
@@ -521,22 +538,23 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                 int q = 0;
 #pragma unroll
                 for (int z = 1; z < kBuckets; ++z) q += (i >= pre[z]) ? 1 : 0;
-                v = a.list[q][i - pre[q]];
+                v = a.list[(unsigned long long)q * a.cap + (i - pre[q])];
                 d = a.vdeg[v];
             }
             uint32_t kd = kTargets;   // none
             uint32_t e = 0;
             if (d > 0) {
-                const uint2 c = a.cand[v];
-                const uint2 cx = a.cand[c.x];
-                if (cx.x == v && cx.y == c.y) {
+                const uint32_t x = a.cand_nbr[v];
+                const uint32_t id = a.cand_id[v];
+                // edge ids / weight keys are unique per edge: same id at x <=> same edge
+                if (a.cand_id[x] == id) {
                     atomicOr(a.matched + (v >> 5), 1u << (v & 31));
-                    if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[c.x];
-                    else a.mate[v] = (long long)c.x;
+                    if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
+                    else a.mate[v] = (long long)x;
                     ++matched_v;
-                    if (v < c.x) {
+                    if (v < x) {
                         kd = kBuckets;
-                        e = c.y;
+                        e = id;
                     }
                 } else {
                     kd = (uint32_t)bucket_of(d);
@@ -578,7 +596,7 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                 const uint32_t bal = __ballot_sync(0xffffffffu, kind[j] == (uint32_t)q);
                 if (kind[j] == (uint32_t)q) {
                     const uint32_t p = pos[q] + __popc(bal & lt);
-                    if (q < kBuckets) a.next[q][p] = vv[j];
+                    if (q < kBuckets) a.next[(unsigned long long)q * a.cap + p] = vv[j];
                     else a.mids[p] = eid[j];
                 }
                 pos[q] += __popc(bal);
@@ -724,7 +742,8 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             RoundArgs a;
             a.vbeg = ctx->vbeg;
             a.vdeg = ctx->vdeg;
-            a.cand = ctx->cand;
+            a.cand_nbr = reinterpret_cast<uint32_t *>(ctx->cand);
+            a.cand_id = a.cand_nbr + cap;
             a.ids0 = ctx->ids0;
             a.wk0 = ctx->wk0;
             a.ids1 = ctx->ids1;
@@ -743,14 +762,14 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             LMX_TRY(tl_mark());
             MatchArgs ma;
             ma.vdeg = ctx->vdeg;
-            ma.cand = ctx->cand;
+            ma.cand_nbr = a.cand_nbr;
+            ma.cand_id = a.cand_id;
             ma.matched = ctx->matched;
             ma.mate = ctx->mate;
             ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
-            for (int q = 0; q < kBuckets; ++q) {
-                ma.list[q] = cur + (size_t)q * cap;
-                ma.next[q] = nxt + (size_t)q * cap;
-            }
+            ma.list = cur;
+            ma.next = nxt;
+            ma.cap = cap;
             ma.mids = ctx->mids;
             ma.mcount = ctx->mcount;
             ma.ctr = ctx->ctr + r;
@@ -770,6 +789,9 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             }
         }
         batch = 4;
+#ifdef LMX_ONLY_BUCKET   // profiling experiments: results are meaningless, stop after one batch
+        if (n_rounds < 0) n_rounds = 0;
+#endif
     }
     if (ctx->kernel_timing && tl_used > 1) {
         for (int i = 1; i < tl_used; ++i) {

@@ -22,7 +22,7 @@ import numpy as np
 from .graph import Graph, Matching, PhaseTrace, RoundStats
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblmx.so")
+LIB_PATH = os.environ.get("LMX_LIBRARY") or os.path.join(_HERE, "liblmx.so")
 _UINT64_MASK = (1 << 64) - 1
 
 LMX_OK, LMX_EINVAL, LMX_ECUDA, LMX_ENOMEM, LMX_ELIMIT, LMX_ESTATE = range(6)
