@@ -167,12 +167,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // For G < 32 a single pass covers d <= G * ITEMS; for G == 32 (v, d) are
 // warp-uniform and the loop runs ceil(d / (32 * ITEMS)) passes.
 template <int MODE, int L, int G, int ITEMS>
-__device__ __forceinline__ uint32_t group_vertex(const RoundArgs &a, uint32_t v, uint32_t d, int lane,
-                                                 Best &b) {
+__device__ __forceinline__ uint32_t group_vertex(const RoundArgs &a, unsigned long long beg, uint32_t d,
+                                                 int lane, Best &b) {
     const int gl = lane & (G - 1);
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const uint32_t lt = lanemask_lt() & gmask;
-    const unsigned long long beg = d ? a.vbeg[v] : 0ULL;
     const uint32_t span = G * ITEMS;
     const uint32_t npass = (G == 32) ? (d + span - 1) / span : 1u;
     uint32_t w = 0;
@@ -305,10 +304,9 @@ __device__ __forceinline__ void team_single(const RoundArgs &a, unsigned long lo
 }
 
 template <int MODE, int L, int TEAM>
-__device__ __forceinline__ uint32_t team_vertex(const RoundArgs &a, uint32_t v, uint32_t d, Best &b,
-                                                uint32_t (*s_cnt)[kWarps]) {
+__device__ __forceinline__ uint32_t team_vertex(const RoundArgs &a, unsigned long long beg, uint32_t d,
+                                                Best &b, uint32_t (*s_cnt)[kWarps]) {
     const uint32_t t = threadIdx.x % TEAM;
-    const unsigned long long beg = a.vbeg[v];
     uint32_t w = 0;
     const uint32_t head = (uint32_t)(beg & 1ULL);
     if (head) team_single<MODE, L, TEAM>(a, beg, 0, w, b, s_cnt);
@@ -383,7 +381,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
             const uint32_t d = a.vdeg[v];
             Best b;
             best_init(b);
-            const uint32_t w = team_vertex<MODE, L, kBlock>(a, v, d, b, s_cnt);
+            const uint32_t w = team_vertex<MODE, L, kBlock>(a, a.vbeg[v], d, b, s_cnt);
             if (lane == 0) s_best[warp] = b;
             __syncthreads();
             if (tid == 0) {
@@ -397,19 +395,32 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         }
     }
 
-    // phase 2: bucket 2, warp per vertex, 4 vertices per grab
+    // The small-vertex phases below fetch the per-vertex metadata (list entry,
+    // live degree, segment start) of a whole grab at once, one vertex per
+    // lane, and broadcast it: the list -> vdeg/vbeg -> slots dependency chain
+    // is paid once per grab instead of once per vertex.
+
+    // phase 2: bucket 2, warp per vertex, 8 vertices per grab
     for (;;) {
         uint32_t i0 = 0;
-        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[2], 4u);
+        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[2], 8u);
         i0 = __shfl_sync(0xffffffffu, i0, 0);
         if (i0 >= nb[2]) break;
-        const uint32_t iend = min(i0 + 4u, nb[2]);
-        for (uint32_t i = i0; i < iend; ++i) {
-            const uint32_t v = a.list[2][i];
-            const uint32_t d = a.vdeg[v];
+        uint32_t mv = kNone, md = 0;
+        unsigned long long mb = 0;
+        if (lane < 8 && i0 + lane < nb[2]) {
+            mv = a.list[2][i0 + lane];
+            md = a.vdeg[mv];
+            mb = a.vbeg[mv];
+        }
+        const uint32_t cnt = min(8u, nb[2] - i0);
+        for (uint32_t k = 0; k < cnt; ++k) {
+            const uint32_t v = __shfl_sync(0xffffffffu, mv, k);
+            const uint32_t d = __shfl_sync(0xffffffffu, md, k);
+            const unsigned long long beg = __shfl_sync(0xffffffffu, mb, k);
             Best b;
             best_init(b);
-            const uint32_t w = team_vertex<MODE, L, 32>(a, v, d, b, s_cnt);
+            const uint32_t w = team_vertex<MODE, L, 32>(a, beg, d, b, s_cnt);
             if (lane == 0) {
                 put_result(a, MODE, v, w, b);
                 live += w;
@@ -424,17 +435,22 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         if (lane == 0) i0 = atomicAdd(&a.ctr->cur[1], 16u);
         i0 = __shfl_sync(0xffffffffu, i0, 0);
         if (i0 >= nb[1]) break;
+        uint32_t mv = kNone, md = 0;
+        unsigned long long mb = 0;
+        if (lane < 16 && i0 + lane < nb[1]) {
+            mv = a.list[1][i0 + lane];
+            md = a.vdeg[mv];
+            mb = a.vbeg[mv];
+        }
 #pragma unroll 1
         for (int it = 0; it < 4; ++it) {
-            const uint32_t i = i0 + it * 4 + (lane >> 3);
-            uint32_t v = kNone, d = 0;
-            if (i < nb[1]) {
-                v = a.list[1][i];
-                d = a.vdeg[v];
-            }
+            const int src = it * 4 + (lane >> 3);
+            const uint32_t v = __shfl_sync(0xffffffffu, mv, src);
+            const uint32_t d = __shfl_sync(0xffffffffu, md, src);
+            const unsigned long long beg = __shfl_sync(0xffffffffu, mb, src);
             Best b;
             best_init(b);
-            const uint32_t w = group_vertex<MODE, L, 8, 4>(a, v, d, lane, b);
+            const uint32_t w = group_vertex<MODE, L, 8, 4>(a, beg, d, lane, b);
             if ((lane & 7) == 0 && d) {
                 put_result(a, MODE, v, w, b);
                 live += w;
@@ -449,17 +465,21 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         if (lane == 0) i0 = atomicAdd(&a.ctr->cur[0], 128u);
         i0 = __shfl_sync(0xffffffffu, i0, 0);
         if (i0 >= nb[0]) break;
-#pragma unroll 1
+        uint32_t mv[4], md[4];
+#pragma unroll
         for (int it = 0; it < 4; ++it) {
             const uint32_t i = i0 + it * 32 + lane;
-            uint32_t v = kNone, d = 0;
-            if (i < nb[0]) {
-                v = a.list[0][i];
-                d = a.vdeg[v];
-            }
+            mv[it] = (i < nb[0]) ? a.list[0][i] : kNone;
+        }
+#pragma unroll
+        for (int it = 0; it < 4; ++it) md[it] = (mv[it] != kNone) ? a.vdeg[mv[it]] : 0u;
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t v = mv[it], d = md[it];
+            const unsigned long long beg = d ? a.vbeg[v] : 0ULL;
             Best b;
             best_init(b);
-            const uint32_t w = group_vertex<MODE, L, 1, 4>(a, v, d, lane, b);
+            const uint32_t w = group_vertex<MODE, L, 1, 4>(a, beg, d, lane, b);
             if (d) {
                 put_result(a, MODE, v, w, b);
                 live += w;
