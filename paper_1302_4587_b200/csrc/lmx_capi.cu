@@ -120,6 +120,7 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
     if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded (call lmx_load_graph first)");
     std::vector<lmx_round_stats> &stats = ctx->rounds;
     unsigned long long nm = 0;
+    ctx->mate_target = (out_where == LMX_DEVICE && mate_out) ? (long long *)mate_out : ctx->mate;
     LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
     LMX_TRY(lmx_emit_outputs(ctx, nm, mate_out, matched_ids_out, out_where));
     if (n_matched_out) *n_matched_out = (int64_t)nm;

@@ -114,13 +114,14 @@ struct lmx_ctx {
     uint2 *cand = nullptr;
     uint32_t *matched = nullptr;
     uint32_t *lists[2] = {nullptr, nullptr}; // ping-pong, kBuckets regions of capacity n
-    uint32_t *mids = nullptr;                // matched ids (u32)
-    uint32_t *mids_sorted = nullptr;
-    unsigned long long *mcount = nullptr;    // total matched edges
+    uint32_t *mids = nullptr;                // matched edge ids, ascending (u32 staging)
+    uint32_t *ebits = nullptr;               // matched edge-id bitmap, (m + 31) / 32 words
+    uint32_t *ebits_off = nullptr;           // per-word exclusive popcount prefix
     lmx::RoundCtr *ctr = nullptr;
     lmx::RoundCtr *ctr_host = nullptr;       // pinned mirror
     int ctr_cap = 0;
     long long *mate = nullptr;               // int64[n]
+    long long *mate_target = nullptr;        // where this lmx_match writes mate
     void *sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
     int64_t dev_bytes = 0;

@@ -520,16 +520,22 @@ struct MatchArgs {
     const uint32_t *list;    // kBuckets regions of capacity `cap`
     uint32_t *next;          // kBuckets regions of capacity `cap`
     unsigned long long cap;
-    uint32_t *mids;
-    unsigned long long *mcount;
+    uint32_t *ebits;            // matched edge-id bitmap (m bits)
+    const uint32_t *eid_of_x;   // DISTINCT layout: weight key -> edge id (else null)
     RoundCtr *ctr;        // this round
     RoundCtr *ctr_next;   // next round (list sizes)
 };
 
-constexpr int kMatchItems = 4;
-constexpr int kTargets = kBuckets + 1;   // next-round buckets + matched-id output
+#ifndef LMX_MATCH_ITEMS
+#define LMX_MATCH_ITEMS 4
+#endif
+#ifndef LMX_MATCH_MINB
+#define LMX_MATCH_MINB 8
+#endif
+constexpr int kMatchItems = LMX_MATCH_ITEMS;
+constexpr int kTargets = kBuckets;   // next-round bucket lists
 
-__global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
+__global__ void __launch_bounds__(kBlock, LMX_MATCH_MINB) lmx_match_kernel(MatchArgs a) {
     __shared__ uint32_t s_cnt[kTargets][kWarps];
     __shared__ uint32_t s_base[kTargets];
     uint32_t nb[kBuckets], pre[kBuckets + 1];
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
     unsigned long long matched_v = 0;
     const uint32_t tile = kBlock * kMatchItems;
     for (uint32_t t0 = blockIdx.x * tile; t0 < total; t0 += gridDim.x * tile) {
-        uint32_t vv[kMatchItems], kind[kMatchItems], eid[kMatchItems];
+        uint32_t vv[kMatchItems], kind[kMatchItems];
         uint32_t wc[kTargets];
 #pragma unroll
         for (int q = 0; q < kTargets; ++q) wc[q] = 0;
@@ -562,7 +568,6 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                 d = a.vdeg[v];
             }
             uint32_t kd = kTargets;   // none
-            uint32_t e = 0;
             if (d > 0) {
                 const uint32_t x = a.cand_nbr[v];
                 const uint32_t id = a.cand_id[v];
@@ -572,9 +577,9 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                     if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
                     else a.mate[v] = (long long)x;
                     ++matched_v;
-                    if (v < x) {
-                        kd = kBuckets;
-                        e = id;
+                    if (v < x) {   // the lower endpoint records the edge (graph.py:195-203)
+                        const uint32_t e = a.eid_of_x ? a.eid_of_x[id] : id;
+                        atomicOr(a.ebits + (e >> 5), 1u << (e & 31));
                     }
                 } else {
                     kd = (uint32_t)bucket_of(d);
@@ -582,7 +587,6 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
             }
             vv[j] = v;
             kind[j] = kd;
-            eid[j] = e;
 #pragma unroll
             for (int q = 0; q < kTargets; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, kd == (uint32_t)q));
         }
@@ -595,10 +599,7 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
             uint32_t sum = 0;
             for (int w = 0; w < kWarps; ++w) sum += s_cnt[tid][w];
             uint32_t base = 0;
-            if (sum) {
-                if (tid < kBuckets) base = atomicAdd(&a.ctr_next->n[tid], sum);
-                else base = (uint32_t)atomicAdd(a.mcount, (unsigned long long)sum);
-            }
+            if (sum) base = atomicAdd(&a.ctr_next->n[tid], sum);
             s_base[tid] = base;
         }
         __syncthreads();
@@ -616,8 +617,7 @@ __global__ void __launch_bounds__(kBlock) lmx_match_kernel(MatchArgs a) {
                 const uint32_t bal = __ballot_sync(0xffffffffu, kind[j] == (uint32_t)q);
                 if (kind[j] == (uint32_t)q) {
                     const uint32_t p = pos[q] + __popc(bal & lt);
-                    if (q < kBuckets) a.next[(unsigned long long)q * a.cap + p] = vv[j];
-                    else a.mids[p] = eid[j];
+                    a.next[(unsigned long long)q * a.cap + p] = vv[j];
                 }
                 pos[q] += __popc(bal);
             }
@@ -640,18 +640,27 @@ __global__ void lmx_init_kernel(uint32_t n, const uint32_t *deg0, uint32_t *vdeg
     }
 }
 
-// DISTINCT layout: matched weight keys -> edge ids (before the sort).
-__global__ void lmx_ids_to_eids(uint32_t *ids, unsigned long long k, const uint32_t *eid_of_x) {
+// K5: matched edge ids, ascending, from the edge-id bitmap.
+__global__ void lmx_word_counts(const uint32_t *ebits, unsigned long long words, uint32_t *cnt) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride)
-        ids[i] = eid_of_x[ids[i]];
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += stride)
+        cnt[i] = __popc(ebits[i]);
 }
 
-__global__ void lmx_widen_kernel(const uint32_t *src, long long *dst, unsigned long long k) {
+template <typename T>
+__global__ void lmx_emit_ids(const uint32_t *ebits, const uint32_t *off, unsigned long long words, T *out) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
-         i += stride)
-        dst[i] = src[i];
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += stride) {
+        uint32_t bits = ebits[i];
+        uint32_t p = off[i];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            out[p++] = (T)(i * 32 + b);
+        }
+    }
 }
 
 }  // namespace lmx
@@ -677,12 +686,12 @@ int lmx_alloc_match_state(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
     for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], n * 4 * kBuckets, "lists"));
+    const size_t words = (size_t)(std::max<int64_t>(ctx->m, 1) + 31) / 32;
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 4, "mids"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids_sorted, (n / 2 + 1) * 4, "mids_sorted"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mcount, 8, "mcount"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits, words * 4, "ebits"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits_off, words * 4, "ebits_off"));
     size_t tmp = 0;
-    LMX_CUDA(ctx, cub::DeviceRadixSort::SortKeys(nullptr, tmp, ctx->mids, ctx->mids_sorted,
-                                                 (long long)(n / 2 + 1)));
+    LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->ebits_off, ctx->ebits_off, (long long)words));
     ctx->sort_tmp_bytes = tmp + 256;
     LMX_TRY(lmx_alloc(ctx, &ctx->sort_tmp, ctx->sort_tmp_bytes, "sort_tmp"));
     return LMX_OK;
@@ -711,7 +720,8 @@ static int ensure_ctr(lmx_ctx *ctx, int need) {
 }
 
 // The round loop of local_max_seq (matchers.py:87-119) on the device.
-// Leaves mate in ctx->mate, matched ids (unsorted) in ctx->mids.
+// Leaves mate in `mate` (ctx->mate or the caller's device buffer) and the
+// matched edge-id bitmap in ctx->ebits.
 int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                    std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
     const uint32_t n = (uint32_t)ctx->n;
@@ -724,7 +734,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     ctx->timing.match_kernel_ms = 0;
     LMX_TRY(ensure_ctr(ctx, 64));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, ctx->stream));
-    LMX_CUDA(ctx, cudaMemsetAsync(ctx->mcount, 0, 8, ctx->stream));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, ctx->stream));
     ctx->ctr_host[0] = RoundCtr{};
     for (int q = 0; q < kBuckets; ++q) ctx->ctr_host[0].n[q] = ctx->n_bins0[q];
     LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice,
@@ -743,7 +753,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         return LMX_OK;
     };
     if (n > 0) {
-        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg, ctx->mate,
+        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg, ctx->mate_target,
                                                                      ctx->matched);
         LMX_CUDA(ctx, cudaGetLastError());
         ctx->timing.round_launches += 1;
@@ -785,13 +795,13 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ma.cand_nbr = a.cand_nbr;
             ma.cand_id = a.cand_id;
             ma.matched = ctx->matched;
-            ma.mate = ctx->mate;
+            ma.mate = ctx->mate_target;
             ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
             ma.list = cur;
             ma.next = nxt;
             ma.cap = cap;
-            ma.mids = ctx->mids;
-            ma.mcount = ctx->mcount;
+            ma.ebits = ctx->ebits;
+            ma.eid_of_x = ctx->layout == kDistinct ? ctx->eid_of_x : nullptr;
             ma.ctr = ctx->ctr + r;
             ma.ctr_next = ctx->ctr + r + 1;
             lmx_match_kernel<<<ctx->match_blocks, kBlock, 0, ctx->stream>>>(ma);
@@ -842,38 +852,38 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     return LMX_OK;
 }
 
-// Sort the matched edge ids (K5) and copy mate / ids out.
+// K5: ascending matched edge ids from the bitmap; mate / ids out.
 int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_out,
                      int64_t *ids_out, int out_where) {
     const size_t n = (size_t)ctx->n;
-    if (n_matched > 0) {
-        if (ctx->layout == kDistinct) {
-            lmx_ids_to_eids<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(ctx->mids, n_matched, ctx->eid_of_x);
-            LMX_CUDA(ctx, cudaGetLastError());
-            ctx->timing.round_launches += 1;
-        }
+    const unsigned long long words = ((unsigned long long)std::max<int64_t>(ctx->m, 1) + 31) / 32;
+    const int grid = ctx->num_sms * 8;
+    if (n_matched > 0 && ids_out) {
+        lmx_word_counts<<<grid, kBlock, 0, ctx->stream>>>(ctx->ebits, words, ctx->ebits_off);
+        LMX_CUDA(ctx, cudaGetLastError());
         size_t tmp = ctx->sort_tmp_bytes;
-        LMX_CUDA(ctx, cub::DeviceRadixSort::SortKeys(ctx->sort_tmp, tmp, ctx->mids, ctx->mids_sorted,
-                                                     (long long)n_matched, 0, 32, ctx->stream));
+        LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->sort_tmp, tmp, ctx->ebits_off, ctx->ebits_off,
+                                                    (long long)words, ctx->stream));
+        if (out_where == LMX_DEVICE)
+            lmx_emit_ids<long long><<<grid, kBlock, 0, ctx->stream>>>(ctx->ebits, ctx->ebits_off, words,
+                                                                     (long long *)ids_out);
+        else
+            lmx_emit_ids<uint32_t><<<grid, kBlock, 0, ctx->stream>>>(ctx->ebits, ctx->ebits_off, words, ctx->mids);
+        LMX_CUDA(ctx, cudaGetLastError());
+        ctx->timing.round_launches += 2;
     }
     if (out_where == LMX_DEVICE) {
-        if (mate_out && n)
-            LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-        if (ids_out && n_matched) {
-            lmx_widen_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
-                ctx->mids_sorted, (long long *)ids_out, n_matched);
-            LMX_CUDA(ctx, cudaGetLastError());
-            ctx->timing.round_launches += 1;
-        }
+        if (mate_out && n && ctx->mate_target != (long long *)mate_out)
+            LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate_target, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     } else {
         if (mate_out && n)
-            LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate_target, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
         std::vector<uint32_t> tmp32((size_t)n_matched);
         if (ids_out && n_matched)
-            LMX_CUDA(ctx, cudaMemcpyAsync(tmp32.data(), ctx->mids_sorted, (size_t)n_matched * 4,
-                                          cudaMemcpyDeviceToHost, ctx->stream));
+            LMX_CUDA(ctx, cudaMemcpyAsync(tmp32.data(), ctx->mids, (size_t)n_matched * 4, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         if (ids_out)

@@ -61,7 +61,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->wk0,      (void **)&ctx->wk1,         (void **)&ctx->deg0,
                      (void **)&ctx->vdeg,     (void **)&ctx->cand,        (void **)&ctx->matched,
                      (void **)&ctx->lists[0], (void **)&ctx->lists[1],    (void **)&ctx->bins0,
-                     (void **)&ctx->mids,     (void **)&ctx->mids_sorted, (void **)&ctx->mcount,
+                     (void **)&ctx->mids,     (void **)&ctx->ebits,       (void **)&ctx->ebits_off,
                      (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
                      (void **)&ctx->tie_rank, (void **)&ctx->oldid};
     for (void **p : ptrs) {
