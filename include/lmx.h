@@ -78,6 +78,8 @@ typedef struct {
                                    (only valid if all weights are equal), 1 distinct, 2 general */
 #define LMX_OPT_RELABEL 3       /* degree-descending vertex relabelling of the next load:
                                    -1 auto (skewed degree distributions), 0 off, 1 on */
+#define LMX_OPT_DIST_P 4        /* number of 1D vertex partitions of the next load (1 = single GPU) */
+#define LMX_OPT_DIST_RANK 5     /* which partition this context owns (set after LMX_OPT_DIST_P) */
 #define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
 #define LMX_QUERY_RELABELED 101 /* lmx_set_option returns 1 if the loaded graph is relabelled */
 
@@ -157,6 +159,34 @@ int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out);
 /* Copy the loaded graph's edge arrays out (graph.py Graph.edge_u/v/weight). */
 int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edge_weight,
                      int out_where);
+
+/*
+ * 1D-partitioned local max (bsp_local_max, bsp.py:101-205).
+ * With LMX_OPT_DIST_P = p and LMX_OPT_DIST_RANK = k set before the load, the
+ * context owns the k-th of p contiguous vertex ranges with equal degree sums
+ * (bsp.py:60-98, cuts rounded to 32 so ranks own whole bitmap words) and the
+ * slots of all edges incident to it.  The host drives each round:
+ *   lmx_dist_round      candidates of the owned vertices
+ *   lmx_dist_propose    records {partner, edge id} for partners owned elsewhere,
+ *                       grouped by destination rank (exchange A, barrier 1)
+ *   lmx_dist_recv_buffer / lmx_dist_accept   received records
+ *   lmx_dist_match      local + confirmed cross-rank matches; returns the
+ *                       owned live-slot and matched-vertex counts
+ * then all-gathers the owned words of the matched bitmap (exchange B,
+ * barrier 2) and all-reduces the counts (RoundStats, termination).  The
+ * matching equals the single-GPU one for every p (bsp.py:113-115).
+ */
+int lmx_dist_bounds(const lmx_ctx *ctx, int64_t *bounds_out);   /* p + 1 device-id cut points */
+int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize);
+int lmx_dist_round(lmx_ctx *ctx);
+int lmx_dist_propose(lmx_ctx *ctx, int64_t *counts_out, void **send_out);
+int lmx_dist_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_out);
+int lmx_dist_accept(lmx_ctx *ctx, int64_t count);
+int lmx_dist_match(lmx_ctx *ctx, int64_t *live_slots_out, int64_t *matched_v_out);
+/* Device pointers: matched bitmap (n bits, global device ids), mate (int64[n],
+ * caller ids, only owned vertices set), matched-edge bitmap (m bits, edges
+ * recorded by this rank), and the context's cudaStream_t. */
+int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge_bits, void **stream);
 
 /* Device memory in use by the context (bytes). */
 int64_t lmx_device_bytes(const lmx_ctx *ctx);

@@ -155,6 +155,16 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
         ctx->force_relabel = (int)value;
         return LMX_OK;
     }
+    if (option == LMX_OPT_DIST_P) {
+        if (value < 1 || value > 64) return lmx_fail(ctx, LMX_EINVAL, "dist p must be in [1, 64]");
+        ctx->dist_p = (int)value;
+        return LMX_OK;
+    }
+    if (option == LMX_OPT_DIST_RANK) {
+        if (value < 0 || value >= ctx->dist_p) return lmx_fail(ctx, LMX_EINVAL, "dist rank out of range");
+        ctx->dist_rank = (int)value;
+        return LMX_OK;
+    }
     if (option == LMX_QUERY_LAYOUT) return ctx->layout;
     if (option == LMX_QUERY_RELABELED) return ctx->relabeled ? 1 : 0;
     return lmx_fail(ctx, LMX_EINVAL, "unknown option");
@@ -183,6 +193,62 @@ int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const
     }
     lmx_destroy(ctx);
     return rc;
+}
+
+// ---- 1D-partitioned (multi-GPU) stepped protocol ---------------------------
+
+int lmx_dist_bounds(const lmx_ctx *ctx, int64_t *bounds_out) {
+    if (!ctx || !bounds_out) return LMX_EINVAL;
+    for (size_t i = 0; i < ctx->bounds.size(); ++i) bounds_out[i] = ctx->bounds[i];
+    return LMX_OK;
+}
+
+int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded");
+    return lmx_dist_begin_impl(ctx, seed_masked, rerandomize != 0);
+}
+
+int lmx_dist_round(lmx_ctx *ctx) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    return lmx_dist_round_impl(ctx);
+}
+
+int lmx_dist_propose(lmx_ctx *ctx, int64_t *counts_out, void **send_out) {
+    if (!ctx || !counts_out || !send_out) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    LMX_TRY(lmx_dist_propose_impl(ctx, counts_out));
+    *send_out = ctx->send;
+    return LMX_OK;
+}
+
+int lmx_dist_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_out) {
+    if (!ctx || !recv_out) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    return lmx_dist_recv_impl(ctx, count, recv_out);
+}
+
+int lmx_dist_accept(lmx_ctx *ctx, int64_t count) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    return lmx_dist_accept_impl(ctx, count);
+}
+
+int lmx_dist_match(lmx_ctx *ctx, int64_t *live_slots_out, int64_t *matched_v_out) {
+    if (!ctx || !live_slots_out || !matched_v_out) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    return lmx_dist_match_impl(ctx, live_slots_out, matched_v_out);
+}
+
+int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge_bits, void **stream) {
+    if (!ctx) return LMX_EINVAL;
+    if (matched_bitmap) *matched_bitmap = ctx->matched;
+    if (mate) *mate = ctx->mate;
+    if (edge_bits) *edge_bits = ctx->ebits;
+    if (stream) *stream = ctx->stream;
+    return LMX_OK;
 }
 
 int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out) {

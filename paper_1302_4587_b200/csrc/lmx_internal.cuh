@@ -135,6 +135,21 @@ struct lmx_ctx {
     int force_relabel = -1;                  // -1 auto (skewed graphs), 0 off, 1 on
     bool relabeled = false;                  // device vertex ids are degree-sorted
     uint32_t *oldid = nullptr;               // device id -> caller's vertex id
+
+    // 1D vertex partition (multi-GPU; single GPU = one range [0, n)).  Per-vertex
+    // arrays (vbeg, deg0, vdeg, cand, lists) are indexed by the local id v - lo;
+    // slot neighbours, the matched bitmap and mate use global (device) ids.
+    int dist_p = 1, dist_rank = 0;           // applied at the next load
+    unsigned long long lo = 0, hi = 0;       // owned device-id range
+    int64_t n_local = 0, slots_local = 0;
+    std::vector<int64_t> bounds;             // p + 1 cut points
+    uint32_t *remote_ok = nullptr;           // [n_local] partner owner confirmed the edge
+    uint2 *send = nullptr, *recv = nullptr;  // proposal records {global target, edge id}
+    uint32_t *send_cnt = nullptr;            // [p] per destination
+    size_t send_cap = 0, recv_cap = 0;
+    int dist_round = 0;                      // next round of the stepped protocol
+    uint64_t dist_seed = 0;
+    bool dist_rr = true;
 };
 
 // helpers shared by the translation units
@@ -152,6 +167,12 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                    std::vector<lmx_round_stats> &stats, unsigned long long &n_matched);
 int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_out,
                      int64_t *ids_out, int out_where);
+int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize);
+int lmx_dist_round_impl(lmx_ctx *ctx);
+int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts);
+int lmx_dist_recv_impl(lmx_ctx *ctx, int64_t count, void **ptr);
+int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count);
+int lmx_dist_match_impl(lmx_ctx *ctx, int64_t *live_slots, int64_t *matched_v);
 
 #define LMX_CUDA(ctx, expr)                                          \
     do {                                                             \

@@ -522,6 +522,8 @@ struct MatchArgs {
     unsigned long long cap;
     uint32_t *ebits;            // matched edge-id bitmap (m bits)
     const uint32_t *eid_of_x;   // DISTINCT layout: weight key -> edge id (else null)
+    uint32_t lo, nl;            // owned device-id range [lo, lo + nl)
+    uint32_t *remote_ok;        // [nl] the remote partner's owner confirmed the edge
     RoundCtr *ctr;        // this round
     RoundCtr *ctr_next;   // next round (list sizes)
 };
@@ -569,15 +571,24 @@ __global__ void __launch_bounds__(kBlock, LMX_MATCH_MINB) lmx_match_kernel(Match
             }
             uint32_t kd = kTargets;   // none
             if (d > 0) {
-                const uint32_t x = a.cand_nbr[v];
+                const uint32_t x = a.cand_nbr[v];   // global id
                 const uint32_t id = a.cand_id[v];
-                // edge ids / weight keys are unique per edge: same id at x <=> same edge
-                if (a.cand_id[x] == id) {
-                    atomicOr(a.matched + (v >> 5), 1u << (v & 31));
-                    if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
-                    else a.mate[v] = (long long)x;
+                const uint32_t gv = v + a.lo;
+                bool mutual;
+                if (x - a.lo < a.nl) {
+                    // edge ids / weight keys are unique per edge: same id at x <=> same edge
+                    mutual = a.cand_id[x - a.lo] == id;
+                } else {
+                    // partner owned by another rank: its owner sent the edge back (exchange A)
+                    mutual = a.remote_ok[v] != 0;
+                    if (mutual) a.remote_ok[v] = 0;
+                }
+                if (mutual) {
+                    atomicOr(a.matched + (gv >> 5), 1u << (gv & 31));
+                    if (a.oldid) a.mate[a.oldid[gv]] = (long long)a.oldid[x];
+                    else a.mate[gv] = (long long)x;
                     ++matched_v;
-                    if (v < x) {   // the lower endpoint records the edge (graph.py:195-203)
+                    if (gv < x) {   // the lower endpoint records the edge (graph.py:195-203)
                         const uint32_t e = a.eid_of_x ? a.eid_of_x[id] : id;
                         atomicOr(a.ebits + (e >> 5), 1u << (e & 31));
                     }
@@ -629,14 +640,71 @@ __global__ void __launch_bounds__(kBlock, LMX_MATCH_MINB) lmx_match_kernel(Match
     if (lane == 0 && matched_v) atomicAdd(&a.ctr->matched_v, matched_v);
 }
 
-// Per-match initialisation: live degrees, mates, matched bitmap.
-__global__ void lmx_init_kernel(uint32_t n, const uint32_t *deg0, uint32_t *vdeg, long long *mate,
+// Per-match initialisation: live degrees (owned), mates and matched bitmap (global).
+__global__ void lmx_init_kernel(uint32_t n, uint32_t nl, const uint32_t *deg0, uint32_t *vdeg, long long *mate,
                                 uint32_t *matched) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-        vdeg[v] = deg0[v];
+        if (v < nl) vdeg[v] = deg0[v];
         mate[v] = -1;
         if ((v & 31) == 0) matched[v >> 5] = 0;
+    }
+}
+
+// ---- multi-GPU exchange A (bsp.py:148-167 as a minimal record exchange) ----
+struct ProposeArgs {
+    const uint32_t *vdeg;
+    const uint32_t *cand_nbr;
+    const uint32_t *cand_id;
+    const uint32_t *list;
+    unsigned long long cap;
+    const RoundCtr *ctr;
+    const uint32_t *eid_of_x;
+    const unsigned long long *bounds;   // p + 1 cut points (global ids)
+    int p;
+    uint32_t lo, nl;
+    uint32_t *cnt;      // [p] records per destination (pass 0)
+    uint32_t *cursor;   // [p] write cursors, preset to the offsets (pass 1)
+    uint2 *out;         // {global target vertex, edge id}
+    int pass;
+};
+
+// For every owned live vertex whose candidate partner is owned elsewhere, send
+// {partner, edge id} to the partner's owner.  Pass 0 counts per destination,
+// pass 1 writes the records grouped by destination.
+__global__ void lmx_propose_kernel(ProposeArgs a) {
+    uint32_t total = 0;
+#pragma unroll
+    for (int q = 0; q < kBuckets; ++q) total += a.ctr->n[q];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        uint32_t q = 0, base = 0;
+        while (q + 1 < (uint32_t)kBuckets && i >= base + a.ctr->n[q]) base += a.ctr->n[q++];
+        const uint32_t v = a.list[(unsigned long long)q * a.cap + (i - base)];
+        if (a.vdeg[v] == 0) continue;
+        const uint32_t x = a.cand_nbr[v];
+        if (x - a.lo < a.nl) continue;   // local partner
+        int k = 0;
+        while (k + 1 < a.p && x >= a.bounds[k + 1]) ++k;
+        const uint32_t id = a.cand_id[v];
+        const uint32_t e = a.eid_of_x ? a.eid_of_x[id] : id;
+        if (a.pass == 0) atomicAdd(a.cnt + k, 1u);
+        else a.out[atomicAdd(a.cursor + k, 1u)] = make_uint2(x, e);
+    }
+}
+
+// Received {x, e}: x (owned) is matched across the cut iff its own candidate is edge e.
+__global__ void lmx_accept_kernel(const uint2 *rec, unsigned long long k, const uint32_t *vdeg,
+                                  const uint32_t *cand_id, const uint32_t *eid_of_x, uint32_t lo,
+                                  uint32_t *remote_ok) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint2 r = rec[i];
+        const uint32_t xl = r.x - lo;
+        if (vdeg[xl] == 0) continue;
+        const uint32_t id = cand_id[xl];
+        const uint32_t e = eid_of_x ? eid_of_x[id] : id;
+        if (e == r.y) remote_ok[xl] = 1u;
     }
 }
 
@@ -680,16 +748,19 @@ static void launch_round(lmx_ctx *ctx, const RoundArgs &a) {
 }
 
 int lmx_alloc_match_state(lmx_ctx *ctx) {
-    const size_t n = (size_t)std::max<int64_t>(ctx->n, 1);
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, n * 4, "vdeg"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, n * 8, "cand"));
+    const size_t n = (size_t)std::max<int64_t>(ctx->n, 1);          // global ids
+    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);   // owned vertices
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, nl * 4, "vdeg"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, nl * 8, "cand"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->remote_ok, nl * 4, "remote_ok"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
-    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], n * 4 * kBuckets, "lists"));
+    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], nl * 4 * kBuckets, "lists"));
     const size_t words = (size_t)(std::max<int64_t>(ctx->m, 1) + 31) / 32;
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 4, "mids"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits, words * 4, "ebits"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits_off, words * 4, "ebits_off"));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, nl * 4, ctx->stream));
     size_t tmp = 0;
     LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->ebits_off, ctx->ebits_off, (long long)words));
     ctx->sort_tmp_bytes = tmp + 256;
@@ -719,19 +790,12 @@ static int ensure_ctr(lmx_ctx *ctx, int need) {
     return LMX_OK;
 }
 
-// The round loop of local_max_seq (matchers.py:87-119) on the device.
-// Leaves mate in `mate` (ctx->mate or the caller's device buffer) and the
-// matched edge-id bitmap in ctx->ebits.
-int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
-                   std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
-    const uint32_t n = (uint32_t)ctx->n;
-    const size_t cap = (size_t)std::max<int64_t>(ctx->n, 1);
-    stats.clear();
-    n_matched = 0;
-    ctx->timing.round_launches = 0;
-    ctx->timing.slot_reads = 0;
-    ctx->timing.round_kernel_ms = 0;
-    ctx->timing.match_kernel_ms = 0;
+// ---- round-loop building blocks (shared by the single-GPU loop and the
+// stepped multi-GPU protocol) ------------------------------------------------
+
+// Reset per-match state: counters, edge bitmap, live degrees, mates, bitmap.
+static int begin_match(lmx_ctx *ctx) {
+    const uint32_t nl = (uint32_t)ctx->n_local;
     LMX_TRY(ensure_ctr(ctx, 64));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, ctx->stream));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, ctx->stream));
@@ -739,7 +803,83 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     for (int q = 0; q < kBuckets; ++q) ctx->ctr_host[0].n[q] = ctx->n_bins0[q];
     LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice,
                                   ctx->stream));
+    if (ctx->n > 0) {
+        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>((uint32_t)ctx->n, nl, ctx->deg0, ctx->vdeg,
+                                                                     ctx->mate_target, ctx->matched);
+        LMX_CUDA(ctx, cudaGetLastError());
+        ctx->timing.round_launches += 1;
+    }
+    return LMX_OK;
+}
+
+static size_t list_cap(const lmx_ctx *ctx) { return (size_t)std::max<int64_t>(ctx->n_local, 1); }
+
+static int enqueue_round_kernel(lmx_ctx *ctx, int r, uint64_t seed_masked, bool rerandomize) {
+    const size_t cap = list_cap(ctx);
+    const int mode = r == 0 ? 0 : (r == 1 ? 1 : 2);
+    const uint32_t *cur = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    RoundArgs a;
+    a.vbeg = ctx->vbeg;
+    a.vdeg = ctx->vdeg;
+    a.cand_nbr = reinterpret_cast<uint32_t *>(ctx->cand);
+    a.cand_id = a.cand_nbr + cap;
+    a.ids0 = ctx->ids0;
+    a.wk0 = ctx->wk0;
+    a.ids1 = ctx->ids1;
+    a.wk1 = ctx->wk1;
+    a.matched = ctx->matched;
+    for (int q = 0; q < kBuckets; ++q) a.list[q] = cur + (size_t)q * cap;
+    a.ctr = ctx->ctr + r;
+    a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
+    a.n_distinct = ctx->n_distinct;
+    a.tie_rank = ctx->tie_rank;
+    a.eid_of_x = ctx->eid_of_x;
+    if (mode == 0) launch_round<0>(ctx, a);
+    else if (mode == 1) launch_round<1>(ctx, a);
+    else launch_round<2>(ctx, a);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+static int enqueue_match_kernel(lmx_ctx *ctx, int r) {
+    const size_t cap = list_cap(ctx);
+    MatchArgs ma;
+    ma.vdeg = ctx->vdeg;
+    ma.cand_nbr = reinterpret_cast<const uint32_t *>(ctx->cand);
+    ma.cand_id = ma.cand_nbr + cap;
+    ma.matched = ctx->matched;
+    ma.mate = ctx->mate_target;
+    ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
+    ma.list = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    ma.next = ctx->lists[(r + 1) & 1];
+    ma.cap = cap;
+    ma.ebits = ctx->ebits;
+    ma.eid_of_x = ctx->layout == kDistinct ? ctx->eid_of_x : nullptr;
+    ma.lo = (uint32_t)ctx->lo;
+    ma.nl = (uint32_t)ctx->n_local;
+    ma.remote_ok = ctx->remote_ok;
+    ma.ctr = ctx->ctr + r;
+    ma.ctr_next = ctx->ctr + r + 1;
+    lmx_match_kernel<<<ctx->match_blocks, kBlock, 0, ctx->stream>>>(ma);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+// The round loop of local_max_seq (matchers.py:87-119) on the device.
+// Leaves mate in `mate` (ctx->mate or the caller's device buffer) and the
+// matched edge-id bitmap in ctx->ebits.
+int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
+                   std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
+    stats.clear();
+    n_matched = 0;
+    ctx->timing.round_launches = 0;
+    ctx->timing.slot_reads = 0;
+    ctx->timing.round_kernel_ms = 0;
+    ctx->timing.match_kernel_ms = 0;
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    LMX_TRY(begin_match(ctx));
     // optional per-kernel timeline: tl[0] after init, then (after round r, after match r)
     int tl_used = 0;
     auto tl_mark = [&]() -> int {
@@ -752,12 +892,6 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_CUDA(ctx, cudaEventRecord(ctx->tl_events[tl_used++], ctx->stream));
         return LMX_OK;
     };
-    if (n > 0) {
-        lmx_init_kernel<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(n, ctx->deg0, ctx->vdeg, ctx->mate_target,
-                                                                     ctx->matched);
-        LMX_CUDA(ctx, cudaGetLastError());
-        ctx->timing.round_launches += 1;
-    }
     LMX_TRY(tl_mark());
     int r = 0;
     int n_rounds = -1;
@@ -766,48 +900,10 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_TRY(ensure_ctr(ctx, r + batch + 1));
         const int r0 = r;
         for (int b = 0; b < batch; ++b, ++r) {
-            const int mode = r == 0 ? 0 : (r == 1 ? 1 : 2);
-            const uint32_t *cur = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
-            uint32_t *nxt = ctx->lists[(r + 1) & 1];
-            RoundArgs a;
-            a.vbeg = ctx->vbeg;
-            a.vdeg = ctx->vdeg;
-            a.cand_nbr = reinterpret_cast<uint32_t *>(ctx->cand);
-            a.cand_id = a.cand_nbr + cap;
-            a.ids0 = ctx->ids0;
-            a.wk0 = ctx->wk0;
-            a.ids1 = ctx->ids1;
-            a.wk1 = ctx->wk1;
-            a.matched = ctx->matched;
-            for (int q = 0; q < kBuckets; ++q) a.list[q] = cur + (size_t)q * cap;
-            a.ctr = ctx->ctr + r;
-            a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
-            a.n_distinct = ctx->n_distinct;
-            a.tie_rank = ctx->tie_rank;
-            a.eid_of_x = ctx->eid_of_x;
-            if (mode == 0) launch_round<0>(ctx, a);
-            else if (mode == 1) launch_round<1>(ctx, a);
-            else launch_round<2>(ctx, a);
-            LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(enqueue_round_kernel(ctx, r, seed_masked, rerandomize));
             LMX_TRY(tl_mark());
-            MatchArgs ma;
-            ma.vdeg = ctx->vdeg;
-            ma.cand_nbr = a.cand_nbr;
-            ma.cand_id = a.cand_id;
-            ma.matched = ctx->matched;
-            ma.mate = ctx->mate_target;
-            ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
-            ma.list = cur;
-            ma.next = nxt;
-            ma.cap = cap;
-            ma.ebits = ctx->ebits;
-            ma.eid_of_x = ctx->layout == kDistinct ? ctx->eid_of_x : nullptr;
-            ma.ctr = ctx->ctr + r;
-            ma.ctr_next = ctx->ctr + r + 1;
-            lmx_match_kernel<<<ctx->match_blocks, kBlock, 0, ctx->stream>>>(ma);
-            LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(enqueue_match_kernel(ctx, r));
             LMX_TRY(tl_mark());
-            ctx->timing.round_launches += 2;
         }
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r0, ctx->ctr + r0, sizeof(RoundCtr) * (size_t)batch,
                                       cudaMemcpyDeviceToHost, ctx->stream));
@@ -849,6 +945,117 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         ctx->timing.slot_reads += (int64_t)c.slot_reads;
     }
     n_matched = total_matched_v / 2;
+    return LMX_OK;
+}
+
+// ---- stepped protocol of the 1D-partitioned engine (bsp.py:101-205) --------
+// Per round, driven by the host (paper_1302_4587_b200/dist.py):
+//   round kernel -> propose (candidate records for remote partners, exchange A)
+//   -> [all-to-all-v] -> accept -> match (local + confirmed remote pairs)
+//   -> [all-gather of the owned matched-bitmap words, exchange B]
+//   -> [all-reduce of (live slots, matched vertices)].
+
+int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
+    ctx->timing.round_launches = 0;
+    ctx->dist_round = 0;
+    ctx->dist_seed = seed_masked;
+    ctx->dist_rr = rerandomize;
+    ctx->mate_target = ctx->mate;
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, (size_t)std::max<int64_t>(ctx->n_local, 1) * 4, ctx->stream));
+    LMX_TRY(begin_match(ctx));
+    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return LMX_OK;
+}
+
+int lmx_dist_round_impl(lmx_ctx *ctx) {
+    LMX_TRY(ensure_ctr(ctx, ctx->dist_round + 2));
+    return enqueue_round_kernel(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
+}
+
+int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
+    const int p = ctx->dist_p;
+    const int r = ctx->dist_round;
+    const size_t cap = list_cap(ctx);
+    const size_t need = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    if (ctx->send_cap < need) {
+        if (ctx->send) cudaFree(ctx->send);
+        ctx->send = nullptr;
+        LMX_CUDA(ctx, cudaMalloc(&ctx->send, need * sizeof(uint2)));
+        ctx->send_cap = need;
+    }
+    if (!ctx->send_cnt) LMX_CUDA(ctx, cudaMalloc(&ctx->send_cnt, 2 * 64 * sizeof(uint32_t)));
+    unsigned long long *bnd = nullptr;
+    LMX_CUDA(ctx, cudaMalloc(&bnd, (size_t)(p + 1) * 8));
+    std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
+    LMX_CUDA(ctx, cudaMemcpyAsync(bnd, hb.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 2 * 64 * sizeof(uint32_t), ctx->stream));
+    ProposeArgs pa;
+    pa.vdeg = ctx->vdeg;
+    pa.cand_nbr = reinterpret_cast<const uint32_t *>(ctx->cand);
+    pa.cand_id = pa.cand_nbr + cap;
+    pa.list = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    pa.cap = cap;
+    pa.ctr = ctx->ctr + r;
+    pa.eid_of_x = ctx->layout == kDistinct ? ctx->eid_of_x : nullptr;
+    pa.bounds = bnd;
+    pa.p = p;
+    pa.lo = (uint32_t)ctx->lo;
+    pa.nl = (uint32_t)ctx->n_local;
+    pa.cnt = ctx->send_cnt;
+    pa.cursor = ctx->send_cnt + 64;
+    pa.out = ctx->send;
+    pa.pass = 0;
+    lmx_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
+    LMX_CUDA(ctx, cudaGetLastError());
+    uint32_t hc[64];
+    LMX_CUDA(ctx, cudaMemcpyAsync(hc, ctx->send_cnt, (size_t)p * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    uint32_t off[65];
+    off[0] = 0;
+    for (int k = 0; k < p; ++k) off[k + 1] = off[k] + hc[k];
+    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->send_cnt + 64, off, (size_t)p * 4, cudaMemcpyHostToDevice, ctx->stream));
+    pa.pass = 1;
+    lmx_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
+    LMX_CUDA(ctx, cudaGetLastError());
+    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(bnd);
+    for (int k = 0; k < p; ++k) counts[k] = hc[k];
+    ctx->timing.round_launches += 2;
+    return LMX_OK;
+}
+
+int lmx_dist_recv_impl(lmx_ctx *ctx, int64_t count, void **ptr) {
+    const size_t need = (size_t)std::max<int64_t>(count, 1);
+    if (ctx->recv_cap < need) {
+        if (ctx->recv) cudaFree(ctx->recv);
+        ctx->recv = nullptr;
+        LMX_CUDA(ctx, cudaMalloc(&ctx->recv, need * sizeof(uint2)));
+        ctx->recv_cap = need;
+    }
+    *ptr = ctx->recv;
+    return LMX_OK;
+}
+
+int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count) {
+    if (count <= 0) return LMX_OK;
+    const size_t cap = list_cap(ctx);
+    lmx_accept_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
+        ctx->recv, (unsigned long long)count, ctx->vdeg, reinterpret_cast<const uint32_t *>(ctx->cand) + cap,
+        ctx->layout == kDistinct ? ctx->eid_of_x : nullptr, (uint32_t)ctx->lo, ctx->remote_ok);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+int lmx_dist_match_impl(lmx_ctx *ctx, int64_t *live_slots, int64_t *matched_v) {
+    const int r = ctx->dist_round;
+    LMX_TRY(enqueue_match_kernel(ctx, r));
+    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r, ctx->ctr + r, sizeof(RoundCtr), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *live_slots = (int64_t)ctx->ctr_host[r].live_slots;
+    *matched_v = (int64_t)ctx->ctr_host[r].matched_v;
+    ctx->dist_round = r + 1;
     return LMX_OK;
 }
 

@@ -63,7 +63,9 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->lists[0], (void **)&ctx->lists[1],    (void **)&ctx->bins0,
                      (void **)&ctx->mids,     (void **)&ctx->ebits,       (void **)&ctx->ebits_off,
                      (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
-                     (void **)&ctx->tie_rank, (void **)&ctx->oldid};
+                     (void **)&ctx->tie_rank, (void **)&ctx->oldid,
+                     (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
+                     (void **)&ctx->send_cnt};
     for (void **p : ptrs) {
         if (*p) cudaFree(*p);
         *p = nullptr;
@@ -73,6 +75,8 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
+    ctx->send_cap = ctx->recv_cap = 0;
+    ctx->n_local = ctx->slots_local = 0;
     for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = 0;
     ctx->sort_tmp_bytes = 0;
 }
@@ -118,8 +122,10 @@ __global__ void k_widen_deg(const uint32_t *deg, unsigned long long *out, unsign
         out[i] = i < n ? deg[i] : 0ULL;
 }
 
+// Slot records of the owned vertices [lo, hi): owner-local offsets, global nbr ids.
 __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long long m,
-                          const unsigned long long *vbeg, const uint32_t *newid, uint32_t *fill, uint2 *ids) {
+                          const unsigned long long *vbeg, const uint32_t *newid, unsigned long long lo,
+                          unsigned long long hi, uint32_t *fill, uint2 *ids) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += stride) {
@@ -128,10 +134,46 @@ __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long 
             a = newid[a];
             b = newid[b];
         }
-        const unsigned long long pa = vbeg[a] + atomicAdd(fill + a, 1u);
-        const unsigned long long pb = vbeg[b] + atomicAdd(fill + b, 1u);
-        ids[pa] = make_uint2(b, (uint32_t)e);
-        ids[pb] = make_uint2(a, (uint32_t)e);
+        if (a >= lo && a < hi) {
+            const unsigned long long pa = vbeg[a - lo] + atomicAdd(fill + (a - lo), 1u);
+            ids[pa] = make_uint2(b, (uint32_t)e);
+        }
+        if (b >= lo && b < hi) {
+            const unsigned long long pb = vbeg[b - lo] + atomicAdd(fill + (b - lo), 1u);
+            ids[pb] = make_uint2(a, (uint32_t)e);
+        }
+    }
+}
+
+// Partition cut points: first vertex whose slot offset reaches k * 2m / p,
+// rounded to a multiple of 32 and made non-decreasing.
+__global__ void k_cuts(const unsigned long long *vbeg, unsigned long long n, int p, unsigned long long *cuts) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long two_m = vbeg[n];
+    cuts[0] = 0;
+    for (int k = 1; k < p; ++k) {
+        const unsigned long long target = (unsigned long long)((double)k * (double)two_m / (double)p);
+        unsigned long long lo = 0, hi = n;   // lower_bound over vbeg[0..n]
+        while (lo < hi) {
+            const unsigned long long mid = (lo + hi) / 2;
+            if (vbeg[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        unsigned long long c = (lo + 16) / 32 * 32;
+        if (c > n) c = n;
+        if (c < cuts[k - 1]) c = cuts[k - 1];
+        cuts[k] = c;
+    }
+    cuts[p] = n;
+}
+
+__global__ void k_slice_local(const unsigned long long *vbeg, const uint32_t *deg, unsigned long long lo,
+                              unsigned long long nl, unsigned long long base, unsigned long long *vl,
+                              uint32_t *dl) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nl; i += stride) {
+        vl[i] = vbeg[lo + i] - base;
+        if (i < nl) dl[i] = deg[lo + i];
     }
 }
 
@@ -251,13 +293,10 @@ static int grid_for(lmx_ctx *ctx, unsigned long long work) {
 // Build vbeg / ids0 / wk0 / deg0 / hubs0 from ctx->eu, ev, w (K0).
 int lmx_setup_slots(lmx_ctx *ctx) {
     const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
-    const unsigned long long slots = 2 * m;
+    unsigned long long slots = 2 * m;   // becomes the owned slot count below
     cudaStream_t st = ctx->stream;
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4, "deg0"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (n + 1) * 8, "vbeg"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
-    LMX_TRY(lmx_alloc_match_state(ctx));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->deg0, 0, std::max<size_t>(n, 1) * 4, st));
     if (m) {
         k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
@@ -338,11 +377,58 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         lmx_free(ctx, &t, tmp);
         LMX_CUDA(ctx, e);
     }
+    // 1D vertex partition (bsp.py:60-98 idea: contiguous ranges with equal
+    // degree sums), cut points rounded to 32 so each rank owns whole words of
+    // the matched bitmap.  Single-GPU: one range [0, n).
+    ctx->lo = 0;
+    ctx->hi = n;
+    ctx->bounds.assign(2, 0);
+    ctx->bounds[1] = (int64_t)n;
+    if (ctx->dist_p > 1) {
+        const int p = ctx->dist_p;
+        unsigned long long *cuts = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&cuts, (size_t)(p + 1) * 8, "cuts"));
+        k_cuts<<<1, 64, 0, st>>>(ctx->vbeg, n, p, cuts);
+        std::vector<unsigned long long> hc((size_t)p + 1);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cuts, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        lmx_free(ctx, (void **)&cuts, (size_t)(p + 1) * 8);
+        LMX_CUDA(ctx, e);
+        ctx->bounds.assign(hc.begin(), hc.end());
+        ctx->lo = hc[(size_t)ctx->dist_rank];
+        ctx->hi = hc[(size_t)ctx->dist_rank + 1];
+    }
+    const unsigned long long lo = ctx->lo, nl = ctx->hi - ctx->lo;
+    ctx->n_local = (int64_t)nl;
+    unsigned long long base = 0, top = 0;
+    LMX_CUDA(ctx, cudaMemcpyAsync(&base, ctx->vbeg + lo, 8, cudaMemcpyDeviceToHost, st));
+    LMX_CUDA(ctx, cudaMemcpyAsync(&top, ctx->vbeg + ctx->hi, 8, cudaMemcpyDeviceToHost, st));
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    slots = top - base;
+    ctx->slots_local = (int64_t)slots;
+    if (ctx->dist_p > 1) {
+        // local segment offsets and degrees of the owned range
+        unsigned long long *vl = nullptr;
+        uint32_t *dl = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&vl, (nl + 1) * 8, "vbeg local"));
+        LMX_TRY(lmx_alloc(ctx, (void **)&dl, std::max<size_t>(nl, 1) * 4, "deg0 local"));
+        k_slice_local<<<grid_for(ctx, nl + 1), kBlock, 0, st>>>(ctx->vbeg, ctx->deg0, lo, nl, base, vl, dl);
+        LMX_CUDA(ctx, cudaGetLastError());
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        lmx_free(ctx, (void **)&ctx->vbeg, (n + 1) * 8);
+        lmx_free(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4);
+        ctx->vbeg = vl;
+        ctx->deg0 = dl;
+    }
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
+    LMX_TRY(lmx_alloc_match_state(ctx));
     if (m) {
-        // fill counters reuse vdeg
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, n * 4, st));
-        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, ctx->vdeg,
-                                                      ctx->ids0);
+        // fill counters reuse vdeg (local)
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
+        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
+                                                      ctx->vdeg, ctx->ids0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
     if (newid) {
@@ -438,22 +524,22 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         lmx_free(ctx, &tmp, tmp_bytes);
         if (rc != LMX_OK) return rc;
     }
-    // round-0 bucket lists (stable: ascending vertex id inside each bucket)
-    const size_t cap = std::max<size_t>(n, 1);
+    // round-0 bucket lists of the owned vertices (local indices, ascending)
+    const size_t cap = std::max<size_t>(nl, 1);
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * kBuckets, "bins0"));
     {
         unsigned long long *cnt = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8 * kBuckets, "bucket counts"));
         cub::CountingInputIterator<uint32_t> it(0);
         size_t tmp = 0;
-        LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->bins0, cnt, (long long)n,
+        LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->bins0, cnt, (long long)nl,
                                             InBucket{ctx->deg0, 0}, st));
         void *t = nullptr;
         LMX_TRY(lmx_alloc(ctx, &t, tmp, "select tmp"));
         cudaError_t e = cudaSuccess;
         for (int q = 0; q < kBuckets && e == cudaSuccess; ++q) {
             size_t tb = tmp;
-            e = cub::DeviceSelect::If(t, tb, it, ctx->bins0 + (size_t)q * cap, cnt + q, (long long)n,
+            e = cub::DeviceSelect::If(t, tb, it, ctx->bins0 + (size_t)q * cap, cnt + q, (long long)nl,
                                       InBucket{ctx->deg0, q}, st);
         }
         unsigned long long h[kBuckets] = {0, 0, 0, 0, 0};

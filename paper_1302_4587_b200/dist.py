@@ -1,0 +1,351 @@
+"""1D-partitioned local max over several GPUs (row (e) of SURVEY.md §8).
+
+Mirrors ``locmax.bsp.bsp_local_max(g, p, seed, rerandomize)``
+(``/root/reference/pkg/src/locmax/bsp.py:101-205``).  The reference
+simulates p workers in one process; here each worker is a liblmx context:
+* it owns one of p contiguous vertex ranges with equal degree sums
+  (``bsp.py:60-98``; cuts rounded to 32 so a rank owns whole bitmap words);
+* it holds the slots of every edge incident to its range.
+
+Each round is driven by the host over a communicator:
+
+1. ``lmx_dist_round``: owned vertices raise candidates (superstep 1,
+   ``bsp.py:139-146``).
+2. Exchange A (barrier 1, ``bsp.py:148-167``): for every owned live vertex
+   whose candidate partner is remote, one record ``{partner, edge id}`` goes
+   to the partner's owner.  This is an all-to-all-v.  A vertex is matched
+   across the cut iff its owner *receives* the record of its own candidate
+   edge.
+3. ``lmx_dist_match``: local plus confirmed cross-rank matches; mate, matched
+   edges, and the next round's lists.
+4. Exchange B (barrier 2, ``bsp.py:169-170``): the owned words of the
+   matched bitmap are all-gathered.  Every rank then filters dead slots in
+   the next round.
+5. An all-reduce of (live slots, matched vertices) gives ``RoundStats`` and
+   termination.
+
+The matching equals the single-GPU one for every p, as ``bsp.py:113-115``
+promises.
+
+Communicators:
+
+* ``LocalComm``: p contexts in one process on one GPU, exchanging through
+  device copies.  This is the reference's own "logical workers" mode
+  (``bsp.py:13-16``).  It drives ``run_matcher(..., engine="b200-dist")``.
+  It also runs the multi-rank kernels on one GPU, sequentially and with no
+  kernel waiting on another.
+* ``TorchComm``: one process per GPU under ``torch.distributed`` (NCCL over
+  NVLink / NVSwitch; ``gloo`` works too), launched by torchrun.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from .engine import Engine, LMX_OK, _raise
+from .graph import Matching, PhaseTrace, RoundStats
+
+LMX_OPT_DIST_P = 4
+LMX_OPT_DIST_RANK = 5
+
+
+def _bind(lib):
+    if getattr(lib, "_dist_bound", False):
+        return
+    p, i64, u64, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+    sig = {
+        "lmx_dist_bounds": (c_int, [p, p]),
+        "lmx_dist_begin": (c_int, [p, u64, c_int]),
+        "lmx_dist_round": (c_int, [p]),
+        "lmx_dist_propose": (c_int, [p, p, ctypes.POINTER(p)]),
+        "lmx_dist_recv_buffer": (c_int, [p, i64, ctypes.POINTER(p)]),
+        "lmx_dist_accept": (c_int, [p, i64]),
+        "lmx_dist_match": (c_int, [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "lmx_dist_state": (c_int, [p, ctypes.POINTER(p), ctypes.POINTER(p), ctypes.POINTER(p),
+                                   ctypes.POINTER(p)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    lib._dist_bound = True
+
+
+class _CudaBuf:
+    """Zero-copy torch view of device memory owned by liblmx."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _view(ptr: int, shape, typestr: str, device):
+    import torch
+    if int(np.prod(shape)) == 0:
+        dt = {"<i4": torch.int32, "<i8": torch.int64}[typestr]
+        return torch.empty(shape, dtype=dt, device=device)
+    return torch.as_tensor(_CudaBuf(ptr, shape, typestr), device=device)
+
+
+class DistRank:
+    """One partition: a liblmx context loaded with LMX_OPT_DIST_P / RANK."""
+
+    def __init__(self, g, p: int, rank: int, device: int = 0, stream=None):
+        import torch
+        self.eng = Engine(device)
+        self.lib = self.eng._lib
+        _bind(self.lib)
+        self.p, self.rank, self.device = p, rank, torch.device("cuda", device)
+        if stream is not None:
+            self.eng.set_stream(stream)
+        self._opt(LMX_OPT_DIST_P, p)
+        self._opt(LMX_OPT_DIST_RANK, rank)
+        self.eng.load_graph(g)
+        self.n, self.m = self.eng.graph_size()
+        b = np.zeros(p + 1, dtype=np.int64)
+        self._chk(self.lib.lmx_dist_bounds(self.eng._h, b.ctypes.data), "lmx_dist_bounds")
+        self.bounds = b
+        bm, mate, eb, st = (ctypes.c_void_p() for _ in range(4))
+        self._chk(self.lib.lmx_dist_state(self.eng._h, ctypes.byref(bm), ctypes.byref(mate), ctypes.byref(eb),
+                                          ctypes.byref(st)), "lmx_dist_state")
+        self.words = (self.n + 31) // 32
+        self.bitmap = _view(bm.value, (max(self.words, 1),), "<i4", self.device)
+        self.mate = _view(mate.value, (max(self.n, 1),), "<i8", self.device)
+        self.ebits = _view(eb.value, ((max(self.m, 1) + 31) // 32,), "<i4", self.device)
+
+    def _opt(self, opt, val):
+        self._chk(self.lib.lmx_set_option(self.eng._h, opt, val), "lmx_set_option")
+
+    def _chk(self, rc, what):
+        if rc != LMX_OK:
+            _raise(rc, f"{what}: " + self.lib.lmx_last_error(self.eng._h).decode())
+
+    def begin(self, seed: int, rerandomize: bool):
+        self._chk(self.lib.lmx_dist_begin(self.eng._h, seed & ((1 << 64) - 1), int(rerandomize)), "lmx_dist_begin")
+
+    def round(self):
+        self._chk(self.lib.lmx_dist_round(self.eng._h), "lmx_dist_round")
+
+    def propose(self):
+        counts = np.zeros(self.p, dtype=np.int64)
+        ptr = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_propose(self.eng._h, counts.ctypes.data, ctypes.byref(ptr)), "lmx_dist_propose")
+        total = int(counts.sum())
+        send = _view(ptr.value or 0, (total, 2), "<i4", self.device)
+        return send, counts
+
+    def recv_buffer(self, count: int):
+        ptr = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_recv_buffer(self.eng._h, int(count), ctypes.byref(ptr)), "lmx_dist_recv_buffer")
+        return _view(ptr.value, (int(count), 2), "<i4", self.device)
+
+    def accept(self, count: int):
+        self._chk(self.lib.lmx_dist_accept(self.eng._h, int(count)), "lmx_dist_accept")
+
+    def match(self):
+        live = ctypes.c_int64()
+        mv = ctypes.c_int64()
+        self._chk(self.lib.lmx_dist_match(self.eng._h, ctypes.byref(live), ctypes.byref(mv)), "lmx_dist_match")
+        return int(live.value), int(mv.value)
+
+    def word_range(self, k: int):
+        return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
+
+    def close(self):
+        self.eng.close()
+
+
+class LocalComm:
+    """All p partitions in this process (one GPU): collectives are device copies."""
+
+    def __init__(self, p: int):
+        self.p = p
+
+    def alltoallv(self, ranks, sends):
+        import torch
+        recvs = []
+        for dst in range(self.p):
+            parts = []
+            for src in range(self.p):
+                send, counts = sends[src]
+                off = int(counts[:dst].sum())
+                parts.append(send[off: off + int(counts[dst])])
+            total = sum(int(x.shape[0]) for x in parts)
+            buf = ranks[dst].recv_buffer(total)
+            if total:
+                buf.copy_(torch.cat(parts, dim=0))
+            recvs.append(total)
+        return recvs
+
+    def allgather_bitmap(self, ranks):
+        for src in range(self.p):
+            w0, w1 = ranks[src].word_range(src)
+            if w1 <= w0:
+                continue
+            seg = ranks[src].bitmap[w0:w1]
+            for dst in range(self.p):
+                if dst != src:
+                    ranks[dst].bitmap[w0:w1].copy_(seg)
+
+    def allreduce_sum(self, values):
+        return [sum(col) for col in zip(*values)]
+
+    def gather_outputs(self, ranks):
+        import torch
+        mate = ranks[0].mate.clone()
+        ebits = ranks[0].ebits.clone()
+        for r in ranks[1:]:
+            mate = torch.maximum(mate, r.mate)
+            ebits = ebits | r.ebits
+        return mate, ebits
+
+
+class TorchComm:
+    """One partition per process under torch.distributed (nccl or gloo)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.p = dist.get_world_size()
+        self.rank = dist.get_rank()
+
+    def alltoallv(self, ranks, sends):
+        import torch
+        (me,), ((send, counts),) = ranks, sends
+        dev = me.device
+        sc = torch.as_tensor(counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc)
+        rcounts = rc.tolist()
+        total = int(sum(rcounts))
+        recv = me.recv_buffer(total)
+        flat_in = send.reshape(-1) if send.numel() else torch.empty(0, dtype=torch.int32, device=dev)
+        flat_out = recv.reshape(-1) if total else torch.empty(0, dtype=torch.int32, device=dev)
+        self.dist.all_to_all_single(flat_out, flat_in, [2 * c for c in rcounts], [2 * int(c) for c in counts])
+        return [total]
+
+    def allgather_bitmap(self, ranks):
+        import torch
+        (me,) = ranks
+        spans = [me.word_range(k) for k in range(self.p)]
+        width = max(max(w1 - w0 for w0, w1 in spans), 1)
+        w0, w1 = spans[self.rank]
+        row = torch.zeros(width, dtype=torch.int32, device=me.device)
+        if w1 > w0:
+            row[: w1 - w0].copy_(me.bitmap[w0:w1])
+        out = torch.empty(self.p * width, dtype=torch.int32, device=me.device)
+        self.dist.all_gather_into_tensor(out, row)
+        for k, (a, b) in enumerate(spans):
+            if k != self.rank and b > a:
+                me.bitmap[a:b].copy_(out[k * width: k * width + (b - a)])
+
+    def allreduce_sum(self, values):
+        import torch
+        (vals,) = values
+        t = torch.tensor(vals, dtype=torch.int64, device=self._dev)
+        self.dist.all_reduce(t)
+        return [int(x) for x in t.tolist()]
+
+    def gather_outputs(self, ranks):
+        (me,) = ranks
+        mate = me.mate.clone()
+        ebits = me.ebits.clone()
+        self.dist.all_reduce(mate, op=self.dist.ReduceOp.MAX)
+        self.dist.all_reduce(ebits)   # disjoint bit sets: sum == or
+        return mate, ebits
+
+    def bind_device(self, device):
+        self._dev = device
+
+
+def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int | None = None):
+    """Drive the stepped protocol on `ranks` (all local partitions) to completion.
+
+    Returns (RoundStats list, per-round exchange-A record counts).
+    """
+    for r in ranks:
+        r.begin(seed, rerandomize)
+    before = []
+    matched = []
+    records = []
+    while True:
+        for r in ranks:
+            r.round()
+        sends = [r.propose() for r in ranks]
+        records.append(int(sum(int(c.sum()) for _, c in sends)))
+        recv_counts = comm.alltoallv(ranks, sends)
+        for r, cnt in zip(ranks, recv_counts):
+            r.accept(cnt)
+        local = [r.match() for r in ranks]
+        comm.allgather_bitmap(ranks)
+        live, mv = comm.allreduce_sum(local)
+        if live == 0:
+            records.pop()
+            break
+        if live % 2 or mv % 2:
+            raise RuntimeError("internal: odd global slot or matched-vertex count")
+        before.append(live // 2)
+        matched.append(mv // 2)
+        if max_rounds is not None and len(before) > max_rounds:
+            raise RuntimeError("round limit exceeded")
+    stats = []
+    for i, b in enumerate(before):
+        nxt = before[i + 1] if i + 1 < len(before) else 0
+        stats.append(RoundStats(b, matched[i], b - nxt))
+    return stats, records
+
+
+def _unpack_ids(ebits, m: int) -> np.ndarray:
+    words = ebits.cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:m]
+    return np.nonzero(bits)[0].astype(np.int64)
+
+
+def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int = 0):
+    """Drop-in for ``bsp_local_max(g, p, seed, rerandomize)`` (bsp.py:101-205):
+    p partitions emulated in this process on one B200.  ``trace.messages``
+    holds the exchange-A record count per round (cf. ``RoundMessages``)."""
+    import torch
+    t0 = time.perf_counter()
+    if p < 1:
+        raise ValueError("p must be >= 1")
+    if p > max(g.num_vertices, 1):
+        raise ValueError(f"p={p} exceeds the vertex count {g.num_vertices}")
+    torch.cuda.set_device(device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    ranks = [DistRank(g, p, k, device, stream) for k in range(p)]
+    try:
+        comm = LocalComm(p)
+        stats, records = run_rounds(ranks, comm, seed, rerandomize)
+        mate, ebits = comm.gather_outputs(ranks)
+        ids = _unpack_ids(ebits, ranks[0].m)
+        mate_h = mate.cpu().numpy()[: g.num_vertices].copy()
+    finally:
+        for r in ranks:
+            r.close()
+    trace = PhaseTrace(rounds=stats, messages=records)
+    trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+    return Matching(ids, mate_h), trace
+
+
+def local_max_torchdist(g, seed: int, rerandomize: bool = True):
+    """One partition per torch.distributed rank (launch with torchrun, NCCL)."""
+    import torch
+    import torch.distributed as dist
+    comm = TorchComm()
+    dev = torch.cuda.current_device()
+    comm.bind_device(torch.device("cuda", dev))
+    me = DistRank(g, comm.p, comm.rank, dev, torch.cuda.current_stream().cuda_stream)
+    try:
+        stats, records = run_rounds([me], comm, seed, rerandomize)
+        mate, ebits = comm.gather_outputs([me])
+        ids = _unpack_ids(ebits, me.m) if comm.rank == 0 else None
+        mate_h = mate.cpu().numpy()[: g.num_vertices].copy() if comm.rank == 0 else None
+    finally:
+        me.close()
+    dist.barrier()
+    trace = PhaseTrace(rounds=stats, messages=records)
+    return (Matching(ids, mate_h) if comm.rank == 0 else None), trace

@@ -33,6 +33,8 @@ EXPORTED_SYMBOLS = (
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
+    "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
+    "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state",
 )
 LMX_OPT_KERNEL_TIMING = 1
 LMX_OPT_LAYOUT = 2

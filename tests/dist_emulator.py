@@ -1,0 +1,124 @@
+"""CPU emulation of one liblmx distributed partition -- TEST INFRASTRUCTURE ONLY.
+
+Implements the per-rank interface ``paper_1302_4587_b200.dist.run_rounds``
+drives (begin / round / propose / recv_buffer / accept / match, plus the
+``bitmap`` / ``mate`` / ``ebits`` tensors and ``word_range``), restating the
+device kernels' semantics in numpy on CPU tensors.  It exists so the
+multi-process transport (``TorchComm`` over gloo, world_size 2) and the
+round protocol can be tested on a machine without a GPU.  The product path
+never uses it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import oracle as O
+
+
+def partition_bounds(n: int, eu, ev, p: int) -> np.ndarray:
+    """Same rule as csrc/lmx_setup.cu:k_cuts (equal degree sums, cuts rounded to 32)."""
+    deg = np.bincount(np.concatenate([eu, ev]), minlength=n).astype(np.int64)
+    vbeg = np.concatenate([[0], np.cumsum(deg)])
+    two_m = int(vbeg[-1])
+    cuts = [0]
+    for k in range(1, p):
+        target = int(float(k) * float(two_m) / float(p))
+        lo = int(np.searchsorted(vbeg, target, side="left"))
+        c = min((lo + 16) // 32 * 32, n)
+        c = max(c, cuts[-1])
+        cuts.append(c)
+    cuts.append(n)
+    return np.array(cuts, dtype=np.int64)
+
+
+class EmulatedRank:
+    def __init__(self, g, p: int, rank: int):
+        self.p, self.rank = p, rank
+        self.device = torch.device("cpu")
+        self.n, self.m = int(g.num_vertices), int(np.asarray(g.edge_u).size)
+        self.eu = np.asarray(g.edge_u, dtype=np.int64)
+        self.ev = np.asarray(g.edge_v, dtype=np.int64)
+        self.wb = O.weight_bits(np.asarray(g.edge_weight, dtype=np.float64))
+        self.bounds = partition_bounds(self.n, self.eu, self.ev, p)
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.words = (self.n + 31) // 32
+        self.bitmap = torch.zeros(max(self.words, 1), dtype=torch.int32)
+        self.mate = torch.full((max(self.n, 1),), -1, dtype=torch.int64)
+        self.ebits = torch.zeros((max(self.m, 1) + 31) // 32, dtype=torch.int32)
+
+    def word_range(self, k: int):
+        return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
+
+    def _owner(self, x: int) -> int:
+        return int(np.searchsorted(self.bounds, x, side="right") - 1)
+
+    def _is_matched(self, v: int) -> bool:
+        w = int(self.bitmap[v >> 5].item()) & 0xFFFFFFFF
+        return bool((w >> (v & 31)) & 1)
+
+    def begin(self, seed: int, rerandomize: bool):
+        self.seed, self.rr, self.r = seed, rerandomize, 0
+        self.adj = {}
+        for e in range(self.m):
+            for a, b in ((self.eu[e], self.ev[e]), (self.ev[e], self.eu[e])):
+                if self.lo <= a < self.hi:
+                    self.adj.setdefault(int(a), []).append((int(b), e))
+        self.bitmap.zero_()
+        self.mate.fill_(-1)
+        self.ebits.zero_()
+        self.cand = {}
+        self.remote_ok = set()
+
+    def round(self):
+        rs = O.round_seed(self.seed, self.r, self.rr)
+        self.cand = {}
+        self.live_slots = 0
+        for v, lst in self.adj.items():
+            if self._is_matched(v):
+                continue
+            lst = [(x, e) for (x, e) in lst if not self._is_matched(x)]
+            self.adj[v] = lst
+            self.live_slots += len(lst)
+            if lst:
+                best = max(lst, key=lambda t: (int(self.wb[t[1]]), int(O.edge_salts(rs, [t[1]])[0])))
+                self.cand[v] = best
+
+    def propose(self):
+        groups = [[] for _ in range(self.p)]
+        for v, (x, e) in self.cand.items():
+            if not (self.lo <= x < self.hi):
+                groups[self._owner(x)].append((x, e))
+        counts = np.array([len(gp) for gp in groups], dtype=np.int64)
+        flat = [rec for gp in groups for rec in gp]
+        send = torch.tensor(flat if flat else np.zeros((0, 2)), dtype=torch.int32).reshape(-1, 2)
+        return send, counts
+
+    def recv_buffer(self, count: int):
+        self.recv = torch.zeros((int(count), 2), dtype=torch.int32)
+        return self.recv
+
+    def accept(self, count: int):
+        self.remote_ok = set()
+        for x, e in self.recv[: int(count)].tolist():
+            if x in self.cand and self.cand[x][1] == e:
+                self.remote_ok.add(x)
+
+    def match(self):
+        mv = 0
+        words = self.bitmap.numpy().view(np.uint32)
+        eb = self.ebits.numpy().view(np.uint32)
+        for v, (x, e) in self.cand.items():
+            if self.lo <= x < self.hi:
+                mutual = x in self.cand and self.cand[x][1] == e
+            else:
+                mutual = v in self.remote_ok
+            if mutual:
+                words[v >> 5] |= np.uint32(1 << (v & 31))
+                self.mate[v] = x
+                mv += 1
+                if v < x:
+                    eb[e >> 5] |= np.uint32(1 << (e & 31))
+        self.r += 1
+        return self.live_slots, mv

@@ -1,0 +1,103 @@
+"""Multi-GPU (1D partition) path.
+
+* CPU: world_size-2 torch.distributed (gloo) run of the real transport
+  (``TorchComm``) and round protocol (``run_rounds``) over emulated partitions
+  (tests/dist_emulator.py), checked against the oracle.
+* GPU: ``local_max_dist`` (p liblmx partitions on one B200, the reference's
+  logical-worker mode, bsp.py:13-16) must equal the single-GPU engine and the
+  reference for every p (bsp.py:113-115; test_bsp.py:68-87).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, instance_graph, mate_digest, small_cases, small_runs
+from oracle import oracle as O
+
+
+def test_partition_bounds_rule():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dist_emulator import partition_bounds
+    n, eu, ev, w = O.gen_random(1 << 12, 4, 0)
+    for p in (1, 2, 3, 8):
+        b = partition_bounds(n, eu, ev, p)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        assert np.all(b[1:-1] % 32 == 0)
+        deg = np.bincount(np.concatenate([eu, ev]), minlength=n)
+        share = [deg[b[k]:b[k + 1]].sum() for k in range(p)]
+        assert max(share) <= 2 * eu.size / p + 32 * deg.max() + 1
+
+
+def test_gloo_world_size_2_matches_oracle():
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517",
+           os.path.join(ROOT, "tests", "dist_gloo_worker.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ok=True") == 8, out[-4000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+def test_dist_equals_single_gpu_small(golden_small, p):
+    from paper_1302_4587_b200 import Graph
+    from paper_1302_4587_b200.dist import local_max_dist
+    graphs = {gi: (n, built) for gi, n, _, built, _ in small_cases(golden_small)}
+    done = 0
+    for gi, seed, rr, mate, ids, rounds in small_runs(golden_small):
+        n, (eu, ev, w) = graphs[gi]
+        if n < p or gi % 7:   # a spread of cases; each run sets up p contexts
+            continue
+        matching, trace = local_max_dist(Graph(n, eu, ev, w), p, seed, rr)
+        assert np.array_equal(matching.mate, mate), (gi, seed, rr, p)
+        assert np.array_equal(matching.sorted_edge_ids(), ids), (gi, seed, rr, p)
+        assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == rounds
+        done += 1
+    assert done > 20
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("name", ["random-x16-a4-wunit-s0", "rgg-x16-euclidean-s0", "random-x12-a16-s5",
+                                  "delaunay_x10"])
+def test_dist_reference_instances(golden_instances, name, p):
+    from paper_1302_4587_b200 import Graph
+    from paper_1302_4587_b200.dist import local_max_dist
+    z = golden_instances
+    n, eu, ev, w = instance_graph(z, name)
+    matching, trace = local_max_dist(Graph(n, eu, ev, w), p, int(z[f"{name}/seed"]), bool(z[f"{name}/rerandomize"]))
+    assert mate_digest(matching.mate) == str(z[f"{name}/mate_digest"])
+    assert [[r.edges_before, r.edges_matched, r.edges_removed] for r in trace.rounds] == \
+        z[f"{name}/rounds"].tolist()
+    assert sum(trace.messages) > 0
+
+
+@pytest.mark.gpu
+def test_dist_rmat_skewed_equals_single(engine):
+    """RMAT (relabelled, hubs) split over 4 partitions equals the single-GPU run."""
+    from paper_1302_4587_b200.dist import local_max_dist
+    engine.gen_rmat(14, 16, seed=5)
+    g = engine.export_graph()
+    mate, ids, rounds = engine.match_raw(5, True)
+    matching, trace = local_max_dist(g, 4, 5, True)
+    assert np.array_equal(matching.mate, mate)
+    assert np.array_equal(matching.sorted_edge_ids(), ids)
+    assert trace.rounds == rounds
+
+
+@pytest.mark.gpu
+def test_run_matcher_dist_engine():
+    from paper_1302_4587_b200 import Graph, run_matcher
+    n, eu, ev, w = O.gen_random(1 << 10, 4, 2)
+    g = Graph(n, eu, ev, w)
+    a, _ = run_matcher(g, "localmax", 2, engine="b200")
+    b, _ = run_matcher(g, "localmax", 2, engine="b200-dist", p=3)
+    assert a == b
