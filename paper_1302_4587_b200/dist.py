@@ -93,7 +93,10 @@ def _view(ptr: int, shape, typestr: str, device):
 class DistRank:
     """One partition: a liblmx context loaded with LMX_OPT_DIST_P / RANK."""
 
-    def __init__(self, g, p: int, rank: int, device: int = 0, stream=None):
+    def __init__(self, g, p: int, rank: int, device: int = 0, stream=None, rmat: dict | None = None):
+        """Load partition `rank` of `p` from a host graph `g`, or, with
+        ``rmat=dict(scale=..., edge_factor=..., seed=...)``, from the device
+        RMAT generator (every rank generates the same graph and keeps its part)."""
         import torch
         self.eng = Engine(device)
         self.lib = self.eng._lib
@@ -103,7 +106,10 @@ class DistRank:
             self.eng.set_stream(stream)
         self._opt(LMX_OPT_DIST_P, p)
         self._opt(LMX_OPT_DIST_RANK, rank)
-        self.eng.load_graph(g)
+        if rmat is not None:
+            self.eng.gen_rmat(**rmat)
+        else:
+            self.eng.load_graph(g)
         self.n, self.m = self.eng.graph_size()
         b = np.zeros(p + 1, dtype=np.int64)
         self._chk(self.lib.lmx_dist_bounds(self.eng._h, b.ctypes.data), "lmx_dist_bounds")
