@@ -983,11 +983,15 @@ int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
         LMX_CUDA(ctx, cudaMalloc(&ctx->send, need * sizeof(uint2)));
         ctx->send_cap = need;
     }
-    if (!ctx->send_cnt) LMX_CUDA(ctx, cudaMalloc(&ctx->send_cnt, 2 * 64 * sizeof(uint32_t)));
+    // send_cnt block: [64] counts, [64] cursors, then the p + 1 bounds (u64), uploaded once per load
     unsigned long long *bnd = nullptr;
-    LMX_CUDA(ctx, cudaMalloc(&bnd, (size_t)(p + 1) * 8));
-    std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
-    LMX_CUDA(ctx, cudaMemcpyAsync(bnd, hb.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (!ctx->send_cnt) {
+        LMX_CUDA(ctx, cudaMalloc(&ctx->send_cnt, 2048));
+        std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
+        LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 512, hb.data(),
+                                      (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    bnd = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 512);
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 2 * 64 * sizeof(uint32_t), ctx->stream));
     ProposeArgs pa;
     pa.vdeg = ctx->vdeg;
@@ -1018,7 +1022,6 @@ int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
     lmx_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
     LMX_CUDA(ctx, cudaGetLastError());
     LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFree(bnd);
     for (int k = 0; k < p; ++k) counts[k] = hc[k];
     ctx->timing.round_launches += 2;
     return LMX_OK;
