@@ -91,7 +91,23 @@ struct RoundArgs {
     uint32_t n_distinct;       // DISTINCT layout: D
     const uint32_t *tie_rank;  // DISTINCT layout
     const uint32_t *eid_of_x;  // DISTINCT layout
+    int round;
 };
+
+#ifdef LMX_PHASE_TIMING   // profiling builds only: warp-cycles spent in each phase per round
+__device__ unsigned long long g_phase_cycles[64][5];
+#define PHASE_MARK(k)                                                                       \
+    do {                                                                                    \
+        const long long _t = clock64();                                                     \
+        if ((threadIdx.x & 31) == 0 && a.round < 64)                                        \
+            atomicAdd(&g_phase_cycles[a.round][k], (unsigned long long)(_t - phase_t0));    \
+        phase_t0 = _t;                                                                      \
+    } while (0)
+#else
+#define PHASE_MARK(k) \
+    do {              \
+    } while (0)
+#endif
 
 // Offer one live slot {nbr, id} (+ weight rank k for GENERAL) to the running max.
 template <int L>
@@ -303,6 +319,9 @@ __device__ __forceinline__ void team_single(const RoundArgs &a, unsigned long lo
     team_commit<MODE, L, TEAM, 1>(a, beg, &x, &k, &alive, &i, w, b, s_cnt);
 }
 
+// (A cp.async per-thread double buffer of the next pass was measured slower:
+// its 24 KB of shared memory per block squeezes the L1 that serves the
+// matched-bitmap lookups.  Register loads at full occupancy win.)
 template <int MODE, int L, int TEAM>
 __device__ __forceinline__ uint32_t team_vertex(const RoundArgs &a, unsigned long long beg, uint32_t d,
                                                 Best &b, uint32_t (*s_cnt)[kWarps]) {
@@ -367,6 +386,9 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
     if (any == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long live = 0, reads = 0;
+#ifdef LMX_PHASE_TIMING
+    long long phase_t0 = clock64();
+#endif
 
     // phase 1: buckets 4 then 3, one block per vertex
 #pragma unroll
@@ -395,6 +417,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         }
     }
 
+    PHASE_MARK(0);
     // The small-vertex phases below fetch the per-vertex metadata (list entry,
     // live degree, segment start) of a whole grab at once, one vertex per
     // lane, and broadcast it: the list -> vdeg/vbeg -> slots dependency chain
@@ -429,6 +452,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         }
     }
 
+    PHASE_MARK(1);
     // phase 3: bucket 1, 8 lanes per vertex, 16 vertices per grab
     for (;;) {
         uint32_t i0 = 0;
@@ -459,6 +483,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         }
     }
 
+    PHASE_MARK(2);
     // phase 4: bucket 0, thread per vertex, 128 vertices per grab
     for (;;) {
         uint32_t i0 = 0;
@@ -488,6 +513,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
         }
     }
 
+    PHASE_MARK(3);
     // block totals -> one atomic per block
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -830,6 +856,7 @@ static int enqueue_round_kernel(lmx_ctx *ctx, int r, uint64_t seed_masked, bool 
     a.matched = ctx->matched;
     for (int q = 0; q < kBuckets; ++q) a.list[q] = cur + (size_t)q * cap;
     a.ctr = ctx->ctr + r;
+    a.round = r;
     a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
     a.n_distinct = ctx->n_distinct;
     a.tie_rank = ctx->tie_rank;
@@ -1131,3 +1158,15 @@ int lmx_configure_grids(lmx_ctx *ctx) {
     ctx->match_blocks = ctx->num_sms * std::max(occ, 1);
     return LMX_OK;
 }
+
+#ifdef LMX_PHASE_TIMING
+extern "C" int lmx_debug_phase_cycles(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, lmx::g_phase_cycles, sizeof(unsigned long long) * 64 * 5);
+    if (reset) {
+        static unsigned long long zero[64 * 5] = {};
+        cudaMemcpyToSymbol(lmx::g_phase_cycles, zero, sizeof(zero));
+    }
+    return 0;
+}
+#endif
