@@ -188,6 +188,26 @@ int lmx_dist_match(lmx_ctx *ctx, int64_t *live_slots_out, int64_t *matched_v_out
  * recorded by this rank), and the context's cudaStream_t. */
 int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge_bits, void **stream);
 
+/*
+ * Coarsening (config C4; the paper's graph-partitioning use, PAPER.md:32-35,
+ * 407-411; absent from the reference).  All pointers are device
+ * pointers; the caller sizes the outputs (m_coarse <= m, n_coarse <= n).
+ *   lmx_mesh_edges  side x side jittered-grid triangulation: (side-1)(3 side-1)
+ *                   unit-weight edges, vertex i*side+j (capacity of eu/ev/w)
+ *   lmx_ratings     r(e) = w(e)^2 / (c(u) c(v))
+ *   lmx_contract    matched pairs / unmatched vertices -> coarse vertices
+ *                   (ascending smallest member), node weights summed, parallel
+ *                   edges merged by summed weight in ascending (min, max) order
+ */
+int lmx_mesh_edges(lmx_ctx *ctx, int64_t side, uint64_t seed, int64_t *edge_u, int64_t *edge_v,
+                   double *edge_weight, int64_t *m_out);
+int lmx_ratings(lmx_ctx *ctx, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
+                const double *edge_weight, const double *node_weight, double *rating_out);
+int lmx_contract(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
+                 const double *edge_weight, const double *node_weight, const int64_t *mate,
+                 int64_t *coarse_id_out, int64_t *n_out, int64_t *m_out, int64_t *coarse_u,
+                 int64_t *coarse_v, double *coarse_w, double *coarse_c);
+
 /* Device memory in use by the context (bytes). */
 int64_t lmx_device_bytes(const lmx_ctx *ctx);
 

@@ -451,3 +451,83 @@ def build_graph_vec(u, v, w, num_vertices=None):
     eo = np.argsort(first, kind="stable")
     kept = kept[eo]
     return n, u[kept], v[kept], w[kept]
+
+
+# ---------------------------------------------------------------- coarsening (config C4, new)
+
+_MESH_TAG = 0x4D4553485F444941
+
+
+def mesh_edges(side: int, seed: int = 0):
+    """Restatement of csrc/lmx_coarsen.cu:k_mesh (jittered-grid triangulation)."""
+    s = side
+    n = s * s
+    v = np.arange(n, dtype=np.int64)
+    i, j = v // s, v % s
+    sm = _mix64_int((seed & _UINT64_MASK) ^ _MESH_TAG)
+    main = (mix64(np.uint64(sm) ^ v.astype(np.uint64)) & np.uint64(1)).astype(bool)
+    us, vs = [], []
+    right = j + 1 < s
+    down = i + 1 < s
+    diag = right & down
+    cnt = right.astype(np.int64) + down + diag
+    off = np.concatenate([[0], np.cumsum(cnt)])
+    m = int(off[-1])
+    eu = np.empty(m, dtype=np.int64)
+    ev = np.empty(m, dtype=np.int64)
+    pos = off[:-1].copy()
+    eu[pos[right]] = v[right]
+    ev[pos[right]] = v[right] + 1
+    pos += right
+    eu[pos[down]] = v[down]
+    ev[pos[down]] = v[down] + s
+    pos += down
+    a = np.where(main, v, v + 1)
+    b = np.where(main, v + s + 1, v + s)
+    eu[pos[diag]] = a[diag]
+    ev[pos[diag]] = b[diag]
+    return n, eu, ev, np.ones(m, dtype=np.float64)
+
+
+def ratings(eu, ev, w, c):
+    """Edge rating w(e)^2 / (c(u) c(v)) (the coarsening match weight)."""
+    w = np.asarray(w, dtype=np.float64)
+    return (w * w) / (c[eu] * c[ev])
+
+
+def contract(n, eu, ev, w, c, mate):
+    """Contraction rules of csrc/lmx_coarsen.cu: coarse ids by ascending
+    representative (unmatched, or the smaller matched endpoint), summed node
+    weights, parallel edges merged by summed weight in ascending (min, max)
+    coarse-pair order."""
+    v = np.arange(n, dtype=np.int64)
+    rep_flag = (mate < 0) | (v < mate)
+    scan = np.concatenate([[0], np.cumsum(rep_flag)])
+    rep = np.where(rep_flag, v, mate)
+    cid = scan[rep]
+    nc = int(scan[-1])
+    cc = np.bincount(cid, weights=c, minlength=nc)
+    a, b = cid[eu], cid[ev]
+    keep = a != b
+    lo = np.minimum(a, b)[keep]
+    hi = np.maximum(a, b)[keep]
+    key = lo * np.int64(max(nc, 1)) + hi
+    uk, inv = np.unique(key, return_inverse=True)
+    cw = np.bincount(inv, weights=np.asarray(w, dtype=np.float64)[keep], minlength=uk.size)
+    return nc, uk // max(nc, 1), uk % max(nc, 1), cw, cc, cid
+
+
+def coarsen_levels(n, eu, ev, w, seed=0, min_n=1024, min_shrink=0.05, max_levels=64):
+    """Reference pipeline for the C4 tests: per level (n, m, mate, matched ids, rounds)."""
+    c = np.ones(n, dtype=np.float64)
+    levels = []
+    for lvl in range(max_levels):
+        r = ratings(eu, ev, w, c)
+        res = c_local_max(n, eu, ev, r, seed + lvl, True)
+        levels.append((n, eu.size, res))
+        nc, eu, ev, w, c, _ = contract(n, eu, ev, w, c, res.mate)
+        if nc < min_n or (n - nc) < min_shrink * n:
+            levels.append((nc, eu.size, None))
+            break
+        n = nc
+    return levels

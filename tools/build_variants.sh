@@ -20,7 +20,7 @@ for spec in "$@"; do
   ( nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $flags -I$CSRC \
       -c $src -o /tmp/var_$name.o -Xptxas -v 2> /tmp/var_$name.ptxas &&
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/build/variants/liblmx_$name.so \
-      /tmp/var_$name.o $OBJ/lmx_setup.o $OBJ/lmx_capi.o $OBJ/lmx_build.o -cudart static ) &
+      /tmp/var_$name.o $OBJ/lmx_setup.o $OBJ/lmx_capi.o $OBJ/lmx_build.o $OBJ/lmx_coarsen.o -cudart static ) &
 done
 wait
 ls $ROOT/build/variants
