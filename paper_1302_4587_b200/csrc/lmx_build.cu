@@ -261,16 +261,16 @@ static int build_from_raw(lmx_ctx *ctx, uint32_t *ru, uint32_t *rv, double *rw, 
     } while (0);
     cudaStreamSynchronize(st);
     // dev_bytes accounting of these temporaries is not tracked after lmx_free_graph; just free
-    if (key) cudaFree(key);
-    if (key2) cudaFree(key2);
-    if (idx) cudaFree(idx);
-    if (idx2) cudaFree(idx2);
-    if (flag) cudaFree(flag);
-    if (kept) cudaFree(kept);
-    if (tmp) cudaFree(tmp);
-    cudaFree(ru);
-    cudaFree(rv);
-    cudaFree(rw);
+    lmx_dfree(ctx, key);
+    lmx_dfree(ctx, key2);
+    lmx_dfree(ctx, idx);
+    lmx_dfree(ctx, idx2);
+    lmx_dfree(ctx, flag);
+    lmx_dfree(ctx, kept);
+    lmx_dfree(ctx, tmp);
+    lmx_dfree(ctx, ru);
+    lmx_dfree(ctx, rv);
+    lmx_dfree(ctx, rw);
     if (rc != LMX_OK) return rc;
     return lmx_setup_slots(ctx);
 }
@@ -311,11 +311,11 @@ int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double 
     uint32_t *ru = nullptr, *rv = nullptr;
     double *rw = nullptr;
     long long *lu = nullptr, *lv = nullptr;
-    LMX_CUDA(ctx, cudaMalloc(&ru, k * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rv, k * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rw, k * 8));
-    LMX_CUDA(ctx, cudaMalloc(&lu, k * 8));
-    LMX_CUDA(ctx, cudaMalloc(&lv, k * 8));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ru, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rv, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rw, k * 8));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&lu, k * 8));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&lv, k * 8));
     k_rmat_raw<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(p, k, ru, rv, rw);
     k_export<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(ru, rv, k, lu, lv);
     const cudaMemcpyKind kind = out_where == LMX_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -323,11 +323,11 @@ int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double 
     if (e == cudaSuccess) e = cudaMemcpyAsync(v_out, lv, k * 8, kind, ctx->stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(w_out, rw, k * 8, kind, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(ru);
-    cudaFree(rv);
-    cudaFree(rw);
-    cudaFree(lu);
-    cudaFree(lv);
+    lmx_dfree(ctx, ru);
+    lmx_dfree(ctx, rv);
+    lmx_dfree(ctx, rw);
+    lmx_dfree(ctx, lu);
+    lmx_dfree(ctx, lv);
     LMX_CUDA(ctx, e);
     return LMX_OK;
 }
@@ -343,13 +343,14 @@ int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, d
     lmx_free_graph(ctx);
     uint32_t *ru = nullptr, *rv = nullptr;
     double *rw = nullptr;
-    LMX_CUDA(ctx, cudaMalloc(&ru, k * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rv, k * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rw, k * 8));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ru, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rv, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rw, k * 8));
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     k_rmat_raw<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(p, k, ru, rv, rw);
     LMX_CUDA(ctx, cudaGetLastError());
     LMX_TRY(build_from_raw(ctx, ru, rv, rw, k, 1LL << scale));
+    lmx_flush_cache(ctx);   // the raw-build temporaries will not be reused
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
     float ms = 0.f;
@@ -372,10 +373,10 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
     uint32_t *ru = nullptr, *rv = nullptr;
     double *rw = nullptr;
     unsigned long long *flags = nullptr;   // [0] first bad, [1] max id + 1
-    LMX_CUDA(ctx, cudaMalloc(&ru, std::max<size_t>(kk, 1) * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rv, std::max<size_t>(kk, 1) * 4));
-    LMX_CUDA(ctx, cudaMalloc(&rw, std::max<size_t>(kk, 1) * 8));
-    LMX_CUDA(ctx, cudaMalloc(&flags, 16));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ru, std::max<size_t>(kk, 1) * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rv, std::max<size_t>(kk, 1) * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rw, std::max<size_t>(kk, 1) * 8));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&flags, 16));
     unsigned long long init[2] = {~0ULL, 0ULL};
     LMX_CUDA(ctx, cudaMemcpyAsync(flags, init, 16, cudaMemcpyHostToDevice, st));
     cudaError_t e = cudaSuccess;
@@ -389,9 +390,9 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
             const size_t cb = std::min<unsigned long long>(chunk, kk);
             long long *su = nullptr, *sv = nullptr;
             double *sw = nullptr;
-            LMX_CUDA(ctx, cudaMalloc(&su, cb * 8));
-            LMX_CUDA(ctx, cudaMalloc(&sv, cb * 8));
-            LMX_CUDA(ctx, cudaMalloc(&sw, cb * 8));
+            LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&su, cb * 8));
+            LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&sv, cb * 8));
+            LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&sw, cb * 8));
             for (unsigned long long off = 0; off < kk && e == cudaSuccess; off += chunk) {
                 const unsigned long long c = std::min(chunk, kk - off);
                 e = cudaMemcpyAsync(su, u + off, c * 8, cudaMemcpyHostToDevice, st);
@@ -404,25 +405,25 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
                 }
             }
             cudaStreamSynchronize(st);
-            cudaFree(su);
-            cudaFree(sv);
-            cudaFree(sw);
+            lmx_dfree(ctx, su);
+            lmx_dfree(ctx, sv);
+            lmx_dfree(ctx, sw);
         }
     }
     unsigned long long got[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(got, flags, 16, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(flags);
+    lmx_dfree(ctx, flags);
     if (e != cudaSuccess) {
-        cudaFree(ru);
-        cudaFree(rv);
-        cudaFree(rw);
+        lmx_dfree(ctx, ru);
+        lmx_dfree(ctx, rv);
+        lmx_dfree(ctx, rw);
         return lmx_cuda_check(ctx, e, "build_graph input");
     }
     if (got[0] != ~0ULL) {
-        cudaFree(ru);
-        cudaFree(rv);
-        cudaFree(rw);
+        lmx_dfree(ctx, ru);
+        lmx_dfree(ctx, rv);
+        lmx_dfree(ctx, rw);
         const unsigned long long pos = got[0];
         int64_t a = 0, b = 0;
         double x = 0;
@@ -448,7 +449,9 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
         return lmx_fail(ctx, LMX_EINVAL, buf);
     }
     const long long n = num_vertices >= 0 ? num_vertices : (long long)got[1];
-    return build_from_raw(ctx, ru, rv, rw, kk, n);
+    const int rc = build_from_raw(ctx, ru, rv, rw, kk, n);
+    lmx_flush_cache(ctx);   // the raw-build temporaries will not be reused
+    return rc;
 }
 
 int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edge_weight, int out_where) {
@@ -461,8 +464,8 @@ int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edg
         lu = (long long *)edge_u;
         lv = (long long *)edge_v;
     } else {
-        LMX_CUDA(ctx, cudaMalloc(&lu, m * 8));
-        LMX_CUDA(ctx, cudaMalloc(&lv, m * 8));
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&lu, m * 8));
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&lv, m * 8));
     }
     k_export<<<bgrid(ctx, m), kBlock, 0, ctx->stream>>>(ctx->eu, ctx->ev, m, lu, lv);
     cudaError_t e = cudaGetLastError();
@@ -474,8 +477,8 @@ int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edg
     if (e == cudaSuccess && edge_weight) e = cudaMemcpyAsync(edge_weight, ctx->w, m * 8, kind, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (out_where != LMX_DEVICE) {
-        cudaFree(lu);
-        cudaFree(lv);
+        lmx_dfree(ctx, lu);
+        lmx_dfree(ctx, lv);
     }
     LMX_CUDA(ctx, e);
     return LMX_OK;

@@ -64,6 +64,10 @@ void lmx_destroy(lmx_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     lmx_free_graph(ctx);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    lmx_flush_cache(ctx);
+    for (auto &kv : ctx->live) cudaFree(kv.first);   // anything still outstanding
+    ctx->live.clear();
     if (ctx->ctr) cudaFree(ctx->ctr);
     if (ctx->ctr_host) cudaFreeHost(ctx->ctr_host);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -164,12 +164,12 @@ int lmx_contract(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *eu, const in
     int rc = LMX_OK;
     cudaError_t e = cudaSuccess;
     do {
-        if ((e = cudaMalloc(&flag, (N + 1) * 8)) != cudaSuccess) break;
-        if ((e = cudaMalloc(&key, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
-        if ((e = cudaMalloc(&key2, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
-        if ((e = cudaMalloc(&ukey, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
-        if ((e = cudaMalloc(&w2, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
-        if ((e = cudaMalloc(&nu, 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&flag, (N + 1) * 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&key, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&key2, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&ukey, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&w2, std::max<unsigned long long>(M, 1) * 8)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&nu, 8)) != cudaSuccess) break;
         // coarse ids
         k_rep_flags<<<cgrid(ctx, N + 1), kBlock, 0, st>>>(N, (const long long *)mate, flag);
         size_t t1 = 0, t2 = 0, t3 = 0;
@@ -181,7 +181,7 @@ int lmx_contract(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *eu, const in
                                                (long long)M, st);
         if (e != cudaSuccess) break;
         tmp_bytes = std::max(t1, std::max(t2, t3));
-        if ((e = cudaMalloc(&tmp, tmp_bytes)) != cudaSuccess) break;
+        if ((e = lmx_dmalloc(ctx, (void **)&tmp, tmp_bytes)) != cudaSuccess) break;
         e = cub::DeviceScan::ExclusiveSum(tmp, t1, flag, flag, (long long)(N + 1), st);
         if (e != cudaSuccess) break;
         unsigned long long nc = 0;
@@ -215,13 +215,13 @@ int lmx_contract(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *eu, const in
         *n_out = (int64_t)nc;
         *m_out = (int64_t)nk;
     } while (0);
-    cudaFree(flag);
-    cudaFree(key);
-    cudaFree(key2);
-    cudaFree(ukey);
-    cudaFree(w2);
-    cudaFree(nu);
-    cudaFree(tmp);
+    lmx_dfree(ctx, flag);
+    lmx_dfree(ctx, key);
+    lmx_dfree(ctx, key2);
+    lmx_dfree(ctx, ukey);
+    lmx_dfree(ctx, w2);
+    lmx_dfree(ctx, nu);
+    lmx_dfree(ctx, tmp);
     if (e != cudaSuccess) rc = lmx_cuda_check(ctx, e, "lmx_contract");
     return rc;
 }

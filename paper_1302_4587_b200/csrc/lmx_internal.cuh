@@ -29,7 +29,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/lmx.h"
@@ -136,6 +138,10 @@ struct lmx_ctx {
     bool relabeled = false;                  // device vertex ids are degree-sorted
     uint32_t *oldid = nullptr;               // device id -> caller's vertex id
 
+    // device block cache (lmx_dmalloc / lmx_dfree)
+    std::unordered_map<void *, size_t> live;
+    std::multimap<size_t, void *> cache;
+
     // 1D vertex partition (multi-GPU; single GPU = one range [0, n)).  Per-vertex
     // arrays (vbeg, deg0, vdeg, cand, lists) are indexed by the local id v - lo;
     // slot neighbours, the matched bitmap and mate use global (device) ids.
@@ -156,6 +162,9 @@ struct lmx_ctx {
 int lmx_fail(lmx_ctx *ctx, int code, const std::string &msg);
 int lmx_cuda_check(lmx_ctx *ctx, cudaError_t e, const char *what);
 int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what);
+cudaError_t lmx_dmalloc(lmx_ctx *ctx, void **p, size_t bytes);   // stream-ordered pool
+void lmx_dfree(lmx_ctx *ctx, void *p);
+void lmx_flush_cache(lmx_ctx *ctx);
 void lmx_free(lmx_ctx *ctx, void **p, size_t bytes);
 void lmx_free_graph(lmx_ctx *ctx);
 int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w

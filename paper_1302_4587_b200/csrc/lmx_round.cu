@@ -1005,15 +1005,15 @@ int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
     const size_t cap = list_cap(ctx);
     const size_t need = (size_t)std::max<int64_t>(ctx->n_local, 1);
     if (ctx->send_cap < need) {
-        if (ctx->send) cudaFree(ctx->send);
+        lmx_dfree(ctx, ctx->send);
         ctx->send = nullptr;
-        LMX_CUDA(ctx, cudaMalloc(&ctx->send, need * sizeof(uint2)));
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send, need * sizeof(uint2)));
         ctx->send_cap = need;
     }
     // send_cnt block: [64] counts, [64] cursors, then the p + 1 bounds (u64), uploaded once per load
     unsigned long long *bnd = nullptr;
     if (!ctx->send_cnt) {
-        LMX_CUDA(ctx, cudaMalloc(&ctx->send_cnt, 2048));
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send_cnt, 2048));
         std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
         LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 512, hb.data(),
                                       (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -1057,9 +1057,9 @@ int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
 int lmx_dist_recv_impl(lmx_ctx *ctx, int64_t count, void **ptr) {
     const size_t need = (size_t)std::max<int64_t>(count, 1);
     if (ctx->recv_cap < need) {
-        if (ctx->recv) cudaFree(ctx->recv);
+        lmx_dfree(ctx, ctx->recv);
         ctx->recv = nullptr;
-        LMX_CUDA(ctx, cudaMalloc(&ctx->recv, need * sizeof(uint2)));
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->recv, need * sizeof(uint2)));
         ctx->recv_cap = need;
     }
     *ptr = ctx->recv;

@@ -15,7 +15,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "lmx_internal.cuh"
 
@@ -33,9 +36,56 @@ int lmx_cuda_check(lmx_ctx *ctx, cudaError_t e, const char *what) {
     return lmx_fail(ctx, LMX_ECUDA, m);
 }
 
+// Single choke point for device allocations, with a per-context block cache:
+// freed blocks are kept and handed out again to requests that fit (at most 2x
+// oversized), so reloading a graph of similar size does not pay cudaFree /
+// cudaMalloc of tens of GB again (measured: seconds of jitter per reload).  The
+// stream-ordered pool was also measured: growing it on first use cost seconds.
+// All work of a context is ordered on its stream, so reuse is safe.
+static size_t round_alloc(size_t bytes) {
+    const size_t g = bytes >= (64u << 20) ? (2u << 20) : 256;
+    return (std::max<size_t>(bytes, 16) + g - 1) / g * g;
+}
+
+void lmx_flush_cache(lmx_ctx *ctx) {
+    for (auto &kv : ctx->cache) cudaFree(kv.second);
+    ctx->cache.clear();
+}
+
+cudaError_t lmx_dmalloc(lmx_ctx *ctx, void **p, size_t bytes) {
+    bytes = round_alloc(bytes);
+    auto it = ctx->cache.lower_bound(bytes);
+    if (it != ctx->cache.end() && it->first <= 2 * bytes) {
+        *p = it->second;
+        ctx->live[*p] = it->first;
+        ctx->cache.erase(it);
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation && !ctx->cache.empty()) {
+        cudaGetLastError();
+        cudaStreamSynchronize(ctx->stream);
+        lmx_flush_cache(ctx);
+        e = cudaMalloc(p, bytes);
+    }
+    if (e == cudaSuccess) ctx->live[*p] = bytes;
+    return e;
+}
+
+void lmx_dfree(lmx_ctx *ctx, void *p) {
+    if (!p) return;
+    auto it = ctx->live.find(p);
+    if (it == ctx->live.end()) {   // not ours (should not happen): release directly
+        cudaFree(p);
+        return;
+    }
+    ctx->cache.emplace(it->second, p);
+    ctx->live.erase(it);
+}
+
 int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what) {
     if (*p) return LMX_OK;
-    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    cudaError_t e = lmx_dmalloc(ctx, p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         *p = nullptr;
@@ -49,7 +99,7 @@ int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what) {
 
 void lmx_free(lmx_ctx *ctx, void **p, size_t bytes) {
     if (*p) {
-        cudaFree(*p);
+        lmx_dfree(ctx, *p);
         ctx->dev_bytes -= (int64_t)bytes;
         *p = nullptr;
     }
@@ -67,7 +117,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
                      (void **)&ctx->send_cnt};
     for (void **p : ptrs) {
-        if (*p) cudaFree(*p);
+        lmx_dfree(ctx, *p);
         *p = nullptr;
     }
     ctx->dev_bytes = 0;
@@ -123,9 +173,12 @@ __global__ void k_widen_deg(const uint32_t *deg, unsigned long long *out, unsign
 }
 
 // Slot records of the owned vertices [lo, hi): owner-local offsets, global nbr ids.
+// The slot id is the edge id, or its weight key x (DISTINCT); GENERAL also
+// writes the weight rank per slot.  kofe = weight key of each edge (or null).
 __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long long m,
                           const unsigned long long *vbeg, const uint32_t *newid, unsigned long long lo,
-                          unsigned long long hi, uint32_t *fill, uint2 *ids) {
+                          unsigned long long hi, uint32_t *fill, uint2 *ids, const uint32_t *kofe, bool distinct,
+                          uint32_t *wk) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += stride) {
@@ -134,13 +187,17 @@ __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long 
             a = newid[a];
             b = newid[b];
         }
+        const uint32_t key = kofe ? kofe[e] : 0u;
+        const uint32_t id = distinct ? key : (uint32_t)e;
         if (a >= lo && a < hi) {
             const unsigned long long pa = vbeg[a - lo] + atomicAdd(fill + (a - lo), 1u);
-            ids[pa] = make_uint2(b, (uint32_t)e);
+            ids[pa] = make_uint2(b, id);
+            if (wk) wk[pa] = key;
         }
         if (b >= lo && b < hi) {
             const unsigned long long pb = vbeg[b - lo] + atomicAdd(fill + (b - lo), 1u);
-            ids[pb] = make_uint2(a, (uint32_t)e);
+            ids[pb] = make_uint2(a, id);
+            if (wk) wk[pb] = key;
         }
     }
 }
@@ -291,7 +348,20 @@ static int grid_for(lmx_ctx *ctx, unsigned long long work) {
 }
 
 // Build vbeg / ids0 / wk0 / deg0 / hubs0 from ctx->eu, ev, w (K0).
+// LMX_TRACE_SETUP=1: synchronise and print the wall time of each K0 stage.
+static void trace_mark(lmx_ctx *ctx, const char *what) {
+    static const bool on = getenv("LMX_TRACE_SETUP") != nullptr;
+    static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[lmx setup] %-24s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 int lmx_setup_slots(lmx_ctx *ctx) {
+    trace_mark(ctx, "edges on device");
     const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
     unsigned long long slots = 2 * m;   // becomes the owned slot count below
     cudaStream_t st = ctx->stream;
@@ -364,6 +434,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             ctx->relabeled = true;
         }
     }
+    trace_mark(ctx, "degrees + relabel");
     k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(ctx->deg0, ctx->vbeg, n);
     LMX_CUDA(ctx, cudaGetLastError());
     {
@@ -424,17 +495,9 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
     LMX_TRY(lmx_alloc_match_state(ctx));
-    if (m) {
-        // fill counters reuse vdeg (local)
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
-        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
-                                                      ctx->vdeg, ctx->ids0);
-        LMX_CUDA(ctx, cudaGetLastError());
-    }
-    if (newid) {
-        LMX_CUDA(ctx, cudaStreamSynchronize(st));
-        lmx_free(ctx, (void **)&newid, n * 4);
-    }
+    trace_mark(ctx, "offsets + allocation");
+    // weight key per edge first (kofe), so the slot scatter writes final records
+    uint32_t *kofe = nullptr;
     // weight key layout
     bool uniform = true;
     if (m) {
@@ -496,7 +559,8 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             ctx->layout = distinct ? kDistinct : kGeneral;
             ctx->n_distinct = (uint32_t)D;
             ctx->n_tied = (uint32_t)T;
-            uint32_t *key_of_eid = (uint32_t *)keys;   // reuse (m u32 fits in m u64)
+            if ((rc = lmx_alloc(ctx, (void **)&kofe, m * 4, "key of edge")) != LMX_OK) break;
+            uint32_t *key_of_eid = kofe;
             if (distinct) {
                 if ((rc = lmx_alloc(ctx, (void **)&ctx->eid_of_x, (D + T) * 4, "eid_of_x")) != LMX_OK) break;
                 if ((rc = lmx_alloc(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4,
@@ -508,8 +572,6 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             }
             k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
                                                            (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
-            k_slot_key<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, key_of_eid,
-                                                               distinct ? nullptr : ctx->wk0);
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
@@ -522,8 +584,24 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         lmx_free(ctx, (void **)&tied, m * 4);
         lmx_free(ctx, (void **)&tidx, m * 4);
         lmx_free(ctx, &tmp, tmp_bytes);
-        if (rc != LMX_OK) return rc;
+        if (rc != LMX_OK) {
+            lmx_free(ctx, (void **)&kofe, m * 4);
+            return rc;
+        }
     }
+    trace_mark(ctx, "weight keys");
+    if (m) {
+        // fill counters reuse vdeg (local)
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
+        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
+                                                      ctx->vdeg, ctx->ids0, kofe,
+                                                      ctx->layout == kDistinct, ctx->wk0);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    lmx_free(ctx, (void **)&newid, n * 4);
+    lmx_free(ctx, (void **)&kofe, m * 4);
+    trace_mark(ctx, "slot scatter");
     // round-0 bucket lists of the owned vertices (local indices, ascending)
     const size_t cap = std::max<size_t>(nl, 1);
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * kBuckets, "bins0"));
@@ -551,6 +629,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = (unsigned int)h[q];
     }
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    trace_mark(ctx, "bucket lists");
     return LMX_OK;
 }
 
@@ -573,8 +652,31 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
     unsigned long long *bad = nullptr;
     LMX_TRY(lmx_alloc(ctx, (void **)&bad, 8, "bad"));
     LMX_CUDA(ctx, cudaMemsetAsync(bad, 0xFF, 8, st));
+    // Pinned (page-locked, UVA-mapped) host arrays are read by the conversion
+    // kernel directly over the host link: no staging copies, full link rate.
+    const void *mapped[3] = {nullptr, nullptr, nullptr};
+    bool zero_copy = false;
+    if (m > 0 && where == LMX_HOST && !getenv("LMX_NO_ZEROCOPY")) {
+        zero_copy = true;
+        const void *hp[3] = {edge_u, edge_v, edge_weight};
+        for (int i = 0; i < 3; ++i) {
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, hp[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+                !at.devicePointer) {
+                cudaGetLastError();
+                zero_copy = false;
+                break;
+            }
+            mapped[i] = at.devicePointer;
+        }
+    }
     if (m > 0) {
-        if (where == LMX_DEVICE) {
+        if (zero_copy) {
+            k_convert<<<ctx->num_sms * 8, kBlock, 0, st>>>((const long long *)mapped[0], (const long long *)mapped[1],
+                                                          (const double *)mapped[2], (unsigned long long)m, n, 0,
+                                                          ctx->eu, ctx->ev, ctx->w, bad);
+            LMX_CUDA(ctx, cudaGetLastError());
+        } else if (where == LMX_DEVICE) {
             k_convert<<<grid_for(ctx, m), kBlock, 0, st>>>((const long long *)edge_u, (const long long *)edge_v,
                                                           edge_weight, (unsigned long long)m, n, 0, ctx->eu,
                                                           ctx->ev, ctx->w, bad);
