@@ -179,10 +179,14 @@ int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edg
 int lmx_dist_bounds(const lmx_ctx *ctx, int64_t *bounds_out);   /* p + 1 device-id cut points */
 int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize);
 int lmx_dist_round(lmx_ctx *ctx);
-int lmx_dist_propose(lmx_ctx *ctx, int64_t *counts_out, void **send_out);
+/* Device outputs, no synchronisation: int64[p] record counts per destination
+ * and the records {partner, edge id} (uint32 pairs) packed in destination order. */
+int lmx_dist_propose(lmx_ctx *ctx, void **counts_dev_out, void **send_dev_out);
 int lmx_dist_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_out);
 int lmx_dist_accept(lmx_ctx *ctx, int64_t count);
-int lmx_dist_match(lmx_ctx *ctx, int64_t *live_slots_out, int64_t *matched_v_out);
+/* Enqueues the match step; *stats_dev_out = device {live slots, matched
+ * vertices} (two uint64) of the round, for the all-reduce.  No synchronisation. */
+int lmx_dist_match(lmx_ctx *ctx, void **stats_dev_out);
 /* Device pointers: matched bitmap (n bits, global device ids), mate (int64[n],
  * caller ids, only owned vertices set), matched-edge bitmap (m bits, edges
  * recorded by this rank), and the context's cudaStream_t. */

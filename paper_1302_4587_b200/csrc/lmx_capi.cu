@@ -220,12 +220,10 @@ int lmx_dist_round(lmx_ctx *ctx) {
     return lmx_dist_round_impl(ctx);
 }
 
-int lmx_dist_propose(lmx_ctx *ctx, int64_t *counts_out, void **send_out) {
-    if (!ctx || !counts_out || !send_out) return LMX_EINVAL;
+int lmx_dist_propose(lmx_ctx *ctx, void **counts_dev_out, void **send_dev_out) {
+    if (!ctx || !counts_dev_out || !send_dev_out) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
-    LMX_TRY(lmx_dist_propose_impl(ctx, counts_out));
-    *send_out = ctx->send;
-    return LMX_OK;
+    return lmx_dist_propose_impl(ctx, counts_dev_out, send_dev_out);
 }
 
 int lmx_dist_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_out) {
@@ -240,10 +238,10 @@ int lmx_dist_accept(lmx_ctx *ctx, int64_t count) {
     return lmx_dist_accept_impl(ctx, count);
 }
 
-int lmx_dist_match(lmx_ctx *ctx, int64_t *live_slots_out, int64_t *matched_v_out) {
-    if (!ctx || !live_slots_out || !matched_v_out) return LMX_EINVAL;
+int lmx_dist_match(lmx_ctx *ctx, void **stats_dev_out) {
+    if (!ctx || !stats_dev_out) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
-    return lmx_dist_match_impl(ctx, live_slots_out, matched_v_out);
+    return lmx_dist_match_impl(ctx, stats_dev_out);
 }
 
 int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge_bits, void **stream) {

@@ -178,10 +178,10 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
                      int64_t *ids_out, int out_where);
 int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize);
 int lmx_dist_round_impl(lmx_ctx *ctx);
-int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts);
+int lmx_dist_propose_impl(lmx_ctx *ctx, void **counts_dev, void **packed_dev);
 int lmx_dist_recv_impl(lmx_ctx *ctx, int64_t count, void **ptr);
 int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count);
-int lmx_dist_match_impl(lmx_ctx *ctx, int64_t *live_slots, int64_t *matched_v);
+int lmx_dist_match_impl(lmx_ctx *ctx, void **stats_dev);
 
 #define LMX_CUDA(ctx, expr)                                          \
     do {                                                             \

@@ -689,10 +689,8 @@ struct ProposeArgs {
     const unsigned long long *bounds;   // p + 1 cut points (global ids)
     int p;
     uint32_t lo, nl;
-    uint32_t *cnt;      // [p] records per destination (pass 0)
-    uint32_t *cursor;   // [p] write cursors, preset to the offsets (pass 1)
-    uint2 *out;         // {global target vertex, edge id}
-    int pass;
+    uint32_t *cnt;      // [p] records per destination
+    uint2 *region;      // p regions of capacity nl: {global target vertex, edge id}
 };
 
 // For every owned live vertex whose candidate partner is owned elsewhere, send
@@ -714,8 +712,25 @@ __global__ void lmx_propose_kernel(ProposeArgs a) {
         while (k + 1 < a.p && x >= a.bounds[k + 1]) ++k;
         const uint32_t id = a.cand_id[v];
         const uint32_t e = a.eid_of_x ? a.eid_of_x[id] : id;
-        if (a.pass == 0) atomicAdd(a.cnt + k, 1u);
-        else a.out[atomicAdd(a.cursor + k, 1u)] = make_uint2(x, e);
+        const uint32_t pos = atomicAdd(a.cnt + k, 1u);
+        a.region[(unsigned long long)k * a.nl + pos] = make_uint2(x, e);
+    }
+}
+
+// Pack the p regions back to back (destination order) and publish the counts
+// as int64 for the collective; no host round trip.
+__global__ void lmx_pack_kernel(const uint2 *region, const uint32_t *cnt, int p, uint32_t nl, uint2 *packed,
+                                long long *counts64) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t tid0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid0 < (uint32_t)p) counts64[tid0] = cnt[tid0];
+    for (uint32_t i = tid0; i < nl; i += stride) {
+        uint32_t off = 0;
+        for (int k = 0; k < p; ++k) {
+            const uint32_t c = cnt[k];
+            if (i < c) packed[off + i] = region[(unsigned long long)k * nl + i];
+            off += c;
+        }
     }
 }
 
@@ -999,27 +1014,32 @@ int lmx_dist_round_impl(lmx_ctx *ctx) {
     return enqueue_round_kernel(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
 }
 
-int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
+// Exchange-A records, fully on the device: fill per-destination regions, pack
+// them, publish int64 counts.  Returns device pointers; no synchronisation.
+int lmx_dist_propose_impl(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
     const int p = ctx->dist_p;
     const int r = ctx->dist_round;
     const size_t cap = list_cap(ctx);
-    const size_t need = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    const size_t need = nl * (size_t)(p + 1);   // p regions + the packed copy
     if (ctx->send_cap < need) {
         lmx_dfree(ctx, ctx->send);
         ctx->send = nullptr;
         LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send, need * sizeof(uint2)));
         ctx->send_cap = need;
     }
-    // send_cnt block: [64] counts, [64] cursors, then the p + 1 bounds (u64), uploaded once per load
+    // send_cnt block: [64] u32 counts, [64] i64 counts at +256, the p + 1 bounds (u64)
+    // at +1024, uploaded once per load
     unsigned long long *bnd = nullptr;
     if (!ctx->send_cnt) {
         LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send_cnt, 2048));
         std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
-        LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 512, hb.data(),
+        LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 1024, hb.data(),
                                       (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
     }
-    bnd = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 512);
-    LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 2 * 64 * sizeof(uint32_t), ctx->stream));
+    bnd = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 1024);
+    long long *counts64 = reinterpret_cast<long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 256);
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 64 * sizeof(uint32_t), ctx->stream));
     ProposeArgs pa;
     pa.vdeg = ctx->vdeg;
     pa.cand_nbr = reinterpret_cast<const uint32_t *>(ctx->cand);
@@ -1033,24 +1053,16 @@ int lmx_dist_propose_impl(lmx_ctx *ctx, int64_t *counts) {
     pa.lo = (uint32_t)ctx->lo;
     pa.nl = (uint32_t)ctx->n_local;
     pa.cnt = ctx->send_cnt;
-    pa.cursor = ctx->send_cnt + 64;
-    pa.out = ctx->send;
-    pa.pass = 0;
+    pa.region = ctx->send;
     lmx_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
     LMX_CUDA(ctx, cudaGetLastError());
-    uint32_t hc[64];
-    LMX_CUDA(ctx, cudaMemcpyAsync(hc, ctx->send_cnt, (size_t)p * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    uint32_t off[65];
-    off[0] = 0;
-    for (int k = 0; k < p; ++k) off[k + 1] = off[k] + hc[k];
-    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->send_cnt + 64, off, (size_t)p * 4, cudaMemcpyHostToDevice, ctx->stream));
-    pa.pass = 1;
-    lmx_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
+    uint2 *packed = ctx->send + nl * (size_t)p;
+    lmx_pack_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(ctx->send, ctx->send_cnt, p, (uint32_t)nl,
+                                                                 packed, counts64);
     LMX_CUDA(ctx, cudaGetLastError());
-    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    for (int k = 0; k < p; ++k) counts[k] = hc[k];
     ctx->timing.round_launches += 2;
+    *counts_dev = counts64;
+    *packed_dev = packed;
     return LMX_OK;
 }
 
@@ -1077,14 +1089,12 @@ int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count) {
     return LMX_OK;
 }
 
-int lmx_dist_match_impl(lmx_ctx *ctx, int64_t *live_slots, int64_t *matched_v) {
+// Enqueue the match kernel; *stats_dev = the round's {live slots, matched
+// vertices} (two u64 on the device) for the host's all-reduce.  No sync.
+int lmx_dist_match_impl(lmx_ctx *ctx, void **stats_dev) {
     const int r = ctx->dist_round;
     LMX_TRY(enqueue_match_kernel(ctx, r));
-    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r, ctx->ctr + r, sizeof(RoundCtr), cudaMemcpyDeviceToHost,
-                                  ctx->stream));
-    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    *live_slots = (int64_t)ctx->ctr_host[r].live_slots;
-    *matched_v = (int64_t)ctx->ctr_host[r].matched_v;
+    *stats_dev = &ctx->ctr[r].live_slots;   // live_slots, matched_v are adjacent
     ctx->dist_round = r + 1;
     return LMX_OK;
 }

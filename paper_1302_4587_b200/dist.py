@@ -60,10 +60,10 @@ def _bind(lib):
         "lmx_dist_bounds": (c_int, [p, p]),
         "lmx_dist_begin": (c_int, [p, u64, c_int]),
         "lmx_dist_round": (c_int, [p]),
-        "lmx_dist_propose": (c_int, [p, p, ctypes.POINTER(p)]),
+        "lmx_dist_propose": (c_int, [p, ctypes.POINTER(p), ctypes.POINTER(p)]),
         "lmx_dist_recv_buffer": (c_int, [p, i64, ctypes.POINTER(p)]),
         "lmx_dist_accept": (c_int, [p, i64]),
-        "lmx_dist_match": (c_int, [p, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "lmx_dist_match": (c_int, [p, ctypes.POINTER(p)]),
         "lmx_dist_state": (c_int, [p, ctypes.POINTER(p), ctypes.POINTER(p), ctypes.POINTER(p),
                                    ctypes.POINTER(p)]),
     }
@@ -114,6 +114,7 @@ class DistRank:
         b = np.zeros(p + 1, dtype=np.int64)
         self._chk(self.lib.lmx_dist_bounds(self.eng._h, b.ctypes.data), "lmx_dist_bounds")
         self.bounds = b
+        self.n_local = int(b[rank + 1] - b[rank])
         bm, mate, eb, st = (ctypes.c_void_p() for _ in range(4))
         self._chk(self.lib.lmx_dist_state(self.eng._h, ctypes.byref(bm), ctypes.byref(mate), ctypes.byref(eb),
                                           ctypes.byref(st)), "lmx_dist_state")
@@ -136,11 +137,13 @@ class DistRank:
         self._chk(self.lib.lmx_dist_round(self.eng._h), "lmx_dist_round")
 
     def propose(self):
-        counts = np.zeros(self.p, dtype=np.int64)
-        ptr = ctypes.c_void_p()
-        self._chk(self.lib.lmx_dist_propose(self.eng._h, counts.ctypes.data, ctypes.byref(ptr)), "lmx_dist_propose")
-        total = int(counts.sum())
-        send = _view(ptr.value or 0, (total, 2), "<i4", self.device)
+        """Exchange-A records on the device: (packed int32 [cap, 2] view, int64[p] counts).
+        Nothing is synchronised; the first `counts.sum()` rows are valid."""
+        cptr = ctypes.c_void_p()
+        sptr = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_propose(self.eng._h, ctypes.byref(cptr), ctypes.byref(sptr)), "lmx_dist_propose")
+        counts = _view(cptr.value, (self.p,), "<i8", self.device)
+        send = _view(sptr.value, (max(self.n_local, 1), 2), "<i4", self.device)
         return send, counts
 
     def recv_buffer(self, count: int):
@@ -152,10 +155,10 @@ class DistRank:
         self._chk(self.lib.lmx_dist_accept(self.eng._h, int(count)), "lmx_dist_accept")
 
     def match(self):
-        live = ctypes.c_int64()
-        mv = ctypes.c_int64()
-        self._chk(self.lib.lmx_dist_match(self.eng._h, ctypes.byref(live), ctypes.byref(mv)), "lmx_dist_match")
-        return int(live.value), int(mv.value)
+        """Enqueue the match step; returns the round's device {live slots, matched} (int64[2] view)."""
+        ptr = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_match(self.eng._h, ctypes.byref(ptr)), "lmx_dist_match")
+        return _view(ptr.value, (2,), "<i8", self.device)
 
     def word_range(self, k: int):
         return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
@@ -170,14 +173,19 @@ class LocalComm:
     def __init__(self, p: int):
         self.p = p
 
+    def record_total(self, recv_counts):
+        return int(sum(recv_counts))
+
     def alltoallv(self, ranks, sends):
         import torch
+        counts_h = [c.tolist() for _, c in sends]
         recvs = []
         for dst in range(self.p):
             parts = []
             for src in range(self.p):
-                send, counts = sends[src]
-                off = int(counts[:dst].sum())
+                send, _ = sends[src]
+                counts = counts_h[src]
+                off = int(sum(counts[:dst]))
                 parts.append(send[off: off + int(counts[dst])])
             total = sum(int(x.shape[0]) for x in parts)
             buf = ranks[dst].recv_buffer(total)
@@ -197,7 +205,7 @@ class LocalComm:
                     ranks[dst].bitmap[w0:w1].copy_(seg)
 
     def allreduce_sum(self, values):
-        return [sum(col) for col in zip(*values)]
+        return [sum(col) for col in zip(*(v.tolist() for v in values))]
 
     def gather_outputs(self, ranks):
         import torch
@@ -225,12 +233,13 @@ class TorchComm:
         sc = torch.as_tensor(counts, dtype=torch.int64, device=dev)
         rc = torch.empty_like(sc)
         self.dist.all_to_all_single(rc, sc)
-        rcounts = rc.tolist()
-        total = int(sum(rcounts))
+        both = torch.cat([sc, rc]).tolist()          # the one host sync of exchange A
+        scounts, rcounts = both[: self.p], both[self.p:]
+        stotal, total = int(sum(scounts)), int(sum(rcounts))
         recv = me.recv_buffer(total)
-        flat_in = send.reshape(-1) if send.numel() else torch.empty(0, dtype=torch.int32, device=dev)
+        flat_in = send[:stotal].reshape(-1) if stotal else torch.empty(0, dtype=torch.int32, device=dev)
         flat_out = recv.reshape(-1) if total else torch.empty(0, dtype=torch.int32, device=dev)
-        self.dist.all_to_all_single(flat_out, flat_in, [2 * c for c in rcounts], [2 * int(c) for c in counts])
+        self.dist.all_to_all_single(flat_out, flat_in, [2 * c for c in rcounts], [2 * int(c) for c in scounts])
         return [total]
 
     def allgather_bitmap(self, ranks):
@@ -249,9 +258,8 @@ class TorchComm:
                 me.bitmap[a:b].copy_(out[k * width: k * width + (b - a)])
 
     def allreduce_sum(self, values):
-        import torch
         (vals,) = values
-        t = torch.tensor(vals, dtype=torch.int64, device=self._dev)
+        t = vals.clone()   # device int64[2]
         self.dist.all_reduce(t)
         return [int(x) for x in t.tolist()]
 
@@ -266,11 +274,17 @@ class TorchComm:
     def bind_device(self, device):
         self._dev = device
 
+    def record_total(self, recv_counts):
+        """Exchange-A records received by this rank (the per-rank share of RoundMessages)."""
+        return int(sum(recv_counts))
+
 
 def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int | None = None):
     """Drive the stepped protocol on `ranks` (all local partitions) to completion.
 
-    Returns (RoundStats list, per-round exchange-A record counts).
+    Returns (RoundStats list, per-round exchange-A record counts).  Host
+    synchronisations per round: the exchange-A counts and the statistics
+    all-reduce (termination).
     """
     for r in ranks:
         r.begin(seed, rerandomize)
@@ -281,8 +295,8 @@ def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int
         for r in ranks:
             r.round()
         sends = [r.propose() for r in ranks]
-        records.append(int(sum(int(c.sum()) for _, c in sends)))
         recv_counts = comm.alltoallv(ranks, sends)
+        records.append(comm.record_total(recv_counts))
         for r, cnt in zip(ranks, recv_counts):
             r.accept(cnt)
         local = [r.match() for r in ranks]

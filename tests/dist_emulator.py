@@ -90,7 +90,7 @@ class EmulatedRank:
         for v, (x, e) in self.cand.items():
             if not (self.lo <= x < self.hi):
                 groups[self._owner(x)].append((x, e))
-        counts = np.array([len(gp) for gp in groups], dtype=np.int64)
+        counts = torch.tensor([len(gp) for gp in groups], dtype=torch.int64)
         flat = [rec for gp in groups for rec in gp]
         send = torch.tensor(flat if flat else np.zeros((0, 2)), dtype=torch.int32).reshape(-1, 2)
         return send, counts
@@ -121,4 +121,4 @@ class EmulatedRank:
                 if v < x:
                     eb[e >> 5] |= np.uint32(1 << (e & 31))
         self.r += 1
-        return self.live_slots, mv
+        return torch.tensor([self.live_slots, mv], dtype=torch.int64)
