@@ -91,7 +91,9 @@ void lmx_destroy(lmx_ctx *ctx);
 const char *lmx_last_error(const lmx_ctx *ctx);
 
 /* Run all work on this stream (a cudaStream_t passed as void*); NULL = the
- * context's own non-blocking stream. */
+ * context's own non-blocking stream.  The legacy default stream (what
+ * PyTorch's torch.cuda.default_stream().cuda_stream == 0 denotes) is passed as
+ * cudaStreamLegacy, (void*)1. */
 int lmx_set_stream(lmx_ctx *ctx, void *cuda_stream);
 
 /*

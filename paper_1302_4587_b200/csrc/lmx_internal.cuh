@@ -162,7 +162,7 @@ struct lmx_ctx {
 int lmx_fail(lmx_ctx *ctx, int code, const std::string &msg);
 int lmx_cuda_check(lmx_ctx *ctx, cudaError_t e, const char *what);
 int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what);
-cudaError_t lmx_dmalloc(lmx_ctx *ctx, void **p, size_t bytes);   // stream-ordered pool
+cudaError_t lmx_dmalloc(lmx_ctx *ctx, void **p, size_t bytes);   // per-context block cache
 void lmx_dfree(lmx_ctx *ctx, void *p);
 void lmx_flush_cache(lmx_ctx *ctx);
 void lmx_free(lmx_ctx *ctx, void **p, size_t bytes);

@@ -102,8 +102,11 @@ class DistRank:
         self.lib = self.eng._lib
         _bind(self.lib)
         self.p, self.rank, self.device = p, rank, torch.device("cuda", device)
-        if stream is not None:
-            self.eng.set_stream(stream)
+        # the device views handed back (counts, records, statistics) are consumed
+        # by torch ops / NCCL on torch's current stream: the engine must run on it
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.eng.set_stream(stream)
         self._opt(LMX_OPT_DIST_P, p)
         self._opt(LMX_OPT_DIST_RANK, rank)
         if rmat is not None:

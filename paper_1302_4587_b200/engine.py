@@ -41,6 +41,7 @@ LMX_OPT_KERNEL_TIMING = 1
 LMX_OPT_LAYOUT = 2
 LMX_OPT_RELABEL = 3
 LMX_QUERY_LAYOUT = 100
+_CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy
 LMX_QUERY_RELABELED = 101
 
 
@@ -153,8 +154,15 @@ class Engine:
             _raise(rc, f"{what}: " + self._lib.lmx_last_error(self._h).decode())
 
     def set_stream(self, stream_handle: int | None):
-        """Run on a given cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
-        self._check(self._lib.lmx_set_stream(self._h, stream_handle or None), "lmx_set_stream")
+        """Run on a given cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``).
+
+        ``None`` = the engine's own non-blocking stream; ``0`` (torch's handle of
+        the legacy default stream) is passed on as cudaStreamLegacy."""
+        if stream_handle is None:
+            handle = None
+        else:
+            handle = int(stream_handle) or _CUDA_STREAM_LEGACY
+        self._check(self._lib.lmx_set_stream(self._h, handle), "lmx_set_stream")
 
     # -- graph loading -------------------------------------------------------
     def load_graph(self, g) -> None:
