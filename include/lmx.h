@@ -80,8 +80,12 @@ typedef struct {
                                    -1 auto (skewed degree distributions), 0 off, 1 on */
 #define LMX_OPT_DIST_P 4        /* number of 1D vertex partitions of the next load (1 = single GPU) */
 #define LMX_OPT_DIST_RANK 5     /* which partition this context owns (set after LMX_OPT_DIST_P) */
+#define LMX_OPT_ALGO 6          /* round loop of the next load: -1 auto, 0 compacting rounds,
+                                   1 weight-ordered scan (taken only for the distinct layout on a
+                                   context without LMX_OPT_DIST_P; results are identical) */
 #define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
 #define LMX_QUERY_RELABELED 101 /* lmx_set_option returns 1 if the loaded graph is relabelled */
+#define LMX_QUERY_ALGO 102      /* lmx_set_option returns the loaded graph's round loop (0 / 1) */
 
 int lmx_abi_version(void);
 
@@ -123,6 +127,11 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value);
 /* Copy the RoundStats trace of the last lmx_match (up to cap entries);
  * returns the number of rounds, or -1 on a bad ctx. */
 int lmx_last_rounds(lmx_ctx *ctx, lmx_round_stats *out, int cap);
+
+/* Diagnostics (LMX_OPT_KERNEL_TIMING on): per executed round of the last
+ * lmx_match, the round-kernel and match-kernel durations in ms, interleaved
+ * (out[2r], out[2r+1]); returns the number of floats available. */
+int lmx_last_kernel_times(const lmx_ctx *ctx, float *out, int cap);
 
 /* One-shot host-buffer entry point: the local_max_seq drop-in for an FFI
  * binding.  err may be NULL. */

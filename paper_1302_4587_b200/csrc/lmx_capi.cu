@@ -49,6 +49,7 @@ int lmx_create(int device, lmx_ctx **out) {
             break;
         }
         rc = lmx_configure_grids(ctx);
+        if (rc == LMX_OK) rc = lmx_scan_configure_grids(ctx);
     } while (0);
     if (rc != LMX_OK) {
         g_create_err = ctx->err;
@@ -125,7 +126,8 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
     std::vector<lmx_round_stats> &stats = ctx->rounds;
     unsigned long long nm = 0;
     ctx->mate_target = (out_where == LMX_DEVICE && mate_out) ? (long long *)mate_out : ctx->mate;
-    LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
+    if (ctx->algo == 1) LMX_TRY(lmx_run_rounds_scan(ctx, seed_masked, rerandomize != 0, stats, nm));
+    else LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
     LMX_TRY(lmx_emit_outputs(ctx, nm, mate_out, matched_ids_out, out_where));
     if (n_matched_out) *n_matched_out = (int64_t)nm;
     if (n_rounds_out) *n_rounds_out = (int)stats.size();
@@ -162,6 +164,12 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
     if (option == LMX_OPT_DIST_P) {
         if (value < 1 || value > 64) return lmx_fail(ctx, LMX_EINVAL, "dist p must be in [1, 64]");
         ctx->dist_p = (int)value;
+        ctx->dist_requested = true;
+        return LMX_OK;
+    }
+    if (option == LMX_OPT_ALGO) {
+        if (value < -1 || value > 1) return lmx_fail(ctx, LMX_EINVAL, "algo must be -1, 0 or 1");
+        ctx->force_algo = (int)value;
         return LMX_OK;
     }
     if (option == LMX_OPT_DIST_RANK) {
@@ -171,6 +179,7 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
     }
     if (option == LMX_QUERY_LAYOUT) return ctx->layout;
     if (option == LMX_QUERY_RELABELED) return ctx->relabeled ? 1 : 0;
+    if (option == LMX_QUERY_ALGO) return ctx->algo;
     return lmx_fail(ctx, LMX_EINVAL, "unknown option");
 }
 
@@ -178,6 +187,13 @@ int lmx_last_timing(const lmx_ctx *ctx, lmx_timing *out) {
     if (!ctx || !out) return LMX_EINVAL;
     *out = ctx->timing;
     return LMX_OK;
+}
+
+int lmx_last_kernel_times(const lmx_ctx *ctx, float *out, int cap) {
+    if (!ctx) return -1;
+    const int k = (int)ctx->kernel_ms.size();
+    for (int i = 0; i < k && i < cap && out; ++i) out[i] = ctx->kernel_ms[i];
+    return k;
 }
 
 int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
@@ -211,6 +227,9 @@ int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize) {
     if (!ctx) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
     if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded");
+    if (ctx->algo != 0)
+        return lmx_fail(ctx, LMX_ESTATE, "graph was loaded for the single-GPU scan loop; set LMX_OPT_DIST_P "
+                                         "before lmx_load_graph to use the stepped protocol");
     return lmx_dist_begin_impl(ctx, seed_masked, rerandomize != 0);
 }
 

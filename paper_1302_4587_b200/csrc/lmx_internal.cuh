@@ -91,6 +91,8 @@ struct lmx_ctx {
     int num_sms = 148;
     int round_grid[3][3] = {};   // persistent grid of each round-kernel instance [MODE][LAYOUT]
     int match_blocks = 0;
+    int scan_grid[2] = {0, 0};   // scan round kernel grids (round 0, rounds >= 1)
+    int scan_match_grid = 0;
     std::string err;
 
     // graph
@@ -133,10 +135,18 @@ struct lmx_ctx {
     std::vector<lmx_round_stats> rounds;     // trace of the last lmx_match
     bool kernel_timing = false;
     std::vector<cudaEvent_t> tl_events;      // per-kernel timeline (kernel_timing)
+    std::vector<float> kernel_ms;            // its durations: round, match, round, ...
     int force_layout = -1;                   // testing: force a weight-key layout
     int force_relabel = -1;                  // -1 auto (skewed graphs), 0 off, 1 on
     bool relabeled = false;                  // device vertex ids are degree-sorted
     uint32_t *oldid = nullptr;               // device id -> caller's vertex id
+    // round-loop algorithm: 0 = compacting rounds (lmx_round.cu),
+    // 1 = weight-ordered scan (lmx_scan.cu; DISTINCT layout, single partition)
+    int algo = 0;
+    int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
+    bool dist_requested = false;             // LMX_OPT_DIST_P was set: stepped protocol
+    uint2 *mf = nullptr;                     // scan: {matched, fresh} bits per 32 vertices
+    uint32_t *mlists[2] = {nullptr, nullptr};   // scan: M_r lists, kBuckets regions of cap n
 
     // device block cache (lmx_dmalloc / lmx_dfree)
     std::unordered_map<void *, size_t> live;
@@ -170,6 +180,11 @@ void lmx_free_graph(lmx_ctx *ctx);
 int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
+int lmx_scan_configure_grids(lmx_ctx *ctx);
+int lmx_scan_alloc(lmx_ctx *ctx);
+int lmx_ensure_ctr(lmx_ctx *ctx, int need);
+int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
+                        std::vector<lmx_round_stats> &stats, unsigned long long &n_matched);
 int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
                    const double *edge_weight, int where);
 int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,

@@ -810,7 +810,7 @@ int lmx_alloc_match_state(lmx_ctx *ctx) {
 }
 
 // Ensure ctr has room for rounds [0, need].  Only called with the stream idle.
-static int ensure_ctr(lmx_ctx *ctx, int need) {
+int lmx_ensure_ctr(lmx_ctx *ctx, int need) {
     if (need < ctx->ctr_cap) return LMX_OK;
     const int ncap = std::max(ctx->ctr_cap * 2, need + 64);
     RoundCtr *nc = nullptr, *nh = nullptr;
@@ -837,7 +837,7 @@ static int ensure_ctr(lmx_ctx *ctx, int need) {
 // Reset per-match state: counters, edge bitmap, live degrees, mates, bitmap.
 static int begin_match(lmx_ctx *ctx) {
     const uint32_t nl = (uint32_t)ctx->n_local;
-    LMX_TRY(ensure_ctr(ctx, 64));
+    LMX_TRY(lmx_ensure_ctr(ctx, 64));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, ctx->stream));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, ctx->stream));
     ctx->ctr_host[0] = RoundCtr{};
@@ -939,7 +939,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     int n_rounds = -1;
     int batch = 6;
     while (n_rounds < 0 && ctx->m > 0) {
-        LMX_TRY(ensure_ctr(ctx, r + batch + 1));
+        LMX_TRY(lmx_ensure_ctr(ctx, r + batch + 1));
         const int r0 = r;
         for (int b = 0; b < batch; ++b, ++r) {
             LMX_TRY(enqueue_round_kernel(ctx, r, seed_masked, rerandomize));
@@ -961,10 +961,12 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         if (n_rounds < 0) n_rounds = 0;
 #endif
     }
+    ctx->kernel_ms.clear();
     if (ctx->kernel_timing && tl_used > 1) {
         for (int i = 1; i < tl_used; ++i) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ctx->tl_events[i - 1], ctx->tl_events[i]);
+            ctx->kernel_ms.push_back(ms);
             if (i & 1) ctx->timing.round_kernel_ms += ms;
             else ctx->timing.match_kernel_ms += ms;
         }
@@ -1010,7 +1012,7 @@ int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
 }
 
 int lmx_dist_round_impl(lmx_ctx *ctx) {
-    LMX_TRY(ensure_ctr(ctx, ctx->dist_round + 2));
+    LMX_TRY(lmx_ensure_ctr(ctx, ctx->dist_round + 2));
     return enqueue_round_kernel(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
 }
 

@@ -115,7 +115,8 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
                      (void **)&ctx->tie_rank, (void **)&ctx->oldid,
                      (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
-                     (void **)&ctx->send_cnt};
+                     (void **)&ctx->send_cnt, (void **)&ctx->mf, (void **)&ctx->mlists[0],
+                     (void **)&ctx->mlists[1]};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -125,6 +126,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
+    ctx->algo = 0;
     ctx->send_cap = ctx->recv_cap = 0;
     ctx->n_local = ctx->slots_local = 0;
     for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = 0;
@@ -337,7 +339,99 @@ struct InBucket {
     __device__ bool operator()(uint32_t v) const { return deg[v] > 0 && bucket_of(deg[v]) == q; }
 };
 
+struct HasEdge {
+    const uint32_t *deg;
+    __device__ bool operator()(uint32_t v) const { return deg[v] > 0; }
+};
+
+// DISTINCT layout: dense weight rank of each slot's edge (tiebreak.py:105-113
+// order; a tied edge x >= D carries its group's rank).
+__global__ void k_slot_rank(const uint2 *ids, unsigned long long slots, uint32_t D, const uint32_t *tie_rank,
+                            uint32_t *rank) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
+         i += stride) {
+        const uint32_t x = ids[i].y;
+        rank[i] = x < D ? x : tie_rank[x - D];
+    }
+}
+
+struct SubBase {
+    unsigned long long base;
+    __host__ __device__ long long operator()(unsigned long long x) const { return (long long)(x - base); }
+};
+
 }  // namespace lmx
+
+static int grid_for(lmx_ctx *ctx, unsigned long long work);
+
+// Sort every vertex segment of ids0 by weight rank, descending (the scan
+// algorithm's fixed candidate order, lmx_scan.cu).  CUB segmented sort, in
+// chunks of whole segments below its int item limit.
+static int sort_segments_by_weight(lmx_ctx *ctx, unsigned long long slots) {
+    cudaStream_t st = ctx->stream;
+    const unsigned long long nl = (unsigned long long)ctx->n_local;
+    if (slots == 0 || nl == 0) return LMX_OK;
+    uint32_t *k0 = nullptr, *k1 = nullptr;
+    LMX_TRY(lmx_alloc(ctx, (void **)&k0, slots * 4, "rank keys"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&k1, slots * 4, "rank keys out"));
+    k_slot_rank<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, ctx->n_distinct, ctx->tie_rank, k0);
+    LMX_CUDA(ctx, cudaGetLastError());
+    // chunk cut points (whole segments) by equal slot sums
+    const unsigned long long kChunk = 1ULL << 30;
+    const int p = (int)std::min<unsigned long long>((slots + kChunk - 1) / kChunk, 64ULL);
+    std::vector<unsigned long long> cuts(2, 0);
+    cuts[1] = nl;
+    if (p > 1) {
+        unsigned long long *dc = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&dc, (size_t)(p + 1) * 8, "sort cuts"));
+        k_cuts<<<1, 64, 0, st>>>(ctx->vbeg, nl, p, dc);
+        cuts.assign((size_t)p + 1, 0);
+        cudaError_t e = cudaMemcpyAsync(cuts.data(), dc, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        lmx_free(ctx, (void **)&dc, (size_t)(p + 1) * 8);
+        LMX_CUDA(ctx, e);
+    }
+    std::vector<unsigned long long> offs(cuts.size());
+    for (size_t i = 0; i < cuts.size(); ++i)
+        LMX_CUDA(ctx, cudaMemcpyAsync(&offs[i], ctx->vbeg + cuts[i], 8, cudaMemcpyDeviceToHost, st));
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = LMX_OK;
+    for (size_t c = 0; c + 1 < cuts.size() && rc == LMX_OK; ++c) {
+        const unsigned long long v0 = cuts[c], v1 = cuts[c + 1];
+        const unsigned long long base = offs[c], items = offs[c + 1] - offs[c];
+        if (v1 <= v0 || items == 0) continue;
+        if (items > 0x7FFFFFFFULL) {
+            rc = lmx_fail(ctx, LMX_ELIMIT, "a vertex chunk exceeds the segmented sort's item limit");
+            break;
+        }
+        cub::TransformInputIterator<long long, SubBase, const unsigned long long *> ob(ctx->vbeg + v0, SubBase{base});
+        size_t need = 0;
+        cudaError_t e = cub::DeviceSegmentedSort::SortPairsDescending(
+            nullptr, need, k0 + base, k1 + base, ctx->ids0 + base, ctx->ids1 + base, (int)items, (int)(v1 - v0), ob,
+            ob + 1, st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "segment sort sizing"); break; }
+        if (need > tmp_bytes) {
+            lmx_free(ctx, &tmp, tmp_bytes);
+            tmp_bytes = need;
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "segment sort tmp")) != LMX_OK) break;
+        }
+        e = cub::DeviceSegmentedSort::SortPairsDescending(tmp, need, k0 + base, k1 + base, ctx->ids0 + base,
+                                                          ctx->ids1 + base, (int)items, (int)(v1 - v0), ob, ob + 1,
+                                                          st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "segment sort"); break; }
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    lmx_free(ctx, (void **)&k0, slots * 4);
+    lmx_free(ctx, (void **)&k1, slots * 4);
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, e);
+    std::swap(ctx->ids0, ctx->ids1);   // sorted records become the pristine copy
+    return LMX_OK;
+}
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work) {
     unsigned long long b = (work + kBlock - 1) / kBlock;
@@ -602,6 +696,17 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     lmx_free(ctx, (void **)&newid, n * 4);
     lmx_free(ctx, (void **)&kofe, m * 4);
     trace_mark(ctx, "slot scatter");
+    // round-loop algorithm: the weight-ordered scan needs (almost) distinct
+    // weights (a fixed key order) and the whole graph in one context
+    ctx->algo = 0;
+    if (m && ctx->layout == kDistinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0)
+        ctx->algo = 1;
+    if (ctx->algo == 1) {
+        LMX_TRY(sort_segments_by_weight(ctx, slots));
+        lmx_free(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8);   // no working copy
+        LMX_TRY(lmx_scan_alloc(ctx));
+        trace_mark(ctx, "weight-ordered segments");
+    }
     // round-0 bucket lists of the owned vertices (local indices, ascending)
     const size_t cap = std::max<size_t>(nl, 1);
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * kBuckets, "bins0"));
@@ -615,7 +720,12 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         void *t = nullptr;
         LMX_TRY(lmx_alloc(ctx, &t, tmp, "select tmp"));
         cudaError_t e = cudaSuccess;
-        for (int q = 0; q < kBuckets && e == cudaSuccess; ++q) {
+        if (ctx->algo == 1) {   // scan: one list of every vertex with an edge
+            LMX_CUDA(ctx, cudaMemsetAsync(cnt, 0, 8 * kBuckets, st));
+            size_t tb = tmp;
+            e = cub::DeviceSelect::If(t, tb, it, ctx->bins0, cnt, (long long)nl, HasEdge{ctx->deg0}, st);
+        }
+        for (int q = 0; q < kBuckets && e == cudaSuccess && ctx->algo == 0; ++q) {
             size_t tb = tmp;
             e = cub::DeviceSelect::If(t, tb, it, ctx->bins0 + (size_t)q * cap, cnt + q, (long long)nl,
                                       InBucket{ctx->deg0, q}, st);

@@ -30,7 +30,8 @@ LMX_HOST, LMX_DEVICE = 0, 1
 
 EXPORTED_SYMBOLS = (
     "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
-    "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_local_max",
+    "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times",
+    "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
@@ -40,9 +41,11 @@ EXPORTED_SYMBOLS = (
 LMX_OPT_KERNEL_TIMING = 1
 LMX_OPT_LAYOUT = 2
 LMX_OPT_RELABEL = 3
+LMX_OPT_ALGO = 6
 LMX_QUERY_LAYOUT = 100
-_CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy
 LMX_QUERY_RELABELED = 101
+LMX_QUERY_ALGO = 102
+_CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy
 
 
 class LmxRoundStats(ctypes.Structure):
@@ -83,6 +86,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_match": (c_int, [p, u64, c_int, p, p, p, p, c_int, p, c_int]),
             "lmx_last_timing": (c_int, [p, ctypes.POINTER(LmxTiming)]),
             "lmx_last_rounds": (c_int, [p, p, c_int]),
+            "lmx_last_kernel_times": (c_int, [p, p, c_int]),
             "lmx_local_max": (c_int, [c_int, i64, i64, p, p, p, u64, c_int, p, p, p, p, c_int, p,
                                       ctypes.c_char_p, ctypes.c_size_t]),
             "lmx_build_graph": (c_int, [p, i64, p, p, p, i64, c_int]),
@@ -253,6 +257,15 @@ class Engine:
         return [RoundStats(int(b.edges_before), int(b.edges_matched), int(b.edges_removed))
                 for b in buf[:k]]
 
+    def last_kernel_times(self) -> list:
+        """[(round kernel ms, match kernel ms)] per executed round of the last match
+        (needs set_kernel_timing(True))."""
+        k = self._lib.lmx_last_kernel_times(self._h, None, 0)
+        buf = (ctypes.c_float * max(k, 1))()
+        self._lib.lmx_last_kernel_times(self._h, buf, k)
+        v = list(buf[:k])
+        return [(v[i], v[i + 1] if i + 1 < k else 0.0) for i in range(0, k, 2)]
+
     def last_timing(self) -> dict:
         t = LmxTiming()
         self._check(self._lib.lmx_last_timing(self._h, ctypes.byref(t)), "lmx_last_timing")
@@ -271,6 +284,17 @@ class Engine:
         """Degree-descending vertex relabelling of the next load: auto / on / off."""
         val = {"auto": -1, "off": 0, "on": 1}[mode]
         self._check(self._lib.lmx_set_option(self._h, LMX_OPT_RELABEL, val), "lmx_set_option")
+
+    ALGOS = {"auto": -1, "compact": 0, "scan": 1}
+
+    def set_algo(self, algo: str = "auto") -> None:
+        """Round loop of the next load: compacting rounds or the weight-ordered
+        scan (distinct weights, single context); results are identical."""
+        self._check(self._lib.lmx_set_option(self._h, LMX_OPT_ALGO, self.ALGOS[algo]), "lmx_set_option")
+
+    def algo(self) -> str:
+        code = self._lib.lmx_set_option(self._h, LMX_QUERY_ALGO, 0)
+        return {v: k for k, v in self.ALGOS.items()}[code]
 
     def relabeled(self) -> bool:
         return bool(self._lib.lmx_set_option(self._h, LMX_QUERY_RELABELED, 0))

@@ -19,17 +19,22 @@ def _graph(n, eu, ev, w):
     return Graph(n, eu, ev, w)
 
 
-VARIANTS = [("auto", "auto"), ("distinct", "on"), ("general", "off"), ("general", "on")]
+# (weight-key layout, relabelling, round loop): the scan loop serves the
+# distinct layout by default; the compacting loop is forced on it as well.
+VARIANTS = [("auto", "auto", "auto"), ("distinct", "on", "scan"), ("distinct", "off", "compact"),
+            ("distinct", "off", "scan"), ("general", "off", "auto"), ("general", "on", "auto")]
 
 
-@pytest.fixture(params=VARIANTS, ids=lambda p: f"{p[0]}-relabel_{p[1]}")
+@pytest.fixture(params=VARIANTS, ids=lambda p: f"{p[0]}-relabel_{p[1]}-{p[2]}")
 def layout_engine(engine, request):
-    """The engine with a forced weight-key layout and vertex relabelling mode."""
+    """The engine with a forced weight-key layout, relabelling mode and round loop."""
     engine.set_layout(request.param[0])
     engine.set_relabel(request.param[1])
+    engine.set_algo(request.param[2])
     yield engine
     engine.set_layout("auto")
     engine.set_relabel("auto")
+    engine.set_algo("auto")
 
 
 def test_small_golden_runs_bit_exact(layout_engine, golden_small):
