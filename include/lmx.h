@@ -133,6 +133,11 @@ int lmx_last_rounds(lmx_ctx *ctx, lmx_round_stats *out, int cap);
  * (out[2r], out[2r+1]); returns the number of floats available. */
 int lmx_last_kernel_times(const lmx_ctx *ctx, float *out, int cap);
 
+/* Diagnostics: per executed round of the last lmx_match, 8 counters
+ * {slot reads, removal/live count, matched vertices, list sizes[5]}
+ * (engine-specific meaning); returns the number of rounds. */
+int lmx_last_round_counters(const lmx_ctx *ctx, int64_t *out, int cap_rounds);
+
 /* One-shot host-buffer entry point: the local_max_seq drop-in for an FFI
  * binding.  err may be NULL. */
 int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u,

@@ -196,6 +196,26 @@ int lmx_last_kernel_times(const lmx_ctx *ctx, float *out, int cap) {
     return k;
 }
 
+int lmx_last_round_counters(const lmx_ctx *ctx, int64_t *out, int cap_rounds) {
+    if (!ctx) return -1;
+    const int k = (int)ctx->timing.rounds_executed;
+    for (int i = 0; i < k && i < cap_rounds && out && ctx->ctr_host; ++i) {
+        const lmx::RoundCtr &c = ctx->ctr_host[i];
+        int64_t *o = out + 8 * i;
+        o[0] = (int64_t)c.slot_reads;
+        o[1] = (int64_t)c.live_slots;
+        o[2] = (int64_t)c.matched_v;
+        // scan loop: |A_r| then |M_{r-1}| buckets 0..3 (4 folded into 3); compact: buckets 0..4
+        if (ctx->algo == 1) {
+            o[3] = c.pad[0];
+            for (int q = 0; q < 4; ++q) o[4 + q] = c.n[q] + (q == 3 ? c.n[4] : 0);
+        } else {
+            for (int q = 0; q < 5; ++q) o[3 + q] = c.n[q];
+        }
+    }
+    return k;
+}
+
 int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
                   const double *edge_weight, uint64_t seed_masked, int rerandomize, int64_t *mate_out,
                   int64_t *matched_ids_out, int64_t *n_matched_out, lmx_round_stats *rounds_out,

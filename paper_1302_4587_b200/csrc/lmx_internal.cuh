@@ -145,8 +145,12 @@ struct lmx_ctx {
     int algo = 0;
     int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
     bool dist_requested = false;             // LMX_OPT_DIST_P was set: stepped protocol
-    uint2 *mf = nullptr;                     // scan: {matched, fresh} bits per 32 vertices
-    uint32_t *mlists[2] = {nullptr, nullptr};   // scan: M_r lists, kBuckets regions of cap n
+    uint32_t *mround = nullptr;              // scan: round each vertex was matched in (~0 never)
+    unsigned long long *lowbeg = nullptr;    // scan (load time only): [n+1] offsets of lowpair
+    uint2 *lowpair = nullptr;                // scan: each edge once as {higher id, lower id}, by higher id
+    uint32_t *mpacked = nullptr;             // scan: mround packed to 4 / 8 bits (n bytes)
+    unsigned long long *hist = nullptr;      // scan: death-round histogram
+    size_t hist_cap = 0;
 
     // device block cache (lmx_dmalloc / lmx_dfree)
     std::unordered_map<void *, size_t> live;
@@ -181,7 +185,6 @@ int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
-int lmx_scan_alloc(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                         std::vector<lmx_round_stats> &stats, unsigned long long &n_matched);

@@ -2,34 +2,30 @@
 // DISTINCT weight-key layout on one GPU.
 //
 // Same result as local_max_seq (matchers.py:61-122) and as the compacting
-// round loop of lmx_round.cu, reached with O(m) total slot traffic instead of
+// round loop of lmx_round.cu, with O(m) total slot traffic instead of
 // O(sum_r m_r + m):
 //
 //   * At load time every vertex segment of ids0 is sorted by weight rank,
 //     descending (lmx_setup.cu).  With (almost) distinct weights the key order
-//     of a vertex's edges is then fixed across rounds: only edges of one tied
-//     weight need the per-round salt (tiebreak.py:55-80), and those sit next to
-//     each other in the segment.
+//     of a vertex's edges is then the same in every round: only the edges of
+//     one tied weight need the per-round salt (tiebreak.py:55-80), and those
+//     sit next to each other in the segment.
 //   * ptr[v] marks the first slot of v not yet known to be dead.  Edges only
 //     ever die (matchers.py:111), so v's candidate in round r is the first live
-//     slot at or after ptr[v] (or the salt-max of its tie run): one probe for
-//     most vertices, and each slot is skipped at most once over all rounds.
-//   * The per-round statistics (edges_before, RoundStats of matchers.py:113-118)
-//     come from the vertices matched in round r: every edge that dies in round
-//     r has an endpoint in M_r, so m_{r+1} = m_r - |{e : e touches M_r}|,
-//     counted by one scan of each matched vertex's remaining slots:
-//     weight 2 for an unmatched neighbour, 1 for a neighbour also matched in
-//     round r (that edge is seen from both sides), 0 for an older match.
-//     Every vertex's slots are streamed once, when it is matched.
+//     slot at or after ptr[v] (or the salt-max of the tied run it starts): one
+//     probe for most vertices, and every slot is skipped at most once.
+//   * Active lists: A_0 = every vertex with an edge; A_{r+1} = the vertices of
+//     A_r that found a candidate and stayed unmatched.  A live edge at round r
+//     has both endpoints in A_r, so "no candidate found in round r" is exactly
+//     "m_r = 0" (the loop's exit test, matchers.py:87-90).
+//   * RoundStats (matchers.py:113-118) without per-round edge counting: an edge
+//     dies in round min(mround[u], mround[v]) (the first round one of its ends
+//     is matched), so one pass over each edge once (the lower-id adjacency,
+//     lowpair) after the loop histograms the death rounds; m_r is the suffix sum.
 //
-// Per round r, two kernels:
-//   lmx_scan_round_kernel: removal count of M_{r-1} (block / warp / 8-lane /
-//     thread per vertex by remaining length) and the candidate probe of every
-//     active vertex A_r (thread per vertex);
-//   lmx_scan_match_kernel: mutual candidates -> matched/fresh bits, mate, the
-//     edge bit; appends M_r (bucketed by remaining length) and A_{r+1}.
-// The vertex state word mf[v / 32] = {matched bits, fresh bits}: fresh marks
-// M_r until the next match kernel clears it.
+// Kernels: lmx_scan_round_kernel (candidate probe of A_r, thread per vertex),
+// lmx_scan_match_kernel (mutual candidates -> bitmap, mate, mround, edge bit;
+// appends A_{r+1}), lmx_scan_hist_kernel (death-round histogram).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -43,6 +39,8 @@
 
 namespace lmx {
 
+constexpr int kHistBins = 256;   // death-round bins kept in shared memory (more go global)
+
 struct ScanArgs {
     const unsigned long long *vbeg;
     const uint32_t *deg0;
@@ -50,55 +48,23 @@ struct ScanArgs {
     uint32_t *cand_nbr;
     uint32_t *cand_id;
     const uint2 *ids;           // ids0, weight-descending per segment
-    const uint2 *mf;            // {matched, fresh} per 32 vertices
+    const uint32_t *matched;    // matched-vertex bitmap
     const uint32_t *alist;      // A_r
-    const uint32_t *mlist;      // M_{r-1}: kBuckets regions of capacity cap
-    unsigned long long cap;
-    RoundCtr *ctr;              // ctr[r]: pad[0] = |A_r|, n[q] = |M_{r-1} bucket q|
+    RoundCtr *ctr;              // ctr[r]: pad[0] = |A_r|, pad[1] = grab cursor
     uint64_t rs;                // round seed (tiebreak.py:40-52)
     uint32_t D;                 // distinct weight values; x >= D is a tied edge
     const uint32_t *tie_rank;
     const uint32_t *eid_of_x;
 };
 
-__device__ __forceinline__ bool mf_matched(const uint2 *mf, uint32_t u) {
-    return (mf[u >> 5].x >> (u & 31)) & 1u;
+__device__ __forceinline__ bool bit_set(const uint32_t *bits, uint32_t u) {
+    return (bits[u >> 5] >> (u & 31)) & 1u;
 }
 
-// Removal weight of slot neighbour u for a vertex matched in the last round.
-__device__ __forceinline__ uint32_t removal_weight(const uint2 *mf, uint32_t u) {
-    const uint2 w = mf[u >> 5];
-    const uint32_t s = u & 31;
-    const uint32_t m = (w.x >> s) & 1u, f = (w.y >> s) & 1u;
-    return m ? f : 2u;
-}
-
-// Removal count over [beg, beg + len) by a team of TEAM threads (t = rank in
-// the team): unaligned head slot, 16-byte slot pairs, tail slot.
-template <int TEAM>
-__device__ __forceinline__ uint32_t team_removal(const ScanArgs &a, unsigned long long beg, uint32_t len, uint32_t t,
-                                                 unsigned long long &reads) {
-    uint32_t acc = 0;
-    const uint32_t head = (uint32_t)(beg & 1ULL) < len ? (uint32_t)(beg & 1ULL) : len;
-    if (head && t == 0) acc += removal_weight(a.mf, __ldcs(a.ids + beg).x);
-    const uint32_t rest = len - head;
-    const uint32_t npairs = rest >> 1;
-    const uint4 *pp = reinterpret_cast<const uint4 *>(a.ids + beg + head);
-    constexpr int U = 4;
-    for (uint32_t c = t; c < npairs; c += TEAM * U) {
-        uint4 q[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const uint32_t i = c + j * TEAM;
-            q[j] = i < npairs ? __ldcs(pp + i) : make_uint4(kNone, 0, kNone, 0);
-        }
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-            if (q[j].x != kNone) acc += removal_weight(a.mf, q[j].x) + removal_weight(a.mf, q[j].z);
-    }
-    if ((rest & 1u) && t == 0) acc += removal_weight(a.mf, __ldcs(a.ids + beg + len - 1).x);
-    if (t == 0) reads += len;
-    return acc;
+__device__ __forceinline__ uint32_t lanemask_lt_u32() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
 // First live slot at or after p (p is left on it).  False when v has none.
@@ -114,7 +80,7 @@ __device__ __forceinline__ bool advance(const ScanArgs &a, unsigned long long b,
         uint32_t live = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if ((uint32_t)j < cnt && (FIRST || !mf_matched(a.mf, s[j].x))) live |= 1u << j;
+            if ((uint32_t)j < cnt && (FIRST || !bit_set(a.matched, s[j].x))) live |= 1u << j;
         if (live) {
             const int j0 = __ffs(live) - 1;
 #pragma unroll
@@ -139,7 +105,7 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
         const uint2 t = a.ids[b + q];
         ++reads;
         if (t.y < a.D || __ldg(a.tie_rank + (t.y - a.D)) != r0) break;
-        if (!FIRST && mf_matched(a.mf, t.x)) continue;
+        if (!FIRST && bit_set(a.matched, t.x)) continue;
         const uint64_t s = mix64((uint64_t)__ldg(a.eid_of_x + t.y) ^ a.rs);
         if (s > best) {
             best = s;
@@ -150,114 +116,12 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 
 template <bool FIRST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
-    __shared__ uint32_t s_item;
     __shared__ unsigned long long s_red[2][kWarps];
-    uint32_t nb[kBuckets];
-    uint32_t any = 0;
-#pragma unroll
-    for (int q = 0; q < kBuckets; ++q) {
-        nb[q] = FIRST ? 0u : a.ctr->n[q];
-        any |= nb[q];
-    }
     const uint32_t na = a.ctr->pad[0];
-    if ((any | na) == 0) return;
+    if (na == 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
-    unsigned long long removed2 = 0, reads = 0;
-
-    if (!FIRST) {
-        // removal of M_{r-1}: buckets 4 and 3, one block per vertex
-#pragma unroll 1
-        for (int q = kBuckets - 1; q >= 3; --q) {
-            for (;;) {
-                if (tid == 0) s_item = atomicAdd(&a.ctr->cur[q], 1u);
-                __syncthreads();
-                const uint32_t i = s_item;
-                __syncthreads();
-                if (i >= nb[q]) break;
-                const uint32_t v = a.mlist[(unsigned long long)q * a.cap + i];
-                const uint32_t p = a.ptr[v];
-                removed2 += team_removal<kBlock>(a, a.vbeg[v] + p, a.deg0[v] - p, tid, reads);
-            }
-        }
-        // bucket 2: warp per vertex, 8 per grab
-        for (;;) {
-            uint32_t i0 = 0;
-            if (lane == 0) i0 = atomicAdd(&a.ctr->cur[2], 8u);
-            i0 = __shfl_sync(0xffffffffu, i0, 0);
-            if (i0 >= nb[2]) break;
-            unsigned long long mb = 0;
-            uint32_t ml = 0;
-            if (lane < 8 && i0 + lane < nb[2]) {
-                const uint32_t v = a.mlist[2 * a.cap + i0 + lane];
-                const uint32_t p = a.ptr[v];
-                mb = a.vbeg[v] + p;
-                ml = a.deg0[v] - p;
-            }
-            const uint32_t cnt = min(8u, nb[2] - i0);
-            for (uint32_t k = 0; k < cnt; ++k) {
-                const unsigned long long beg = __shfl_sync(0xffffffffu, mb, k);
-                const uint32_t len = __shfl_sync(0xffffffffu, ml, k);
-                removed2 += team_removal<32>(a, beg, len, lane, reads);
-            }
-        }
-        // bucket 1: 8 lanes per vertex (<= 32 slots), 4 vertices per warp pass
-        for (;;) {
-            uint32_t i0 = 0;
-            if (lane == 0) i0 = atomicAdd(&a.ctr->cur[1], 16u);
-            i0 = __shfl_sync(0xffffffffu, i0, 0);
-            if (i0 >= nb[1]) break;
-            unsigned long long mb = 0;
-            uint32_t ml = 0;
-            if (lane < 16 && i0 + lane < nb[1]) {
-                const uint32_t v = a.mlist[a.cap + i0 + lane];
-                const uint32_t p = a.ptr[v];
-                mb = a.vbeg[v] + p;
-                ml = a.deg0[v] - p;
-            }
-#pragma unroll 1
-            for (int it = 0; it < 4; ++it) {
-                const int src = it * 4 + (lane >> 3);
-                const unsigned long long beg = __shfl_sync(0xffffffffu, mb, src);
-                const uint32_t len = __shfl_sync(0xffffffffu, ml, src);
-                const uint32_t gl = lane & 7;
-                uint32_t u[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t i = gl + 8 * j;
-                    u[j] = i < len ? __ldcs(a.ids + beg + i).x : kNone;
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (u[j] != kNone) removed2 += removal_weight(a.mf, u[j]);
-                if (gl == 0) reads += len;
-            }
-        }
-        // bucket 0: thread per vertex (<= 4 slots), 128 per grab
-        for (;;) {
-            uint32_t i0 = 0;
-            if (lane == 0) i0 = atomicAdd(&a.ctr->cur[0], 128u);
-            i0 = __shfl_sync(0xffffffffu, i0, 0);
-            if (i0 >= nb[0]) break;
-#pragma unroll 1
-            for (int it = 0; it < 4; ++it) {
-                const uint32_t i = i0 + it * 32 + lane;
-                if (i >= nb[0]) continue;
-                const uint32_t v = a.mlist[i];
-                const uint32_t p = a.ptr[v];
-                const unsigned long long beg = a.vbeg[v] + p;
-                const uint32_t len = a.deg0[v] - p;
-                uint32_t u[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) u[j] = (uint32_t)j < len ? __ldcs(a.ids + beg + j).x : kNone;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (u[j] != kNone) removed2 += removal_weight(a.mf, u[j]);
-                reads += len;
-            }
-        }
-    }
-
-    // candidate probe of A_r: thread per vertex, 4 vertices per lane per grab
+    unsigned long long found_n = 0, reads = 0;
+    // thread per vertex, 4 vertices per lane per grab
     for (;;) {
         uint32_t i0 = 0;
         if (lane == 0) i0 = atomicAdd(&a.ctr->pad[1], 128u);
@@ -281,13 +145,13 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
                 b[it] = 0;
             }
         }
-        // first probe of all four vertices at once (their chains overlap)
+        // first probe of all four vertices at once (their load chains overlap)
         uint2 s[4];
 #pragma unroll
         for (int it = 0; it < 4; ++it) s[it] = p[it] < d[it] ? a.ids[b[it] + p[it]] : make_uint2(kNone, kNone);
         bool live[4];
 #pragma unroll
-        for (int it = 0; it < 4; ++it) live[it] = s[it].x != kNone && (FIRST || !mf_matched(a.mf, s[it].x));
+        for (int it = 0; it < 4; ++it) live[it] = s[it].x != kNone && (FIRST || !bit_set(a.matched, s[it].x));
         // fast path: the probed slot is live and of a unique weight
         uint32_t slow = 0;
 #pragma unroll
@@ -297,6 +161,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             if (live[it] && s[it].y < a.D) {
                 a.cand_nbr[v[it]] = s[it].x;
                 a.cand_id[v[it]] = s[it].y;
+                ++found_n;
             } else {
                 slow |= 1u << it;
             }
@@ -329,17 +194,17 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             a.cand_nbr[vk] = found ? c.x : kNone;
             a.cand_id[vk] = found ? c.y : kNone;
             if (pp != pk) a.ptr[vk] = pp;
+            found_n += found ? 1u : 0u;
         }
     }
-
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        removed2 += __shfl_xor_sync(0xffffffffu, removed2, off);
+        found_n += __shfl_xor_sync(0xffffffffu, found_n, off);
         reads += __shfl_xor_sync(0xffffffffu, reads, off);
     }
     const int warp = tid >> 5;
     if (lane == 0) {
-        s_red[0][warp] = removed2;
+        s_red[0][warp] = found_n;
         s_red[1][warp] = reads;
     }
     __syncthreads();
@@ -349,7 +214,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             t0 += s_red[0][q];
             t1 += s_red[1][q];
         }
-        if (t0) atomicAdd(&a.ctr->live_slots, t0);
+        if (t0) atomicAdd(&a.ctr->live_slots, t0);   // scan loop: candidates found
         if (t1) atomicAdd(&a.ctr->slot_reads, t1);
     }
 }
@@ -357,124 +222,186 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
 struct ScanMatchArgs {
     const uint32_t *cand_nbr;
     const uint32_t *cand_id;
-    const uint32_t *ptr;
-    const uint32_t *deg0;
-    uint32_t *mf;                 // uint2 words viewed as u32 pairs
+    uint32_t *matched;
+    uint32_t *mround;             // round each vertex was matched in (~0 = never)
     long long *mate;
     const uint32_t *oldid;
     const uint32_t *alist;        // A_r
     uint32_t *anext;              // A_{r+1}
-    const uint32_t *mprev;        // M_{r-1} (fresh bits cleared here)
-    uint32_t *mnext;              // M_r, kBuckets regions
-    unsigned long long cap;
     uint32_t *ebits;
     const uint32_t *eid_of_x;
     RoundCtr *ctr;
     RoundCtr *ctr_next;
+    int round;
 };
 
-constexpr int kScanTargets = kBuckets + 1;   // M_r buckets, then A_{r+1}
-
-__device__ __forceinline__ uint32_t lanemask_lt_u32() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
 __global__ void __launch_bounds__(kBlock, 8) lmx_scan_match_kernel(ScanMatchArgs a) {
-    __shared__ uint32_t s_cnt[kScanTargets][kWarps];
-    __shared__ uint32_t s_base[kScanTargets];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned long long gtid = (unsigned long long)blockIdx.x * kBlock + tid;
-    const unsigned long long gstride = (unsigned long long)gridDim.x * kBlock;
-    // fresh bits of M_{r-1} end here (disjoint from the M_r bits set below)
-#pragma unroll 1
-    for (int q = 0; q < kBuckets; ++q) {
-        const uint32_t c = a.ctr->n[q];
-        for (unsigned long long i = gtid; i < c; i += gstride) {
-            const uint32_t v = a.mprev[(unsigned long long)q * a.cap + i];
-            atomicAnd(a.mf + 2 * (v >> 5) + 1, ~(1u << (v & 31)));
-        }
-    }
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ uint32_t s_base;
     const uint32_t total = a.ctr->pad[0];
     if (total == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = lanemask_lt_u32();
     unsigned long long matched_v = 0;
     constexpr int kItems = 4;
     const uint32_t tile = kBlock * kItems;
     for (uint32_t t0 = blockIdx.x * tile; t0 < total; t0 += gridDim.x * tile) {
-        uint32_t vv[kItems], kind[kItems];
-        uint32_t wc[kScanTargets];
-#pragma unroll
-        for (int q = 0; q < kScanTargets; ++q) wc[q] = 0;
+        uint32_t vv[kItems];
+        bool keep[kItems];
+        uint32_t wc = 0;
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
             const uint32_t i = t0 + j * kBlock + tid;
             const uint32_t v = i < total ? a.alist[i] : kNone;
-            uint32_t kd = kScanTargets;   // dropped
+            bool k = false;
             if (v != kNone) {
                 const uint32_t x = a.cand_nbr[v];
                 if (x != kNone) {
                     const uint32_t id = a.cand_id[v];
                     if (a.cand_id[x] == id) {   // weight keys are unique per edge
-                        atomicOr(a.mf + 2 * (v >> 5), 1u << (v & 31));
-                        atomicOr(a.mf + 2 * (v >> 5) + 1, 1u << (v & 31));
+                        atomicOr(a.matched + (v >> 5), 1u << (v & 31));
+                        a.mround[v] = (uint32_t)a.round;
                         if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
                         else a.mate[v] = (long long)x;
                         ++matched_v;
-                        if (v < x) {
+                        if (v < x) {   // the lower endpoint records the edge (graph.py:195-203)
                             const uint32_t e = a.eid_of_x[id];
                             atomicOr(a.ebits + (e >> 5), 1u << (e & 31));
                         }
-                        kd = (uint32_t)bucket_of(a.deg0[v] - a.ptr[v]);
                     } else {
-                        kd = kBuckets;   // stays active
+                        k = true;   // stays active
                     }
                 }
             }
             vv[j] = v;
-            kind[j] = kd;
-#pragma unroll
-            for (int q = 0; q < kScanTargets; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, kd == (uint32_t)q));
+            keep[j] = k;
+            wc += __popc(__ballot_sync(0xffffffffu, k));
         }
-        if (lane == 0) {
-#pragma unroll
-            for (int q = 0; q < kScanTargets; ++q) s_cnt[q][warp] = wc[q];
-        }
+        if (lane == 0) s_cnt[warp] = wc;
         __syncthreads();
-        if (tid < kScanTargets) {
+        if (tid == 0) {
             uint32_t sum = 0;
-            for (int w = 0; w < kWarps; ++w) sum += s_cnt[tid][w];
-            uint32_t base = 0;
-            if (sum) base = atomicAdd(tid < kBuckets ? &a.ctr_next->n[tid] : &a.ctr_next->pad[0], sum);
-            s_base[tid] = base;
+            for (int w = 0; w < kWarps; ++w) sum += s_cnt[w];
+            s_base = sum ? atomicAdd(&a.ctr_next->pad[0], sum) : 0u;
         }
         __syncthreads();
-        uint32_t pos[kScanTargets];
-#pragma unroll
-        for (int q = 0; q < kScanTargets; ++q) {
-            uint32_t p = s_base[q];
-            for (int w = 0; w < warp; ++w) p += s_cnt[q][w];
-            pos[q] = p;
-        }
+        uint32_t pos = s_base;
+        for (int w = 0; w < warp; ++w) pos += s_cnt[w];
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
-#pragma unroll
-            for (int q = 0; q < kScanTargets; ++q) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, kind[j] == (uint32_t)q);
-                if (kind[j] == (uint32_t)q) {
-                    const uint32_t p = pos[q] + __popc(bal & lt);
-                    if (q < kBuckets) a.mnext[(unsigned long long)q * a.cap + p] = vv[j];
-                    else a.anext[p] = vv[j];
-                }
-                pos[q] += __popc(bal);
-            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep[j]);
+            if (keep[j]) a.anext[pos + __popc(bal & lt)] = vv[j];
+            pos += __popc(bal);
         }
         __syncthreads();
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) matched_v += __shfl_xor_sync(0xffffffffu, matched_v, off);
     if (lane == 0 && matched_v) atomicAdd(&a.ctr->matched_v, matched_v);
+}
+
+// Death-round histogram: every edge once; it dies in round min(mround[v],
+// mround[u]).  Bins: [0, R) rounds, R = outlived the loop (must stay empty).
+// Most edges die in the first rounds: those bins count in registers.
+
+// mround packed for the histogram's random lookups (BITS = 4 or 8: small
+// enough to stay in L2; values saturate at the top value)
+template <int BITS>
+__global__ void lmx_pack_mround(const uint32_t *mround, unsigned long long n, uint32_t *packed) {
+    constexpr uint32_t kPer = 32 / BITS, kTop = (1u << BITS) - 1;
+    const unsigned long long words = (n + kPer - 1) / kPer;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+        uint32_t x = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; ++j) {
+            const unsigned long long v = w * kPer + j;
+            const uint32_t r = v < n ? min(mround[v], kTop) : kTop;
+            x |= r << (j * BITS);
+        }
+        packed[w] = x;
+    }
+}
+
+// The packed width is chosen so that every round of this run fits below the
+// top value (R < 2^BITS - 1): the top value means "never matched", exactly.
+template <int BITS>
+__device__ __forceinline__ uint32_t mround_of(const uint32_t *mround, const uint32_t *packed, uint32_t v) {
+    if (BITS == 32) return __ldg(mround + v);
+    constexpr uint32_t kPer = 32 / BITS, kTop = (1u << BITS) - 1;
+    return (__ldg(packed + v / kPer) >> ((v % kPer) * BITS)) & kTop;
+}
+
+// Per-thread counters of the first 4 * NACC bins: 16-bit fields in u64
+// registers (a thread sees far fewer than 2^16 edges); the rest use atomics.
+template <int NACC>
+struct HistAcc {
+    unsigned long long a[4] = {0, 0, 0, 0};
+    __device__ __forceinline__ void add(uint32_t d, uint32_t *s_hist, unsigned long long *hist) {
+        const unsigned long long inc = 1ULL << ((d & 3u) * 16u);
+        if (d < 4u) a[0] += inc;
+        else if (d < 8u) a[1] += inc;
+        else if (NACC > 2 && d < 12u) a[2] += inc;
+        else if (NACC > 2 && d < 16u) a[3] += inc;
+        else if (d < (uint32_t)kHistBins) atomicAdd(&s_hist[d], 1u);
+        else atomicAdd(hist + d, 1ULL);
+    }
+    __device__ __forceinline__ void flush(uint32_t *s_hist) {
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                uint32_t x = (uint32_t)((a[k] >> (16 * f)) & 0xFFFFULL);
+                for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+                if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_hist[4 * k + f], x);
+            }
+        }
+    }
+};
+
+// lowpair = {v, u} per edge, u < v, grouped by v: the v lookups walk mround
+// in order (cache lines reused), the u lookups go to the lower ids -- the
+// high-degree end after relabelling.  A flat, coalesced pass, 4 edges per
+// thread in flight.
+// (Staging the hubs' packed words in 64 KB of shared memory per block was
+// measured slower: the occupancy it costs outweighs the L2 lookups it saves.)
+template <int BITS>
+__global__ void __launch_bounds__(kBlock) lmx_scan_hist_kernel(const uint2 *lowpair, unsigned long long m,
+                                                             const uint32_t *mround, const uint32_t *packed,
+                                                             unsigned long long n, uint32_t R,
+                                                             unsigned long long *hist) {
+    __shared__ uint32_t s_hist[kHistBins];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kHistBins; i += kBlock) s_hist[i] = 0;
+    __syncthreads();
+    HistAcc<BITS == 4 ? 4 : 2> acc;
+    const uint4 *q = reinterpret_cast<const uint4 *>(lowpair);
+    const uint32_t nq = (uint32_t)(m / 2);   // m < 2^32
+    const uint32_t stride = gridDim.x * kBlock;
+    for (uint32_t i = blockIdx.x * kBlock + tid; i < nq; i += 2 * stride) {
+        const uint4 x0 = __ldcs(q + i);
+        const bool has1 = i + stride < nq;
+        const uint4 x1 = has1 ? __ldcs(q + i + stride) : make_uint4(0, 0, 0, 0);
+        const uint32_t a0 = mround_of<BITS>(mround, packed, x0.x), b0 = mround_of<BITS>(mround, packed, x0.y);
+        const uint32_t a1 = mround_of<BITS>(mround, packed, x0.z), b1 = mround_of<BITS>(mround, packed, x0.w);
+        const uint32_t a2 = mround_of<BITS>(mround, packed, x1.x), b2 = mround_of<BITS>(mround, packed, x1.y);
+        const uint32_t a3 = mround_of<BITS>(mround, packed, x1.z), b3 = mround_of<BITS>(mround, packed, x1.w);
+        acc.add(min(min(a0, b0), R), s_hist, hist);
+        acc.add(min(min(a1, b1), R), s_hist, hist);
+        if (has1) {
+            acc.add(min(min(a2, b2), R), s_hist, hist);
+            acc.add(min(min(a3, b3), R), s_hist, hist);
+        }
+    }
+    if ((m & 1ULL) && blockIdx.x == 0 && tid == 0) {
+        const uint2 x = lowpair[m - 1];
+        acc.add(min(min(mround_of<BITS>(mround, packed, x.x), mround_of<BITS>(mround, packed, x.y)), R), s_hist,
+                hist);
+    }
+    acc.flush(s_hist);
+    __syncthreads();
+    for (int i = tid; i < kHistBins; i += kBlock)
+        if (s_hist[i]) atomicAdd(hist + i, (unsigned long long)s_hist[i]);
 }
 
 }  // namespace lmx
@@ -489,14 +416,6 @@ int lmx_scan_configure_grids(lmx_ctx *ctx) {
     ctx->scan_grid[0] = ctx->num_sms * std::max(occ0, 1);
     ctx->scan_grid[1] = ctx->num_sms * std::max(occ1, 1);
     ctx->scan_match_grid = ctx->num_sms * std::max(occm, 1);
-    return LMX_OK;
-}
-
-int lmx_scan_alloc(lmx_ctx *ctx) {
-    const size_t n = (size_t)std::max<int64_t>(ctx->n, 1);
-    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mf, ((n + 31) / 32) * 8, "matched/fresh"));
-    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mlists[i], nl * 4 * kBuckets, "mlists"));
     return LMX_OK;
 }
 
@@ -517,7 +436,8 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, st));
     if (n) {
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->mate_target, 0xFF, n * 8, st));   // -1
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mf, 0, (n + 31) / 32 * 8, st));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->matched, 0, (n + 31) / 32 * 4, st));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mround, 0xFF, n * 4, st));
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, cap * 4, st));
     }
     ctx->ctr_host[0] = RoundCtr{};
@@ -539,7 +459,6 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
 
     uint32_t *cand_nbr = reinterpret_cast<uint32_t *>(ctx->cand);
     uint32_t *cand_id = cand_nbr + cap;
-    std::vector<long long> live_m(1, (long long)ctx->m);   // m_r
     int r = 0, n_rounds = -1, batch = 6;
     while (n_rounds < 0 && ctx->m > 0) {
         LMX_TRY(lmx_ensure_ctr(ctx, r + batch + 1));
@@ -553,10 +472,8 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             a.cand_nbr = cand_nbr;
             a.cand_id = cand_id;
             a.ids = ctx->ids0;
-            a.mf = ctx->mf;
+            a.matched = ctx->matched;
             a.alist = alist;
-            a.mlist = ctx->mlists[(r + 1) & 1];   // M_{r-1}
-            a.cap = cap;
             a.ctr = ctx->ctr + r;
             a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
             a.D = ctx->n_distinct;
@@ -569,20 +486,17 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ScanMatchArgs ma;
             ma.cand_nbr = cand_nbr;
             ma.cand_id = cand_id;
-            ma.ptr = ctx->vdeg;
-            ma.deg0 = ctx->deg0;
-            ma.mf = reinterpret_cast<uint32_t *>(ctx->mf);
+            ma.matched = ctx->matched;
+            ma.mround = ctx->mround;
             ma.mate = ctx->mate_target;
             ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
             ma.alist = alist;
             ma.anext = ctx->lists[(r + 1) & 1];
-            ma.mprev = ctx->mlists[(r + 1) & 1];
-            ma.mnext = ctx->mlists[r & 1];
-            ma.cap = cap;
             ma.ebits = ctx->ebits;
             ma.eid_of_x = ctx->eid_of_x;
             ma.ctr = ctx->ctr + r;
             ma.ctr_next = ctx->ctr + r + 1;
+            ma.round = r;
             lmx_scan_match_kernel<<<ctx->scan_match_grid, kBlock, 0, st>>>(ma);
             LMX_CUDA(ctx, cudaGetLastError());
             LMX_TRY(tl_mark());
@@ -591,22 +505,50 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r0, ctx->ctr + r0, sizeof(RoundCtr) * (size_t)batch,
                                       cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
-        for (int i = std::max(r0, 1); i < r; ++i) {
-            const unsigned long long rem2 = ctx->ctr_host[i].live_slots;
-            if (rem2 & 1ULL) return lmx_fail(ctx, LMX_ECUDA, "internal: odd removal count");
-            live_m.push_back(live_m.back() - (long long)(rem2 / 2));
-            if (live_m.back() < 0) return lmx_fail(ctx, LMX_ECUDA, "internal: negative live edge count");
-        }
         for (int i = r0; i < r; ++i) {
-            if (live_m[(size_t)i] == 0) {
+            if (ctx->ctr_host[i].live_slots == 0) {   // no candidate anywhere: m_i = 0
                 n_rounds = i;
                 break;
             }
         }
         batch = 4;
     }
+    if (n_rounds < 0) n_rounds = 0;
+    // death-round histogram -> RoundStats: bins [0, n_rounds) plus "outlived"
+    const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
+    std::vector<unsigned long long> hist(nbins, 0);
+    if (ctx->m > 0) {
+        if (ctx->hist_cap < nbins) {
+            lmx_free(ctx, (void **)&ctx->hist, ctx->hist_cap * 8);
+            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, nbins * 8, "death histogram"));
+            ctx->hist_cap = nbins;
+        }
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
+        const int grid = ctx->num_sms * 8;
+        const int hgrid = grid;
+        const size_t hsm = 0;
+        const unsigned long long nn = (unsigned long long)n, mm = (unsigned long long)ctx->m;
+        const uint32_t R = (uint32_t)n_rounds;
+        if (n_rounds < 15) {
+            lmx_pack_mround<4><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
+            lmx_scan_hist_kernel<4><<<hgrid, kBlock, hsm, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                               ctx->hist);
+        } else if (n_rounds < 255) {
+            lmx_pack_mround<8><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
+            lmx_scan_hist_kernel<8><<<hgrid, kBlock, hsm, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                               ctx->hist);
+        } else {
+            lmx_scan_hist_kernel<32><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                             ctx->hist);
+        }
+        LMX_CUDA(ctx, cudaGetLastError());
+        LMX_TRY(tl_mark());
+        ctx->timing.round_launches += n_rounds < 255 ? 2 : 1;
+        LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    }
+    ctx->kernel_ms.clear();
     if (ctx->kernel_timing && tl_used > 1) {
-        ctx->kernel_ms.clear();
         for (int i = 1; i < tl_used; ++i) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ctx->tl_events[i - 1], ctx->tl_events[i]);
@@ -614,21 +556,26 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             if (i & 1) ctx->timing.round_kernel_ms += ms;
             else ctx->timing.match_kernel_ms += ms;
         }
-    } else {
-        ctx->kernel_ms.clear();
     }
     ctx->timing.rounds_executed = r;
-    if (n_rounds < 0) n_rounds = 0;
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+    unsigned long long total = 0;
+    for (size_t i = 0; i < nbins; ++i) total += hist[i];
+    if (total != (unsigned long long)ctx->m) return lmx_fail(ctx, LMX_ECUDA, "internal: death histogram size");
+    for (size_t i = (size_t)n_rounds; i < nbins; ++i)
+        if (hist[i]) return lmx_fail(ctx, LMX_ECUDA, "internal: an edge outlived the round loop");
+    long long live = ctx->m;
     unsigned long long total_matched_v = 0;
     for (int i = 0; i < n_rounds; ++i) {
         const RoundCtr &c = ctx->ctr_host[i];
         if (c.matched_v & 1ULL) return lmx_fail(ctx, LMX_ECUDA, "internal: odd matched-vertex count");
+        if (live <= 0) return lmx_fail(ctx, LMX_ECUDA, "internal: a round without live edges");
         lmx_round_stats s;
-        s.edges_before = (int64_t)live_m[(size_t)i];
+        s.edges_before = live;
         s.edges_matched = (int64_t)(c.matched_v / 2);
-        s.edges_removed = (int64_t)(live_m[(size_t)i] - live_m[(size_t)i + 1]);
+        s.edges_removed = (int64_t)hist[(size_t)i];
         stats.push_back(s);
+        live -= (long long)hist[(size_t)i];
         total_matched_v += c.matched_v;
     }
     for (int i = 0; i < r; ++i) ctx->timing.slot_reads += (int64_t)ctx->ctr_host[i].slot_reads;

@@ -115,8 +115,8 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->mate,     (void **)&ctx->sort_tmp,    (void **)&ctx->eid_of_x,
                      (void **)&ctx->tie_rank, (void **)&ctx->oldid,
                      (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
-                     (void **)&ctx->send_cnt, (void **)&ctx->mf, (void **)&ctx->mlists[0],
-                     (void **)&ctx->mlists[1]};
+                     (void **)&ctx->send_cnt, (void **)&ctx->mround, (void **)&ctx->lowbeg,
+                     (void **)&ctx->lowpair, (void **)&ctx->hist, (void **)&ctx->mpacked};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -127,6 +127,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
     ctx->algo = 0;
+    ctx->hist_cap = 0;
     ctx->send_cap = ctx->recv_cap = 0;
     ctx->n_local = ctx->slots_local = 0;
     for (int q = 0; q < kBuckets; ++q) ctx->n_bins0[q] = 0;
@@ -356,6 +357,33 @@ __global__ void k_slot_rank(const uint2 *ids, unsigned long long slots, uint32_t
     }
 }
 
+__global__ void k_low_count(const uint32_t *eu, const uint32_t *ev, unsigned long long m, const uint32_t *newid,
+                            uint32_t *cnt) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        uint32_t a = eu[e], b = ev[e];
+        if (newid) {
+            a = newid[a];
+            b = newid[b];
+        }
+        atomicAdd(cnt + max(a, b), 1u);
+    }
+}
+
+__global__ void k_low_fill(const uint32_t *eu, const uint32_t *ev, unsigned long long m, const uint32_t *newid,
+                           const unsigned long long *lowbeg, uint32_t *fill, uint2 *lowpair) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        uint32_t a = eu[e], b = ev[e];
+        if (newid) {
+            a = newid[a];
+            b = newid[b];
+        }
+        const uint32_t hi = max(a, b), lo = min(a, b);
+        lowpair[lowbeg[hi] + atomicAdd(fill + hi, 1u)] = make_uint2(hi, lo);
+    }
+}
+
 struct SubBase {
     unsigned long long base;
     __host__ __device__ long long operator()(unsigned long long x) const { return (long long)(x - base); }
@@ -364,6 +392,36 @@ struct SubBase {
 }  // namespace lmx
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work);
+
+// lowpair: every edge once as {higher id, lower id} (device ids), grouped by
+// the higher id -- the death-round histogram's edge list (lmx_scan.cu).
+static int build_low_adjacency(lmx_ctx *ctx, const uint32_t *newid) {
+    cudaStream_t st = ctx->stream;
+    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lowbeg, (n + 1) * 8, "lowbeg"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(m, 1) * 8, "lowpair"));
+    uint32_t *cnt = ctx->vdeg;   // scratch u32[n] (single partition: n_local == n)
+    LMX_CUDA(ctx, cudaMemsetAsync(cnt, 0, std::max<size_t>(n, 1) * 4, st));
+    k_low_count<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, newid, cnt);
+    LMX_CUDA(ctx, cudaGetLastError());
+    k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(cnt, ctx->lowbeg, n);
+    LMX_CUDA(ctx, cudaGetLastError());
+    size_t tmp = 0;
+    LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->lowbeg, ctx->lowbeg, (long long)(n + 1), st));
+    void *t = nullptr;
+    LMX_TRY(lmx_alloc(ctx, &t, tmp, "scan tmp"));
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(t, tmp, ctx->lowbeg, ctx->lowbeg, (long long)(n + 1), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, std::max<size_t>(n, 1) * 4, st);
+    if (e == cudaSuccess) {
+        k_low_fill<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, newid, ctx->lowbeg, cnt, ctx->lowpair);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    lmx_free(ctx, &t, tmp);
+    lmx_free(ctx, (void **)&ctx->lowbeg, (n + 1) * 8);
+    LMX_CUDA(ctx, e);
+    return LMX_OK;
+}
 
 // Sort every vertex segment of ids0 by weight rank, descending (the scan
 // algorithm's fixed candidate order, lmx_scan.cu).  CUB segmented sort, in
@@ -692,19 +750,21 @@ int lmx_setup_slots(lmx_ctx *ctx) {
                                                       ctx->layout == kDistinct, ctx->wk0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
-    LMX_CUDA(ctx, cudaStreamSynchronize(st));
-    lmx_free(ctx, (void **)&newid, n * 4);
-    lmx_free(ctx, (void **)&kofe, m * 4);
-    trace_mark(ctx, "slot scatter");
     // round-loop algorithm: the weight-ordered scan needs (almost) distinct
     // weights (a fixed key order) and the whole graph in one context
     ctx->algo = 0;
     if (m && ctx->layout == kDistinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0)
         ctx->algo = 1;
+    if (ctx->algo == 1) LMX_TRY(build_low_adjacency(ctx, newid));
+    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    lmx_free(ctx, (void **)&newid, n * 4);
+    lmx_free(ctx, (void **)&kofe, m * 4);
+    trace_mark(ctx, "slot scatter");
     if (ctx->algo == 1) {
         LMX_TRY(sort_segments_by_weight(ctx, slots));
         lmx_free(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8);   // no working copy
-        LMX_TRY(lmx_scan_alloc(ctx));
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mround, std::max<size_t>(n, 1) * 4, "mround"));
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mpacked, (std::max<size_t>(n, 1) + 3) / 4 * 4, "mround packed"));
         trace_mark(ctx, "weight-ordered segments");
     }
     // round-0 bucket lists of the owned vertices (local indices, ascending)

@@ -30,7 +30,7 @@ LMX_HOST, LMX_DEVICE = 0, 1
 
 EXPORTED_SYMBOLS = (
     "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
-    "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times",
+    "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times", "lmx_last_round_counters",
     "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
@@ -87,6 +87,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_last_timing": (c_int, [p, ctypes.POINTER(LmxTiming)]),
             "lmx_last_rounds": (c_int, [p, p, c_int]),
             "lmx_last_kernel_times": (c_int, [p, p, c_int]),
+            "lmx_last_round_counters": (c_int, [p, p, c_int]),
             "lmx_local_max": (c_int, [c_int, i64, i64, p, p, p, u64, c_int, p, p, p, p, c_int, p,
                                       ctypes.c_char_p, ctypes.c_size_t]),
             "lmx_build_graph": (c_int, [p, i64, p, p, p, i64, c_int]),
@@ -265,6 +266,13 @@ class Engine:
         self._lib.lmx_last_kernel_times(self._h, buf, k)
         v = list(buf[:k])
         return [(v[i], v[i + 1] if i + 1 < k else 0.0) for i in range(0, k, 2)]
+
+    def last_round_counters(self) -> np.ndarray:
+        """int64 [rounds_executed, 8] device counters of the last match (diagnostics)."""
+        k = self._lib.lmx_last_round_counters(self._h, None, 0)
+        out = np.zeros((max(k, 1), 8), dtype=np.int64)
+        self._lib.lmx_last_round_counters(self._h, out.ctypes.data, k)
+        return out[:k]
 
     def last_timing(self) -> dict:
         t = LmxTiming()
