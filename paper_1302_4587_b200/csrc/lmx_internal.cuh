@@ -149,6 +149,7 @@ struct lmx_ctx {
     unsigned long long *lowbeg = nullptr;    // scan (load time only): [n+1] offsets of lowpair
     uint2 *lowpair = nullptr;                // scan: each edge once as {higher id, lower id}, by higher id
     uint32_t *mpacked = nullptr;             // scan: mround packed to 4 / 8 bits (n bytes)
+    uint2 *cand0 = nullptr;                  // scan: first slot of each segment (round-0 candidates)
     unsigned long long *hist = nullptr;      // scan: death-round histogram
     size_t hist_cap = 0;
 

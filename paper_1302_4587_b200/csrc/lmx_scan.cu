@@ -45,8 +45,8 @@ struct ScanArgs {
     const unsigned long long *vbeg;
     const uint32_t *deg0;
     uint32_t *ptr;              // first possibly-live slot of each vertex (segment offset)
-    uint32_t *cand_nbr;
-    uint32_t *cand_id;
+    uint2 *cand;                // {nbr, weight key} of each vertex's candidate
+    const uint2 *cand0;         // round-0 candidates: the first slot of each segment
     const uint2 *ids;           // ids0, weight-descending per segment
     const uint32_t *matched;    // matched-vertex bitmap
     const uint32_t *alist;      // A_r
@@ -114,6 +114,11 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
     }
 }
 
+// Round 0: every candidate is the first slot of its segment (cand0, built at
+// load), unless that slot's weight is tied.  Round r >= 1: the last round's
+// candidate is re-checked first -- it is still the candidate if its
+// neighbour is unmatched and its weight unique, so most vertices read 12
+// bytes (list, cand) plus one bitmap bit and write nothing.
 template <bool FIRST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
     __shared__ unsigned long long s_red[2][kWarps];
@@ -127,72 +132,60 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
         if (lane == 0) i0 = atomicAdd(&a.ctr->pad[1], 128u);
         i0 = __shfl_sync(0xffffffffu, i0, 0);
         if (i0 >= na) break;
-        uint32_t v[4], p[4], d[4];
-        unsigned long long b[4];
+        uint32_t v[4];
+        uint2 c[4];
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
             const uint32_t i = i0 + it * 32 + lane;
             v[it] = i < na ? a.alist[i] : kNone;
         }
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            if (v[it] != kNone) {
-                p[it] = FIRST ? 0u : a.ptr[v[it]];
-                d[it] = a.deg0[v[it]];
-                b[it] = a.vbeg[v[it]];
-            } else {
-                p[it] = d[it] = 0;
-                b[it] = 0;
-            }
-        }
-        // first probe of all four vertices at once (their load chains overlap)
-        uint2 s[4];
+        for (int it = 0; it < 4; ++it) c[it] = v[it] != kNone ? (FIRST ? a.cand0[v[it]] : a.cand[v[it]])
+                                                             : make_uint2(kNone, kNone);
+        bool keep[4];
 #pragma unroll
-        for (int it = 0; it < 4; ++it) s[it] = p[it] < d[it] ? a.ids[b[it] + p[it]] : make_uint2(kNone, kNone);
-        bool live[4];
-#pragma unroll
-        for (int it = 0; it < 4; ++it) live[it] = s[it].x != kNone && (FIRST || !bit_set(a.matched, s[it].x));
-        // fast path: the probed slot is live and of a unique weight
+        for (int it = 0; it < 4; ++it)
+            keep[it] = c[it].x != kNone && c[it].y < a.D && (FIRST || !bit_set(a.matched, c[it].x));
         uint32_t slow = 0;
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
             if (v[it] == kNone) continue;
-            reads += 1;
-            if (live[it] && s[it].y < a.D) {
-                a.cand_nbr[v[it]] = s[it].x;
-                a.cand_id[v[it]] = s[it].y;
+            if (keep[it]) {
+                if (FIRST) a.cand[v[it]] = c[it];
                 ++found_n;
             } else {
                 slow |= 1u << it;
             }
         }
-        // slow path (dead probe or tied weight), one vertex at a time
+        // slow path: the candidate died (advance past dead slots) or its weight is tied
         while (slow) {
             const int k = __ffs(slow) - 1;
             slow &= slow - 1;
-            uint32_t vk = 0, pk = 0, dk = 0;
-            unsigned long long bk = 0;
-            uint2 c = make_uint2(kNone, kNone);
-            bool found = false;
+            uint32_t vk = 0;
+            uint2 ck = make_uint2(kNone, kNone);
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
                 if (it == k) {
                     vk = v[it];
-                    pk = p[it];
-                    dk = d[it];
-                    bk = b[it];
-                    c = s[it];
-                    found = live[it];
+                    ck = c[it];
                 }
             }
+            const uint32_t pk = FIRST ? 0u : a.ptr[vk];
+            const uint32_t dk = a.deg0[vk];
+            const unsigned long long bk = a.vbeg[vk];
             uint32_t pp = pk;
-            if (!found && pk < dk) {
+            uint2 out = make_uint2(kNone, kNone);
+            bool found;
+            if (ck.x != kNone && (FIRST || !bit_set(a.matched, a.ids[bk + pk].x))) {
+                out = a.ids[bk + pk];   // live slot at ptr (a tied run starts here)
+                reads += 1;
+                found = true;
+            } else {
                 pp = pk + 1;
-                found = advance<FIRST>(a, bk, pp, dk, c, reads);
+                found = advance<FIRST>(a, bk, pp, dk, out, reads);
             }
-            if (found && c.y >= a.D) resolve_tie<FIRST>(a, bk, pp, dk, c, reads);
-            a.cand_nbr[vk] = found ? c.x : kNone;
-            a.cand_id[vk] = found ? c.y : kNone;
+            if (found && out.y >= a.D) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
+            a.cand[vk] = found ? out : make_uint2(kNone, kNone);
             if (pp != pk) a.ptr[vk] = pp;
             found_n += found ? 1u : 0u;
         }
@@ -220,8 +213,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
 }
 
 struct ScanMatchArgs {
-    const uint32_t *cand_nbr;
-    const uint32_t *cand_id;
+    const uint2 *cand;
     uint32_t *matched;
     uint32_t *mround;             // round each vertex was matched in (~0 = never)
     long long *mate;
@@ -255,10 +247,11 @@ __global__ void __launch_bounds__(kBlock, 8) lmx_scan_match_kernel(ScanMatchArgs
             const uint32_t v = i < total ? a.alist[i] : kNone;
             bool k = false;
             if (v != kNone) {
-                const uint32_t x = a.cand_nbr[v];
+                const uint2 cv = a.cand[v];
+                const uint32_t x = cv.x;
                 if (x != kNone) {
-                    const uint32_t id = a.cand_id[v];
-                    if (a.cand_id[x] == id) {   // weight keys are unique per edge
+                    const uint32_t id = cv.y;
+                    if (a.cand[x].y == id) {   // weight keys are unique per edge
                         atomicOr(a.matched + (v >> 5), 1u << (v & 31));
                         a.mround[v] = (uint32_t)a.round;
                         if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
@@ -457,8 +450,6 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     };
     LMX_TRY(tl_mark());
 
-    uint32_t *cand_nbr = reinterpret_cast<uint32_t *>(ctx->cand);
-    uint32_t *cand_id = cand_nbr + cap;
     int r = 0, n_rounds = -1, batch = 6;
     while (n_rounds < 0 && ctx->m > 0) {
         LMX_TRY(lmx_ensure_ctr(ctx, r + batch + 1));
@@ -469,8 +460,8 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             a.vbeg = ctx->vbeg;
             a.deg0 = ctx->deg0;
             a.ptr = ctx->vdeg;
-            a.cand_nbr = cand_nbr;
-            a.cand_id = cand_id;
+            a.cand = ctx->cand;
+            a.cand0 = ctx->cand0;
             a.ids = ctx->ids0;
             a.matched = ctx->matched;
             a.alist = alist;
@@ -484,8 +475,7 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             LMX_CUDA(ctx, cudaGetLastError());
             LMX_TRY(tl_mark());
             ScanMatchArgs ma;
-            ma.cand_nbr = cand_nbr;
-            ma.cand_id = cand_id;
+            ma.cand = ctx->cand;
             ma.matched = ctx->matched;
             ma.mround = ctx->mround;
             ma.mate = ctx->mate_target;

@@ -116,7 +116,8 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->tie_rank, (void **)&ctx->oldid,
                      (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
                      (void **)&ctx->send_cnt, (void **)&ctx->mround, (void **)&ctx->lowbeg,
-                     (void **)&ctx->lowpair, (void **)&ctx->hist, (void **)&ctx->mpacked};
+                     (void **)&ctx->lowpair, (void **)&ctx->hist, (void **)&ctx->mpacked,
+                     (void **)&ctx->cand0};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -382,6 +383,13 @@ __global__ void k_low_fill(const uint32_t *eu, const uint32_t *ev, unsigned long
         const uint32_t hi = max(a, b), lo = min(a, b);
         lowpair[lowbeg[hi] + atomicAdd(fill + hi, 1u)] = make_uint2(hi, lo);
     }
+}
+
+__global__ void k_cand0(const unsigned long long *vbeg, const uint32_t *deg, const uint2 *ids,
+                        unsigned long long n, uint2 *cand0) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+        cand0[v] = deg[v] ? ids[vbeg[v]] : make_uint2(kNone, kNone);
 }
 
 struct SubBase {
@@ -765,6 +773,9 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         lmx_free(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8);   // no working copy
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mround, std::max<size_t>(n, 1) * 4, "mround"));
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mpacked, (std::max<size_t>(n, 1) + 3) / 4 * 4, "mround packed"));
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand0, std::max<size_t>(n, 1) * 8, "cand0"));
+        k_cand0<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->vbeg, ctx->deg0, ctx->ids0, n, ctx->cand0);
+        LMX_CUDA(ctx, cudaGetLastError());
         trace_mark(ctx, "weight-ordered segments");
     }
     // round-0 bucket lists of the owned vertices (local indices, ascending)
