@@ -189,6 +189,64 @@ def cpu_baseline_leg(eng_sample_scale: int):
     }
 
 
+def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_rounds, B_floor, peak, peak_src,
+                  traffic):
+    """Roofline of the dominant kernel.  Scan loop: the
+    candidate-probe kernel (largest share of the step), with its algorithmic
+    bytes from the device counters of the step: per probed vertex 12 B (list
+    entry + candidate; round 0 also writes the candidate, +8 B), per slow-path
+    vertex 28 B (ptr, degree, offset, candidate write), 8 B per slot read.
+    Compacting loop: SURVEY.md §8d's B_floor over the round kernel."""
+    src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else \
+        "fallback 6.65 TB/s (B200_PROFILING.md)"
+    want = "lmx_scan_round_kernel" if algo == "scan" else "lmx_round_kernel"
+    if traffic and traffic.get("kernel") != want:
+        traffic = None   # a capture of another kernel
+    if algo == "scan":
+        A = [int(c[3]) for c in ctr]
+        slow = [int(c[4]) for c in ctr]
+        reads = [int(c[0]) for c in ctr]
+        probe_bytes = sum(12 * a + 28 * s + 8 * r for a, s, r in zip(A, slow, reads)) + (8 * A[0] if A else 0)
+        launches = sum(1 for a in A if a > 0)
+        match_bytes = sum(20 * a for a in A)
+        hist_bytes = 8 * m + 5 * n
+        achieved = probe_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else None
+        return {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "kernel": "lmx_scan_round_kernel (candidate probes, all rounds)",
+            "algorithmic_bytes_per_step": probe_bytes,
+            "algorithmic_bytes_per_launch": probe_bytes / max(launches, 1),
+            "kernel_ms_per_step": probe_ms, "peak_source": src,
+            "traffic_source": traffic.get("source") if traffic else None,
+            "other_kernels": {
+                "lmx_scan_match_kernel": {"ms_per_step": match_ms, "algorithmic_bytes": match_bytes,
+                                          "achieved_gbs": match_bytes / (match_ms / 1000.0) / 1e9
+                                          if match_ms > 0 else None},
+                "lmx_scan_hist_kernel (+ pack)": {"ms_per_step": hist_ms, "algorithmic_bytes": hist_bytes,
+                                                  "achieved_gbs": hist_bytes / (hist_ms / 1000.0) / 1e9
+                                                  if hist_ms > 0 else None},
+            },
+            "compacting_floor": {
+                "bytes": B_floor, "ms_at_peak": B_floor / (peak * 1e9) * 1000.0,
+                "note": "SURVEY.md 8d floor of the per-round compacting algorithm (every live slot read and "
+                        "every survivor written each round); the weight-ordered scan moves less than this, so "
+                        "the step can finish below ms_at_peak"},
+        }
+    achieved = B_floor / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else None
+    return {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak if achieved else None,
+        "traffic": traffic.get("bytes_per_launch") if traffic else None,
+        "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds)",
+        "algorithmic_bytes_per_step": B_floor, "algorithmic_bytes_per_launch": B_floor / max(n_rounds, 1),
+        "kernel_ms_per_step": probe_ms, "match_kernel_ms_per_step": match_ms,
+        "step_frac": (B_floor / (ms_per_step / 1000.0) / 1e9) / peak, "peak_source": src,
+        "traffic_source": traffic.get("source") if traffic else None,
+    }
+
+
 def load_traffic(workload: str):
     p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     try:
@@ -305,7 +363,7 @@ def run_b200(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    rk_ms = mk_ms = 0.0
+    rk_ms = mk_ms = hk_ms = 0.0
     launches = 0
     rounds_exec = 0
     for _ in range(args.steps):
@@ -313,6 +371,7 @@ def run_b200(args):
         t = eng.last_timing()
         rk_ms += t["round_kernel_ms"]
         mk_ms += t["match_kernel_ms"]
+        hk_ms += t["hist_kernel_ms"]
         launches += t["round_launches"]
         rounds_exec += t["rounds_executed"]
     ev1.record(stream)
@@ -334,22 +393,10 @@ def run_b200(args):
     ms_per_step = T / args.steps
     value = world * m * args.steps / (T / 1000.0)
     peak, peak_src = measured_hbm_gbs()
-    rk_per_step = rk_ms / args.steps
-    achieved = B_floor / (rk_per_step / 1000.0) / 1e9 if rk_per_step > 0 else None
-    traffic = load_traffic(args.workload)
-    roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": (achieved / peak) if achieved else None,
-        "traffic": traffic.get("bytes_per_launch") if traffic else None,
-        "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds)",
-        "algorithmic_bytes_per_step": B_floor,
-        "algorithmic_bytes_per_launch": B_floor / max(len(rounds), 1),
-        "kernel_ms_per_step": rk_per_step, "match_kernel_ms_per_step": mk_ms / args.steps,
-        "step_frac": (B_floor / (ms_per_step / 1000.0) / 1e9) / peak,
-        "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else
-        "fallback 6.65 TB/s (B200_PROFILING.md)",
-        "traffic_source": traffic.get("source") if traffic else None,
-    }
+    algo = eng.algo()
+    roofline = step_roofline(algo, eng.last_round_counters(), rk_ms / args.steps, mk_ms / args.steps,
+                             hk_ms / args.steps, ms_per_step, n, m, len(rounds), B_floor, peak, peak_src,
+                             load_traffic(args.workload))
 
     # ---- e2e: public API with pinned host buffers, H2D + device build + match + D2H every step
     e2e = None
@@ -403,7 +450,7 @@ def run_b200(args):
             "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor 16",
                        "rmat_abc": list(RMAT_ABC), "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
                        "permuted_labels": True, "n": n, "m": m, "rounds": len(rounds),
-                       "matched_edges": n_matched, "S_over_m0": S / m0,
+                       "matched_edges": n_matched, "S_over_m0": S / m0, "round_loop": algo,
                        "parallelism": "dp1" if world == 1 else f"replicas{world}",
                        "l2": "inputs larger than L2 (slot records %.1f GB >> 126 MB)" % (2 * m * 12 / 1e9),
                        "setup_ms": setup_ms},

@@ -70,6 +70,7 @@ typedef struct {
     double round_kernel_ms; /* sum of round-kernel durations (LMX_OPT_KERNEL_TIMING) */
     double match_kernel_ms; /* sum of match-kernel durations (LMX_OPT_KERNEL_TIMING) */
     int64_t rounds_executed;/* rounds enqueued, incl. empty speculative ones */
+    double hist_kernel_ms;  /* scan loop: death-round histogram (LMX_OPT_KERNEL_TIMING) */
 } lmx_timing;
 
 /* options for lmx_set_option */

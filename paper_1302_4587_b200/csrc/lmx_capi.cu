@@ -205,10 +205,11 @@ int lmx_last_round_counters(const lmx_ctx *ctx, int64_t *out, int cap_rounds) {
         o[0] = (int64_t)c.slot_reads;
         o[1] = (int64_t)c.live_slots;
         o[2] = (int64_t)c.matched_v;
-        // scan loop: |A_r| then |M_{r-1}| buckets 0..3 (4 folded into 3); compact: buckets 0..4
+        // scan loop: |A_r| (vertices probed), slow-path probes; compact: bucket sizes 0..4
         if (ctx->algo == 1) {
             o[3] = c.pad[0];
-            for (int q = 0; q < 4; ++q) o[4 + q] = c.n[q] + (q == 3 ? c.n[4] : 0);
+            o[4] = c.n[0];
+            o[5] = o[6] = o[7] = 0;
         } else {
             for (int q = 0; q < 5; ++q) o[3 + q] = c.n[q];
         }

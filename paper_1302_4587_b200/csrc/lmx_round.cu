@@ -920,6 +920,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     ctx->timing.slot_reads = 0;
     ctx->timing.round_kernel_ms = 0;
     ctx->timing.match_kernel_ms = 0;
+    ctx->timing.hist_kernel_ms = 0;
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     LMX_TRY(begin_match(ctx));
     // optional per-kernel timeline: tl[0] after init, then (after round r, after match r)

@@ -121,11 +121,11 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 // bytes (list, cand) plus one bitmap bit and write nothing.
 template <bool FIRST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
-    __shared__ unsigned long long s_red[2][kWarps];
+    __shared__ unsigned long long s_red[3][kWarps];
     const uint32_t na = a.ctr->pad[0];
     if (na == 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
-    unsigned long long found_n = 0, reads = 0;
+    unsigned long long found_n = 0, reads = 0, slow_n = 0;
     // thread per vertex, 4 vertices per lane per grab
     for (;;) {
         uint32_t i0 = 0;
@@ -188,27 +188,32 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             a.cand[vk] = found ? out : make_uint2(kNone, kNone);
             if (pp != pk) a.ptr[vk] = pp;
             found_n += found ? 1u : 0u;
+            ++slow_n;
         }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         found_n += __shfl_xor_sync(0xffffffffu, found_n, off);
         reads += __shfl_xor_sync(0xffffffffu, reads, off);
+        slow_n += __shfl_xor_sync(0xffffffffu, slow_n, off);
     }
     const int warp = tid >> 5;
     if (lane == 0) {
         s_red[0][warp] = found_n;
         s_red[1][warp] = reads;
+        s_red[2][warp] = slow_n;
     }
     __syncthreads();
     if (tid == 0) {
-        unsigned long long t0 = 0, t1 = 0;
+        unsigned long long t0 = 0, t1 = 0, t2 = 0;
         for (int q = 0; q < kWarps; ++q) {
             t0 += s_red[0][q];
             t1 += s_red[1][q];
+            t2 += s_red[2][q];
         }
         if (t0) atomicAdd(&a.ctr->live_slots, t0);   // scan loop: candidates found
         if (t1) atomicAdd(&a.ctr->slot_reads, t1);
+        if (t2) atomicAdd(&a.ctr->n[0], (unsigned int)t2);   // scan loop: slow-path vertices
     }
 }
 
@@ -538,10 +543,17 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
     }
     ctx->kernel_ms.clear();
+    ctx->timing.hist_kernel_ms = 0;
     if (ctx->kernel_timing && tl_used > 1) {
+        // timeline: init | round, match (per round) | histogram (pack + count)
+        const int hist_mark = ctx->m > 0 ? tl_used - 1 : -1;
         for (int i = 1; i < tl_used; ++i) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ctx->tl_events[i - 1], ctx->tl_events[i]);
+            if (i == hist_mark) {
+                ctx->timing.hist_kernel_ms = ms;
+                continue;
+            }
             ctx->kernel_ms.push_back(ms);
             if (i & 1) ctx->timing.round_kernel_ms += ms;
             else ctx->timing.match_kernel_ms += ms;

@@ -346,42 +346,61 @@ struct HasEdge {
     __device__ bool operator()(uint32_t v) const { return deg[v] > 0; }
 };
 
-// DISTINCT layout: dense weight rank of each slot's edge (tiebreak.py:105-113
-// order; a tied edge x >= D carries its group's rank).
-__global__ void k_slot_rank(const uint2 *ids, unsigned long long slots, uint32_t D, const uint32_t *tie_rank,
-                            uint32_t *rank) {
+// Scan loop slot stream: the edges in descending weight order (sorted
+// position j = m-1-i), two slot records each, keyed by their owner.  x is the
+// DISTINCT weight key of the sorted position (rank, or D + tie index).
+__global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
+                              const uint32_t *tidx, uint32_t D, unsigned long long m, const uint32_t *eu,
+                              const uint32_t *ev, const uint32_t *newid, uint32_t *okey, uint2 *sval) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < slots;
-         i += stride) {
-        const uint32_t x = ids[i].y;
-        rank[i] = x < D ? x : tie_rank[x - D];
-    }
-}
-
-__global__ void k_low_count(const uint32_t *eu, const uint32_t *ev, unsigned long long m, const uint32_t *newid,
-                            uint32_t *cnt) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const unsigned long long j = m - 1 - i;
+        const uint32_t e = eid_sorted[j];
+        const uint32_t x = tied[j] ? D + tidx[j] : rank[j];
         uint32_t a = eu[e], b = ev[e];
         if (newid) {
             a = newid[a];
             b = newid[b];
         }
-        atomicAdd(cnt + max(a, b), 1u);
+        okey[2 * i] = a;
+        sval[2 * i] = make_uint2(b, x);
+        okey[2 * i + 1] = b;
+        sval[2 * i + 1] = make_uint2(a, x);
     }
 }
 
-__global__ void k_low_fill(const uint32_t *eu, const uint32_t *ev, unsigned long long m, const uint32_t *newid,
-                           const unsigned long long *lowbeg, uint32_t *fill, uint2 *lowpair) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        uint32_t a = eu[e], b = ev[e];
-        if (newid) {
-            a = newid[a];
-            b = newid[b];
+// lowpair: every edge once as {owner v, neighbour u} with u < v, in slot order
+// (so grouped by v up to block interleaving).
+__global__ void k_low_select(const uint32_t *owner, const uint2 *ids, unsigned long long slots, uint2 *lowpair,
+                             unsigned long long *count) {
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ unsigned long long s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * kBlock; i0 < slots;
+         i0 += (unsigned long long)gridDim.x * kBlock) {
+        const unsigned long long i = i0 + tid;
+        uint32_t v = 0, u = 0;
+        bool take = false;
+        if (i < slots) {
+            v = owner[i];
+            u = ids[i].x;
+            take = u < v;
         }
-        const uint32_t hi = max(a, b), lo = min(a, b);
-        lowpair[lowbeg[hi] + atomicAdd(fill + hi, 1u)] = make_uint2(hi, lo);
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) s_cnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+            s_base = t ? atomicAdd(count, (unsigned long long)t) : 0ULL;
+        }
+        __syncthreads();
+        unsigned long long pos = s_base;
+        for (int w = 0; w < warp; ++w) pos += s_cnt[w];
+        if (take) lowpair[pos + __popc(bal & lt)] = make_uint2(v, u);
+        __syncthreads();
     }
 }
 
@@ -392,111 +411,66 @@ __global__ void k_cand0(const unsigned long long *vbeg, const uint32_t *deg, con
         cand0[v] = deg[v] ? ids[vbeg[v]] : make_uint2(kNone, kNone);
 }
 
-struct SubBase {
-    unsigned long long base;
-    __host__ __device__ long long operator()(unsigned long long x) const { return (long long)(x - base); }
-};
-
 }  // namespace lmx
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work);
 
-// lowpair: every edge once as {higher id, lower id} (device ids), grouped by
-// the higher id -- the death-round histogram's edge list (lmx_scan.cu).
-static int build_low_adjacency(lmx_ctx *ctx, const uint32_t *newid) {
+// Scan loop slots (lmx_scan.cu): ids0 with every vertex segment in descending
+// weight order, built by a stable radix sort by owner of the weight-descending
+// slot stream (no scatter, no per-segment sort), plus lowpair and cand0.
+// eid_sorted / rank / tied / tidx: the weight-key stage's sorted arrays.
+static int build_scan_slots(lmx_ctx *ctx, const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
+                            const uint32_t *tidx, const uint32_t *newid) {
     cudaStream_t st = ctx->stream;
-    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lowbeg, (n + 1) * 8, "lowbeg"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(m, 1) * 8, "lowpair"));
-    uint32_t *cnt = ctx->vdeg;   // scratch u32[n] (single partition: n_local == n)
-    LMX_CUDA(ctx, cudaMemsetAsync(cnt, 0, std::max<size_t>(n, 1) * 4, st));
-    k_low_count<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, newid, cnt);
-    LMX_CUDA(ctx, cudaGetLastError());
-    k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(cnt, ctx->lowbeg, n);
-    LMX_CUDA(ctx, cudaGetLastError());
-    size_t tmp = 0;
-    LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->lowbeg, ctx->lowbeg, (long long)(n + 1), st));
-    void *t = nullptr;
-    LMX_TRY(lmx_alloc(ctx, &t, tmp, "scan tmp"));
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(t, tmp, ctx->lowbeg, ctx->lowbeg, (long long)(n + 1), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, std::max<size_t>(n, 1) * 4, st);
-    if (e == cudaSuccess) {
-        k_low_fill<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, newid, ctx->lowbeg, cnt, ctx->lowpair);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    lmx_free(ctx, &t, tmp);
-    lmx_free(ctx, (void **)&ctx->lowbeg, (n + 1) * 8);
-    LMX_CUDA(ctx, e);
-    return LMX_OK;
-}
-
-// Sort every vertex segment of ids0 by weight rank, descending (the scan
-// algorithm's fixed candidate order, lmx_scan.cu).  CUB segmented sort, in
-// chunks of whole segments below its int item limit.
-static int sort_segments_by_weight(lmx_ctx *ctx, unsigned long long slots) {
-    cudaStream_t st = ctx->stream;
-    const unsigned long long nl = (unsigned long long)ctx->n_local;
-    if (slots == 0 || nl == 0) return LMX_OK;
-    uint32_t *k0 = nullptr, *k1 = nullptr;
-    LMX_TRY(lmx_alloc(ctx, (void **)&k0, slots * 4, "rank keys"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&k1, slots * 4, "rank keys out"));
-    k_slot_rank<<<grid_for(ctx, slots), kBlock, 0, st>>>(ctx->ids0, slots, ctx->n_distinct, ctx->tie_rank, k0);
-    LMX_CUDA(ctx, cudaGetLastError());
-    // chunk cut points (whole segments) by equal slot sums
-    const unsigned long long kChunk = 1ULL << 30;
-    const int p = (int)std::min<unsigned long long>((slots + kChunk - 1) / kChunk, 64ULL);
-    std::vector<unsigned long long> cuts(2, 0);
-    cuts[1] = nl;
-    if (p > 1) {
-        unsigned long long *dc = nullptr;
-        LMX_TRY(lmx_alloc(ctx, (void **)&dc, (size_t)(p + 1) * 8, "sort cuts"));
-        k_cuts<<<1, 64, 0, st>>>(ctx->vbeg, nl, p, dc);
-        cuts.assign((size_t)p + 1, 0);
-        cudaError_t e = cudaMemcpyAsync(cuts.data(), dc, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        lmx_free(ctx, (void **)&dc, (size_t)(p + 1) * 8);
-        LMX_CUDA(ctx, e);
-    }
-    std::vector<unsigned long long> offs(cuts.size());
-    for (size_t i = 0; i < cuts.size(); ++i)
-        LMX_CUDA(ctx, cudaMemcpyAsync(&offs[i], ctx->vbeg + cuts[i], 8, cudaMemcpyDeviceToHost, st));
-    LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m, slots = 2 * m;
+    uint32_t *okey = nullptr, *okey2 = nullptr;
+    uint2 *sval = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
+    int bits = 1;
+    while (bits < 32 && (1ULL << bits) < n) ++bits;
     int rc = LMX_OK;
-    for (size_t c = 0; c + 1 < cuts.size() && rc == LMX_OK; ++c) {
-        const unsigned long long v0 = cuts[c], v1 = cuts[c + 1];
-        const unsigned long long base = offs[c], items = offs[c + 1] - offs[c];
-        if (v1 <= v0 || items == 0) continue;
-        if (items > 0x7FFFFFFFULL) {
-            rc = lmx_fail(ctx, LMX_ELIMIT, "a vertex chunk exceeds the segmented sort's item limit");
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&okey, slots * 4, "owner keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&okey2, slots * 4, "owner keys out")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&sval, slots * 8, "slot stream")) != LMX_OK) break;
+        k_desc_stream<<<grid_for(ctx, m), kBlock, 0, st>>>(eid_sorted, rank, tied, tidx, ctx->n_distinct, m,
+                                                          ctx->eu, ctx->ev, newid, okey, sval);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots,
+                                                0, bits, st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots, 0, bits,
+                                            st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
+        lmx_free(ctx, (void **)&sval, slots * 8);
+        lmx_free(ctx, &tmp, tmp_bytes);
+        // lowpair: each edge once, from its higher-id end
+        unsigned long long *cnt = nullptr;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(m, 1) * 8, "lowpair")) !=
+            LMX_OK)
             break;
+        if ((rc = lmx_alloc(ctx, (void **)&cnt, 8, "lowpair count")) != LMX_OK) break;
+        e = cudaMemsetAsync(cnt, 0, 8, st);
+        if (e == cudaSuccess) {
+            k_low_select<<<ctx->num_sms * 8, kBlock, 0, st>>>(okey2, ctx->ids0, slots, ctx->lowpair, cnt);
+            e = cudaGetLastError();
         }
-        cub::TransformInputIterator<long long, SubBase, const unsigned long long *> ob(ctx->vbeg + v0, SubBase{base});
-        size_t need = 0;
-        cudaError_t e = cub::DeviceSegmentedSort::SortPairsDescending(
-            nullptr, need, k0 + base, k1 + base, ctx->ids0 + base, ctx->ids1 + base, (int)items, (int)(v1 - v0), ob,
-            ob + 1, st);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "segment sort sizing"); break; }
-        if (need > tmp_bytes) {
-            lmx_free(ctx, &tmp, tmp_bytes);
-            tmp_bytes = need;
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "segment sort tmp")) != LMX_OK) break;
-        }
-        e = cub::DeviceSegmentedSort::SortPairsDescending(tmp, need, k0 + base, k1 + base, ctx->ids0 + base,
-                                                          ctx->ids1 + base, (int)items, (int)(v1 - v0), ob, ob + 1,
-                                                          st);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "segment sort"); break; }
-    }
-    cudaError_t e = cudaStreamSynchronize(st);
+        unsigned long long got = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&got, cnt, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        lmx_free(ctx, (void **)&cnt, 8);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "lowpair"); break; }
+        if (got != m) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count"); break; }
+    } while (0);
+    cudaStreamSynchronize(st);
+    lmx_free(ctx, (void **)&okey, slots * 4);
+    lmx_free(ctx, (void **)&okey2, slots * 4);
+    lmx_free(ctx, (void **)&sval, slots * 8);
     lmx_free(ctx, &tmp, tmp_bytes);
-    lmx_free(ctx, (void **)&k0, slots * 4);
-    lmx_free(ctx, (void **)&k1, slots * 4);
-    if (rc != LMX_OK) return rc;
-    LMX_CUDA(ctx, e);
-    std::swap(ctx->ids0, ctx->ids1);   // sorted records become the pristine copy
-    return LMX_OK;
+    return rc;
 }
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work) {
@@ -653,7 +627,6 @@ int lmx_setup_slots(lmx_ctx *ctx) {
         ctx->deg0 = dl;
     }
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
     LMX_TRY(lmx_alloc_match_state(ctx));
     trace_mark(ctx, "offsets + allocation");
     // weight key per edge first (kofe), so the slot scatter writes final records
@@ -735,6 +708,16 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
+            // round-loop algorithm: the weight-ordered scan needs (almost) distinct
+            // weights (a fixed key order) and the whole graph in one context
+            if (distinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0) {
+                ctx->algo = 1;
+                lmx_free(ctx, (void **)&keys, m * 8);
+                lmx_free(ctx, (void **)&keys2, m * 8);
+                lmx_free(ctx, &tmp, tmp_bytes);
+                trace_mark(ctx, "weight keys");
+                if ((rc = build_scan_slots(ctx, vals2, vals, tied, tidx, newid)) != LMX_OK) break;
+            }
         } while (0);
         cudaStreamSynchronize(st);
         lmx_free(ctx, (void **)&keys, m * 8);
@@ -749,8 +732,9 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             return rc;
         }
     }
-    trace_mark(ctx, "weight keys");
-    if (m) {
+    trace_mark(ctx, ctx->algo == 1 ? "ordered slots + lowpair" : "weight keys");
+    if (m && ctx->algo == 0) {
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
         // fill counters reuse vdeg (local)
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
         k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
@@ -758,25 +742,17 @@ int lmx_setup_slots(lmx_ctx *ctx) {
                                                       ctx->layout == kDistinct, ctx->wk0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
-    // round-loop algorithm: the weight-ordered scan needs (almost) distinct
-    // weights (a fixed key order) and the whole graph in one context
-    ctx->algo = 0;
-    if (m && ctx->layout == kDistinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0)
-        ctx->algo = 1;
-    if (ctx->algo == 1) LMX_TRY(build_low_adjacency(ctx, newid));
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     lmx_free(ctx, (void **)&newid, n * 4);
     lmx_free(ctx, (void **)&kofe, m * 4);
     trace_mark(ctx, "slot scatter");
     if (ctx->algo == 1) {
-        LMX_TRY(sort_segments_by_weight(ctx, slots));
-        lmx_free(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8);   // no working copy
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mround, std::max<size_t>(n, 1) * 4, "mround"));
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mpacked, (std::max<size_t>(n, 1) + 3) / 4 * 4, "mround packed"));
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand0, std::max<size_t>(n, 1) * 8, "cand0"));
         k_cand0<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->vbeg, ctx->deg0, ctx->ids0, n, ctx->cand0);
         LMX_CUDA(ctx, cudaGetLastError());
-        trace_mark(ctx, "weight-ordered segments");
+        trace_mark(ctx, "scan state");
     }
     // round-0 bucket lists of the owned vertices (local indices, ascending)
     const size_t cap = std::max<size_t>(nl, 1);

@@ -57,7 +57,8 @@ class LmxTiming(ctypes.Structure):
     _fields_ = [("setup_ms", ctypes.c_double), ("rounds_ms", ctypes.c_double),
                 ("output_ms", ctypes.c_double), ("round_launches", ctypes.c_int64),
                 ("slot_reads", ctypes.c_int64), ("round_kernel_ms", ctypes.c_double),
-                ("match_kernel_ms", ctypes.c_double), ("rounds_executed", ctypes.c_int64)]
+                ("match_kernel_ms", ctypes.c_double), ("rounds_executed", ctypes.c_int64),
+                ("hist_kernel_ms", ctypes.c_double)]
 
 
 _lib = None
@@ -280,7 +281,7 @@ class Engine:
         return {"setup_ms": t.setup_ms, "rounds_ms": t.rounds_ms, "output_ms": t.output_ms,
                 "round_launches": int(t.round_launches), "slot_reads": int(t.slot_reads),
                 "round_kernel_ms": t.round_kernel_ms, "match_kernel_ms": t.match_kernel_ms,
-                "rounds_executed": int(t.rounds_executed)}
+                "rounds_executed": int(t.rounds_executed), "hist_kernel_ms": t.hist_kernel_ms}
 
     LAYOUTS = {"auto": -1, "uniform": 0, "distinct": 1, "general": 2}
 

@@ -7,14 +7,15 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from launches import load  # noqa: E402
 
 csv_path, workload, out = sys.argv[1], sys.argv[2], sys.argv[3]
+kernel = sys.argv[4] if len(sys.argv) > 4 else "lmx_scan_round_kernel"
 K = load(csv_path)
-rk = [v for v in K.values() if "lmx_round_kernel" in v["name"]]
+rk = [v for v in K.values() if kernel in v["name"]]
 tot_bytes = sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in rk)
 tot_ms = sum(v["gpu__time_duration.sum"] for v in rk)
 all_ms = sum(v["gpu__time_duration.sum"] for v in K.values())
 json.dump({
     "workload": workload,
-    "kernel": "lmx_round_kernel",
+    "kernel": kernel,
     "launches": len(rk),
     "bytes_per_launch": tot_bytes / max(len(rk), 1),
     "bytes_per_step": tot_bytes,
