@@ -272,7 +272,7 @@ static int build_from_raw(lmx_ctx *ctx, uint32_t *ru, uint32_t *rv, double *rw, 
     lmx_dfree(ctx, rv);
     lmx_dfree(ctx, rw);
     if (rc != LMX_OK) return rc;
-    return lmx_setup_slots(ctx);
+    return lmx_setup_device_edges(ctx);
 }
 
 static RmatParams rmat_params(int scale, double a, double b, double c, uint64_t seed, int permute) {

@@ -75,6 +75,9 @@ void lmx_destroy(lmx_ctx *ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
     for (cudaEvent_t e : ctx->tl_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->ev_copy)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

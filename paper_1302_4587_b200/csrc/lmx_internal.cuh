@@ -150,6 +150,11 @@ struct lmx_ctx {
     uint2 *lowpair = nullptr;                // scan: each edge once as {higher id, lower id}, by higher id
     uint32_t *mpacked = nullptr;             // scan: mround packed to 4 / 8 bits (n bytes)
     uint2 *cand0 = nullptr;                  // scan: first slot of each segment (round-0 candidates)
+    // weight-key stage results held until the slot build (load time only)
+    uint32_t *ws_kofe = nullptr;             // weight key per edge (compacting loop)
+    uint32_t *ws_rank = nullptr, *ws_eid = nullptr, *ws_tied = nullptr, *ws_tidx = nullptr;   // by sorted position
+    cudaStream_t copy_stream = nullptr;      // pinned-host loads: copy engine stream
+    cudaEvent_t ev_copy[3] = {nullptr, nullptr, nullptr};
     unsigned long long *hist = nullptr;      // scan: death-round histogram
     size_t hist_cap = 0;
 
@@ -182,7 +187,8 @@ void lmx_dfree(lmx_ctx *ctx, void *p);
 void lmx_flush_cache(lmx_ctx *ctx);
 void lmx_free(lmx_ctx *ctx, void **p, size_t bytes);
 void lmx_free_graph(lmx_ctx *ctx);
-int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w
+int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w (+ deg0, weight stage)
+int lmx_setup_device_edges(lmx_ctx *ctx);   // deg0 + weight stage + lmx_setup_slots for built eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);

@@ -117,7 +117,8 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->remote_ok, (void **)&ctx->send, (void **)&ctx->recv,
                      (void **)&ctx->send_cnt, (void **)&ctx->mround, (void **)&ctx->lowbeg,
                      (void **)&ctx->lowpair, (void **)&ctx->hist, (void **)&ctx->mpacked,
-                     (void **)&ctx->cand0};
+                     (void **)&ctx->cand0,    (void **)&ctx->ws_kofe,     (void **)&ctx->ws_rank,
+                     (void **)&ctx->ws_eid,   (void **)&ctx->ws_tied,     (void **)&ctx->ws_tidx};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -143,21 +144,54 @@ __device__ __forceinline__ unsigned long long canon_bits(double w) {
 }
 
 // graph.py:80-88: ids in range, weights finite and >= 0; plus no self loops
-// (a built Graph has none, graph.py:89-91).  Records the first bad position.
+// (a built Graph has none, graph.py:89-91).  Records the first bad position
+// and counts the degrees of the edges it narrows.
+__device__ __forceinline__ bool check_uv(long long a, long long b, long long n) {
+    return a >= 0 && b >= 0 && a < n && b < n && a != b;
+}
+__device__ __forceinline__ bool check_w(double x) { return isfinite(x) && !(x < 0.0); }
+
 __global__ void k_convert(const long long *u, const long long *v, const double *w,
                           unsigned long long k, long long n, unsigned long long base, uint32_t *eu,
-                          uint32_t *ev, double *wout, unsigned long long *bad) {
+                          uint32_t *ev, double *wout, uint32_t *deg, unsigned long long *bad) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += stride) {
         const long long a = u[i], b = v[i];
         const double x = w[i];
-        const bool ok = a >= 0 && b >= 0 && a < n && b < n && a != b && isfinite(x) && !(x < 0.0);
-        if (!ok) atomicMin(bad, base + i);
+        const bool uv = check_uv(a, b, n);
+        if (!uv || !check_w(x)) atomicMin(bad, base + i);
         eu[base + i] = (uint32_t)a;
         ev[base + i] = (uint32_t)b;
         wout[base + i] = x;
+        if (uv) {
+            atomicAdd(deg + a, 1u);
+            atomicAdd(deg + b, 1u);
+        }
     }
+}
+
+// Pinned-host load: endpoints staged by the copy engine, narrowed here.
+__global__ void k_convert_uv(const long long *u, const long long *v, unsigned long long m, long long n,
+                             uint32_t *eu, uint32_t *ev, uint32_t *deg, unsigned long long *bad) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const long long a = u[i], b = v[i];
+        eu[i] = (uint32_t)a;
+        ev[i] = (uint32_t)b;
+        if (check_uv(a, b, n)) {
+            atomicAdd(deg + a, 1u);
+            atomicAdd(deg + b, 1u);
+        } else {
+            atomicMin(bad, i);
+        }
+    }
+}
+
+__global__ void k_check_w(const double *w, unsigned long long m, unsigned long long *bad) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+        if (!check_w(w[i])) atomicMin(bad, i);
 }
 
 __global__ void k_degrees(const uint32_t *eu, const uint32_t *ev, unsigned long long m, uint32_t *deg) {
@@ -349,23 +383,52 @@ struct HasEdge {
 // Scan loop slot stream: the edges in descending weight order (sorted
 // position j = m-1-i), two slot records each, keyed by their owner.  x is the
 // DISTINCT weight key of the sorted position (rank, or D + tie index).
-__global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
-                              const uint32_t *tidx, uint32_t D, unsigned long long m, const uint32_t *eu,
-                              const uint32_t *ev, const uint32_t *newid, uint32_t *okey, uint2 *sval) {
+// Endpoints in device ids, packed per edge (one random 8-byte gather below
+// instead of two 4-byte ones; the relabel lookups run in edge order here).
+__global__ void k_pack_endpoints(const uint32_t *eu, const uint32_t *ev, const uint32_t *newid,
+                                 unsigned long long m, uint2 *euv) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-        const unsigned long long j = m - 1 - i;
-        const uint32_t e = eid_sorted[j];
-        const uint32_t x = tied[j] ? D + tidx[j] : rank[j];
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         uint32_t a = eu[e], b = ev[e];
         if (newid) {
             a = newid[a];
             b = newid[b];
         }
-        okey[2 * i] = a;
-        sval[2 * i] = make_uint2(b, x);
-        okey[2 * i + 1] = b;
-        sval[2 * i + 1] = make_uint2(a, x);
+        euv[e] = make_uint2(a, b);
+    }
+}
+
+// 4 edges per thread per step: the gathers of the step are in flight together.
+__global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
+                              const uint32_t *tidx, uint32_t D, unsigned long long m, const uint2 *euv,
+                              uint32_t *okey, uint2 *sval) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < m;
+         i0 += 4 * stride) {
+        uint32_t e[4], x[4];
+        uint2 p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long i = i0 + k * stride;
+            if (i < m) {
+                const unsigned long long j = m - 1 - i;
+                e[k] = eid_sorted[j];
+                x[k] = tied[j] ? D + tidx[j] : rank[j];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (i0 + k * stride < m) p[k] = euv[e[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long i = i0 + k * stride;
+            if (i < m) {
+                okey[2 * i] = p[k].x;
+                sval[2 * i] = make_uint2(p[k].y, x[k]);
+                okey[2 * i + 1] = p[k].y;
+                sval[2 * i + 1] = make_uint2(p[k].x, x[k]);
+            }
+        }
     }
 }
 
@@ -414,6 +477,7 @@ __global__ void k_cand0(const unsigned long long *vbeg, const uint32_t *deg, con
 }  // namespace lmx
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work);
+static void trace_mark(lmx_ctx *ctx, const char *what);
 
 // Scan loop slots (lmx_scan.cu): ids0 with every vertex segment in descending
 // weight order, built by a stable radix sort by owner of the weight-descending
@@ -434,17 +498,22 @@ static int build_scan_slots(lmx_ctx *ctx, const uint32_t *eid_sorted, const uint
         if ((rc = lmx_alloc(ctx, (void **)&okey, slots * 4, "owner keys")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&okey2, slots * 4, "owner keys out")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&sval, slots * 8, "slot stream")) != LMX_OK) break;
-        k_desc_stream<<<grid_for(ctx, m), kBlock, 0, st>>>(eid_sorted, rank, tied, tidx, ctx->n_distinct, m,
-                                                          ctx->eu, ctx->ev, newid, okey, sval);
+        // the packed endpoints borrow the owner-key output buffer (same size)
+        uint2 *euv = reinterpret_cast<uint2 *>(okey2);
+        k_pack_endpoints<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, newid, m, euv);
+        k_desc_stream<<<grid_for(ctx, m), kBlock, 0, st>>>(eid_sorted, rank, tied, tidx, ctx->n_distinct, m, euv,
+                                                          okey, sval);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess)
             e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots,
                                                 0, bits, st);
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
         if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
+        trace_mark(ctx, "  slot stream");
         e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots, 0, bits,
                                             st);
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
+        trace_mark(ctx, "  owner sort");
         lmx_free(ctx, (void **)&sval, slots * 8);
         lmx_free(ctx, &tmp, tmp_bytes);
         // lowpair: each edge once, from its higher-id end
@@ -494,18 +563,151 @@ static void trace_mark(lmx_ctx *ctx, const char *what) {
     last = now;
 }
 
-int lmx_setup_slots(lmx_ctx *ctx) {
-    trace_mark(ctx, "edges on device");
+// Weight keys (tiebreak.py:105-113 order) from ctx->w alone, so a pinned-host
+// load can run it while the endpoint arrays are still in flight: layout
+// choice, dense ranks and tie indices, and the round-loop algorithm.  Leaves
+// ctx->ws_kofe (weight key per edge; compacting loop) or ctx->ws_{rank, eid,
+// tied, tidx} (sorted-position arrays; scan loop) for lmx_setup_slots.
+static int weight_stage(lmx_ctx *ctx) {
+    const unsigned long long m = (unsigned long long)ctx->m;
+    cudaStream_t st = ctx->stream;
+    uint32_t *kofe = nullptr;
+    // weight key layout
+    bool uniform = true;
+    if (m) {
+        unsigned long long *mm = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&mm, 16, "minmax"));
+        unsigned long long init[2] = {~0ULL, 0ULL};
+        LMX_CUDA(ctx, cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
+        k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
+        LMX_CUDA(ctx, cudaGetLastError());
+        unsigned long long got[2];
+        LMX_CUDA(ctx, cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        lmx_free(ctx, (void **)&mm, 16);
+        uniform = got[0] == got[1];
+    }
+    ctx->layout = kUniform;
+    if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
+        unsigned long long *keys = nullptr, *keys2 = nullptr;
+        uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        int rc = LMX_OK;
+        do {
+            if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
+            if ((rc = lmx_alloc(ctx, (void **)&tidx, m * 4, "tie idx")) != LMX_OK) break;
+            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
+            size_t t1 = 0, t2 = 0;
+            cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, vals, vals2,
+                                                            (long long)m, 0, 64, st);
+            if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort sizing"); break; }
+            tmp_bytes = std::max(t1, t2);
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
+            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort"); break; }
+            // dense rank of the weight value (vals reused)
+            k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
+            e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank scan"); break; }
+            // tied flags and tie indices
+            k_tied<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, tied);
+            e = cub::DeviceScan::ExclusiveSum(tmp, t2, tied, tidx, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "tie scan"); break; }
+            uint32_t last_rank = 0, last_tidx = 0, last_tied = 0;
+            e = cudaMemcpyAsync(&last_rank, vals + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tidx, tidx + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tied, tied + m - 1, 4, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank readback"); break; }
+            const unsigned long long D = (unsigned long long)last_rank + 1;
+            const unsigned long long T = (unsigned long long)last_tidx + last_tied;
+            bool distinct = (T <= m / 16) && (D + T < 0xFFFFFFFFULL);
+            if (ctx->force_layout == kDistinct) distinct = D + T < 0xFFFFFFFFULL;
+            if (ctx->force_layout == kGeneral) distinct = false;
+            ctx->layout = distinct ? kDistinct : kGeneral;
+            ctx->n_distinct = (uint32_t)D;
+            ctx->n_tied = (uint32_t)T;
+            if ((rc = lmx_alloc(ctx, (void **)&kofe, m * 4, "key of edge")) != LMX_OK) break;
+            uint32_t *key_of_eid = kofe;
+            if (distinct) {
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->eid_of_x, (D + T) * 4, "eid_of_x")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4,
+                                    "tie_rank")) != LMX_OK)
+                    break;
+            }
+            k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
+                                                           (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
+            // round-loop algorithm: the weight-ordered scan needs (almost) distinct
+            // weights (a fixed key order) and the whole graph in one context
+            if (distinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0) {
+                ctx->algo = 1;
+                lmx_free(ctx, (void **)&keys, m * 8);
+                lmx_free(ctx, (void **)&keys2, m * 8);
+                lmx_free(ctx, &tmp, tmp_bytes);
+                // kept for the slot build (lmx_setup_slots: needs the relabelling)
+                ctx->ws_rank = vals;
+                ctx->ws_eid = vals2;
+                ctx->ws_tied = tied;
+                ctx->ws_tidx = tidx;
+                vals = vals2 = tied = tidx = nullptr;
+            }
+        } while (0);
+        cudaStreamSynchronize(st);
+        lmx_free(ctx, (void **)&keys, m * 8);
+        lmx_free(ctx, (void **)&keys2, m * 8);
+        lmx_free(ctx, (void **)&vals, m * 4);
+        lmx_free(ctx, (void **)&vals2, m * 4);
+        lmx_free(ctx, (void **)&tied, m * 4);
+        lmx_free(ctx, (void **)&tidx, m * 4);
+        lmx_free(ctx, &tmp, tmp_bytes);
+        if (rc != LMX_OK) {
+            lmx_free(ctx, (void **)&kofe, m * 4);
+            return rc;
+        }
+        if (ctx->algo == 1) lmx_free(ctx, (void **)&kofe, m * 4);   // the scan build derives x itself
+    }
+    ctx->ws_kofe = kofe;
+    return LMX_OK;
+}
+
+// Edge arrays already on the device (lmx_build.cu): degrees, weight stage, slots.
+int lmx_setup_device_edges(lmx_ctx *ctx) {
     const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
-    unsigned long long slots = 2 * m;   // becomes the owned slot count below
     cudaStream_t st = ctx->stream;
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4, "deg0"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (n + 1) * 8, "vbeg"));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->deg0, 0, std::max<size_t>(n, 1) * 4, st));
     if (m) {
         k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
+    LMX_TRY(weight_stage(ctx));
+    return lmx_setup_slots(ctx);
+}
+
+void lmx_free_weight_stage(lmx_ctx *ctx) {
+    const size_t m4 = (size_t)std::max<int64_t>(ctx->m, 1) * 4;
+    lmx_free(ctx, (void **)&ctx->ws_kofe, m4);
+    lmx_free(ctx, (void **)&ctx->ws_rank, m4);
+    lmx_free(ctx, (void **)&ctx->ws_eid, m4);
+    lmx_free(ctx, (void **)&ctx->ws_tied, m4);
+    lmx_free(ctx, (void **)&ctx->ws_tidx, m4);
+}
+
+int lmx_setup_slots(lmx_ctx *ctx) {
+    trace_mark(ctx, "edges on device");
+    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
+    unsigned long long slots = 2 * m;   // becomes the owned slot count below
+    cudaStream_t st = ctx->stream;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (n + 1) * 8, "vbeg"));   // deg0: counted at conversion
     // degree-descending relabelling of skewed graphs: hubs get
     // the low ids, so the matched bitmap and candidate lookups that follow
     // the skew hit a small, cache-resident id range, and equal-bucket
@@ -629,123 +831,27 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
     LMX_TRY(lmx_alloc_match_state(ctx));
     trace_mark(ctx, "offsets + allocation");
-    // weight key per edge first (kofe), so the slot scatter writes final records
-    uint32_t *kofe = nullptr;
-    // weight key layout
-    bool uniform = true;
-    if (m) {
-        unsigned long long *mm = nullptr;
-        LMX_TRY(lmx_alloc(ctx, (void **)&mm, 16, "minmax"));
-        unsigned long long init[2] = {~0ULL, 0ULL};
-        LMX_CUDA(ctx, cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
-        k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
-        LMX_CUDA(ctx, cudaGetLastError());
-        unsigned long long got[2];
-        LMX_CUDA(ctx, cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st));
-        LMX_CUDA(ctx, cudaStreamSynchronize(st));
-        lmx_free(ctx, (void **)&mm, 16);
-        uniform = got[0] == got[1];
+    if (ctx->algo == 1) {
+        LMX_TRY(build_scan_slots(ctx, ctx->ws_eid, ctx->ws_rank, ctx->ws_tied, ctx->ws_tidx, newid));
+        trace_mark(ctx, "ordered slots + lowpair");
     }
-    ctx->layout = kUniform;
-    if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
-        unsigned long long *keys = nullptr, *keys2 = nullptr;
-        uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
-        void *tmp = nullptr;
-        size_t tmp_bytes = 0;
-        int rc = LMX_OK;
-        do {
-            if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&tidx, m * 4, "tie idx")) != LMX_OK) break;
-            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
-            size_t t1 = 0, t2 = 0;
-            cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, vals, vals2,
-                                                            (long long)m, 0, 64, st);
-            if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort sizing"); break; }
-            tmp_bytes = std::max(t1, t2);
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort"); break; }
-            // dense rank of the weight value (vals reused)
-            k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
-            e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank scan"); break; }
-            // tied flags and tie indices
-            k_tied<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, tied);
-            e = cub::DeviceScan::ExclusiveSum(tmp, t2, tied, tidx, (long long)m, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "tie scan"); break; }
-            uint32_t last_rank = 0, last_tidx = 0, last_tied = 0;
-            e = cudaMemcpyAsync(&last_rank, vals + m - 1, 4, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tidx, tidx + m - 1, 4, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(&last_tied, tied + m - 1, 4, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank readback"); break; }
-            const unsigned long long D = (unsigned long long)last_rank + 1;
-            const unsigned long long T = (unsigned long long)last_tidx + last_tied;
-            bool distinct = (T <= m / 16) && (D + T < 0xFFFFFFFFULL);
-            if (ctx->force_layout == kDistinct) distinct = D + T < 0xFFFFFFFFULL;
-            if (ctx->force_layout == kGeneral) distinct = false;
-            ctx->layout = distinct ? kDistinct : kGeneral;
-            ctx->n_distinct = (uint32_t)D;
-            ctx->n_tied = (uint32_t)T;
-            if ((rc = lmx_alloc(ctx, (void **)&kofe, m * 4, "key of edge")) != LMX_OK) break;
-            uint32_t *key_of_eid = kofe;
-            if (distinct) {
-                if ((rc = lmx_alloc(ctx, (void **)&ctx->eid_of_x, (D + T) * 4, "eid_of_x")) != LMX_OK) break;
-                if ((rc = lmx_alloc(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4,
-                                    "tie_rank")) != LMX_OK)
-                    break;
-            } else {
-                if ((rc = lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0")) != LMX_OK) break;
-                if ((rc = lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1")) != LMX_OK) break;
-            }
-            k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
-                                                           (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
-            e = cudaGetLastError();
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
-            // round-loop algorithm: the weight-ordered scan needs (almost) distinct
-            // weights (a fixed key order) and the whole graph in one context
-            if (distinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0) {
-                ctx->algo = 1;
-                lmx_free(ctx, (void **)&keys, m * 8);
-                lmx_free(ctx, (void **)&keys2, m * 8);
-                lmx_free(ctx, &tmp, tmp_bytes);
-                trace_mark(ctx, "weight keys");
-                if ((rc = build_scan_slots(ctx, vals2, vals, tied, tidx, newid)) != LMX_OK) break;
-            }
-        } while (0);
-        cudaStreamSynchronize(st);
-        lmx_free(ctx, (void **)&keys, m * 8);
-        lmx_free(ctx, (void **)&keys2, m * 8);
-        lmx_free(ctx, (void **)&vals, m * 4);
-        lmx_free(ctx, (void **)&vals2, m * 4);
-        lmx_free(ctx, (void **)&tied, m * 4);
-        lmx_free(ctx, (void **)&tidx, m * 4);
-        lmx_free(ctx, &tmp, tmp_bytes);
-        if (rc != LMX_OK) {
-            lmx_free(ctx, (void **)&kofe, m * 4);
-            return rc;
-        }
-    }
-    trace_mark(ctx, ctx->algo == 1 ? "ordered slots + lowpair" : "weight keys");
     if (m && ctx->algo == 0) {
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
+        if (ctx->layout == kGeneral) {
+            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0"));
+            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1"));
+        }
         // fill counters reuse vdeg (local)
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
         k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
-                                                      ctx->vdeg, ctx->ids0, kofe,
+                                                      ctx->vdeg, ctx->ids0, ctx->ws_kofe,
                                                       ctx->layout == kDistinct, ctx->wk0);
         LMX_CUDA(ctx, cudaGetLastError());
+        trace_mark(ctx, "slot scatter");
     }
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     lmx_free(ctx, (void **)&newid, n * 4);
-    lmx_free(ctx, (void **)&kofe, m * 4);
-    trace_mark(ctx, "slot scatter");
+    lmx_free_weight_stage(ctx);
     if (ctx->algo == 1) {
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mround, std::max<size_t>(n, 1) * 4, "mround"));
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mpacked, (std::max<size_t>(n, 1) + 3) / 4 * 4, "mround packed"));
@@ -806,37 +912,67 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->eu, mm * 4, "edge_u"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ev, mm * 4, "edge_v"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->w, mm * 8, "edge_weight"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4, "deg0"));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->deg0, 0, std::max<size_t>(n, 1) * 4, st));
     unsigned long long *bad = nullptr;
     LMX_TRY(lmx_alloc(ctx, (void **)&bad, 8, "bad"));
     LMX_CUDA(ctx, cudaMemsetAsync(bad, 0xFF, 8, st));
-    // Pinned (page-locked, UVA-mapped) host arrays are read by the conversion
-    // kernel directly over the host link: no staging copies, full link rate.
-    const void *mapped[3] = {nullptr, nullptr, nullptr};
-    bool zero_copy = false;
+    // Pinned (page-locked) host arrays: the copy engine brings the weights
+    // first and the weight-key stage (sorts) runs on the device while the
+    // endpoint arrays are still crossing the host link.
+    bool pinned = false;
     if (m > 0 && where == LMX_HOST && !getenv("LMX_NO_ZEROCOPY")) {
-        zero_copy = true;
+        pinned = true;
         const void *hp[3] = {edge_u, edge_v, edge_weight};
         for (int i = 0; i < 3; ++i) {
             cudaPointerAttributes at;
-            if (cudaPointerGetAttributes(&at, hp[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
-                !at.devicePointer) {
+            if (cudaPointerGetAttributes(&at, hp[i]) != cudaSuccess || at.type != cudaMemoryTypeHost) {
                 cudaGetLastError();
-                zero_copy = false;
+                pinned = false;
                 break;
             }
-            mapped[i] = at.devicePointer;
         }
     }
+    bool weights_done = false;
     if (m > 0) {
-        if (zero_copy) {
-            k_convert<<<ctx->num_sms * 8, kBlock, 0, st>>>((const long long *)mapped[0], (const long long *)mapped[1],
-                                                          (const double *)mapped[2], (unsigned long long)m, n, 0,
-                                                          ctx->eu, ctx->ev, ctx->w, bad);
+        if (pinned) {
+            if (!ctx->copy_stream) {
+                LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+                LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_copy[0], cudaEventDisableTiming));
+                LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_copy[1], cudaEventDisableTiming));
+                LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_copy[2], cudaEventDisableTiming));
+            }
+            cudaStream_t cs = ctx->copy_stream;
+            long long *su = nullptr, *sv = nullptr;
+            LMX_TRY(lmx_alloc(ctx, (void **)&su, mm * 8, "stage u"));
+            LMX_TRY(lmx_alloc(ctx, (void **)&sv, mm * 8, "stage v"));
+            LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[0], st));   // blocks reused from the cache are idle
+            LMX_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_copy[0], 0));
+            LMX_CUDA(ctx, cudaMemcpyAsync(ctx->w, edge_weight, (size_t)m * 8, cudaMemcpyHostToDevice, cs));
+            LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[1], cs));
+            LMX_CUDA(ctx, cudaMemcpyAsync(su, edge_u, (size_t)m * 8, cudaMemcpyHostToDevice, cs));
+            LMX_CUDA(ctx, cudaMemcpyAsync(sv, edge_v, (size_t)m * 8, cudaMemcpyHostToDevice, cs));
+            LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[2], cs));
+            LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copy[1], 0));
+            k_check_w<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, (unsigned long long)m, bad);
             LMX_CUDA(ctx, cudaGetLastError());
+            int rc = weight_stage(ctx);   // overlaps the endpoint copies
+            cudaError_t e = cudaStreamWaitEvent(st, ctx->ev_copy[2], 0);
+            if (e == cudaSuccess) {
+                k_convert_uv<<<grid_for(ctx, m), kBlock, 0, st>>>(su, sv, (unsigned long long)m, n, ctx->eu,
+                                                                 ctx->ev, ctx->deg0, bad);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            lmx_free(ctx, (void **)&su, mm * 8);
+            lmx_free(ctx, (void **)&sv, mm * 8);
+            if (rc != LMX_OK) return rc;
+            LMX_CUDA(ctx, e);
+            weights_done = true;
         } else if (where == LMX_DEVICE) {
             k_convert<<<grid_for(ctx, m), kBlock, 0, st>>>((const long long *)edge_u, (const long long *)edge_v,
                                                           edge_weight, (unsigned long long)m, n, 0, ctx->eu,
-                                                          ctx->ev, ctx->w, bad);
+                                                          ctx->ev, ctx->w, ctx->deg0, bad);
             LMX_CUDA(ctx, cudaGetLastError());
         } else {
             // chunked H2D through two staging buffers of int64 ids
@@ -855,7 +991,7 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
                 if (e == cudaSuccess) e = cudaMemcpyAsync(sw, edge_weight + off, k * 8, cudaMemcpyHostToDevice, st);
                 if (e == cudaSuccess) {
                     k_convert<<<grid_for(ctx, k), kBlock, 0, st>>>(su, sv, sw, k, n, off, ctx->eu, ctx->ev,
-                                                                  ctx->w, bad);
+                                                                  ctx->w, ctx->deg0, bad);
                     e = cudaGetLastError();
                 }
             }
@@ -895,5 +1031,6 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
                      (unsigned long long)badpos, w);
         return lmx_fail(ctx, LMX_EINVAL, buf);
     }
+    if (!weights_done) LMX_TRY(weight_stage(ctx));
     return lmx_setup_slots(ctx);
 }
