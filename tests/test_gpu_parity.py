@@ -170,6 +170,61 @@ def test_long_chain_many_rounds(engine):
     assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == res.rounds
 
 
+@pytest.mark.parametrize("m", [6, 28, 40, 300, 520])
+@pytest.mark.parametrize("algo", ["scan", "compact"])
+def test_chains_across_round_count_regimes(engine, m, algo):
+    """Paths with increasing weights: ~m/2 rounds, so the scan loop's death-round
+    histogram runs with 4-bit (< 15 rounds), 8-bit (< 255) and 32-bit round
+    codes; the compacting loop on the same graphs."""
+    eu = np.arange(m, dtype=np.int64)
+    ev = eu + 1
+    w = np.arange(m, dtype=np.float64)
+    g = _graph(m + 1, eu, ev, w)
+    engine.set_algo(algo)
+    try:
+        engine.load_graph(g)
+        assert engine.algo() == algo
+        for rr in (False, True):
+            res = O.c_local_max(m + 1, eu, ev, w, 3, rr)
+            matching, trace = engine.match(g, 3, rr)
+            assert np.array_equal(matching.mate, res.mate)
+            assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == res.rounds
+    finally:
+        engine.set_algo("auto")
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_scan_loop_ties_and_rerandomize(engine, seed):
+    """Distinct layout with tied weight groups (so tied runs inside the weight-
+    ordered segments are resolved by the per-round salt), both rerandomize
+    modes, scan loop against the oracle and against the compacting loop."""
+    rng = np.random.default_rng(seed)
+    n = 3000
+    _, eu, ev, _ = O.gen_random(n, 8, seed)
+    m = eu.size
+    w = rng.random(m)
+    tied = rng.random(m) < 0.05           # 5% of the edges share a few weights
+    w[tied] = rng.choice([0.25, 0.5, 0.75], size=int(tied.sum()))
+    g = _graph(n, eu, ev, w)
+    outs = {}
+    for algo in ("scan", "compact"):
+        engine.set_algo(algo)
+        engine.set_layout("distinct")
+        try:
+            engine.load_graph(g)
+            assert engine.algo() == algo and engine.layout() == "distinct"
+            for rr in (True, False):
+                res = O.c_local_max(n, eu, ev, w, seed, rr)
+                matching, trace = engine.match(g, seed, rr)
+                assert np.array_equal(matching.mate, res.mate)
+                assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == res.rounds
+                outs[(algo, rr)] = matching.mate.copy()
+        finally:
+            engine.set_algo("auto")
+            engine.set_layout("auto")
+    assert np.array_equal(outs[("scan", True)], outs[("compact", True)])
+
+
 def test_domain_errors_raise_value_error(engine):
     from paper_1302_4587_b200 import local_max_b200
     bad = [
