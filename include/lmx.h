@@ -232,6 +232,18 @@ int lmx_contract(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, cons
 /* Device memory in use by the context (bytes). */
 int64_t lmx_device_bytes(const lmx_ctx *ctx);
 
+/*
+ * validate_matching(g, m) (graph.py:212-237) and Matching.weight(g)
+ * (graph.py:54-56,191-192) against the loaded graph (caller's vertex and edge
+ * ids).  mate: int64[n]; ids: the matched edge ids, ascending (as
+ * Matching.sorted_edge_ids()), n_ids of them; both where `where` says.
+ * valid / maximal: the MatchingCheck flags; weight: edge_weight[ids].sum()
+ * with numpy's pairwise summation order, bit-identical; detail: the first
+ * offence by smallest id ("" when valid).  Any out may be NULL.
+ */
+int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
+                 int *valid, int *maximal, double *weight, char *detail, size_t detail_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -305,5 +305,16 @@ int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out) {
 
 int64_t lmx_device_bytes(const lmx_ctx *ctx) { return ctx ? ctx->dev_bytes : 0; }
 
+int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
+                 int *valid, int *maximal, double *weight, char *detail, size_t detail_len) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (!ctx->eu && ctx->m > 0) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded");
+    if (n_ids < 0 || (n_ids > 0 && !ids) || (ctx->n > 0 && !mate))
+        return lmx_fail(ctx, LMX_EINVAL, "null or negative validate inputs");
+    return lmx_validate_impl(ctx, mate, ids, n_ids, where, valid, maximal, weight, detail, detail_len);
+}
+
 }  // extern "C"
 

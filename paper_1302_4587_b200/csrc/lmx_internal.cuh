@@ -193,6 +193,8 @@ int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);
+int lmx_validate_impl(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
+                      int *valid, int *maximal, double *weight, char *detail, size_t detail_len);
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                         std::vector<lmx_round_stats> &stats, unsigned long long &n_matched);
 int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,

@@ -19,7 +19,7 @@ import time
 
 import numpy as np
 
-from .graph import Graph, Matching, PhaseTrace, RoundStats
+from .graph import Graph, Matching, MatchingCheck, PhaseTrace, RoundStats
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LMX_LIBRARY") or os.path.join(_HERE, "liblmx.so")
@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times", "lmx_last_round_counters",
     "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
-    "lmx_graph_export", "lmx_device_bytes", "lmx_set_option",
+    "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_graph_export": (c_int, [p, p, p, p, c_int]),
             "lmx_device_bytes": (i64, [p]),
             "lmx_set_option": (c_int, [p, c_int, i64]),
+            "lmx_validate": (c_int, [p, p, p, i64, c_int, p, p, p, p, ctypes.c_size_t]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -324,6 +325,25 @@ class Engine:
         trace.device_millis = self.last_timing()["rounds_ms"]
         trace.wall_millis = (time.perf_counter() - t0) * 1000.0
         return Matching(ids, mate), trace
+
+    def validate(self, matching) -> tuple[MatchingCheck, float]:
+        """``validate_matching(g, m)`` (graph.py:212-237) and ``m.weight(g)``
+        (graph.py:54-56) on the device, for the graph loaded in this engine.
+        The weight is bit-identical to numpy's ``edge_weight[ids].sum()``."""
+        n, _ = self.graph_size()
+        mate = np.ascontiguousarray(np.asarray(matching.mate), dtype=np.int64)
+        if mate.shape != (n,):
+            return MatchingCheck(False, False, "mate table has wrong length"), 0.0
+        ids = matching.sorted_edge_ids() if hasattr(matching, "sorted_edge_ids") else \
+            np.array(sorted(matching.edges), dtype=np.int64)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        valid, maximal = ctypes.c_int(), ctypes.c_int()
+        weight = ctypes.c_double()
+        detail = ctypes.create_string_buffer(256)
+        self._check(self._lib.lmx_validate(self._h, mate.ctypes.data, ids.ctypes.data if ids.size else None,
+                                           int(ids.size), LMX_HOST, ctypes.byref(valid), ctypes.byref(maximal),
+                                           ctypes.byref(weight), detail, 256), "lmx_validate")
+        return MatchingCheck(bool(valid.value), bool(maximal.value), detail.value.decode()), float(weight.value)
 
 
 _default_engines: dict[int, Engine] = {}
