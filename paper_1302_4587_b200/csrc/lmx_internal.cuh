@@ -118,7 +118,7 @@ struct lmx_ctx {
     uint2 *cand = nullptr;
     uint32_t *matched = nullptr;
     uint32_t *lists[2] = {nullptr, nullptr}; // ping-pong, kBuckets regions of capacity n
-    uint32_t *mids = nullptr;                // matched edge ids, ascending (u32 staging)
+    long long *mids = nullptr;               // matched edge ids, ascending (staging for host outputs)
     uint32_t *ebits = nullptr;               // matched edge-id bitmap, (m + 31) / 32 words
     uint32_t *ebits_off = nullptr;           // per-word exclusive popcount prefix
     lmx::RoundCtr *ctr = nullptr;

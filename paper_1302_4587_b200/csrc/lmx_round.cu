@@ -798,7 +798,7 @@ int lmx_alloc_match_state(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
     for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], nl * 4 * kBuckets, "lists"));
     const size_t words = (size_t)(std::max<int64_t>(ctx->m, 1) + 31) / 32;
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 4, "mids"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 8, "mids"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits, words * 4, "ebits"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits_off, words * 4, "ebits_off"));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, nl * 4, ctx->stream));
@@ -1114,11 +1114,10 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
         size_t tmp = ctx->sort_tmp_bytes;
         LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->sort_tmp, tmp, ctx->ebits_off, ctx->ebits_off,
                                                     (long long)words, ctx->stream));
-        if (out_where == LMX_DEVICE)
-            lmx_emit_ids<long long><<<grid, kBlock, 0, ctx->stream>>>(ctx->ebits, ctx->ebits_off, words,
-                                                                     (long long *)ids_out);
-        else
-            lmx_emit_ids<uint32_t><<<grid, kBlock, 0, ctx->stream>>>(ctx->ebits, ctx->ebits_off, words, ctx->mids);
+        // int64 ids straight into the caller's device buffer, or staged on the
+        // device and copied once (a pinned host buffer takes it at link rate)
+        lmx_emit_ids<long long><<<grid, kBlock, 0, ctx->stream>>>(
+            ctx->ebits, ctx->ebits_off, words, out_where == LMX_DEVICE ? (long long *)ids_out : ctx->mids);
         LMX_CUDA(ctx, cudaGetLastError());
         ctx->timing.round_launches += 2;
     }
@@ -1130,14 +1129,11 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
     } else {
         if (mate_out && n)
             LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate_target, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        std::vector<uint32_t> tmp32((size_t)n_matched);
         if (ids_out && n_matched)
-            LMX_CUDA(ctx, cudaMemcpyAsync(tmp32.data(), ctx->mids, (size_t)n_matched * 4, cudaMemcpyDeviceToHost,
+            LMX_CUDA(ctx, cudaMemcpyAsync(ids_out, ctx->mids, (size_t)n_matched * 8, cudaMemcpyDeviceToHost,
                                           ctx->stream));
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        if (ids_out)
-            for (size_t i = 0; i < (size_t)n_matched; ++i) ids_out[i] = (int64_t)tmp32[i];
     }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);

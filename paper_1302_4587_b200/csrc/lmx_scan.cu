@@ -45,6 +45,9 @@
 #ifndef LMX_SCAN_MATCH_MINB
 #define LMX_SCAN_MATCH_MINB 8
 #endif
+#ifndef LMX_HIST_U
+#define LMX_HIST_U 2   // uint4 (2 edges) loads per thread per step of the histogram
+#endif
 
 namespace lmx {
 
@@ -394,19 +397,24 @@ __global__ void __launch_bounds__(kBlock) lmx_scan_hist_kernel(const uint2 *lowp
     const uint4 *q = reinterpret_cast<const uint4 *>(lowpair);
     const uint32_t nq = (uint32_t)(m / 2);   // m < 2^32
     const uint32_t stride = gridDim.x * kBlock;
-    for (uint32_t i = blockIdx.x * kBlock + tid; i < nq; i += 2 * stride) {
-        const uint4 x0 = __ldcs(q + i);
-        const bool has1 = i + stride < nq;
-        const uint4 x1 = has1 ? __ldcs(q + i + stride) : make_uint4(0, 0, 0, 0);
-        const uint32_t a0 = mround_of<BITS>(mround, packed, x0.x), b0 = mround_of<BITS>(mround, packed, x0.y);
-        const uint32_t a1 = mround_of<BITS>(mround, packed, x0.z), b1 = mround_of<BITS>(mround, packed, x0.w);
-        const uint32_t a2 = mround_of<BITS>(mround, packed, x1.x), b2 = mround_of<BITS>(mround, packed, x1.y);
-        const uint32_t a3 = mround_of<BITS>(mround, packed, x1.z), b3 = mround_of<BITS>(mround, packed, x1.w);
-        acc.add(min(min(a0, b0), R), s_hist, hist);
-        acc.add(min(min(a1, b1), R), s_hist, hist);
-        if (has1) {
-            acc.add(min(min(a2, b2), R), s_hist, hist);
-            acc.add(min(min(a3, b3), R), s_hist, hist);
+    constexpr int HU = LMX_HIST_U;   // edge pairs (uint4) per thread per step
+    for (uint32_t i = blockIdx.x * kBlock + tid; i < nq; i += HU * stride) {
+        uint4 x[HU];
+#pragma unroll
+        for (int j = 0; j < HU; ++j) x[j] = i + j * stride < nq ? __ldcs(q + i + j * stride) : make_uint4(0, 0, 0, 0);
+        uint32_t d[2 * HU];
+#pragma unroll
+        for (int j = 0; j < HU; ++j) {
+            d[2 * j] = min(min(mround_of<BITS>(mround, packed, x[j].x), mround_of<BITS>(mround, packed, x[j].y)), R);
+            d[2 * j + 1] =
+                min(min(mround_of<BITS>(mround, packed, x[j].z), mround_of<BITS>(mround, packed, x[j].w)), R);
+        }
+#pragma unroll
+        for (int j = 0; j < HU; ++j) {
+            if (i + j * stride < nq) {
+                acc.add(d[2 * j], s_hist, hist);
+                acc.add(d[2 * j + 1], s_hist, hist);
+            }
         }
     }
     if ((m & 1ULL) && blockIdx.x == 0 && tid == 0) {

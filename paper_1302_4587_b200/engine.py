@@ -234,8 +234,8 @@ class Engine:
     def match_raw(self, seed: int, rerandomize: bool = True):
         """Run the round loop; returns (mate int64[n], sorted ids int64, [RoundStats])."""
         n, _ = self.graph_size()
-        mate = np.empty(max(n, 1), dtype=np.int64)
-        ids = np.empty(max(n // 2 + 1, 1), dtype=np.int64)
+        mate = _host_buffer(max(n, 1))
+        ids = _host_buffer(max(n // 2 + 1, 1))
         nm = ctypes.c_int64()
         nr = ctypes.c_int()
         self._check(self._lib.lmx_match(self._h, seed & _UINT64_MASK, int(bool(rerandomize)),
@@ -344,6 +344,20 @@ class Engine:
                                            int(ids.size), LMX_HOST, ctypes.byref(valid), ctypes.byref(maximal),
                                            ctypes.byref(weight), detail, 256), "lmx_validate")
         return MatchingCheck(bool(valid.value), bool(maximal.value), detail.value.decode()), float(weight.value)
+
+
+def _host_buffer(count: int) -> np.ndarray:
+    """int64 host output array.  Large ones come from torch's caching pinned
+    allocator (already page-locked and faulted in, so the device writes them at
+    link rate and reuses freed blocks); the array keeps its block alive."""
+    if count >= (1 << 20):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.empty(count, dtype=torch.int64, pin_memory=True).numpy()
+        except Exception:   # no torch / no pinning: plain pageable memory
+            pass
+    return np.empty(count, dtype=np.int64)
 
 
 _default_engines: dict[int, Engine] = {}

@@ -26,5 +26,6 @@ for _ in range(args.steps):
     if best is None or t["rounds_ms"] < best["rounds_ms"]:
         best = t
 print(os.path.basename(os.environ.get("LMX_LIBRARY", "default")),
-      "rounds_ms %.3f round_k %.3f match_k %.3f out %.3f" % (best["rounds_ms"], best["round_kernel_ms"],
-                                                             best["match_kernel_ms"], best["output_ms"]))
+      "rounds_ms %.3f round_k %.3f match_k %.3f hist_k %.3f out %.3f" % (
+          best["rounds_ms"], best["round_kernel_ms"], best["match_kernel_ms"], best["hist_kernel_ms"],
+          best["output_ms"]))
