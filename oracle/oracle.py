@@ -214,6 +214,68 @@ def numpy_local_max(n: int, edge_u, edge_v, edge_weight, seed: int,
     return OracleResult(mate, matched, rounds)
 
 
+# ---------------------------------------------------------------- red-blue matching
+_COIN_STREAM = np.uint64(0xD6E8FEB86659FD93)   # tiebreak.py:25
+
+
+def vertex_coins(round_seed_value: int, vertex_ids) -> np.ndarray:
+    """tiebreak.py:62-71: True = blue; a stream separate from the edge salts."""
+    ids = np.asarray(vertex_ids, dtype=np.uint64)
+    h = mix64(ids ^ np.uint64(round_seed_value & _UINT64_MASK) ^ _COIN_STREAM)
+    return (h & np.uint64(1)).astype(bool)
+
+
+def numpy_rbm(n: int, edge_u, edge_v, edge_weight, seed: int, max_rounds: int = 10_000) -> OracleResult:
+    """Restatement of rbm (matchers.py:357-410): per round every live vertex
+    flips a coin; a blue vertex proposes along its max-key edge to a red
+    neighbour, a red vertex accepts its max-key incoming proposal.  The key is
+    local max's (weight, salt, edge id) with rerandomized salts; ranks from a
+    lexsort of the live edges (tiebreak.py:92-102).  Raises RuntimeError after
+    max_rounds rounds (RbmDidNotConverge)."""
+    edge_u = np.asarray(edge_u, dtype=np.int64)
+    edge_v = np.asarray(edge_v, dtype=np.int64)
+    edge_weight = np.asarray(edge_weight, dtype=np.float64)
+    prop = np.full(n, -1, dtype=np.int64)
+    acc = np.full(n, -1, dtype=np.int64)
+    done = np.zeros(n, dtype=bool)
+    live = np.arange(edge_u.size, dtype=np.int64)
+    parts, rounds = [], []
+    r = 0
+    while live.size:
+        if r >= max_rounds:
+            raise RuntimeError(f"no progress after {max_rounds} rounds")
+        rs = round_seed(seed, r, True)
+        order = np.lexsort((live, edge_salts(rs, live), edge_weight[live]))
+        rank = np.empty(live.size, dtype=np.int64)
+        rank[order] = np.arange(live.size, dtype=np.int64)
+        us, vs = edge_u[live], edge_v[live]
+        bu, bv = vertex_coins(rs, us), vertex_coins(rs, vs)
+        fwd, bwd = bu & ~bv, bv & ~bu
+        np.maximum.at(prop, us[fwd], rank[fwd])
+        np.maximum.at(prop, vs[bwd], rank[bwd])
+        pf = fwd & (prop[us] == rank)
+        pb = bwd & (prop[vs] == rank)
+        np.maximum.at(acc, vs[pf], rank[pf])
+        np.maximum.at(acc, us[pb], rank[pb])
+        won = (pf & (acc[vs] == rank)) | (pb & (acc[us] == rank))
+        parts.append(live[won])
+        done[us[won]] = True
+        done[vs[won]] = True
+        alive = ~(done[us] | done[vs])
+        for ends in (us[alive], vs[alive]):
+            prop[ends] = -1
+            acc[ends] = -1
+        rounds.append((int(live.size), int(won.sum()), int(live.size - alive.sum())))
+        live = live[alive]
+        r += 1
+    matched = np.sort(np.concatenate(parts)) if parts else np.empty(0, dtype=np.int64)
+    mate = np.full(n, -1, dtype=np.int64)
+    if matched.size:
+        mate[edge_u[matched]] = edge_v[matched]
+        mate[edge_v[matched]] = edge_u[matched]
+    return OracleResult(mate, matched, rounds)
+
+
 # ---------------------------------------------------------------- generators
 
 def build_graph_loop(edge_list, num_vertices=None):
