@@ -244,6 +244,18 @@ int64_t lmx_device_bytes(const lmx_ctx *ctx);
 int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
                  int *valid, int *maximal, double *weight, char *detail, size_t detail_len);
 
+/*
+ * rbm(g, seed) (matchers.py:357-410): red-blue matching on the loaded graph,
+ * the paper's GPU competitor.  Outputs as lmx_match (mate, ascending matched
+ * ids, RoundStats).  max_rounds (the reference uses 10 000; <= 0 means that):
+ * LMX_ELIMIT when the loop has not finished by then (RbmDidNotConverge).
+ * rounds_out (may be NULL) receives up to max_rounds entries; the full trace
+ * is in lmx_last_rounds.
+ */
+int lmx_rbm(lmx_ctx *ctx, uint64_t seed_masked, int64_t *mate_out, int64_t *matched_ids_out,
+            int64_t *n_matched_out, lmx_round_stats *rounds_out, int max_rounds, int *n_rounds_out,
+            int out_where);
+
 #ifdef __cplusplus
 }
 #endif

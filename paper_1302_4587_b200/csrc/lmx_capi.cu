@@ -305,6 +305,24 @@ int lmx_graph_size(const lmx_ctx *ctx, int64_t *n_out, int64_t *m_out) {
 
 int64_t lmx_device_bytes(const lmx_ctx *ctx) { return ctx ? ctx->dev_bytes : 0; }
 
+int lmx_rbm(lmx_ctx *ctx, uint64_t seed_masked, int64_t *mate_out, int64_t *matched_ids_out,
+            int64_t *n_matched_out, lmx_round_stats *rounds_out, int max_rounds, int *n_rounds_out, int out_where) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded (call lmx_load_graph first)");
+    std::vector<lmx_round_stats> &stats = ctx->rounds;
+    unsigned long long nm = 0;
+    ctx->mate_target = (out_where == LMX_DEVICE && mate_out) ? (long long *)mate_out : ctx->mate;
+    LMX_TRY(lmx_rbm_impl(ctx, seed_masked, max_rounds > 0 ? max_rounds : 10000, stats, nm));
+    LMX_TRY(lmx_emit_outputs(ctx, nm, mate_out, matched_ids_out, out_where));
+    if (n_matched_out) *n_matched_out = (int64_t)nm;
+    if (n_rounds_out) *n_rounds_out = (int)stats.size();
+    if (rounds_out)
+        for (int i = 0; i < (int)stats.size() && i < max_rounds; ++i) rounds_out[i] = stats[i];
+    return LMX_OK;
+}
+
 int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
                  int *valid, int *maximal, double *weight, char *detail, size_t detail_len) {
     if (!ctx) return LMX_EINVAL;

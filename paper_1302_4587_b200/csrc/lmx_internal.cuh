@@ -150,6 +150,12 @@ struct lmx_ctx {
     uint2 *lowpair = nullptr;                // scan: each edge once as {higher id, lower id}, by higher id
     uint32_t *mpacked = nullptr;             // scan: mround packed to 4 / 8 bits (n bytes)
     uint2 *cand0 = nullptr;                  // scan: first slot of each segment (round-0 candidates)
+    // red-blue matching (lmx_rbm.cu), allocated on first use per graph
+    uint2 *rbm_prop = nullptr, *rbm_acc = nullptr;
+    uint32_t *rbm_blue = nullptr;
+    uint32_t *rbm_list[2] = {nullptr, nullptr};
+    uint32_t *rbm_list0 = nullptr;
+    uint32_t rbm_n0 = 0;
     // weight-key stage results held until the slot build (load time only)
     uint32_t *ws_kofe = nullptr;             // weight key per edge (compacting loop)
     uint32_t *ws_rank = nullptr, *ws_eid = nullptr, *ws_tied = nullptr, *ws_tidx = nullptr;   // by sorted position
@@ -193,6 +199,8 @@ int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);
+int lmx_rbm_impl(lmx_ctx *ctx, uint64_t seed_masked, int max_rounds, std::vector<lmx_round_stats> &stats,
+                 unsigned long long &n_matched);
 int lmx_validate_impl(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
                       int *valid, int *maximal, double *weight, char *detail, size_t detail_len);
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,

@@ -118,7 +118,9 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->send_cnt, (void **)&ctx->mround, (void **)&ctx->lowbeg,
                      (void **)&ctx->lowpair, (void **)&ctx->hist, (void **)&ctx->mpacked,
                      (void **)&ctx->cand0,    (void **)&ctx->ws_kofe,     (void **)&ctx->ws_rank,
-                     (void **)&ctx->ws_eid,   (void **)&ctx->ws_tied,     (void **)&ctx->ws_tidx};
+                     (void **)&ctx->ws_eid,   (void **)&ctx->ws_tied,     (void **)&ctx->ws_tidx,
+                     (void **)&ctx->rbm_prop, (void **)&ctx->rbm_acc,     (void **)&ctx->rbm_blue,
+                     (void **)&ctx->rbm_list[0], (void **)&ctx->rbm_list[1], (void **)&ctx->rbm_list0};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times", "lmx_last_round_counters",
     "lmx_local_max",
     "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
-    "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate",
+    "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_device_bytes": (i64, [p]),
             "lmx_set_option": (c_int, [p, c_int, i64]),
             "lmx_validate": (c_int, [p, p, p, i64, c_int, p, p, p, p, ctypes.c_size_t]),
+            "lmx_rbm": (c_int, [p, u64, p, p, p, p, c_int, p, c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -326,6 +327,24 @@ class Engine:
         trace.wall_millis = (time.perf_counter() - t0) * 1000.0
         return Matching(ids, mate), trace
 
+    def rbm(self, g, seed: int, max_rounds: int = 10_000) -> tuple[Matching, PhaseTrace]:
+        """Red-blue matching (matchers.py:357-410) on the graph loaded in this engine."""
+        t0 = time.perf_counter()
+        n, _ = self.graph_size()
+        mate = _host_buffer(max(n, 1))
+        ids = _host_buffer(max(n // 2 + 1, 1))
+        nm = ctypes.c_int64()
+        nr = ctypes.c_int()
+        rc = self._lib.lmx_rbm(self._h, seed & _UINT64_MASK, mate.ctypes.data, ids.ctypes.data, ctypes.byref(nm),
+                               None, int(max_rounds), ctypes.byref(nr), LMX_HOST)
+        if rc == LMX_ELIMIT:
+            raise RbmDidNotConverge(self._lib.lmx_last_error(self._h).decode())
+        self._check(rc, "lmx_rbm")
+        trace = PhaseTrace(rounds=self.last_rounds())
+        trace.device_millis = self.last_timing()["rounds_ms"]
+        trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+        return Matching(ids[: nm.value].copy(), mate[:n]), trace
+
     def validate(self, matching) -> tuple[MatchingCheck, float]:
         """``validate_matching(g, m)`` (graph.py:212-237) and ``m.weight(g)``
         (graph.py:54-56) on the device, for the graph loaded in this engine.
@@ -385,6 +404,21 @@ def local_max_b200(g, seed: int, rerandomize: bool = True, device: int = 0) -> t
     return matching, trace
 
 
+class RbmDidNotConverge(RuntimeError):
+    """matchers.py:353-354: rbm made no progress within its round limit."""
+
+
+def rbm_b200(g, seed: int, device: int = 0, max_rounds: int = 10_000) -> tuple[Matching, PhaseTrace]:
+    """Drop-in for ``locmax.matchers.rbm(g, seed)`` (matchers.py:357-410), the
+    paper's GPU competitor: same Matching and RoundStats trace."""
+    t0 = time.perf_counter()
+    eng = default_engine(device)
+    eng.load_graph(g)
+    matching, trace = eng.rbm(g, seed, max_rounds)
+    trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+    return matching, trace
+
+
 def run_matcher(g, algorithm: str, seed: int, engine: str = "b200", p: int = 4,
                 rerandomize: bool = True):
     """bench.py:119-142 dispatch with the B200 engines added.
@@ -396,6 +430,8 @@ def run_matcher(g, algorithm: str, seed: int, engine: str = "b200", p: int = 4,
     """
     if algorithm == "localmax" and engine == "b200":
         return local_max_b200(g, seed, rerandomize)
+    if algorithm == "rbm" and engine == "b200":
+        return rbm_b200(g, seed)
     if algorithm == "localmax" and engine == "b200-dist":
         from .dist import local_max_dist
         return local_max_dist(g, p, seed, rerandomize)
