@@ -265,18 +265,30 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
         uint32_t vv[kItems];
         bool keep[kItems];
         uint32_t wc = 0;
+        // staged gathers: list entries, then candidates, then the partners'
+        // keys, each stage for all items at once (their latencies overlap)
+        uint2 cc[kItems];
+        uint32_t px[kItems];
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
             const uint32_t i = t0 + j * kBlock + tid;
-            const uint32_t v = i < total ? a.alist[i] : kNone;
+            vv[j] = i < total ? a.alist[i] : kNone;
+        }
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cand[vv[j]] : make_uint2(kNone, kNone);
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) px[j] = cc[j].x != kNone ? a.cand[cc[j].x].y : kNone;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const uint32_t v = vv[j];
             bool k = false;
             if (v != kNone) {
-                const uint2 cv = a.cand[v];
+                const uint2 cv = cc[j];
                 const uint32_t x = cv.x;
                 if (x != kNone) {
                     const uint32_t id = cv.y;
                     // weight keys are unique per edge
-                    const bool mutual = a.cand[x].y == id;
+                    const bool mutual = px[j] == id;
                     if (mutual) {
                         atomicOr(a.matched + (v >> 5), 1u << (v & 31));
                         a.mround[v] = (uint32_t)a.round;
@@ -292,7 +304,6 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
                     }
                 }
             }
-            vv[j] = v;
             keep[j] = k;
             wc += __popc(__ballot_sync(0xffffffffu, k));
         }
