@@ -461,6 +461,14 @@ def run_b200(args):
                        "setup_ms": setup_ms},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "rounds_enqueued": rounds_exec,
+            # BASELINE north_star target: >= 50 % of HBM-roofline edges/s, the roofline being
+            # SURVEY 8d's floor of the matching (B_floor bytes at the measured peak bandwidth)
+            "north_star": {
+                "target_frac": 0.5,
+                "roofline_edges_per_s": m / (B_floor / (peak * 1e9)),
+                "achieved_frac": value / world / (m / (B_floor / (peak * 1e9))),
+                "roofline_definition": "m / (B_floor / peak), B_floor = 32 (2S - m0) bytes (SURVEY.md 8d)",
+            },
         }
         print(json.dumps(line), flush=True)
     if world > 1:
