@@ -796,7 +796,9 @@ int lmx_alloc_match_state(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->remote_ok, nl * 4, "remote_ok"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
-    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], nl * 4 * kBuckets, "lists"));
+    // the scan loop keeps one list per round; the compacting loop one per live-degree bucket
+    const size_t regions = ctx->algo == 1 ? 1 : kBuckets;
+    for (int i = 0; i < 2; ++i) LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lists[i], nl * 4 * regions, "lists"));
     const size_t words = (size_t)(std::max<int64_t>(ctx->m, 1) + 31) / 32;
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mids, (n / 2 + 1) * 8, "mids"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ebits, words * 4, "ebits"));

@@ -864,7 +864,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     }
     // round-0 bucket lists of the owned vertices (local indices, ascending)
     const size_t cap = std::max<size_t>(nl, 1);
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * kBuckets, "bins0"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * (ctx->algo == 1 ? 1 : kBuckets), "bins0"));
     {
         unsigned long long *cnt = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8 * kBuckets, "bucket counts"));
