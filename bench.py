@@ -220,6 +220,11 @@ def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_r
             "algorithmic_bytes_per_launch": probe_bytes / max(launches, 1),
             "kernel_ms_per_step": probe_ms, "peak_source": src,
             "traffic_source": traffic.get("source") if traffic else None,
+            # The probe's useful bytes are gathered 4-8 B at a time from scattered
+            # vertices; a DRAM sector is 32 B.  The measured DRAM traffic over the
+            # kernel time is the bandwidth the access pattern actually draws.
+            "measured_traffic_gbs": (traffic["bytes_per_launch"] * launches / (probe_ms / 1000.0) / 1e9)
+            if traffic and probe_ms > 0 else None,
             "other_kernels": {
                 "lmx_scan_match_kernel": {"ms_per_step": match_ms, "algorithmic_bytes": match_bytes,
                                           "achieved_gbs": match_bytes / (match_ms / 1000.0) / 1e9
