@@ -208,6 +208,17 @@ int lmx_dist_match(lmx_ctx *ctx, void **stats_dev_out);
  * caller ids, only owned vertices set), matched-edge bitmap (m bits, edges
  * recorded by this rank), and the context's cudaStream_t. */
 int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge_bits, void **stream);
+/*
+ * Contexts whose load chose the weight-ordered scan loop (LMX_QUERY_ALGO == 1)
+ * run the same protocol, with {candidates found, matched vertices} as the
+ * round's counts ("none found" ends the loop).  RoundStats then come from the
+ * death rounds of the edges: the host all-gathers the owned slices of the
+ * match-round array (lmx_dist_mround: uint32[n], global device ids) and sums
+ * the partitions' histograms (lmx_dist_hist: uint64[*nbins] on the device,
+ * bins [0, n_rounds), bin n_rounds = outlived).
+ */
+int lmx_dist_mround(lmx_ctx *ctx, void **mround_dev);
+int lmx_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
 
 /*
  * Coarsening (config C4; the paper's graph-partitioning use, PAPER.md:32-35,

@@ -251,10 +251,21 @@ int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize) {
     if (!ctx) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
     if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded");
-    if (ctx->algo != 0)
-        return lmx_fail(ctx, LMX_ESTATE, "graph was loaded for the single-GPU scan loop; set LMX_OPT_DIST_P "
-                                         "before lmx_load_graph to use the stepped protocol");
     return lmx_dist_begin_impl(ctx, seed_masked, rerandomize != 0);
+}
+
+int lmx_dist_mround(lmx_ctx *ctx, void **mround_dev) {
+    if (!ctx || !mround_dev) return LMX_EINVAL;
+    if (ctx->algo != 1) return lmx_fail(ctx, LMX_ESTATE, "the compacting round loop keeps no match rounds");
+    *mround_dev = ctx->mround;
+    return LMX_OK;
+}
+
+int lmx_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins) {
+    if (!ctx || !hist_dev || !nbins) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (ctx->algo != 1) return lmx_fail(ctx, LMX_ESTATE, "the compacting round loop counts edges per round");
+    return lmx_scan_dist_hist(ctx, n_rounds, hist_dev, nbins);
 }
 
 int lmx_dist_round(lmx_ctx *ctx) {

@@ -150,6 +150,7 @@ struct lmx_ctx {
     uint2 *lowpair = nullptr;                // scan: each edge once as {higher id, lower id}, by higher id
     uint32_t *mpacked = nullptr;             // scan: mround packed to 4 / 8 bits (n bytes)
     uint2 *cand0 = nullptr;                  // scan: first slot of each segment (round-0 candidates)
+    unsigned long long lowpair_n = 0;        // scan: lowpair entries (m; a partition's share when p > 1)
     // red-blue matching (lmx_rbm.cu), allocated on first use per graph
     uint2 *rbm_prop = nullptr, *rbm_acc = nullptr;
     uint32_t *rbm_blue = nullptr;
@@ -199,6 +200,18 @@ int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);
+// the stepped multi-GPU protocol on the scan loop (lmx_scan.cu)
+int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize);
+int lmx_scan_dist_round(lmx_ctx *ctx);
+int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev);
+int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count);
+int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev);
+int lmx_scan_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
+namespace lmx {
+// exchange-A packing (lmx_round.cu), shared by both round loops
+__global__ void lmx_pack_kernel(const uint2 *region, const uint32_t *cnt, int p, uint32_t nl, uint2 *packed,
+                                long long *counts64);
+}  // namespace lmx
 int lmx_rbm_impl(lmx_ctx *ctx, uint64_t seed_masked, int max_rounds, std::vector<lmx_round_stats> &stats,
                  unsigned long long &n_matched);
 int lmx_validate_impl(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,

@@ -791,8 +791,10 @@ static void launch_round(lmx_ctx *ctx, const RoundArgs &a) {
 int lmx_alloc_match_state(lmx_ctx *ctx) {
     const size_t n = (size_t)std::max<int64_t>(ctx->n, 1);          // global ids
     const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);   // owned vertices
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, nl * 4, "vdeg"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, nl * 8, "cand"));
+    // the scan loop indexes its per-vertex arrays by global id on every partition
+    const size_t nv = ctx->algo == 1 ? n : nl;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, nv * 4, "vdeg"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, nv * 8, "cand"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->remote_ok, nl * 4, "remote_ok"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
@@ -1003,6 +1005,7 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
 //   -> [all-reduce of (live slots, matched vertices)].
 
 int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
+    if (ctx->algo == 1) return lmx_scan_dist_begin(ctx, seed_masked, rerandomize);
     ctx->timing.round_launches = 0;
     ctx->dist_round = 0;
     ctx->dist_seed = seed_masked;
@@ -1015,6 +1018,7 @@ int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
 }
 
 int lmx_dist_round_impl(lmx_ctx *ctx) {
+    if (ctx->algo == 1) return lmx_scan_dist_round(ctx);
     LMX_TRY(lmx_ensure_ctr(ctx, ctx->dist_round + 2));
     return enqueue_round_kernel(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
 }
@@ -1022,6 +1026,7 @@ int lmx_dist_round_impl(lmx_ctx *ctx) {
 // Exchange-A records, fully on the device: fill per-destination regions, pack
 // them, publish int64 counts.  Returns device pointers; no synchronisation.
 int lmx_dist_propose_impl(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
+    if (ctx->algo == 1) return lmx_scan_dist_propose(ctx, counts_dev, packed_dev);
     const int p = ctx->dist_p;
     const int r = ctx->dist_round;
     const size_t cap = list_cap(ctx);
@@ -1084,6 +1089,7 @@ int lmx_dist_recv_impl(lmx_ctx *ctx, int64_t count, void **ptr) {
 }
 
 int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count) {
+    if (ctx->algo == 1) return lmx_scan_dist_accept(ctx, count);
     if (count <= 0) return LMX_OK;
     const size_t cap = list_cap(ctx);
     lmx_accept_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
@@ -1097,6 +1103,7 @@ int lmx_dist_accept_impl(lmx_ctx *ctx, int64_t count) {
 // Enqueue the match kernel; *stats_dev = the round's {live slots, matched
 // vertices} (two u64 on the device) for the host's all-reduce.  No sync.
 int lmx_dist_match_impl(lmx_ctx *ctx, void **stats_dev) {
+    if (ctx->algo == 1) return lmx_scan_dist_match(ctx, stats_dev);
     const int r = ctx->dist_round;
     LMX_TRY(enqueue_match_kernel(ctx, r));
     *stats_dev = &ctx->ctr[r].live_slots;   // live_slots, matched_v are adjacent

@@ -249,6 +249,8 @@ struct ScanMatchArgs {
     RoundCtr *ctr;
     RoundCtr *ctr_next;
     int round;
+    uint32_t lo, nl;              // owned id range (single GPU: [0, n))
+    uint32_t *remote_ok;          // [nl] cross-partition matches confirmed by exchange A
 };
 
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_kernel(ScanMatchArgs a) {
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 #pragma unroll
         for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cand[vv[j]] : make_uint2(kNone, kNone);
 #pragma unroll
-        for (int j = 0; j < kItems; ++j) px[j] = cc[j].x != kNone ? a.cand[cc[j].x].y : kNone;
+        for (int j = 0; j < kItems; ++j)
+            px[j] = (cc[j].x != kNone && cc[j].x - a.lo < a.nl) ? a.cand[cc[j].x].y : kNone;
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
             const uint32_t v = vv[j];
@@ -288,7 +291,13 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
                 if (x != kNone) {
                     const uint32_t id = cv.y;
                     // weight keys are unique per edge
-                    const bool mutual = px[j] == id;
+                    bool mutual;
+                    if (x - a.lo < a.nl) {
+                        mutual = px[j] == id;
+                    } else {   // partner on another partition: its owner confirmed the edge (exchange A)
+                        mutual = a.remote_ok[v - a.lo] != 0;
+                        if (mutual) a.remote_ok[v - a.lo] = 0;
+                    }
                     if (mutual) {
                         atomicOr(a.matched + (v >> 5), 1u << (v & 31));
                         a.mround[v] = (uint32_t)a.round;
@@ -454,6 +463,105 @@ int lmx_scan_configure_grids(lmx_ctx *ctx) {
     return LMX_OK;
 }
 
+// Per-match state: counters, outputs, bitmap, match rounds, pointers; round 0's
+// list is A_0 = bins0.
+static int scan_begin(lmx_ctx *ctx) {
+    const size_t n = (size_t)ctx->n;
+    cudaStream_t st = ctx->stream;
+    LMX_TRY(lmx_ensure_ctr(ctx, 64));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, st));
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, st));
+    if (n) {
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mate_target, 0xFF, n * 8, st));   // -1
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->matched, 0, (n + 31) / 32 * 4, st));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mround, 0xFF, n * 4, st));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, n * 4, st));
+    }
+    ctx->ctr_host[0] = RoundCtr{};
+    ctx->ctr_host[0].pad[0] = ctx->n_bins0[0];
+    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice, st));
+    return LMX_OK;
+}
+
+// Round r's candidate probe over A_r.
+static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool rerandomize) {
+    ScanArgs a;
+    a.vbeg = ctx->vbeg;
+    a.deg0 = ctx->deg0;
+    a.ptr = ctx->vdeg;
+    a.cand = ctx->cand;
+    a.cand0 = ctx->cand0;
+    a.ids = ctx->ids0;
+    a.matched = ctx->matched;
+    a.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    a.ctr = ctx->ctr + r;
+    a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
+    a.D = ctx->n_distinct;
+    a.tie_rank = ctx->tie_rank;
+    a.eid_of_x = ctx->eid_of_x;
+    if (r == 0) lmx_scan_round_kernel<true><<<ctx->scan_grid[0], kBlock, 0, ctx->stream>>>(a);
+    else lmx_scan_round_kernel<false><<<ctx->scan_grid[1], kBlock, 0, ctx->stream>>>(a);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+// Round r's match kernel over A_r; appends A_{r+1}.
+static int scan_enqueue_match(lmx_ctx *ctx, int r) {
+    ScanMatchArgs ma;
+    ma.cand = ctx->cand;
+    ma.matched = ctx->matched;
+    ma.mround = ctx->mround;
+    ma.mate = ctx->mate_target;
+    ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
+    ma.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    ma.anext = ctx->lists[(r + 1) & 1];
+    ma.ebits = ctx->ebits;
+    ma.eid_of_x = ctx->eid_of_x;
+    ma.ctr = ctx->ctr + r;
+    ma.ctr_next = ctx->ctr + r + 1;
+    ma.round = r;
+    ma.lo = (uint32_t)ctx->lo;
+    ma.nl = (uint32_t)ctx->n_local;
+    ma.remote_ok = ctx->remote_ok;
+    lmx_scan_match_kernel<<<ctx->scan_match_grid, kBlock, 0, ctx->stream>>>(ma);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+// Death-round histogram of this context's lowpair (all edges; a partition's
+// share when p > 1) into ctx->hist, bins [0, n_rounds] (max(., 256) of them).
+static int scan_hist_launch(lmx_ctx *ctx, int n_rounds) {
+    cudaStream_t st = ctx->stream;
+    const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
+    if (ctx->hist_cap < nbins) {
+        lmx_free(ctx, (void **)&ctx->hist, ctx->hist_cap * 8);
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, nbins * 8, "death histogram"));
+        ctx->hist_cap = nbins;
+    }
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
+    const int grid = ctx->num_sms * 8;
+    const unsigned long long nn = (unsigned long long)ctx->n, mm = ctx->lowpair_n;
+    const uint32_t R = (uint32_t)n_rounds;
+    if (mm == 0) return LMX_OK;
+    if (n_rounds < 15) {
+        lmx_pack_mround<4><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
+        lmx_scan_hist_kernel<4><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                        ctx->hist);
+    } else if (n_rounds < 255) {
+        lmx_pack_mround<8><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
+        lmx_scan_hist_kernel<8><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                        ctx->hist);
+    } else {
+        lmx_scan_hist_kernel<32><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
+                                                         ctx->hist);
+    }
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += n_rounds < 255 ? 2 : 1;
+    return LMX_OK;
+}
+
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                         std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
     stats.clear();
@@ -463,21 +571,9 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     ctx->timing.round_kernel_ms = 0;
     ctx->timing.match_kernel_ms = 0;
     const size_t n = (size_t)ctx->n;
-    const size_t cap = (size_t)std::max<int64_t>(ctx->n_local, 1);
     cudaStream_t st = ctx->stream;
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
-    LMX_TRY(lmx_ensure_ctr(ctx, 64));
-    LMX_CUDA(ctx, cudaMemsetAsync(ctx->ctr, 0, sizeof(RoundCtr) * (size_t)ctx->ctr_cap, st));
-    LMX_CUDA(ctx, cudaMemsetAsync(ctx->ebits, 0, ((size_t)std::max<int64_t>(ctx->m, 1) + 31) / 32 * 4, st));
-    if (n) {
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mate_target, 0xFF, n * 8, st));   // -1
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->matched, 0, (n + 31) / 32 * 4, st));
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mround, 0xFF, n * 4, st));
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, cap * 4, st));
-    }
-    ctx->ctr_host[0] = RoundCtr{};
-    ctx->ctr_host[0].pad[0] = ctx->n_bins0[0];
-    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr, ctx->ctr_host, sizeof(RoundCtr), cudaMemcpyHostToDevice, st));
+    LMX_TRY(scan_begin(ctx));
 
     int tl_used = 0;
     auto tl_mark = [&]() -> int {
@@ -497,42 +593,10 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_TRY(lmx_ensure_ctr(ctx, r + batch + 1));
         const int r0 = r;
         for (int b = 0; b < batch; ++b, ++r) {
-            const uint32_t *alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
-            ScanArgs a;
-            a.vbeg = ctx->vbeg;
-            a.deg0 = ctx->deg0;
-            a.ptr = ctx->vdeg;
-            a.cand = ctx->cand;
-            a.cand0 = ctx->cand0;
-            a.ids = ctx->ids0;
-            a.matched = ctx->matched;
-            a.alist = alist;
-            a.ctr = ctx->ctr + r;
-            a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
-            a.D = ctx->n_distinct;
-            a.tie_rank = ctx->tie_rank;
-            a.eid_of_x = ctx->eid_of_x;
-            if (r == 0) lmx_scan_round_kernel<true><<<ctx->scan_grid[0], kBlock, 0, st>>>(a);
-            else lmx_scan_round_kernel<false><<<ctx->scan_grid[1], kBlock, 0, st>>>(a);
-            LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(scan_enqueue_probe(ctx, r, seed_masked, rerandomize));
             LMX_TRY(tl_mark());
-            ScanMatchArgs ma;
-            ma.cand = ctx->cand;
-            ma.matched = ctx->matched;
-            ma.mround = ctx->mround;
-            ma.mate = ctx->mate_target;
-            ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
-            ma.alist = alist;
-            ma.anext = ctx->lists[(r + 1) & 1];
-            ma.ebits = ctx->ebits;
-            ma.eid_of_x = ctx->eid_of_x;
-            ma.ctr = ctx->ctr + r;
-            ma.ctr_next = ctx->ctr + r + 1;
-            ma.round = r;
-            lmx_scan_match_kernel<<<ctx->scan_match_grid, kBlock, 0, st>>>(ma);
-            LMX_CUDA(ctx, cudaGetLastError());
+            LMX_TRY(scan_enqueue_match(ctx, r));
             LMX_TRY(tl_mark());
-            ctx->timing.round_launches += 2;
         }
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r0, ctx->ctr + r0, sizeof(RoundCtr) * (size_t)batch,
                                       cudaMemcpyDeviceToHost, st));
@@ -550,32 +614,8 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
     std::vector<unsigned long long> hist(nbins, 0);
     if (ctx->m > 0) {
-        if (ctx->hist_cap < nbins) {
-            lmx_free(ctx, (void **)&ctx->hist, ctx->hist_cap * 8);
-            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, nbins * 8, "death histogram"));
-            ctx->hist_cap = nbins;
-        }
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
-        const int grid = ctx->num_sms * 8;
-        const int hgrid = grid;
-        const size_t hsm = 0;
-        const unsigned long long nn = (unsigned long long)n, mm = (unsigned long long)ctx->m;
-        const uint32_t R = (uint32_t)n_rounds;
-        if (n_rounds < 15) {
-            lmx_pack_mround<4><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-            lmx_scan_hist_kernel<4><<<hgrid, kBlock, hsm, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
-                                                               ctx->hist);
-        } else if (n_rounds < 255) {
-            lmx_pack_mround<8><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-            lmx_scan_hist_kernel<8><<<hgrid, kBlock, hsm, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
-                                                               ctx->hist);
-        } else {
-            lmx_scan_hist_kernel<32><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
-                                                             ctx->hist);
-        }
-        LMX_CUDA(ctx, cudaGetLastError());
+        LMX_TRY(scan_hist_launch(ctx, n_rounds));
         LMX_TRY(tl_mark());
-        ctx->timing.round_launches += n_rounds < 255 ? 2 : 1;
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
     }
@@ -619,5 +659,143 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     }
     for (int i = 0; i < r; ++i) ctx->timing.slot_reads += (int64_t)ctx->ctr_host[i].slot_reads;
     n_matched = total_matched_v / 2;
+    return LMX_OK;
+}
+
+// ---- the stepped multi-GPU protocol on the scan loop (bsp.py:101-205) -------
+// Every partition keeps the global weight-ordered segments and global
+// per-vertex arrays and works on the vertices it owns: A_0 = owned vertices
+// with an edge.  Per round: probe (owned A_r) -> propose (a candidate whose
+// partner is owned elsewhere is sent to the partner's owner, exchange A) ->
+// accept (the owner confirms iff its own candidate is the same edge) -> match
+// -> all-gather of the owned bitmap words (exchange B) -> all-reduce of
+// (candidates found, matched vertices): "none found" ends the loop.  After it
+// the owned mround slices are all-gathered and each partition histograms the
+// death rounds of its own lowpair share; the histograms add up.
+
+namespace lmx {
+
+struct ScanProposeArgs {
+    const uint32_t *alist;
+    const RoundCtr *ctr;
+    const uint2 *cand;
+    const uint32_t *eid_of_x;
+    const unsigned long long *bounds;   // p + 1 cut points (global ids)
+    int p;
+    uint32_t lo, nl;
+    uint32_t *cnt;      // [p] records per destination
+    uint2 *region;      // p regions of capacity nl: {partner (global id), edge id}
+};
+
+__global__ void lmx_scan_propose_kernel(ScanProposeArgs a) {
+    const uint32_t total = a.ctr->pad[0];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint32_t v = a.alist[i];
+        const uint2 c = a.cand[v];
+        if (c.x == kNone || c.x - a.lo < a.nl) continue;   // no candidate, or a local partner
+        int k = 0;
+        while (k + 1 < a.p && c.x >= a.bounds[k + 1]) ++k;
+        const uint32_t pos = atomicAdd(a.cnt + k, 1u);
+        a.region[(unsigned long long)k * a.nl + pos] = make_uint2(c.x, a.eid_of_x[c.y]);
+    }
+}
+
+__global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, const uint2 *cand,
+                                       const uint32_t *eid_of_x, uint32_t lo, uint32_t *remote_ok) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint2 r = rec[i];
+        const uint2 c = cand[r.x];
+        if (c.x != kNone && eid_of_x[c.y] == r.y) remote_ok[r.x - lo] = 1u;
+    }
+}
+
+}  // namespace lmx
+
+int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
+    ctx->timing.round_launches = 0;
+    ctx->dist_round = 0;
+    ctx->dist_seed = seed_masked;
+    ctx->dist_rr = rerandomize;
+    ctx->mate_target = ctx->mate;
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, (size_t)std::max<int64_t>(ctx->n_local, 1) * 4, ctx->stream));
+    LMX_TRY(scan_begin(ctx));
+    LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return LMX_OK;
+}
+
+int lmx_scan_dist_round(lmx_ctx *ctx) {
+    LMX_TRY(lmx_ensure_ctr(ctx, ctx->dist_round + 2));
+    return scan_enqueue_probe(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
+}
+
+int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
+    const int p = ctx->dist_p;
+    const int r = ctx->dist_round;
+    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    const size_t need = nl * (size_t)(p + 1);   // p regions + the packed copy
+    if (ctx->send_cap < need) {
+        lmx_dfree(ctx, ctx->send);
+        ctx->send = nullptr;
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send, need * sizeof(uint2)));
+        ctx->send_cap = need;
+    }
+    // send_cnt block: [64] u32 counts, [64] i64 counts at +256, the p + 1 bounds at +1024
+    if (!ctx->send_cnt) {
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->send_cnt, 2048));
+        std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
+        LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 1024, hb.data(),
+                                      (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    unsigned long long *bnd =
+        reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 1024);
+    long long *counts64 = reinterpret_cast<long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 256);
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 64 * sizeof(uint32_t), ctx->stream));
+    ScanProposeArgs pa;
+    pa.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
+    pa.ctr = ctx->ctr + r;
+    pa.cand = ctx->cand;
+    pa.eid_of_x = ctx->eid_of_x;
+    pa.bounds = bnd;
+    pa.p = p;
+    pa.lo = (uint32_t)ctx->lo;
+    pa.nl = (uint32_t)ctx->n_local;
+    pa.cnt = ctx->send_cnt;
+    pa.region = ctx->send;
+    lmx_scan_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
+    LMX_CUDA(ctx, cudaGetLastError());
+    uint2 *packed = ctx->send + nl * (size_t)p;
+    lmx_pack_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(ctx->send, ctx->send_cnt, p, (uint32_t)nl, packed,
+                                                                 counts64);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 2;
+    *counts_dev = counts64;
+    *packed_dev = packed;
+    return LMX_OK;
+}
+
+int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count) {
+    if (count <= 0) return LMX_OK;
+    lmx_scan_accept_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
+        ctx->recv, (unsigned long long)count, ctx->cand, ctx->eid_of_x, (uint32_t)ctx->lo, ctx->remote_ok);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
+int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev) {
+    const int r = ctx->dist_round;
+    LMX_TRY(scan_enqueue_match(ctx, r));
+    *stats_dev = &ctx->ctr[r].live_slots;   // {candidates found, matched vertices}
+    ctx->dist_round = r + 1;
+    return LMX_OK;
+}
+
+int lmx_scan_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins) {
+    if (n_rounds < 0) return lmx_fail(ctx, LMX_EINVAL, "negative round count");
+    LMX_TRY(scan_hist_launch(ctx, n_rounds));
+    *hist_dev = ctx->hist;
+    *nbins = (int)std::max<size_t>((size_t)n_rounds + 1, kHistBins);
     return LMX_OK;
 }

@@ -436,8 +436,8 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *rank, 
 
 // lowpair: every edge once as {owner v, neighbour u} with u < v, in slot order
 // (so grouped by v up to block interleaving).
-__global__ void k_low_select(const uint32_t *owner, const uint2 *ids, unsigned long long slots, uint2 *lowpair,
-                             unsigned long long *count) {
+__global__ void k_low_select(const uint32_t *owner, const uint2 *ids, unsigned long long slots, uint32_t lo,
+                             uint32_t hi, uint2 *lowpair, unsigned long long *count) {
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ unsigned long long s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -451,7 +451,7 @@ __global__ void k_low_select(const uint32_t *owner, const uint2 *ids, unsigned l
         if (i < slots) {
             v = owner[i];
             u = ids[i].x;
-            take = u < v;
+            take = u < v && v >= lo && v < hi;   // a partition counts the edges of its own higher ends
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, take);
         if (lane == 0) s_cnt[warp] = __popc(bal);
@@ -526,7 +526,8 @@ static int build_scan_slots(lmx_ctx *ctx, const uint32_t *eid_sorted, const uint
         if ((rc = lmx_alloc(ctx, (void **)&cnt, 8, "lowpair count")) != LMX_OK) break;
         e = cudaMemsetAsync(cnt, 0, 8, st);
         if (e == cudaSuccess) {
-            k_low_select<<<ctx->num_sms * 8, kBlock, 0, st>>>(okey2, ctx->ids0, slots, ctx->lowpair, cnt);
+            k_low_select<<<ctx->num_sms * 8, kBlock, 0, st>>>(okey2, ctx->ids0, slots, (uint32_t)ctx->lo,
+                                                             (uint32_t)ctx->hi, ctx->lowpair, cnt);
             e = cudaGetLastError();
         }
         unsigned long long got = 0;
@@ -534,7 +535,11 @@ static int build_scan_slots(lmx_ctx *ctx, const uint32_t *eid_sorted, const uint
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         lmx_free(ctx, (void **)&cnt, 8);
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "lowpair"); break; }
-        if (got != m) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count"); break; }
+        if (got > m || (ctx->dist_p == 1 && got != m)) {
+            rc = lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count");
+            break;
+        }
+        ctx->lowpair_n = got;
     } while (0);
     cudaStreamSynchronize(st);
     lmx_free(ctx, (void **)&okey, slots * 4);
@@ -649,8 +654,8 @@ static int weight_stage(lmx_ctx *ctx) {
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
             // round-loop algorithm: the weight-ordered scan needs (almost) distinct
-            // weights (a fixed key order) and the whole graph in one context
-            if (distinct && ctx->dist_p == 1 && !ctx->dist_requested && ctx->force_algo != 0) {
+            // weights (a fixed key order); partitions keep the global segments
+            if (distinct && ctx->force_algo != 0) {
                 ctx->algo = 1;
                 lmx_free(ctx, (void **)&keys, m * 8);
                 lmx_free(ctx, (void **)&keys2, m * 8);
@@ -815,8 +820,9 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     LMX_CUDA(ctx, cudaMemcpyAsync(&top, ctx->vbeg + ctx->hi, 8, cudaMemcpyDeviceToHost, st));
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     slots = top - base;
+    if (ctx->algo == 1) slots = 2 * m;   // scan loop: every partition keeps the global segments
     ctx->slots_local = (int64_t)slots;
-    if (ctx->dist_p > 1) {
+    if (ctx->dist_p > 1 && ctx->algo == 0) {
         // local segment offsets and degrees of the owned range
         unsigned long long *vl = nullptr;
         uint32_t *dl = nullptr;
@@ -868,7 +874,8 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     {
         unsigned long long *cnt = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8 * kBuckets, "bucket counts"));
-        cub::CountingInputIterator<uint32_t> it(0);
+        // compacting loop: local indices; scan loop: global ids of the owned range
+        cub::CountingInputIterator<uint32_t> it(ctx->algo == 1 ? (uint32_t)lo : 0u);
         size_t tmp = 0;
         LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->bins0, cnt, (long long)nl,
                                             InBucket{ctx->deg0, 0}, st));

@@ -66,6 +66,8 @@ def _bind(lib):
         "lmx_dist_match": (c_int, [p, ctypes.POINTER(p)]),
         "lmx_dist_state": (c_int, [p, ctypes.POINTER(p), ctypes.POINTER(p), ctypes.POINTER(p),
                                    ctypes.POINTER(p)]),
+        "lmx_dist_mround": (c_int, [p, ctypes.POINTER(p)]),
+        "lmx_dist_hist": (c_int, [p, c_int, ctypes.POINTER(p), ctypes.POINTER(c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -93,10 +95,13 @@ def _view(ptr: int, shape, typestr: str, device):
 class DistRank:
     """One partition: a liblmx context loaded with LMX_OPT_DIST_P / RANK."""
 
-    def __init__(self, g, p: int, rank: int, device: int = 0, stream=None, rmat: dict | None = None):
+    def __init__(self, g, p: int, rank: int, device: int = 0, stream=None, rmat: dict | None = None,
+                 algo: str = "auto"):
         """Load partition `rank` of `p` from a host graph `g`, or, with
         ``rmat=dict(scale=..., edge_factor=..., seed=...)``, from the device
-        RMAT generator (every rank generates the same graph and keeps its part)."""
+        RMAT generator (every rank generates the same graph and keeps its part).
+        ``algo`` picks the round loop as ``Engine.set_algo`` does ("auto":
+        the scan loop when the weights are distinct)."""
         import torch
         self.eng = Engine(device)
         self.lib = self.eng._lib
@@ -109,6 +114,7 @@ class DistRank:
         self.eng.set_stream(stream)
         self._opt(LMX_OPT_DIST_P, p)
         self._opt(LMX_OPT_DIST_RANK, rank)
+        self.eng.set_algo(algo)
         if rmat is not None:
             self.eng.gen_rmat(**rmat)
         else:
@@ -125,6 +131,13 @@ class DistRank:
         self.bitmap = _view(bm.value, (max(self.words, 1),), "<i4", self.device)
         self.mate = _view(mate.value, (max(self.n, 1),), "<i8", self.device)
         self.ebits = _view(eb.value, ((max(self.m, 1) + 31) // 32,), "<i4", self.device)
+        # round loop chosen by the load: "scan" (weight-ordered, distinct weights) or "compact"
+        self.algo = self.eng.algo()
+        self.mround = None
+        if self.algo == "scan":
+            mr = ctypes.c_void_p()
+            self._chk(self.lib.lmx_dist_mround(self.eng._h, ctypes.byref(mr)), "lmx_dist_mround")
+            self.mround = _view(mr.value, (max(self.n, 1),), "<i4", self.device)
 
     def _opt(self, opt, val):
         self._chk(self.lib.lmx_set_option(self.eng._h, opt, val), "lmx_set_option")
@@ -166,6 +179,17 @@ class DistRank:
     def word_range(self, k: int):
         return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
 
+    def vertex_range(self, k: int):
+        return int(self.bounds[k]), int(self.bounds[k + 1])
+
+    def hist(self, n_rounds: int):
+        """Scan loop: this partition's death-round histogram (device int64 view)."""
+        hp = ctypes.c_void_p()
+        nb = ctypes.c_int()
+        self._chk(self.lib.lmx_dist_hist(self.eng._h, int(n_rounds), ctypes.byref(hp), ctypes.byref(nb)),
+                  "lmx_dist_hist")
+        return _view(hp.value, (nb.value,), "<i8", self.device)
+
     def close(self):
         self.eng.close()
 
@@ -206,6 +230,16 @@ class LocalComm:
             for dst in range(self.p):
                 if dst != src:
                     ranks[dst].bitmap[w0:w1].copy_(seg)
+
+    def allgather_mround(self, ranks):
+        for src in range(self.p):
+            a, b = ranks[src].vertex_range(src)
+            if b <= a:
+                continue
+            seg = ranks[src].mround[a:b]
+            for dst in range(self.p):
+                if dst != src:
+                    ranks[dst].mround[a:b].copy_(seg)
 
     def allreduce_sum(self, values):
         return [sum(col) for col in zip(*(v.tolist() for v in values))]
@@ -260,9 +294,24 @@ class TorchComm:
             if k != self.rank and b > a:
                 me.bitmap[a:b].copy_(out[k * width: k * width + (b - a)])
 
+    def allgather_mround(self, ranks):
+        import torch
+        (me,) = ranks
+        spans = [me.vertex_range(k) for k in range(self.p)]
+        width = max(max(b - a for a, b in spans), 1)
+        a, b = spans[self.rank]
+        row = torch.zeros(width, dtype=torch.int32, device=me.device)
+        if b > a:
+            row[: b - a].copy_(me.mround[a:b])
+        out = torch.empty(self.p * width, dtype=torch.int32, device=me.device)
+        self.dist.all_gather_into_tensor(out, row)
+        for k, (x, y) in enumerate(spans):
+            if k != self.rank and y > x:
+                me.mround[x:y].copy_(out[k * width: k * width + (y - x)])
+
     def allreduce_sum(self, values):
         (vals,) = values
-        t = vals.clone()   # device int64[2]
+        t = vals.clone()   # device int64[k]
         self.dist.all_reduce(t)
         return [int(x) for x in t.tolist()]
 
@@ -289,6 +338,11 @@ def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int
     synchronisations per round: the exchange-A counts and the statistics
     all-reduce (termination).
     """
+    algos = {r.algo for r in ranks}
+    if len(algos) != 1:
+        raise RuntimeError(f"internal: partitions disagree on the round loop {sorted(algos)}")
+    if algos == {"scan"}:
+        return _run_rounds_scan(ranks, comm, seed, rerandomize, max_rounds)
     for r in ranks:
         r.begin(seed, rerandomize)
     before = []
@@ -321,13 +375,56 @@ def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int
     return stats, records
 
 
+def _run_rounds_scan(ranks, comm, seed: int, rerandomize: bool, max_rounds: int | None):
+    """The protocol on the weight-ordered scan loop (lmx_scan.cu): the loop ends
+    when no partition finds a candidate; RoundStats come afterwards from the
+    summed death-round histograms (each edge counted by the owner of its
+    higher end), as in the single-GPU scan loop."""
+    for r in ranks:
+        r.begin(seed, rerandomize)
+    matched = []
+    records = []
+    while True:
+        for r in ranks:
+            r.round()
+        sends = [r.propose() for r in ranks]
+        recv_counts = comm.alltoallv(ranks, sends)
+        records.append(comm.record_total(recv_counts))
+        for r, cnt in zip(ranks, recv_counts):
+            r.accept(cnt)
+        local = [r.match() for r in ranks]
+        comm.allgather_bitmap(ranks)
+        found, mv = comm.allreduce_sum(local)
+        if found == 0:
+            records.pop()
+            break
+        if mv % 2:
+            raise RuntimeError("internal: odd global matched-vertex count")
+        matched.append(mv // 2)
+        if max_rounds is not None and len(matched) > max_rounds:
+            raise RuntimeError("round limit exceeded")
+    n_rounds = len(matched)
+    comm.allgather_mround(ranks)
+    hist = comm.allreduce_sum([r.hist(n_rounds) for r in ranks])
+    m = ranks[0].m
+    if hist[n_rounds] != 0 or sum(hist) != m:
+        raise RuntimeError(f"internal: death-round histogram covers {sum(hist)} of {m} edges, "
+                           f"{hist[n_rounds]} outlived the loop")
+    stats = []
+    alive = m
+    for i in range(n_rounds):
+        stats.append(RoundStats(alive, matched[i], hist[i]))
+        alive -= hist[i]
+    return stats, records
+
+
 def _unpack_ids(ebits, m: int) -> np.ndarray:
     words = ebits.cpu().numpy().view(np.uint32)
     bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:m]
     return np.nonzero(bits)[0].astype(np.int64)
 
 
-def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int = 0):
+def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int = 0, algo: str = "auto"):
     """Drop-in for ``bsp_local_max(g, p, seed, rerandomize)`` (bsp.py:101-205):
     p partitions emulated in this process on one B200.  ``trace.messages``
     holds the exchange-A record count per round (cf. ``RoundMessages``)."""
@@ -339,7 +436,7 @@ def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int =
         raise ValueError(f"p={p} exceeds the vertex count {g.num_vertices}")
     torch.cuda.set_device(device)
     stream = torch.cuda.current_stream(device).cuda_stream
-    ranks = [DistRank(g, p, k, device, stream) for k in range(p)]
+    ranks = [DistRank(g, p, k, device, stream, algo=algo) for k in range(p)]
     try:
         comm = LocalComm(p)
         stats, records = run_rounds(ranks, comm, seed, rerandomize)

@@ -34,8 +34,12 @@ def partition_bounds(n: int, eu, ev, p: int) -> np.ndarray:
 
 
 class EmulatedRank:
-    def __init__(self, g, p: int, rank: int):
-        self.p, self.rank = p, rank
+    """``algo`` mirrors the device loop the partition emulates: "compact"
+    (match reports live slots) or "scan" (match reports candidates found;
+    ``mround`` + ``hist`` give the statistics after the loop)."""
+
+    def __init__(self, g, p: int, rank: int, algo: str = "compact"):
+        self.p, self.rank, self.algo = p, rank, algo
         self.device = torch.device("cpu")
         self.n, self.m = int(g.num_vertices), int(np.asarray(g.edge_u).size)
         self.eu = np.asarray(g.edge_u, dtype=np.int64)
@@ -47,6 +51,18 @@ class EmulatedRank:
         self.bitmap = torch.zeros(max(self.words, 1), dtype=torch.int32)
         self.mate = torch.full((max(self.n, 1),), -1, dtype=torch.int64)
         self.ebits = torch.zeros((max(self.m, 1) + 31) // 32, dtype=torch.int32)
+        self.mround = torch.full((max(self.n, 1),), -1, dtype=torch.int32) if algo == "scan" else None
+
+    def vertex_range(self, k: int):
+        return int(self.bounds[k]), int(self.bounds[k + 1])
+
+    def hist(self, n_rounds: int):
+        """Death rounds of the edges whose higher end this partition owns."""
+        mr = self.mround.numpy().view(np.uint32).astype(np.int64)
+        hi = np.maximum(self.eu, self.ev)
+        own = (hi >= self.lo) & (hi < self.hi)
+        d = np.minimum(np.minimum(mr[self.eu[own]], mr[self.ev[own]]), n_rounds)
+        return torch.from_numpy(np.bincount(d, minlength=max(n_rounds + 1, 256)).astype(np.int64))
 
     def word_range(self, k: int):
         return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
@@ -70,6 +86,8 @@ class EmulatedRank:
         self.ebits.zero_()
         self.cand = {}
         self.remote_ok = set()
+        if self.mround is not None:
+            self.mround.fill_(-1)
 
     def round(self):
         rs = O.round_seed(self.seed, self.r, self.rr)
@@ -117,8 +135,11 @@ class EmulatedRank:
             if mutual:
                 words[v >> 5] |= np.uint32(1 << (v & 31))
                 self.mate[v] = x
+                if self.mround is not None:
+                    self.mround[v] = self.r
                 mv += 1
                 if v < x:
                     eb[e >> 5] |= np.uint32(1 << (e & 31))
         self.r += 1
-        return torch.tensor([self.live_slots, mv], dtype=torch.int64)
+        first = len(self.cand) if self.algo == "scan" else self.live_slots
+        return torch.tensor([first, mv], dtype=torch.int64)

@@ -34,8 +34,8 @@ def main():
                                                     else np.ones(m))
         gn, eu, ev, ew = O.build_graph_vec(u, v, w, n)
         g = Graph(gn, eu, ev, ew)
-        me = EmulatedRank(g, comm.p, comm.rank)
-        for rr in (True, False):
+        for algo, rr in (("compact", True), ("compact", False), ("scan", True), ("scan", False)):
+            me = EmulatedRank(g, comm.p, comm.rank, algo)
             stats, records = run_rounds([me], comm, seed, rr)
             mate, ebits = comm.gather_outputs([me])
             if comm.rank == 0:
@@ -43,7 +43,7 @@ def main():
                 ref = O.c_local_max(gn, eu, ev, ew, seed, rr)
                 ok = (np.array_equal(mate.numpy()[:gn], ref.mate) and np.array_equal(ids, ref.matched_ids)
                       and [(s.edges_before, s.edges_matched, s.edges_removed) for s in stats] == ref.rounds)
-                print(f"case seed={seed} n={n} kind={kind} rr={rr} rounds={len(stats)} "
+                print(f"case seed={seed} n={n} kind={kind} algo={algo} rr={rr} rounds={len(stats)} "
                       f"cut-records={sum(records)} ok={ok}", flush=True)
                 failures += 0 if ok else 1
     dist.barrier()

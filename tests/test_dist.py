@@ -42,12 +42,13 @@ def test_gloo_world_size_2_matches_oracle():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
-    assert out.count("ok=True") == 8, out[-4000:]
+    assert out.count("ok=True") == 16 and "algo=scan" in out, out[-4000:]
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["auto", "compact"])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
-def test_dist_equals_single_gpu_small(golden_small, p):
+def test_dist_equals_single_gpu_small(golden_small, p, algo):
     from paper_1302_4587_b200 import Graph
     from paper_1302_4587_b200.dist import local_max_dist
     graphs = {gi: (n, built) for gi, n, _, built, _ in small_cases(golden_small)}
@@ -56,7 +57,7 @@ def test_dist_equals_single_gpu_small(golden_small, p):
         n, (eu, ev, w) = graphs[gi]
         if n < p or gi % 7:   # a spread of cases; each run sets up p contexts
             continue
-        matching, trace = local_max_dist(Graph(n, eu, ev, w), p, seed, rr)
+        matching, trace = local_max_dist(Graph(n, eu, ev, w), p, seed, rr, algo=algo)
         assert np.array_equal(matching.mate, mate), (gi, seed, rr, p)
         assert np.array_equal(matching.sorted_edge_ids(), ids), (gi, seed, rr, p)
         assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == rounds
@@ -81,13 +82,14 @@ def test_dist_reference_instances(golden_instances, name, p):
 
 
 @pytest.mark.gpu
-def test_dist_rmat_skewed_equals_single(engine):
+@pytest.mark.parametrize("algo", ["auto", "compact"])
+def test_dist_rmat_skewed_equals_single(engine, algo):
     """RMAT (relabelled, hubs) split over 4 partitions equals the single-GPU run."""
     from paper_1302_4587_b200.dist import local_max_dist
     engine.gen_rmat(14, 16, seed=5)
     g = engine.export_graph()
     mate, ids, rounds = engine.match_raw(5, True)
-    matching, trace = local_max_dist(g, 4, 5, True)
+    matching, trace = local_max_dist(g, 4, 5, True, algo=algo)
     assert np.array_equal(matching.mate, mate)
     assert np.array_equal(matching.sorted_edge_ids(), ids)
     assert trace.rounds == rounds
@@ -101,3 +103,17 @@ def test_run_matcher_dist_engine():
     a, _ = run_matcher(g, "localmax", 2, engine="b200")
     b, _ = run_matcher(g, "localmax", 2, engine="b200-dist", p=3)
     assert a == b
+
+
+@pytest.mark.gpu
+def test_dist_round_loop_choice():
+    """Distinct weights put the partitions on the scan loop; ties on the compacting loop."""
+    from paper_1302_4587_b200 import Graph
+    from paper_1302_4587_b200.dist import DistRank
+    n, eu, ev, w = O.gen_random(1 << 9, 4, 3)
+    for weights, want in ((w, "scan"), (np.ones_like(w), "compact")):
+        r = DistRank(Graph(n, eu, ev, weights), 2, 1)
+        try:
+            assert r.algo == want
+        finally:
+            r.close()
