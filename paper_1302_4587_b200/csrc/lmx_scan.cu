@@ -402,8 +402,11 @@ struct HistAcc {
 // in order (cache lines reused), the u lookups go to the lower ids -- the
 // high-degree end after relabelling.  A flat, coalesced pass, 4 edges per
 // thread in flight.
-// (Staging the hubs' packed words in 64 KB of shared memory per block was
-// measured slower: the occupancy it costs outweighs the L2 lookups it saves.)
+// Used for the u32 rounds (>= 255 rounds); the packed widths use the
+// persistent, pipelined lmx_scan_hist_hub_kernel below.  (A low-CSR variant
+// -- 4 B per edge, owners rebuilt per tile in shared memory -- moved half the
+// bytes but ran 3.1 ms against 2.2: its dependent loads per tile cost more
+// than the stream it saved.)
 template <int BITS>
 __global__ void __launch_bounds__(kBlock) lmx_scan_hist_kernel(const uint2 *lowpair, unsigned long long m,
                                                              const uint32_t *mround, const uint32_t *packed,
@@ -448,9 +451,77 @@ __global__ void __launch_bounds__(kBlock) lmx_scan_hist_kernel(const uint2 *lowp
         if (s_hist[i]) atomicAdd(hist + i, (unsigned long long)s_hist[i]);
 }
 
+#ifndef LMX_HIST_HUB_KB
+#define LMX_HIST_HUB_KB 80   // packed match rounds of the lowest ids staged in shared memory
+#endif
+constexpr int kHistThreads = 1024;
+
+// The same pass, persistent (two 1024-thread blocks per SM) and software-
+// pipelined: the next step's edge pairs are loaded before this step's
+// lookups, so the stream's DRAM latency overlaps the lookups.  The packed
+// rounds of the lowest `hw` words -- the highest-degree vertices after
+// relabelling, the target of most u lookups -- are staged once per block in
+// shared memory; L1 and L2 serve the rest.
+template <int BITS>
+__global__ void __launch_bounds__(kHistThreads, 2)
+    lmx_scan_hist_hub_kernel(const uint2 *lowpair, unsigned long long m, const uint32_t *packed, uint32_t R,
+                             uint32_t hw, unsigned long long *hist) {
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t *s_hist = s_dyn;
+    uint32_t *s_pk = s_dyn + kHistBins;
+    constexpr uint32_t kPer = 32 / BITS, kTop = (1u << BITS) - 1;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kHistBins; i += kHistThreads) s_hist[i] = 0;
+    for (uint32_t i = tid; i < hw; i += kHistThreads) s_pk[i] = __ldg(packed + i);
+    __syncthreads();
+    auto rnd = [&](uint32_t v) -> uint32_t {
+        const uint32_t w = v / kPer;
+        const uint32_t x = w < hw ? s_pk[w] : __ldg(packed + w);
+        return (x >> ((v % kPer) * BITS)) & kTop;
+    };
+    HistAcc<BITS == 4 ? 4 : 2> acc;
+    const uint4 *q = reinterpret_cast<const uint4 *>(lowpair);
+    const uint32_t nq = (uint32_t)(m / 2);
+    const uint32_t stride = gridDim.x * kHistThreads;
+    uint32_t i = blockIdx.x * kHistThreads + tid;
+    uint4 xn = i < nq ? __ldcs(q + i) : make_uint4(0, 0, 0, 0);
+    for (; i < nq; i += stride) {
+        const uint4 x = xn;
+        if (i + stride < nq) xn = __ldcs(q + i + stride);
+        const uint32_t d0 = min(min(rnd(x.x), rnd(x.y)), R);
+        const uint32_t d1 = min(min(rnd(x.z), rnd(x.w)), R);
+        acc.add(d0, s_hist, hist);
+        acc.add(d1, s_hist, hist);
+    }
+    if ((m & 1ULL) && blockIdx.x == 0 && tid == 0) {
+        const uint2 x = lowpair[m - 1];
+        acc.add(min(min(rnd(x.x), rnd(x.y)), R), s_hist, hist);
+    }
+    acc.flush(s_hist);
+    __syncthreads();
+    for (int i2 = tid; i2 < kHistBins; i2 += kHistThreads)
+        if (s_hist[i2]) atomicAdd(hist + i2, (unsigned long long)s_hist[i2]);
+}
+
 }  // namespace lmx
 
 using namespace lmx;
+
+template <int BITS>
+static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R) {
+    const unsigned long long nn = (unsigned long long)ctx->n;
+    constexpr uint32_t kPer = 32 / BITS;
+    const unsigned long long words = (nn + kPer - 1) / kPer;
+    const uint32_t cap = (uint32_t)(LMX_HIST_HUB_KB * 1024 / 4) - kHistBins;
+    const uint32_t hw = (uint32_t)std::min<unsigned long long>(words, cap);
+    const size_t smem = (size_t)(kHistBins + hw) * 4;
+    LMX_CUDA(ctx, cudaFuncSetAttribute(lmx_scan_hist_hub_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(LMX_HIST_HUB_KB * 1024)));
+    lmx_scan_hist_hub_kernel<BITS><<<ctx->num_sms * 2, kHistThreads, smem, ctx->stream>>>(ctx->lowpair, mm,
+                                                                                          ctx->mpacked, R, hw,
+                                                                                          ctx->hist);
+    return LMX_OK;
+}
 
 int lmx_scan_configure_grids(lmx_ctx *ctx) {
     int occ0 = 0, occ1 = 0, occm = 0;
@@ -547,12 +618,10 @@ static int scan_hist_launch(lmx_ctx *ctx, int n_rounds) {
     if (mm == 0) return LMX_OK;
     if (n_rounds < 15) {
         lmx_pack_mround<4><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-        lmx_scan_hist_kernel<4><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
-                                                        ctx->hist);
+        LMX_TRY(hist_hub_launch<4>(ctx, mm, R));
     } else if (n_rounds < 255) {
         lmx_pack_mround<8><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-        lmx_scan_hist_kernel<8><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
-                                                        ctx->hist);
+        LMX_TRY(hist_hub_launch<8>(ctx, mm, R));
     } else {
         lmx_scan_hist_kernel<32><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
                                                          ctx->hist);
