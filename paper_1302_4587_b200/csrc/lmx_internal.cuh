@@ -92,6 +92,8 @@ struct lmx_ctx {
     int round_grid[3][3] = {};   // persistent grid of each round-kernel instance [MODE][LAYOUT]
     int match_blocks = 0;
     int scan_grid[2] = {0, 0};   // scan round kernel grids (round 0, rounds >= 1)
+    int scan_last_rounds = -1;   // rounds of this context's last scan-loop matching (-1: none yet); a
+                                 // hint for the first batch only, kept across loads (results never depend on it)
     int scan_match_grid = 0;
     std::string err;
 

@@ -465,7 +465,8 @@ constexpr int kHistThreads = 1024;
 template <int BITS>
 __global__ void __launch_bounds__(kHistThreads, 2)
     lmx_scan_hist_hub_kernel(const uint2 *lowpair, unsigned long long m, const uint32_t *packed, uint32_t R,
-                             uint32_t hw, unsigned long long *hist) {
+                             const uint32_t *R_dev, uint32_t hw, unsigned long long *hist) {
+    if (R_dev) R = *R_dev;   // speculative batch: the round count is found on the device
     extern __shared__ uint32_t s_dyn[];
     uint32_t *s_hist = s_dyn;
     uint32_t *s_pk = s_dyn + kHistBins;
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kHistThreads, 2)
 using namespace lmx;
 
 template <int BITS>
-static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R) {
+static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R, const uint32_t *R_dev) {
     const unsigned long long nn = (unsigned long long)ctx->n;
     constexpr uint32_t kPer = 32 / BITS;
     const unsigned long long words = (nn + kPer - 1) / kPer;
@@ -518,8 +519,8 @@ static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R) {
     LMX_CUDA(ctx, cudaFuncSetAttribute(lmx_scan_hist_hub_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(LMX_HIST_HUB_KB * 1024)));
     lmx_scan_hist_hub_kernel<BITS><<<ctx->num_sms * 2, kHistThreads, smem, ctx->stream>>>(ctx->lowpair, mm,
-                                                                                          ctx->mpacked, R, hw,
-                                                                                          ctx->hist);
+                                                                                          ctx->mpacked, R, R_dev,
+                                                                                          hw, ctx->hist);
     return LMX_OK;
 }
 
@@ -601,15 +602,42 @@ static int scan_enqueue_match(lmx_ctx *ctx, int r) {
     return LMX_OK;
 }
 
+// The round count of a speculative batch of k rounds, on the device: the
+// first round that found no candidate (k if none did).  Stored after the bins.
+__global__ void lmx_find_rounds(const RoundCtr *ctr, int k, uint32_t *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        uint32_t r = (uint32_t)k;
+        for (int i = 0; i < k; ++i)
+            if (ctr[i].live_slots == 0) {
+                r = (uint32_t)i;
+                break;
+            }
+        *out = r;
+    }
+}
+
 // Death-round histogram of this context's lowpair (all edges; a partition's
 // share when p > 1) into ctx->hist, bins [0, n_rounds] (max(., 256) of them).
-static int scan_hist_launch(lmx_ctx *ctx, int n_rounds) {
+// spec_k > 0: a speculative batch of spec_k <= 14 rounds whose end is not
+// known on the host yet; the count is found on the device (n_rounds unused).
+static int scan_hist_launch(lmx_ctx *ctx, int n_rounds, int spec_k = 0) {
     cudaStream_t st = ctx->stream;
     const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
     if (ctx->hist_cap < nbins) {
-        lmx_free(ctx, (void **)&ctx->hist, ctx->hist_cap * 8);
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, nbins * 8, "death histogram"));
+        lmx_free(ctx, (void **)&ctx->hist, (ctx->hist_cap + 1) * 8);
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, (nbins + 1) * 8, "death histogram"));
         ctx->hist_cap = nbins;
+    }
+    if (spec_k > 0) {
+        uint32_t *R_dev = reinterpret_cast<uint32_t *>(ctx->hist + ctx->hist_cap);
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
+        lmx_find_rounds<<<1, 32, 0, st>>>(ctx->ctr, spec_k, R_dev);
+        if (ctx->lowpair_n == 0) return LMX_OK;
+        lmx_pack_mround<4><<<ctx->num_sms * 8, kBlock, 0, st>>>(ctx->mround, (unsigned long long)ctx->n, ctx->mpacked);
+        LMX_TRY(hist_hub_launch<4>(ctx, ctx->lowpair_n, 0u, R_dev));
+        LMX_CUDA(ctx, cudaGetLastError());
+        ctx->timing.round_launches += 3;
+        return LMX_OK;
     }
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
     const int grid = ctx->num_sms * 8;
@@ -618,10 +646,10 @@ static int scan_hist_launch(lmx_ctx *ctx, int n_rounds) {
     if (mm == 0) return LMX_OK;
     if (n_rounds < 15) {
         lmx_pack_mround<4><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-        LMX_TRY(hist_hub_launch<4>(ctx, mm, R));
+        LMX_TRY(hist_hub_launch<4>(ctx, mm, R, nullptr));
     } else if (n_rounds < 255) {
         lmx_pack_mround<8><<<grid, kBlock, 0, st>>>(ctx->mround, nn, ctx->mpacked);
-        LMX_TRY(hist_hub_launch<8>(ctx, mm, R));
+        LMX_TRY(hist_hub_launch<8>(ctx, mm, R, nullptr));
     } else {
         lmx_scan_hist_kernel<32><<<grid, kBlock, 0, st>>>(ctx->lowpair, mm, ctx->mround, ctx->mpacked, nn, R,
                                                          ctx->hist);
@@ -658,6 +686,36 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     LMX_TRY(tl_mark());
 
     int r = 0, n_rounds = -1, batch = 6;
+    const size_t nbins0 = kHistBins;
+    std::vector<unsigned long long> hist(nbins0, 0);
+    bool have_hist = false;
+    // Speculative first batch: the previous matching of this context took R
+    // rounds; enqueue R + 2 rounds (those past the end exit at once), the
+    // histogram with the round count found on the device, and read back
+    // everything with one synchronisation.  A longer run continues below.
+    // (Off under per-kernel timing, whose timeline expects one histogram.)
+    const int spec = (!ctx->kernel_timing && ctx->scan_last_rounds >= 0 && ctx->scan_last_rounds + 2 <= 14 &&
+                      ctx->m > 0) ? ctx->scan_last_rounds + 2 : 0;
+    if (spec) {
+        LMX_TRY(lmx_ensure_ctr(ctx, spec + 1));
+        for (; r < spec; ++r) {
+            LMX_TRY(scan_enqueue_probe(ctx, r, seed_masked, rerandomize));
+            LMX_TRY(scan_enqueue_match(ctx, r));
+        }
+        LMX_TRY(scan_hist_launch(ctx, 0, spec));
+        LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)spec,
+                                      cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins0 * 8, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        for (int i = 0; i < spec; ++i) {
+            if (ctx->ctr_host[i].live_slots == 0) {
+                n_rounds = i;
+                break;
+            }
+        }
+        have_hist = n_rounds >= 0;
+        batch = 4;
+    }
     while (n_rounds < 0 && ctx->m > 0) {
         LMX_TRY(lmx_ensure_ctr(ctx, r + batch + 1));
         const int r0 = r;
@@ -679,10 +737,12 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         batch = 4;
     }
     if (n_rounds < 0) n_rounds = 0;
+    ctx->scan_last_rounds = n_rounds;
     // death-round histogram -> RoundStats: bins [0, n_rounds) plus "outlived"
     const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
-    std::vector<unsigned long long> hist(nbins, 0);
-    if (ctx->m > 0) {
+    hist.resize(nbins, 0);
+    if (ctx->m > 0 && !have_hist) {
+        std::fill(hist.begin(), hist.end(), 0ULL);
         LMX_TRY(scan_hist_launch(ctx, n_rounds));
         LMX_TRY(tl_mark());
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));

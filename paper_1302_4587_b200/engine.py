@@ -404,6 +404,33 @@ def local_max_b200(g, seed: int, rerandomize: bool = True, device: int = 0) -> t
     return matching, trace
 
 
+def pram_local_max_b200(g, seed: int, checked: bool = False, rerandomize: bool = True,
+                        device: int = 0) -> tuple[Matching, PhaseTrace]:
+    """Drop-in for ``locmax.pram.pram_local_max(g, seed, checked, rerandomize)``
+    (pram.py:276-315): the same matching and RoundStats (the reference's PRAM
+    phases equal the sequential rounds, pram.py:276-281), and the same
+    ``trace.slot_ops`` linear-work meter, ``n + 3m`` for the set-up plus
+    ``m_r + 2 m_r`` (live edges and incidence slots) per phase (pram.py:293,300).
+
+    ``checked=True`` validates the result on the device (valid and maximal,
+    graph.py:212-237) and raises ``RuntimeError`` if it is not; the
+    reference's per-step write log (a property of its PRAM simulation) is not
+    produced, so ``trace.write_log`` stays ``None``.
+    """
+    t0 = time.perf_counter()
+    eng = default_engine(device)
+    eng.load_graph(g)
+    matching, trace = eng.match(g, seed, rerandomize)
+    trace.slot_ops = int(g.num_vertices) + 3 * int(np.asarray(g.edge_u).size) + \
+        3 * sum(int(r.edges_before) for r in trace.rounds)
+    if checked:
+        chk, _ = eng.validate(matching)
+        if not (chk.valid and chk.maximal):
+            raise RuntimeError(f"pram_local_max_b200: device validation failed: {chk}")
+    trace.wall_millis = (time.perf_counter() - t0) * 1000.0
+    return matching, trace
+
+
 class RbmDidNotConverge(RuntimeError):
     """matchers.py:353-354: rbm made no progress within its round limit."""
 
@@ -424,7 +451,9 @@ def run_matcher(g, algorithm: str, seed: int, engine: str = "b200", p: int = 4,
     """bench.py:119-142 dispatch with the B200 engines added.
 
     ``engine="b200"`` runs :func:`local_max_b200`; ``"b200-dist"`` runs the
-    1D-partitioned multi-GPU engine over ``p`` ranks (see ``dist.py``).  Other
+    1D-partitioned multi-GPU engine over ``p`` ranks (see ``dist.py``);
+    ``"b200-pram"`` runs :func:`pram_local_max_b200` (the "pram" engine's
+    trace, with ``slot_ops``).  Other
     engines / algorithms are the reference's and are delegated to ``locmax``
     when it is importable.
     """
@@ -432,10 +461,12 @@ def run_matcher(g, algorithm: str, seed: int, engine: str = "b200", p: int = 4,
         return local_max_b200(g, seed, rerandomize)
     if algorithm == "rbm" and engine == "b200":
         return rbm_b200(g, seed)
+    if algorithm == "localmax" and engine == "b200-pram":
+        return pram_local_max_b200(g, seed, rerandomize=rerandomize)
     if algorithm == "localmax" and engine == "b200-dist":
         from .dist import local_max_dist
         return local_max_dist(g, p, seed, rerandomize)
-    if engine in ("b200", "b200-dist"):
+    if engine in ("b200", "b200-dist", "b200-pram"):
         raise ValueError(f"algorithm {algorithm!r} only runs on the seq engine")
     try:
         from locmax.bench import run_matcher as ref_run_matcher

@@ -311,3 +311,33 @@ def test_rmat20_vs_oracle(engine):
     assert np.array_equal(mate, res.mate)
     assert np.array_equal(ids, res.matched_ids)
     assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in rounds] == res.rounds
+
+
+@pytest.mark.gpu
+def test_scan_speculative_batch_across_round_counts(engine):
+    """A repeated matching of one loaded graph enqueues its first batch from the
+    previous round count (one synchronisation).  Tied pairs on a decreasing
+    path make the round count depend on the seed (2 .. 8 rounds without
+    rerandomize), so later seeds run past the speculated batch, and shorter
+    ones end inside it; every result equals the oracle."""
+    n = 30
+    eu = np.arange(n - 1, dtype=np.int64)
+    ev = eu + 1
+    w = np.repeat(np.arange(40)[::-1].astype(np.float64) + 1.0, 2)[: n - 1]
+    g = _graph(n, eu, ev, w)
+    engine.set_algo("scan")
+    engine.set_layout("distinct")
+    try:
+        engine.load_graph(g)
+        assert engine.algo() == "scan"
+        counts = []
+        for seed in (14, 0, 1, 3, 15, 0, 14, 4):
+            res = O.c_local_max(n, eu, ev, w, seed, False)
+            matching, trace = engine.match(g, seed, False)
+            assert np.array_equal(matching.mate, res.mate), seed
+            assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == res.rounds
+            counts.append(len(res.rounds))
+        assert max(b - a for a, b in zip(counts, counts[1:])) >= 2
+    finally:
+        engine.set_algo("auto")
+        engine.set_layout("auto")
