@@ -150,10 +150,27 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
     const int tid = threadIdx.x, lane = tid & 31;
     unsigned long long found_n = 0, reads = 0, slow_n = 0;
     // thread per vertex, 4 vertices per lane per grab
+#ifndef LMX_SCAN_STATIC_PCT
+#define LMX_SCAN_STATIC_PCT 0   // rounds >= 1: share of the list split statically (measured: no gain)
+#endif
+    // The first part of the list is split statically (warp-strided chunks, no
+    // atomics); the rest is grabbed chunk by chunk, which balances the slow
+    // paths.  Round 0 has no dead slots to skip (only rare tied runs): all
+    // static.  (The grab atomics on one address serialise: ~1 per ns.)
+    constexpr uint32_t kChunk = 32u * kVpl;
+    const uint32_t nchunks = (na + kChunk - 1) / kChunk;
+    const uint32_t nstat = FIRST ? nchunks : (uint32_t)((unsigned long long)nchunks * LMX_SCAN_STATIC_PCT / 100);
+    uint32_t c = blockIdx.x * (uint32_t)kWarps + (uint32_t)(tid >> 5);
+    const uint32_t cstride = gridDim.x * (uint32_t)kWarps;
     for (;;) {
         uint32_t i0 = 0;
-        if (lane == 0) i0 = atomicAdd(&a.ctr->pad[1], 32u * kVpl);
-        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        if (c < nstat) {
+            i0 = c * kChunk;
+            c += cstride;
+        } else {
+            if (lane == 0) i0 = nstat * kChunk + atomicAdd(&a.ctr->pad[1], kChunk);
+            i0 = __shfl_sync(0xffffffffu, i0, 0);
+        }
         if (i0 >= na) break;
         uint32_t v[kVpl];
         uint2 c[kVpl];

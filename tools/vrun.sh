@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-python -m pytest tests -x -q -m gpu > gpurun_out/par.log 2>&1
-echo parity rc=$? >> gpurun_out/par.log
-python bench.py > gpurun_out/bench_spec.log 2>&1
-python tools/configs.py > gpurun_out/configs.log 2>&1
+for k in 1 2; do
+for so in build/variants/*.so; do LMX_LIBRARY=$so timeout 300 python tools/variant_bench.py --steps 4; LMX_LIBRARY=$so timeout 300 python tools/round_profile.py 26 | sed -n 3,4p; done
+done > gpurun_out/var.log 2>&1
