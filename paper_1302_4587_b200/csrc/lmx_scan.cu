@@ -54,11 +54,24 @@ namespace lmx {
 constexpr int kHistBins = 256;   // death-round bins kept in shared memory (more go global)
 constexpr int kVpl = LMX_SCAN_VPL;
 
+constexpr uint32_t kTiedFlag = 0x80000000u;   // scan loop: n < 2^31
+constexpr uint32_t kNbrMask = 0x7FFFFFFFu;
+
+// Weight key of v's current candidate (neighbour word w != kNone).
+__device__ __forceinline__ uint32_t cand_key(uint32_t v, uint32_t w, const uint32_t *ckey, const uint32_t *ptr,
+                                             const unsigned long long *vbeg, const uint2 *ids) {
+    return (w & kTiedFlag) ? ckey[v] : ids[vbeg[v] + ptr[v]].y;
+}
+
 struct ScanArgs {
     const unsigned long long *vbeg;
     const uint32_t *deg0;
     uint32_t *ptr;              // first possibly-live slot of each vertex (segment offset)
-    uint2 *cand;                // {nbr, weight key} of each vertex's candidate
+    // each vertex's candidate: the neighbour word (bit 31: the weight is tied)
+    // -- the probe's fast path and the match kernel read 4 bytes -- and, for a
+    // tied candidate only, its weight key; an untied candidate sits at slot
+    // ptr (cand_key() reads it there when a matched edge needs its id)
+    uint32_t *cnbr, *ckey;
     const uint2 *cand0;         // round-0 candidates: the first slot of each segment
     const uint2 *ids;           // ids0, weight-descending per segment
     const uint32_t *matched;    // matched-vertex bitmap
@@ -180,8 +193,14 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             v[it] = i < na ? a.alist[i] : kNone;
         }
 #pragma unroll
-        for (int it = 0; it < kVpl; ++it) c[it] = v[it] != kNone ? (FIRST ? a.cand0[v[it]] : a.cand[v[it]])
-                                                             : make_uint2(kNone, kNone);
+        for (int it = 0; it < kVpl; ++it) {
+            if (FIRST) {
+                c[it] = v[it] != kNone ? a.cand0[v[it]] : make_uint2(kNone, kNone);
+            } else {   // the neighbour word alone: {nbr, 0} or {nbr, tied marker >= D}
+                const uint32_t w = v[it] != kNone ? a.cnbr[v[it]] : kNone;
+                c[it] = w == kNone ? make_uint2(kNone, kNone) : make_uint2(w & kNbrMask, (w >> 31) ? kNone - 1 : 0u);
+            }
+        }
         bool keep[kVpl];
 #pragma unroll
         for (int it = 0; it < kVpl; ++it)
@@ -191,7 +210,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
         for (int it = 0; it < kVpl; ++it) {
             if (v[it] == kNone) continue;
             if (keep[it]) {
-                if (FIRST) a.cand[v[it]] = c[it];
+                if (FIRST) a.cnbr[v[it]] = c[it].x;   // not tied: flag clear; the key is slot ptr = 0
                 ++found_n;
             } else {
                 slow |= 1u << it;
@@ -221,7 +240,9 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             uint2 out = make_uint2(kNone, kNone);
             const bool found = advance<FIRST>(a, bk, pp, dk, out, reads);
             if (found && out.y >= a.D) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
-            a.cand[vk] = found ? out : make_uint2(kNone, kNone);
+            const bool tied = found && out.y >= a.D;
+            a.cnbr[vk] = found ? (out.x | (tied ? kTiedFlag : 0u)) : kNone;
+            if (tied) a.ckey[vk] = out.y;   // an untied candidate's key is the slot at ptr
             if (pp != pk) a.ptr[vk] = pp;
             found_n += found ? 1u : 0u;
             ++slow_n;
@@ -254,7 +275,11 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
 }
 
 struct ScanMatchArgs {
-    const uint2 *cand;
+    bool defer_ebits;             // single GPU: edge bits set after the loop (lmx_scan_edge_bits)
+    const uint32_t *cnbr, *ckey;
+    const uint32_t *ptr;
+    const unsigned long long *vbeg;
+    const uint2 *ids;
     uint32_t *matched;
     uint32_t *mround;             // round each vertex was matched in (~0 = never)
     long long *mate;
@@ -286,7 +311,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
         uint32_t wc = 0;
         // staged gathers: list entries, then candidates, then the partners'
         // keys, each stage for all items at once (their latencies overlap)
-        uint2 cc[kItems];
+        uint32_t cc[kItems];
         uint32_t px[kItems];
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
@@ -294,23 +319,25 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
             vv[j] = i < total ? a.alist[i] : kNone;
         }
 #pragma unroll
-        for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cand[vv[j]] : make_uint2(kNone, kNone);
+        for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cnbr[vv[j]] : kNone;
+        // mutual iff the partner's candidate neighbour is v: both are edges
+        // between v and x that are maximal at both ends, hence the same edge
+        // (also with parallel edges), so the 4-byte neighbour array suffices
 #pragma unroll
-        for (int j = 0; j < kItems; ++j)
-            px[j] = (cc[j].x != kNone && cc[j].x - a.lo < a.nl) ? a.cand[cc[j].x].y : kNone;
+        for (int j = 0; j < kItems; ++j) {
+            const uint32_t x = cc[j] != kNone ? (cc[j] & kNbrMask) : kNone;
+            px[j] = (x != kNone && x - a.lo < a.nl) ? (a.cnbr[x] & kNbrMask) : kNone;
+        }
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
             const uint32_t v = vv[j];
             bool k = false;
             if (v != kNone) {
-                const uint2 cv = cc[j];
-                const uint32_t x = cv.x;
+                const uint32_t x = cc[j] != kNone ? (cc[j] & kNbrMask) : kNone;
                 if (x != kNone) {
-                    const uint32_t id = cv.y;
-                    // weight keys are unique per edge
                     bool mutual;
                     if (x - a.lo < a.nl) {
-                        mutual = px[j] == id;
+                        mutual = px[j] == v;
                     } else {   // partner on another partition: its owner confirmed the edge (exchange A)
                         mutual = a.remote_ok[v - a.lo] != 0;
                         if (mutual) a.remote_ok[v - a.lo] = 0;
@@ -321,8 +348,8 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
                         if (a.oldid) a.mate[a.oldid[v]] = (long long)a.oldid[x];
                         else a.mate[v] = (long long)x;
                         ++matched_v;
-                        if (v < x) {   // the lower endpoint records the edge (graph.py:195-203)
-                            const uint32_t e = a.eid_of_x[id];
+                        if (!a.defer_ebits && v < x) {   // the lower endpoint records the edge (graph.py:195-203)
+                            const uint32_t e = a.eid_of_x[cand_key(v, cc[j], a.ckey, a.ptr, a.vbeg, a.ids)];
                             atomicOr(a.ebits + (e >> 5), 1u << (e & 31));
                         }
                     } else {
@@ -354,6 +381,26 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) matched_v += __shfl_xor_sync(0xffffffffu, matched_v, off);
     if (lane == 0 && matched_v) atomicAdd(&a.ctr->matched_v, matched_v);
+}
+
+// Matched-edge bits after the loop (graph.py:195-203: the lower endpoint
+// records its edge).  A matched vertex is never probed again, so its
+// candidate word and ptr still name its matched edge.  Done here rather than
+// in the match kernel, whose tiles would otherwise wait on the key's
+// dependent gathers (ptr -> offset -> slot) for their few matched vertices.
+__global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long n, const uint32_t *cnbr,
+                                   const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
+                                   const uint2 *ids, const uint32_t *eid_of_x, uint32_t *ebits) {
+    // thread per vertex: the matched lanes' gather chains run side by side
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+        if (!((matched[v >> 5] >> (v & 31)) & 1u)) continue;
+        const uint32_t w = cnbr[v];
+        if ((uint32_t)v < (w & kNbrMask)) {
+            const uint32_t e = eid_of_x[cand_key((uint32_t)v, w, ckey, ptr, vbeg, ids)];
+            atomicOr(ebits + (e >> 5), 1u << (e & 31));
+        }
+    }
 }
 
 // Death-round histogram: every edge once; it dies in round min(mround[v],
@@ -578,7 +625,8 @@ static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool re
     a.vbeg = ctx->vbeg;
     a.deg0 = ctx->deg0;
     a.ptr = ctx->vdeg;
-    a.cand = ctx->cand;
+    a.cnbr = reinterpret_cast<uint32_t *>(ctx->cand);
+    a.ckey = reinterpret_cast<uint32_t *>(ctx->cand) + ctx->n;
     a.cand0 = ctx->cand0;
     a.ids = ctx->ids0;
     a.matched = ctx->matched;
@@ -596,9 +644,16 @@ static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool re
 }
 
 // Round r's match kernel over A_r; appends A_{r+1}.
-static int scan_enqueue_match(lmx_ctx *ctx, int r) {
+// defer_ebits: the single-GPU loop sets the matched-edge bits after the loop
+// (lmx_scan_edge_bits); the stepped multi-GPU protocol sets them per round.
+static int scan_enqueue_match(lmx_ctx *ctx, int r, bool defer_ebits) {
     ScanMatchArgs ma;
-    ma.cand = ctx->cand;
+    ma.cnbr = reinterpret_cast<const uint32_t *>(ctx->cand);
+    ma.ckey = reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n;
+    ma.ptr = ctx->vdeg;
+    ma.vbeg = ctx->vbeg;
+    ma.ids = ctx->ids0;
+    ma.defer_ebits = defer_ebits;
     ma.matched = ctx->matched;
     ma.mround = ctx->mround;
     ma.mate = ctx->mate_target;
@@ -676,6 +731,20 @@ static int scan_hist_launch(lmx_ctx *ctx, int n_rounds, int spec_k = 0) {
     return LMX_OK;
 }
 
+static int scan_edge_bits_launch(lmx_ctx *ctx) {
+    const unsigned long long n = (unsigned long long)ctx->n;
+    if (n == 0) return LMX_OK;
+    const unsigned long long blocks = std::min<unsigned long long>((n + kBlock - 1) / kBlock,
+                                                                   (unsigned long long)ctx->num_sms * 32);
+    lmx_scan_edge_bits<<<(unsigned)blocks, kBlock, 0, ctx->stream>>>(
+        ctx->matched, n, reinterpret_cast<const uint32_t *>(ctx->cand),
+        reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n, ctx->vdeg, ctx->vbeg, ctx->ids0, ctx->eid_of_x,
+        ctx->ebits);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    return LMX_OK;
+}
+
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                         std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
     stats.clear();
@@ -717,9 +786,10 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         LMX_TRY(lmx_ensure_ctr(ctx, spec + 1));
         for (; r < spec; ++r) {
             LMX_TRY(scan_enqueue_probe(ctx, r, seed_masked, rerandomize));
-            LMX_TRY(scan_enqueue_match(ctx, r));
+            LMX_TRY(scan_enqueue_match(ctx, r, true));
         }
         LMX_TRY(scan_hist_launch(ctx, 0, spec));
+        LMX_TRY(scan_edge_bits_launch(ctx));   // (rerun below if the loop goes on: it only sets bits)
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)spec,
                                       cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins0 * 8, cudaMemcpyDeviceToHost, st));
@@ -739,7 +809,7 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         for (int b = 0; b < batch; ++b, ++r) {
             LMX_TRY(scan_enqueue_probe(ctx, r, seed_masked, rerandomize));
             LMX_TRY(tl_mark());
-            LMX_TRY(scan_enqueue_match(ctx, r));
+            LMX_TRY(scan_enqueue_match(ctx, r, true));
             LMX_TRY(tl_mark());
         }
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host + r0, ctx->ctr + r0, sizeof(RoundCtr) * (size_t)batch,
@@ -761,6 +831,7 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     if (ctx->m > 0 && !have_hist) {
         std::fill(hist.begin(), hist.end(), 0ULL);
         LMX_TRY(scan_hist_launch(ctx, n_rounds));
+        LMX_TRY(scan_edge_bits_launch(ctx));
         LMX_TRY(tl_mark());
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
@@ -824,7 +895,10 @@ namespace lmx {
 struct ScanProposeArgs {
     const uint32_t *alist;
     const RoundCtr *ctr;
-    const uint2 *cand;
+    const uint32_t *cnbr, *ckey;
+    const uint32_t *ptr;
+    const unsigned long long *vbeg;
+    const uint2 *ids;
     const uint32_t *eid_of_x;
     const unsigned long long *bounds;   // p + 1 cut points (global ids)
     int p;
@@ -838,8 +912,10 @@ __global__ void lmx_scan_propose_kernel(ScanProposeArgs a) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const uint32_t v = a.alist[i];
-        const uint2 c = a.cand[v];
-        if (c.x == kNone || c.x - a.lo < a.nl) continue;   // no candidate, or a local partner
+        const uint32_t w = a.cnbr[v];
+        if (w == kNone) continue;
+        const uint2 c = make_uint2(w & kNbrMask, cand_key(v, w, a.ckey, a.ptr, a.vbeg, a.ids));
+        if (c.x - a.lo < a.nl) continue;   // a local partner
         int k = 0;
         while (k + 1 < a.p && c.x >= a.bounds[k + 1]) ++k;
         const uint32_t pos = atomicAdd(a.cnt + k, 1u);
@@ -847,13 +923,15 @@ __global__ void lmx_scan_propose_kernel(ScanProposeArgs a) {
     }
 }
 
-__global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, const uint2 *cand,
-                                       const uint32_t *eid_of_x, uint32_t lo, uint32_t *remote_ok) {
+__global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, const uint32_t *cnbr,
+                                       const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
+                                       const uint2 *ids, const uint32_t *eid_of_x, uint32_t lo,
+                                       uint32_t *remote_ok) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
         const uint2 r = rec[i];
-        const uint2 c = cand[r.x];
-        if (c.x != kNone && eid_of_x[c.y] == r.y) remote_ok[r.x - lo] = 1u;
+        const uint32_t w = cnbr[r.x];
+        if (w != kNone && eid_of_x[cand_key(r.x, w, ckey, ptr, vbeg, ids)] == r.y) remote_ok[r.x - lo] = 1u;
     }
 }
 
@@ -901,7 +979,11 @@ int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
     ScanProposeArgs pa;
     pa.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
     pa.ctr = ctx->ctr + r;
-    pa.cand = ctx->cand;
+    pa.cnbr = reinterpret_cast<const uint32_t *>(ctx->cand);
+    pa.ckey = reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n;
+    pa.ptr = ctx->vdeg;
+    pa.vbeg = ctx->vbeg;
+    pa.ids = ctx->ids0;
     pa.eid_of_x = ctx->eid_of_x;
     pa.bounds = bnd;
     pa.p = p;
@@ -924,7 +1006,9 @@ int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
 int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count) {
     if (count <= 0) return LMX_OK;
     lmx_scan_accept_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
-        ctx->recv, (unsigned long long)count, ctx->cand, ctx->eid_of_x, (uint32_t)ctx->lo, ctx->remote_ok);
+        ctx->recv, (unsigned long long)count, reinterpret_cast<const uint32_t *>(ctx->cand),
+        reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n, ctx->vdeg, ctx->vbeg, ctx->ids0, ctx->eid_of_x,
+        (uint32_t)ctx->lo, ctx->remote_ok);
     LMX_CUDA(ctx, cudaGetLastError());
     ctx->timing.round_launches += 1;
     return LMX_OK;
@@ -932,7 +1016,7 @@ int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count) {
 
 int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev) {
     const int r = ctx->dist_round;
-    LMX_TRY(scan_enqueue_match(ctx, r));
+    LMX_TRY(scan_enqueue_match(ctx, r, false));
     *stats_dev = &ctx->ctr[r].live_slots;   // {candidates found, matched vertices}
     ctx->dist_round = r + 1;
     return LMX_OK;

@@ -655,7 +655,7 @@ static int weight_stage(lmx_ctx *ctx) {
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
             // round-loop algorithm: the weight-ordered scan needs (almost) distinct
             // weights (a fixed key order); partitions keep the global segments
-            if (distinct && ctx->force_algo != 0) {
+            if (distinct && ctx->force_algo != 0 && ctx->n < (1LL << 31)) {   // (bit 31 of a candidate word is a flag)
                 ctx->algo = 1;
                 lmx_free(ctx, (void **)&keys, m * 8);
                 lmx_free(ctx, (void **)&keys2, m * 8);
