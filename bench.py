@@ -191,11 +191,16 @@ def cpu_baseline_leg(eng_sample_scale: int):
 
 def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_rounds, B_floor, peak, peak_src,
                   traffic):
-    """Roofline of the dominant kernel (DESIGN.md §5).  Scan loop: the
+    """Roofline of the dominant kernel (DESIGN.md §4.3).  Scan loop: the
     candidate-probe kernel (largest share of the step), with its algorithmic
-    bytes from the device counters of the step: per probed vertex 12 B (list
-    entry + candidate; round 0 also writes the candidate, +8 B), per slow-path
-    vertex 28 B (ptr, degree, offset, candidate write), 8 B per slot read.
+    bytes from the device counters of the step: per probed vertex 8 B (list
+    entry + 4-byte candidate word; round 0 reads the 8-byte first slot and
+    writes the word: 16 B), per slow-path vertex 20 B (ptr, degree, offset,
+    word write), 8 B per slot read.  Match kernel: 16 B per listed vertex (list
+    entry, own and partner words, survivor append) + 12 B per matched vertex
+    (match round, mate).  Histogram pass: 8 B per edge + 5 B per vertex, plus
+    the matched-edge bit pass (bitmap, and per matched lower endpoint word,
+    ptr, offset, slot, edge id, bit: 32 B).
     Compacting loop: SURVEY.md §8d's B_floor over the round kernel."""
     src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else \
         "fallback 6.65 TB/s (B200_PROFILING.md)"
@@ -206,10 +211,11 @@ def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_r
         A = [int(c[3]) for c in ctr]
         slow = [int(c[4]) for c in ctr]
         reads = [int(c[0]) for c in ctr]
-        probe_bytes = sum(12 * a + 28 * s + 8 * r for a, s, r in zip(A, slow, reads)) + (8 * A[0] if A else 0)
+        mv = [int(c[2]) for c in ctr]
+        probe_bytes = sum(8 * a + 20 * s + 8 * r for a, s, r in zip(A, slow, reads)) + (8 * A[0] if A else 0)
         launches = sum(1 for a in A if a > 0)
-        match_bytes = sum(20 * a for a in A)
-        hist_bytes = 8 * m + 5 * n
+        match_bytes = sum(16 * a + 12 * v for a, v in zip(A, mv))
+        hist_bytes = 8 * m + 5 * n + n // 8 + 32 * (sum(mv) // 2)
         achieved = probe_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else None
         return {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -229,7 +235,8 @@ def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_r
                 "lmx_scan_match_kernel": {"ms_per_step": match_ms, "algorithmic_bytes": match_bytes,
                                           "achieved_gbs": match_bytes / (match_ms / 1000.0) / 1e9
                                           if match_ms > 0 else None},
-                "lmx_scan_hist_kernel (+ pack)": {"ms_per_step": hist_ms, "algorithmic_bytes": hist_bytes,
+                "lmx_scan_hist_hub_kernel (+ pack, + lmx_scan_edge_bits)": {
+                    "ms_per_step": hist_ms, "algorithmic_bytes": hist_bytes,
                                                   "achieved_gbs": hist_bytes / (hist_ms / 1000.0) / 1e9
                                                   if hist_ms > 0 else None},
             },

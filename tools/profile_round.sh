@@ -12,6 +12,6 @@ timeout 900 ncu --profile-from-start off --set full --import-source on --clock-c
   -k regex:"lmx_scan_round_kernel|lmx_scan_match_kernel" -c 5 -f -o gpurun_out/scan_kernels_rmat26 \
   python tools/profile_step.py --scale 26 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
-  -k regex:"lmx_scan_hist_hub_kernel" -c 1 -f -o gpurun_out/hist_kernel_rmat26 \
+  -k regex:"lmx_scan_hist_hub_kernel|lmx_scan_edge_bits" -c 2 -f -o gpurun_out/hist_kernel_rmat26 \
   python tools/profile_step.py --scale 26 > gpurun_out/ncu_hist.log 2>&1
 echo done
