@@ -388,17 +388,37 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 // candidate word and ptr still name its matched edge.  Done here rather than
 // in the match kernel, whose tiles would otherwise wait on the key's
 // dependent gathers (ptr -> offset -> slot) for their few matched vertices.
+#ifndef LMX_EDGE_ITEMS
+#define LMX_EDGE_ITEMS 4
+#endif
 __global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long n, const uint32_t *cnbr,
                                    const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
                                    const uint2 *ids, const uint32_t *eid_of_x, uint32_t *ebits) {
-    // thread per vertex: the matched lanes' gather chains run side by side
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-        if (!((matched[v >> 5] >> (v & 31)) & 1u)) continue;
-        const uint32_t w = cnbr[v];
-        if ((uint32_t)v < (w & kNbrMask)) {
-            const uint32_t e = eid_of_x[cand_key((uint32_t)v, w, ckey, ptr, vbeg, ids)];
-            atomicOr(ebits + (e >> 5), 1u << (e & 31));
+    // thread per vertex, LMX_EDGE_ITEMS vertices per thread per step with each
+    // stage of the gather chain (word; ptr + offset; slot or key; edge id)
+    // issued for all of them at once, so their latencies overlap
+    constexpr int K = LMX_EDGE_ITEMS;
+    const unsigned long long tile = (unsigned long long)blockDim.x * K;
+    for (unsigned long long t0 = (unsigned long long)blockIdx.x * tile; t0 < n; t0 += (unsigned long long)gridDim.x * tile) {
+        uint32_t w[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const unsigned long long v = t0 + (unsigned long long)j * blockDim.x + threadIdx.x;
+            w[j] = (v < n && ((matched[v >> 5] >> (v & 31)) & 1u)) ? cnbr[v] : kNone;
+        }
+        uint32_t key[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const uint32_t v = (uint32_t)(t0 + (unsigned long long)j * blockDim.x + threadIdx.x);
+            key[j] = kNone;
+            if (w[j] != kNone && v < (w[j] & kNbrMask)) key[j] = cand_key(v, w[j], ckey, ptr, vbeg, ids);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (key[j] != kNone) {
+                const uint32_t e = eid_of_x[key[j]];
+                atomicOr(ebits + (e >> 5), 1u << (e & 31));
+            }
         }
     }
 }
