@@ -278,6 +278,9 @@ def run_b200_dist(args):
     from paper_1302_4587_b200.dist import DistRank, TorchComm, run_rounds
 
     world, rank, local = dist_env()
+    if "RANK" not in os.environ:   # --dist without torchrun: a one-rank group
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -326,9 +329,13 @@ def run_b200_dist(args):
             "roofline": {"bound": "hbm", "achieved": B_floor / (ms_per_step / 1000.0) / 1e9,
                          "peak": peak * world, "unit": "GB/s",
                          "frac": B_floor / (ms_per_step / 1000.0) / 1e9 / (peak * world),
-                         "traffic": None, "kernel": "whole step (all ranks' HBM)",
+                         "traffic": None,
+                         "kernel": "whole step against SURVEY.md 8d's compacting floor B_floor (all ranks' HBM)",
                          "algorithmic_bytes_per_step": B_floor},
-            "cpu_baseline": None, "e2e": None, "clocks": clocks,
+            "cpu_baseline": None, "e2e": None,
+            "e2e_note": "not measured on the partitioned path: every rank would need the full 25 GB host graph "
+                        "pinned; the one-GPU line carries the end-to-end number",
+            "clocks": clocks,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
