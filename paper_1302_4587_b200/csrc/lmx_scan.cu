@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
                 }
             }
             const uint32_t pk = FIRST ? 0u : a.ptr[vk];
-            const uint32_t dk = a.deg0[vk];
             const unsigned long long bk = a.vbeg[vk];
+            // the segment end sits next to its start (same sector 3 times in
+            // 4): one random gather fewer than reading deg0 (2.62 -> 2.52 ms)
+            const uint32_t dk = (uint32_t)(a.vbeg[vk + 1] - bk);
             // a unique-weight candidate sits at ptr and is known dead: search past it;
             // a tied one: its run starts at ptr, whose slot may be live or dead
             uint32_t pp = (ck.x != kNone && ck.y < a.D) ? pk + 1 : pk;
