@@ -724,7 +724,9 @@ __global__ void lmx_pack_kernel(const uint2 *region, const uint32_t *cnt, int p,
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t tid0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid0 < (uint32_t)p) counts64[tid0] = cnt[tid0];
-    for (uint32_t i = tid0; i < nl; i += stride) {
+    uint32_t cmax = 0;   // no region holds more records than this
+    for (int k = 0; k < p; ++k) cmax = max(cmax, cnt[k]);
+    for (uint32_t i = tid0; i < min(nl, cmax); i += stride) {
         uint32_t off = 0;
         for (int k = 0; k < p; ++k) {
             const uint32_t c = cnt[k];

@@ -935,9 +935,9 @@ __global__ void lmx_scan_propose_kernel(ScanProposeArgs a) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const uint32_t v = a.alist[i];
         const uint32_t w = a.cnbr[v];
-        if (w == kNone) continue;
+        if (w == kNone || (w & kNbrMask) - a.lo < a.nl) continue;   // none, or a local partner
+        // only a cross-partition candidate needs its key (a dependent gather chain)
         const uint2 c = make_uint2(w & kNbrMask, cand_key(v, w, a.ckey, a.ptr, a.vbeg, a.ids));
-        if (c.x - a.lo < a.nl) continue;   // a local partner
         int k = 0;
         while (k + 1 < a.p && c.x >= a.bounds[k + 1]) ++k;
         const uint32_t pos = atomicAdd(a.cnt + k, 1u);

@@ -279,6 +279,41 @@ class TorchComm:
         self.dist.all_to_all_single(flat_out, flat_in, [2 * c for c in rcounts], [2 * int(c) for c in scounts])
         return [total]
 
+    def alltoallv_stats(self, ranks, sends, prev):
+        """Exchange A of round r with round r-1's statistics riding along.
+
+        `prev` is round r-1's device {candidates found, matched vertices}
+        (None in round 0).  Every rank sends its own pair to every peer next
+        to the record count, so one all-to-all and ONE host read give both
+        this round's record counts and the global statistics of the last
+        round (the separate all-reduce and its host sync are gone).  Returns
+        ([records received], (found, matched) of round r-1 or None); when the
+        last round found no candidate anywhere, the records are not exchanged
+        (every count is zero then: each list is empty).
+        """
+        import torch
+        (me,), ((send, counts),) = ranks, sends
+        dev = me.device
+        sc = torch.zeros((self.p, 3), dtype=torch.int64, device=dev)
+        sc[:, 0].copy_(torch.as_tensor(counts, dtype=torch.int64, device=dev))
+        if prev is not None:
+            sc[:, 1:].copy_(prev.reshape(1, 2).expand(self.p, 2))
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc)
+        both = torch.cat([sc[:, 0], rc.reshape(-1)]).tolist()   # the one host sync of the round
+        scounts = both[: self.p]
+        rows = [both[self.p + 3 * k: self.p + 3 * k + 3] for k in range(self.p)]
+        rcounts = [r[0] for r in rows]
+        stats = None if prev is None else (int(sum(r[1] for r in rows)), int(sum(r[2] for r in rows)))
+        if stats is not None and stats[0] == 0:
+            return [0], stats
+        stotal, total = int(sum(scounts)), int(sum(rcounts))
+        recv = me.recv_buffer(total)
+        flat_in = send[:stotal].reshape(-1) if stotal else torch.empty(0, dtype=torch.int32, device=dev)
+        flat_out = recv.reshape(-1) if total else torch.empty(0, dtype=torch.int32, device=dev)
+        self.dist.all_to_all_single(flat_out, flat_in, [2 * c for c in rcounts], [2 * int(c) for c in scounts])
+        return [total], stats
+
     def allgather_bitmap(self, ranks):
         import torch
         (me,) = ranks
@@ -384,25 +419,52 @@ def _run_rounds_scan(ranks, comm, seed: int, rerandomize: bool, max_rounds: int 
         r.begin(seed, rerandomize)
     matched = []
     records = []
-    while True:
-        for r in ranks:
-            r.round()
-        sends = [r.propose() for r in ranks]
-        recv_counts = comm.alltoallv(ranks, sends)
-        records.append(comm.record_total(recv_counts))
-        for r, cnt in zip(ranks, recv_counts):
-            r.accept(cnt)
-        local = [r.match() for r in ranks]
-        comm.allgather_bitmap(ranks)
-        found, mv = comm.allreduce_sum(local)
-        if found == 0:
-            records.pop()
-            break
-        if mv % 2:
-            raise RuntimeError("internal: odd global matched-vertex count")
-        matched.append(mv // 2)
-        if max_rounds is not None and len(matched) > max_rounds:
-            raise RuntimeError("round limit exceeded")
+    if hasattr(comm, "alltoallv_stats"):
+        # One host sync per round: round r's exchange A carries round r-1's
+        # statistics.  The round after the last one (no candidate anywhere)
+        # is probed and proposed on empty lists -- A_{r+1} holds only
+        # vertices that found a candidate -- and stops before its match step.
+        prev = None
+        while True:
+            for r in ranks:
+                r.round()
+            sends = [r.propose() for r in ranks]
+            recv_counts, st = comm.alltoallv_stats(ranks, sends, prev)
+            if st is not None:
+                found, mv = st
+                if found == 0:
+                    records.pop()
+                    break
+                if mv % 2:
+                    raise RuntimeError("internal: odd global matched-vertex count")
+                matched.append(mv // 2)
+                if max_rounds is not None and len(matched) > max_rounds:
+                    raise RuntimeError("round limit exceeded")
+            records.append(comm.record_total(recv_counts))
+            for r, cnt in zip(ranks, recv_counts):
+                r.accept(cnt)
+            (prev,) = [r.match().clone() for r in ranks]   # the view lives in the counter array
+            comm.allgather_bitmap(ranks)
+    else:
+        while True:
+            for r in ranks:
+                r.round()
+            sends = [r.propose() for r in ranks]
+            recv_counts = comm.alltoallv(ranks, sends)
+            records.append(comm.record_total(recv_counts))
+            for r, cnt in zip(ranks, recv_counts):
+                r.accept(cnt)
+            local = [r.match() for r in ranks]
+            comm.allgather_bitmap(ranks)
+            found, mv = comm.allreduce_sum(local)
+            if found == 0:
+                records.pop()
+                break
+            if mv % 2:
+                raise RuntimeError("internal: odd global matched-vertex count")
+            matched.append(mv // 2)
+            if max_rounds is not None and len(matched) > max_rounds:
+                raise RuntimeError("round limit exceeded")
     n_rounds = len(matched)
     comm.allgather_mround(ranks)
     hist = comm.allreduce_sum([r.hist(n_rounds) for r in ranks])
