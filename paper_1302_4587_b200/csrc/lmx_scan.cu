@@ -393,15 +393,18 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 #ifndef LMX_EDGE_ITEMS
 #define LMX_EDGE_ITEMS 4
 #endif
-__global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long n, const uint32_t *cnbr,
+__global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long lo, unsigned long long n,
+                                   const uint32_t *cnbr,
                                    const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
                                    const uint2 *ids, const uint32_t *eid_of_x, uint32_t *ebits) {
     // thread per vertex, LMX_EDGE_ITEMS vertices per thread per step with each
     // stage of the gather chain (word; ptr + offset; slot or key; edge id)
     // issued for all of them at once, so their latencies overlap
     constexpr int K = LMX_EDGE_ITEMS;
+    // vertices [lo, n): the owned range (single GPU: all of them)
     const unsigned long long tile = (unsigned long long)blockDim.x * K;
-    for (unsigned long long t0 = (unsigned long long)blockIdx.x * tile; t0 < n; t0 += (unsigned long long)gridDim.x * tile) {
+    for (unsigned long long t0 = lo + (unsigned long long)blockIdx.x * tile; t0 < n;
+         t0 += (unsigned long long)gridDim.x * tile) {
         uint32_t w[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
@@ -666,8 +669,9 @@ static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool re
 }
 
 // Round r's match kernel over A_r; appends A_{r+1}.
-// defer_ebits: the single-GPU loop sets the matched-edge bits after the loop
-// (lmx_scan_edge_bits); the stepped multi-GPU protocol sets them per round.
+// defer_ebits: the matched-edge bits are set after the loop
+// (lmx_scan_edge_bits; the stepped multi-GPU protocol does it in
+// lmx_scan_dist_hist) rather than per matched vertex here.
 static int scan_enqueue_match(lmx_ctx *ctx, int r, bool defer_ebits) {
     ScanMatchArgs ma;
     ma.cnbr = reinterpret_cast<const uint32_t *>(ctx->cand);
@@ -753,13 +757,14 @@ static int scan_hist_launch(lmx_ctx *ctx, int n_rounds, int spec_k = 0) {
     return LMX_OK;
 }
 
-static int scan_edge_bits_launch(lmx_ctx *ctx) {
-    const unsigned long long n = (unsigned long long)ctx->n;
-    if (n == 0) return LMX_OK;
-    const unsigned long long blocks = std::min<unsigned long long>((n + kBlock - 1) / kBlock,
+// Matched-edge bits of the vertices [lo, hi) (single GPU: all; a partition:
+// its owned range, whose lower endpoints record their edges).
+static int scan_edge_bits_launch(lmx_ctx *ctx, unsigned long long lo, unsigned long long hi) {
+    if (hi <= lo) return LMX_OK;
+    const unsigned long long blocks = std::min<unsigned long long>((hi - lo + kBlock - 1) / kBlock,
                                                                    (unsigned long long)ctx->num_sms * 32);
     lmx_scan_edge_bits<<<(unsigned)blocks, kBlock, 0, ctx->stream>>>(
-        ctx->matched, n, reinterpret_cast<const uint32_t *>(ctx->cand),
+        ctx->matched, lo, hi, reinterpret_cast<const uint32_t *>(ctx->cand),
         reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n, ctx->vdeg, ctx->vbeg, ctx->ids0, ctx->eid_of_x,
         ctx->ebits);
     LMX_CUDA(ctx, cudaGetLastError());
@@ -811,7 +816,7 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             LMX_TRY(scan_enqueue_match(ctx, r, true));
         }
         LMX_TRY(scan_hist_launch(ctx, 0, spec));
-        LMX_TRY(scan_edge_bits_launch(ctx));   // (rerun below if the loop goes on: it only sets bits)
+        LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));   // (rerun below if the loop goes on: it only sets bits)
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)spec,
                                       cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins0 * 8, cudaMemcpyDeviceToHost, st));
@@ -853,7 +858,7 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
     if (ctx->m > 0 && !have_hist) {
         std::fill(hist.begin(), hist.end(), 0ULL);
         LMX_TRY(scan_hist_launch(ctx, n_rounds));
-        LMX_TRY(scan_edge_bits_launch(ctx));
+        LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));
         LMX_TRY(tl_mark());
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
@@ -1038,7 +1043,7 @@ int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count) {
 
 int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev) {
     const int r = ctx->dist_round;
-    LMX_TRY(scan_enqueue_match(ctx, r, false));
+    LMX_TRY(scan_enqueue_match(ctx, r, true));   // edge bits after the loop (lmx_scan_dist_hist)
     *stats_dev = &ctx->ctr[r].live_slots;   // {candidates found, matched vertices}
     ctx->dist_round = r + 1;
     return LMX_OK;
@@ -1046,6 +1051,9 @@ int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev) {
 
 int lmx_scan_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins) {
     if (n_rounds < 0) return lmx_fail(ctx, LMX_EINVAL, "negative round count");
+    // the loop is over: the owned range's matched-edge bits (as on one GPU,
+    // kept out of the per-round match kernel), then the histogram
+    LMX_TRY(scan_edge_bits_launch(ctx, (unsigned long long)ctx->lo, (unsigned long long)ctx->hi));
     LMX_TRY(scan_hist_launch(ctx, n_rounds));
     *hist_dev = ctx->hist;
     *nbins = (int)std::max<size_t>((size_t)n_rounds + 1, kHistBins);
