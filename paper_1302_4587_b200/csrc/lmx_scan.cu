@@ -81,7 +81,23 @@ struct ScanArgs {
     uint32_t D;                 // distinct weight values; x >= D is a tied edge
     const uint32_t *tie_rank;
     const uint32_t *eid_of_x;
+    // stepped multi-GPU protocol (DIST): exchange A's records are appended by
+    // the probe itself -- a candidate whose partner is owned elsewhere goes to
+    // that owner's region -- so no second pass over A_r is needed
+    const unsigned long long *bounds;   // p + 1 cut points (global ids)
+    int p;
+    uint32_t lo, nl;
+    uint32_t *cnt;                      // [p] records per destination
+    uint2 *region;                      // p regions of capacity nl: {partner, edge id}
 };
+
+// Exchange-A record {x, edge id of key} to the owner of x.
+__device__ __forceinline__ void propose_record(const ScanArgs &a, uint32_t x, uint32_t key) {
+    int k = 0;
+    while (k + 1 < a.p && x >= a.bounds[k + 1]) ++k;
+    const uint32_t pos = atomicAdd(a.cnt + k, 1u);
+    a.region[(unsigned long long)k * a.nl + pos] = make_uint2(x, a.eid_of_x[key]);
+}
 
 // (Measured and rejected, match kernel: an 8-bit fingerprint array of the
 // candidates' neighbours screening the partner gather (-0.08 ms matching,
@@ -155,7 +171,7 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 // candidate is re-checked first -- it is still the candidate if its
 // neighbour is unmatched and its weight unique, so most vertices read 12
 // bytes (list, cand) plus one bitmap bit and write nothing.
-template <bool FIRST>
+template <bool FIRST, bool DIST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
     __shared__ unsigned long long s_red[3][kWarps];
     const uint32_t na = a.ctr->pad[0];
@@ -212,6 +228,8 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             if (keep[it]) {
                 if (FIRST) a.cnbr[v[it]] = c[it].x;   // not tied: flag clear; the key is slot ptr = 0
                 ++found_n;
+                if (DIST && c[it].x - a.lo >= a.nl)   // untied: round 0 carries the key, later it sits at ptr
+                    propose_record(a, c[it].x, FIRST ? c[it].y : a.ids[a.vbeg[v[it]] + a.ptr[v[it]]].y);
             } else {
                 slow |= 1u << it;
             }
@@ -246,6 +264,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
             a.cnbr[vk] = found ? (out.x | (tied ? kTiedFlag : 0u)) : kNone;
             if (tied) a.ckey[vk] = out.y;   // an untied candidate's key is the slot at ptr
             if (pp != pk) a.ptr[vk] = pp;
+            if (DIST && found && out.x - a.lo >= a.nl) propose_record(a, out.x, out.y);
             found_n += found ? 1u : 0u;
             ++slow_n;
         }
@@ -615,8 +634,8 @@ static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R, cons
 
 int lmx_scan_configure_grids(lmx_ctx *ctx) {
     int occ0 = 0, occ1 = 0, occm = 0;
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, lmx_scan_round_kernel<true>, kBlock, 0));
-    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, lmx_scan_round_kernel<false>, kBlock, 0));
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, lmx_scan_round_kernel<true, false>, kBlock, 0));
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, lmx_scan_round_kernel<false, false>, kBlock, 0));
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occm, lmx_scan_match_kernel, kBlock, 0));
     ctx->scan_grid[0] = ctx->num_sms * std::max(occ0, 1);
     ctx->scan_grid[1] = ctx->num_sms * std::max(occ1, 1);
@@ -645,8 +664,10 @@ static int scan_begin(lmx_ctx *ctx) {
 }
 
 // Round r's candidate probe over A_r.
-static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool rerandomize) {
-    ScanArgs a;
+// dist: the stepped multi-GPU protocol (records appended to ctx->send;
+// lmx_scan_dist_round sets up the buffers and zeroes the counts first).
+static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool rerandomize, bool dist = false) {
+    ScanArgs a = {};
     a.vbeg = ctx->vbeg;
     a.deg0 = ctx->deg0;
     a.ptr = ctx->vdeg;
@@ -661,8 +682,19 @@ static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool re
     a.D = ctx->n_distinct;
     a.tie_rank = ctx->tie_rank;
     a.eid_of_x = ctx->eid_of_x;
-    if (r == 0) lmx_scan_round_kernel<true><<<ctx->scan_grid[0], kBlock, 0, ctx->stream>>>(a);
-    else lmx_scan_round_kernel<false><<<ctx->scan_grid[1], kBlock, 0, ctx->stream>>>(a);
+    if (dist) {
+        a.bounds = reinterpret_cast<const unsigned long long *>(reinterpret_cast<const char *>(ctx->send_cnt) + 1024);
+        a.p = ctx->dist_p;
+        a.lo = (uint32_t)ctx->lo;
+        a.nl = (uint32_t)ctx->n_local;
+        a.cnt = ctx->send_cnt;
+        a.region = ctx->send;
+        if (r == 0) lmx_scan_round_kernel<true, true><<<ctx->scan_grid[0], kBlock, 0, ctx->stream>>>(a);
+        else lmx_scan_round_kernel<false, true><<<ctx->scan_grid[1], kBlock, 0, ctx->stream>>>(a);
+    } else {
+        if (r == 0) lmx_scan_round_kernel<true, false><<<ctx->scan_grid[0], kBlock, 0, ctx->stream>>>(a);
+        else lmx_scan_round_kernel<false, false><<<ctx->scan_grid[1], kBlock, 0, ctx->stream>>>(a);
+    }
     LMX_CUDA(ctx, cudaGetLastError());
     ctx->timing.round_launches += 1;
     return LMX_OK;
@@ -919,37 +951,6 @@ int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
 
 namespace lmx {
 
-struct ScanProposeArgs {
-    const uint32_t *alist;
-    const RoundCtr *ctr;
-    const uint32_t *cnbr, *ckey;
-    const uint32_t *ptr;
-    const unsigned long long *vbeg;
-    const uint2 *ids;
-    const uint32_t *eid_of_x;
-    const unsigned long long *bounds;   // p + 1 cut points (global ids)
-    int p;
-    uint32_t lo, nl;
-    uint32_t *cnt;      // [p] records per destination
-    uint2 *region;      // p regions of capacity nl: {partner (global id), edge id}
-};
-
-__global__ void lmx_scan_propose_kernel(ScanProposeArgs a) {
-    const uint32_t total = a.ctr->pad[0];
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const uint32_t v = a.alist[i];
-        const uint32_t w = a.cnbr[v];
-        if (w == kNone || (w & kNbrMask) - a.lo < a.nl) continue;   // none, or a local partner
-        // only a cross-partition candidate needs its key (a dependent gather chain)
-        const uint2 c = make_uint2(w & kNbrMask, cand_key(v, w, a.ckey, a.ptr, a.vbeg, a.ids));
-        int k = 0;
-        while (k + 1 < a.p && c.x >= a.bounds[k + 1]) ++k;
-        const uint32_t pos = atomicAdd(a.cnt + k, 1u);
-        a.region[(unsigned long long)k * a.nl + pos] = make_uint2(c.x, a.eid_of_x[c.y]);
-    }
-}
-
 __global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, const uint32_t *cnbr,
                                        const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
                                        const uint2 *ids, const uint32_t *eid_of_x, uint32_t lo,
@@ -976,14 +977,10 @@ int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
     return LMX_OK;
 }
 
-int lmx_scan_dist_round(lmx_ctx *ctx) {
-    LMX_TRY(lmx_ensure_ctr(ctx, ctx->dist_round + 2));
-    return scan_enqueue_probe(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr);
-}
-
-int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
+// Exchange-A buffers: p regions of nl records + the packed copy; the counts
+// block holds [64] u32 counts, [64] i64 counts at +256, the p + 1 bounds at +1024.
+static int scan_dist_send_buffers(lmx_ctx *ctx) {
     const int p = ctx->dist_p;
-    const int r = ctx->dist_round;
     const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
     const size_t need = nl * (size_t)(p + 1);   // p regions + the packed copy
     if (ctx->send_cap < need) {
@@ -999,32 +996,28 @@ int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
         LMX_CUDA(ctx, cudaMemcpyAsync(reinterpret_cast<char *>(ctx->send_cnt) + 1024, hb.data(),
                                       (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
     }
-    unsigned long long *bnd =
-        reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 1024);
-    long long *counts64 = reinterpret_cast<long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 256);
+    return LMX_OK;
+}
+
+// Round r's probe on the owned lists; it also appends exchange A's records.
+int lmx_scan_dist_round(lmx_ctx *ctx) {
+    LMX_TRY(lmx_ensure_ctr(ctx, ctx->dist_round + 2));
+    LMX_TRY(scan_dist_send_buffers(ctx));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->send_cnt, 0, 64 * sizeof(uint32_t), ctx->stream));
-    ScanProposeArgs pa;
-    pa.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
-    pa.ctr = ctx->ctr + r;
-    pa.cnbr = reinterpret_cast<const uint32_t *>(ctx->cand);
-    pa.ckey = reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n;
-    pa.ptr = ctx->vdeg;
-    pa.vbeg = ctx->vbeg;
-    pa.ids = ctx->ids0;
-    pa.eid_of_x = ctx->eid_of_x;
-    pa.bounds = bnd;
-    pa.p = p;
-    pa.lo = (uint32_t)ctx->lo;
-    pa.nl = (uint32_t)ctx->n_local;
-    pa.cnt = ctx->send_cnt;
-    pa.region = ctx->send;
-    lmx_scan_propose_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(pa);
-    LMX_CUDA(ctx, cudaGetLastError());
+    return scan_enqueue_probe(ctx, ctx->dist_round, ctx->dist_seed, ctx->dist_rr, true);
+}
+
+// Exchange A: the probe appended the records; pack them by destination.
+int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
+    const int p = ctx->dist_p;
+    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    if (!ctx->send || !ctx->send_cnt) return lmx_fail(ctx, LMX_ESTATE, "propose before round");
+    long long *counts64 = reinterpret_cast<long long *>(reinterpret_cast<char *>(ctx->send_cnt) + 256);
     uint2 *packed = ctx->send + nl * (size_t)p;
     lmx_pack_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(ctx->send, ctx->send_cnt, p, (uint32_t)nl, packed,
                                                                  counts64);
     LMX_CUDA(ctx, cudaGetLastError());
-    ctx->timing.round_launches += 2;
+    ctx->timing.round_launches += 1;
     *counts_dev = counts64;
     *packed_dev = packed;
     return LMX_OK;
