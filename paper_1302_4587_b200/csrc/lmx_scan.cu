@@ -45,6 +45,9 @@
 #ifndef LMX_SCAN_MATCH_MINB
 #define LMX_SCAN_MATCH_MINB 8
 #endif
+#ifndef LMX_HIST_V_GLOBAL
+#define LMX_HIST_V_GLOBAL 1
+#endif
 #ifndef LMX_HIST_U
 #define LMX_HIST_U 2   // uint4 (2 edges) loads per thread per step of the histogram
 #endif
@@ -588,6 +591,13 @@ __global__ void __launch_bounds__(kHistThreads, 2)
         const uint32_t x = w < hw ? s_pk[w] : __ldg(packed + w);
         return (x >> ((v % kPer) * BITS)) & kTop;
     };
+#if LMX_HIST_V_GLOBAL
+    // the higher end v: rarely a hub, and consecutive pairs share its word
+    // (lowpair is grouped by v), so L1 serves it without the hub test
+    auto rnd_v = [&](uint32_t v) -> uint32_t { return (__ldg(packed + v / kPer) >> ((v % kPer) * BITS)) & kTop; };
+#else
+    auto rnd_v = rnd;
+#endif
     HistAcc<BITS == 4 ? 4 : 2> acc;
     const uint4 *q = reinterpret_cast<const uint4 *>(lowpair);
     const uint32_t nq = (uint32_t)(m / 2);
@@ -597,8 +607,8 @@ __global__ void __launch_bounds__(kHistThreads, 2)
     for (; i < nq; i += stride) {
         const uint4 x = xn;
         if (i + stride < nq) xn = __ldcs(q + i + stride);
-        const uint32_t d0 = min(min(rnd(x.x), rnd(x.y)), R);
-        const uint32_t d1 = min(min(rnd(x.z), rnd(x.w)), R);
+        const uint32_t d0 = min(min(rnd_v(x.x), rnd(x.y)), R);
+        const uint32_t d1 = min(min(rnd_v(x.z), rnd(x.w)), R);
         acc.add(d0, s_hist, hist);
         acc.add(d1, s_hist, hist);
     }
