@@ -48,6 +48,9 @@
 #ifndef LMX_HIST_V_GLOBAL
 #define LMX_HIST_V_GLOBAL 1
 #endif
+#ifndef LMX_HIST_PF2
+#define LMX_HIST_PF2 1
+#endif
 #ifndef LMX_HIST_U
 #define LMX_HIST_U 2   // uint4 (2 edges) loads per thread per step of the histogram
 #endif
@@ -604,9 +607,18 @@ __global__ void __launch_bounds__(kHistThreads, 2)
     const uint32_t stride = gridDim.x * kHistThreads;
     uint32_t i = blockIdx.x * kHistThreads + tid;
     uint4 xn = i < nq ? __ldcs(q + i) : make_uint4(0, 0, 0, 0);
+#if LMX_HIST_PF2
+    // two steps of the stream in flight
+    uint4 xn2 = i + stride < nq ? __ldcs(q + i + stride) : make_uint4(0, 0, 0, 0);
+    for (; i < nq; i += stride) {
+        const uint4 x = xn;
+        xn = xn2;
+        if (i + 2 * stride < nq) xn2 = __ldcs(q + i + 2 * stride);
+#else
     for (; i < nq; i += stride) {
         const uint4 x = xn;
         if (i + stride < nq) xn = __ldcs(q + i + stride);
+#endif
         const uint32_t d0 = min(min(rnd_v(x.x), rnd(x.y)), R);
         const uint32_t d1 = min(min(rnd_v(x.z), rnd(x.w)), R);
         acc.add(d0, s_hist, hist);
