@@ -185,12 +185,18 @@ int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edg
  * slots of all edges incident to it.  The host drives each round:
  *   lmx_dist_round      candidates of the owned vertices
  *   lmx_dist_propose    records {partner, edge id} for partners owned elsewhere,
- *                       grouped by destination rank (exchange A, barrier 1)
+ *                       grouped by destination rank (exchange A, barrier 1);
+ *                       on the scan loop the round kernel already appended
+ *                       them, and this call only packs them (call it after
+ *                       lmx_dist_round of the same round)
  *   lmx_dist_recv_buffer / lmx_dist_accept   received records
  *   lmx_dist_match      local + confirmed cross-rank matches; returns the
  *                       owned live-slot and matched-vertex counts
  * then all-gathers the owned words of the matched bitmap (exchange B,
- * barrier 2) and all-reduces the counts (RoundStats, termination).  The
+ * barrier 2) and all-reduces the counts (RoundStats, termination; on the
+ * scan loop dist.py sends them with the next round's record counts).
+ * Scan loop: after the loop, lmx_dist_hist also sets the owned range's
+ * matched-edge bits.  The
  * matching equals the single-GPU one for every p (bsp.py:113-115).
  */
 int lmx_dist_bounds(const lmx_ctx *ctx, int64_t *bounds_out);   /* p + 1 device-id cut points */
