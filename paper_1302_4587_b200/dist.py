@@ -317,13 +317,20 @@ class TorchComm:
     def allgather_bitmap(self, ranks):
         import torch
         (me,) = ranks
-        spans = [me.word_range(k) for k in range(self.p)]
-        width = max(max(w1 - w0 for w0, w1 in spans), 1)
+        # exchange B runs every round: the spans and the padded send/receive
+        # buffers are kept per partition (the pad words stay zero)
+        spans = tuple(me.word_range(k) for k in range(self.p))
+        key = (spans, str(me.bitmap.device))
+        cache = getattr(self, "_bm_cache", None)
+        if cache is None or cache[0] != key:
+            width = max(max(w1 - w0 for w0, w1 in spans), 1)
+            row = torch.zeros(width, dtype=torch.int32, device=me.device)
+            out = torch.empty(self.p * width, dtype=torch.int32, device=me.device)
+            self._bm_cache = cache = (key, row, out, spans, width)
+        _, row, out, spans, width = cache
         w0, w1 = spans[self.rank]
-        row = torch.zeros(width, dtype=torch.int32, device=me.device)
         if w1 > w0:
             row[: w1 - w0].copy_(me.bitmap[w0:w1])
-        out = torch.empty(self.p * width, dtype=torch.int32, device=me.device)
         self.dist.all_gather_into_tensor(out, row)
         for k, (a, b) in enumerate(spans):
             if k != self.rank and b > a:
