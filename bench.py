@@ -12,10 +12,10 @@ e2e = the same metric through the public API with pinned HOST buffers:
 load_graph (H2D of edge_u/edge_v/edge_weight + device slot build) + match +
 D2H of mate and matched ids, every step.
 
---impl reference times the reference algorithm's CPU implementation (the
-oracle's numpy port of local_max_seq, same whole-array numpy operations as
-matchers.py:87-119, single-threaded like the reference) on a bounded sample
-of the same workload family, on rank 0 only.
+--impl reference times the reference's own CPU implementation of the path,
+the unmodified locmax.local_max_seq (installed into baseline/_ref by
+tools/install_reference.sh; the oracle's numpy port if it is absent), on a
+bounded RMAT sample of the workload recipe, on rank 0 only.
 """
 
 from __future__ import annotations
@@ -125,30 +125,92 @@ def rmat_floor_bytes(rounds):
 
 
 def cpu_sample_graph(scale: int):
-    """RMAT sample of the same recipe, generated on the CPU by the oracle's restatement."""
+    """RMAT sample of the same recipe, generated on the host by the oracle's C
+    restatement of the device generator + build_graph (test infrastructure,
+    used here only to make the CPU arm's input)."""
     from oracle import oracle as O
-    u, v, w = O.rmat_raw(scale, 16, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
-    return O.build_graph_vec(u, v, w, 1 << scale)
+    u, v, w = O.c_rmat_raw(scale, 16, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
+    return O.c_build_graph(u, v, w, 1 << scale)
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The UNMODIFIED reference package installed by tools/install_reference.sh
+    into baseline/_ref (pip --target of /root/reference/pkg).  None if absent."""
+    if os.path.isdir(os.path.join(REF_DIR, "locmax")) and REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import locmax.graph as lg
+        import locmax.matchers as lm
+    except ImportError:
+        return None
+    return lg, lm
+
+
+def reference_graph(lg, n, eu, ev, w):
+    """locmax.Graph from build_graph-ordered arrays: the CSR
+    arrays as graph.py:108-115 lays them out; local_max_seq reads the edge arrays."""
+    m = int(eu.size)
+    sv = np.concatenate([eu, ev])
+    se = np.concatenate([np.arange(m, dtype=np.int64), np.arange(m, dtype=np.int64)])
+    order = np.argsort(sv * np.int64(max(m, 1)) + se, kind="stable")
+    sv, se = sv[order], se[order]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(sv, minlength=n), out=offsets[1:])
+    arrs = [offsets, sv, se, np.ascontiguousarray(eu, dtype=np.int64), np.ascontiguousarray(ev, dtype=np.int64),
+            np.ascontiguousarray(w, dtype=np.float64)]
+    for a in arrs:
+        a.setflags(write=False)
+    return lg.Graph(int(n), *arrs)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (numpy port, 1 core) on a bounded sample."""
+    """--impl reference: the reference's own CPU implementation of the path,
+    locmax.local_max_seq (matchers.py:61-122) from baseline/_ref, on a bounded
+    RMAT sample of the workload recipe, rank 0 only.  If the reference is not
+    installed, the oracle's numpy port of it (kind "port")."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import oracle as O
     scale = args.cpu_sample_scale
     n, eu, ev, w = cpu_sample_graph(scale)
     m = int(eu.size)
+    ref = import_reference()
+    if ref is not None:
+        lg, lm = ref
+        g = reference_graph(lg, n, eu, ev, w)
+        run = lambda: lm.local_max_seq(g, MATCH_SEED, True)   # noqa: E731
+        kind, what = "reference", "locmax.local_max_seq (unmodified reference, baseline/_ref)"
+    else:
+        from oracle import oracle as O
+        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)   # noqa: E731
+        kind, what = "port", "oracle numpy port of local_max_seq (baseline/_ref not installed)"
     for _ in range(args.warmup):
-        O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)
-    t0 = time.perf_counter()
+        run()
+    times = []
     for _ in range(args.steps):
-        res = O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)
-    dt = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        res = run()
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
     value = m * args.steps / dt
-    sample = (f"RMAT-{scale} ef16 (a,b,c)={RMAT_ABC} seed {GRAPH_SEED} permuted, m={m}, "
-              f"{args.steps} timed runs of numpy_local_max (matchers.py:61-122 numpy ops)")
+    rounds = len(res[1].rounds) if kind == "reference" else len(res.rounds)
+    sample = (f"RMAT-{scale} ef16 (a,b,c)={RMAT_ABC} graph seed {GRAPH_SEED} permuted, n={n}, m={m}; "
+              f"{args.steps} timed calls of {what}, match seed {MATCH_SEED}; 1 of {os.cpu_count()} host "
+              f"cores ({cpu_model()}); the path is single-threaded numpy")
     line = {
         "impl": "reference", "metric": "input edges/s to full local max maximal matching",
         "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
@@ -156,106 +218,57 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"rmat{scale}-sample-of-{args.workload}", "scale": scale,
                    "edge_factor": 16, "rmat_abc": list(RMAT_ABC), "n": n, "m": m,
-                   "rounds": len(res.rounds), "parallelism": "1 host core"},
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "port",
-                         "sample": sample},
+                   "rounds": rounds, "parallelism": "1 host core"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": kind, "sample": sample,
+                         "best_s": min(times), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_leg(eng_sample_scale: int):
-    """Time the oracle's numpy port (the reference's algorithm, 1 core) on a
-    bounded RMAT sample and check the GPU gives the identical matching on it."""
-    from oracle import oracle as O
+def cpu_baseline_leg(scale: int, reps: int = 3):
+    """The reference's local_max_seq (baseline/_ref; else the oracle's numpy
+    port) on a bounded RMAT sample, best of `reps`, and the
+    GPU result on the same sample checked identical to it."""
     from paper_1302_4587_b200 import Engine, Graph
-    n, eu, ev, w = cpu_sample_graph(eng_sample_scale)
-    t0 = time.perf_counter()
-    res = O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)
-    dt = time.perf_counter() - t0
+    n, eu, ev, w = cpu_sample_graph(scale)
+    ref = import_reference()
+    if ref is not None:
+        lg, lm = ref
+        g = reference_graph(lg, n, eu, ev, w)
+        kind = "reference"
+        run = lambda: lm.local_max_seq(g, MATCH_SEED, True)   # noqa: E731
+    else:
+        from oracle import oracle as O
+        kind = "port"
+        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)   # noqa: E731
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = run()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    if kind == "reference":
+        mm, tr = res
+        ref_mate = np.asarray(mm.mate)
+        ref_ids = np.array(sorted(mm.edges), dtype=np.int64)
+        ref_rounds = [(r.edges_before, r.edges_matched, r.edges_removed) for r in tr.rounds]
+    else:
+        ref_mate, ref_ids, ref_rounds = res.mate, res.matched_ids, res.rounds
     with Engine(0) as eng:
-        g = Graph(n, eu, ev, w)
-        eng.load_graph(g)
+        eng.load_graph(Graph(n, eu, ev, w))
         mate, ids, rounds = eng.match_raw(MATCH_SEED, True)
-    same = bool(np.array_equal(mate, res.mate) and np.array_equal(ids, res.matched_ids)
-                and [(r.edges_before, r.edges_matched, r.edges_removed) for r in rounds] == res.rounds)
+    same = bool(np.array_equal(mate, ref_mate) and np.array_equal(ids, ref_ids)
+                and [(r.edges_before, r.edges_matched, r.edges_removed) for r in rounds] == ref_rounds)
+    what = "locmax.local_max_seq (unmodified reference, baseline/_ref)" if kind == "reference" else \
+        "the oracle's numpy port of local_max_seq (baseline/_ref not installed)"
     return {
-        "value": eu.size / dt, "unit": "edges/s", "cores": 1, "kind": "port",
-        "sample": (f"RMAT-{eng_sample_scale} ef16 same recipe (m={eu.size}), one run of the oracle's "
-                   f"numpy port of local_max_seq (matchers.py:61-122 ops) on {os.cpu_count()} host cores "
-                   f"(1 used); GPU result identical on this sample: {same}"),
-        "parity_on_sample": same,
-    }
-
-
-def step_roofline(algo, ctr, probe_ms, match_ms, hist_ms, ms_per_step, n, m, n_rounds, B_floor, peak, peak_src,
-                  traffic):
-    """Roofline of the dominant kernel.  Scan loop: the
-    candidate-probe kernel (largest share of the step), with its algorithmic
-    bytes from the device counters of the step: per probed vertex 8 B (list
-    entry + 4-byte candidate word; round 0 reads the 8-byte first slot and
-    writes the word: 16 B), per slow-path vertex 20 B (ptr, degree, offset,
-    word write), 8 B per slot read.  Match kernel: 16 B per listed vertex (list
-    entry, own and partner words, survivor append) + 12 B per matched vertex
-    (match round, mate).  Histogram pass: 8 B per edge + 5 B per vertex, plus
-    the matched-edge bit pass (bitmap, and per matched lower endpoint word,
-    ptr, offset, slot, edge id, bit: 32 B).
-    Compacting loop: SURVEY.md §8d's B_floor over the round kernel."""
-    src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else \
-        "fallback 6.65 TB/s (B200_PROFILING.md)"
-    want = "lmx_scan_round_kernel" if algo == "scan" else "lmx_round_kernel"
-    if traffic and traffic.get("kernel") != want:
-        traffic = None   # a capture of another kernel
-    if algo == "scan":
-        A = [int(c[3]) for c in ctr]
-        slow = [int(c[4]) for c in ctr]
-        reads = [int(c[0]) for c in ctr]
-        mv = [int(c[2]) for c in ctr]
-        probe_bytes = sum(8 * a + 20 * s + 8 * r for a, s, r in zip(A, slow, reads)) + (8 * A[0] if A else 0)
-        launches = sum(1 for a in A if a > 0)
-        match_bytes = sum(16 * a + 12 * v for a, v in zip(A, mv))
-        hist_bytes = 8 * m + 5 * n + n // 8 + 32 * (sum(mv) // 2)
-        achieved = probe_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else None
-        return {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak if achieved else None,
-            "traffic": traffic.get("bytes_per_launch") if traffic else None,
-            "kernel": "lmx_scan_round_kernel (candidate probes, all rounds)",
-            "algorithmic_bytes_per_step": probe_bytes,
-            "algorithmic_bytes_per_launch": probe_bytes / max(launches, 1),
-            "kernel_ms_per_step": probe_ms, "peak_source": src,
-            "traffic_source": traffic.get("source") if traffic else None,
-            # The probe's useful bytes are gathered 4-8 B at a time from scattered
-            # vertices; a DRAM sector is 32 B.  The measured DRAM traffic over the
-            # kernel time is the bandwidth the access pattern actually draws.
-            "measured_traffic_gbs": (traffic["bytes_per_launch"] * launches / (probe_ms / 1000.0) / 1e9)
-            if traffic and probe_ms > 0 else None,
-            "other_kernels": {
-                "lmx_scan_match_kernel": {"ms_per_step": match_ms, "algorithmic_bytes": match_bytes,
-                                          "achieved_gbs": match_bytes / (match_ms / 1000.0) / 1e9
-                                          if match_ms > 0 else None},
-                "lmx_scan_hist_hub_kernel (+ pack, + lmx_scan_edge_bits)": {
-                    "ms_per_step": hist_ms, "algorithmic_bytes": hist_bytes,
-                                                  "achieved_gbs": hist_bytes / (hist_ms / 1000.0) / 1e9
-                                                  if hist_ms > 0 else None},
-            },
-            "compacting_floor": {
-                "bytes": B_floor, "ms_at_peak": B_floor / (peak * 1e9) * 1000.0,
-                "note": "SURVEY.md 8d floor of the per-round compacting algorithm (every live slot read and "
-                        "every survivor written each round); the weight-ordered scan moves less than this, so "
-                        "the step can finish below ms_at_peak"},
-        }
-    achieved = B_floor / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else None
-    return {
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak if achieved else None,
-        "traffic": traffic.get("bytes_per_launch") if traffic else None,
-        "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds)",
-        "algorithmic_bytes_per_step": B_floor, "algorithmic_bytes_per_launch": B_floor / max(n_rounds, 1),
-        "kernel_ms_per_step": probe_ms, "match_kernel_ms_per_step": match_ms,
-        "step_frac": (B_floor / (ms_per_step / 1000.0) / 1e9) / peak, "peak_source": src,
-        "traffic_source": traffic.get("source") if traffic else None,
+        "value": eu.size / best, "unit": "edges/s", "cores": 1, "kind": kind,
+        "sample": (f"RMAT-{scale} ef16 same recipe (n={n}, m={eu.size}); best of {reps} calls of {what}; "
+                   f"1 of {os.cpu_count()} host cores used ({cpu_model()}); GPU result identical on this "
+                   f"sample: {same}"),
+        "best_s": best, "cpu_model": cpu_model(), "parity_on_sample": same,
     }
 
 
@@ -313,9 +326,14 @@ def run_b200_dist(args):
     tt = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     T = float(tt.item())
-    B_floor, S, m0 = rmat_floor_bytes(rounds)
     peak, _ = measured_hbm_gbs()
     ms_per_step = T / args.steps
+    # per-rank algorithmic bytes from the rank's own device counters, summed
+    by = scan_step_bytes(me.eng.last_round_counters(), me.n_local, me.m // world) if me.algo == "scan" else None
+    tb = torch.tensor([float(by["probe"] + by["match"] + by["hist"]) if by else 0.0], device=dev,
+                      dtype=torch.float64)
+    dist.all_reduce(tb)
+    step_bytes = float(tb.item())
     if rank == 0:
         line = {
             "metric": "input edges/s to full local max maximal matching",
@@ -326,12 +344,13 @@ def run_b200_dist(args):
                        "n": n, "m": m, "rounds": len(rounds), "parallelism": f"1d-vertex-partition{world}",
                        "exchange_a_records": int(sum(records)),
                        "l2": "inputs larger than L2"},
-            "roofline": {"bound": "hbm", "achieved": B_floor / (ms_per_step / 1000.0) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1000.0) / 1e9 if step_bytes else None,
                          "peak": peak * world, "unit": "GB/s",
-                         "frac": B_floor / (ms_per_step / 1000.0) / 1e9 / (peak * world),
+                         "frac": step_bytes / (ms_per_step / 1000.0) / 1e9 / (peak * world) if step_bytes else None,
                          "traffic": None,
-                         "kernel": "whole step against SURVEY.md 8d's compacting floor B_floor (all ranks' HBM)",
-                         "algorithmic_bytes_per_step": B_floor},
+                         "kernel": "whole step: the scan loop's algorithmic bytes (probe + match + histogram, "
+                                   "DESIGN.md 4.3; histogram share taken as m/p) summed over ranks, against all ranks' HBM",
+                         "algorithmic_bytes_per_step": step_bytes},
             "cpu_baseline": None, "e2e": None,
             "e2e_note": "not measured on the partitioned path: every rank would need the full 25 GB host graph "
                         "pinned; the one-GPU line carries the end-to-end number",
@@ -344,6 +363,70 @@ def run_b200_dist(args):
     return 0
 
 
+def load_golden(workload: str):
+    """Digests of the reference matching on this workload (tests/golden/scale.json,
+    made by tests/golden/make_golden_scale.py from the pinned C oracle)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "scale.json")) as f:
+            return json.load(f).get(workload)
+    except OSError:
+        return None
+
+
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).data).hexdigest()
+
+
+def _edges_digest(eu, ev, w) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(eu, dtype="<i8").data)
+    h.update(np.ascontiguousarray(ev, dtype="<i8").data)
+    h.update(np.ascontiguousarray(w, dtype="<f8").view("<u8").data)
+    return h.hexdigest()[:32]
+
+
+def parity_check(golden, g_host, mate_h, ids_h, rounds):
+    """The timed workload's matching against the reference digests: graph
+    (edge arrays), mate, matched ids, RoundStats, Matching.weight bits."""
+    if golden is None:
+        return {"checked": False, "why": "no golden digest for this workload"}
+    weight = float(np.asarray(g_host.edge_weight)[ids_h].sum()) if ids_h.size else 0.0
+    got = {
+        "edges": _edges_digest(g_host.edge_u, g_host.edge_v, g_host.edge_weight),
+        "mate": _sha(np.asarray(mate_h, dtype="<i8")), "ids": _sha(np.asarray(ids_h, dtype="<i8")),
+        "rounds": [[r.edges_before, r.edges_matched, r.edges_removed] for r in rounds],
+        "weight": weight.hex(),
+    }
+    fields = {k: got[k] == golden[k] for k in ("edges", "mate", "ids", "rounds", "weight")}
+    return {"checked": True, "equal": all(fields.values()), "fields": fields,
+            "oracle": "tests/golden/scale.json (pinned C oracle of matchers.py:61-122"
+                      + (", = unmodified local_max_seq" if golden.get("reference_checked") else "") + ")",
+            "matched": int(ids_h.size), "weight": weight}
+
+
+def scan_step_bytes(ctr, n, m):
+    """Algorithmic bytes of one scan-loop matching per kernel,
+    from the device counters of the step.
+    probe: per listed vertex 8 B (list entry + 4-byte candidate word; round 0:
+      the 8-byte first slot + the word write, 16 B), per slow-path vertex 20 B
+      (ptr, segment bounds, word write), 8 B per slot read;
+    match: per listed vertex 16 B (list entry, own and partner word, survivor
+      append), per matched vertex 12 B (match round, mate);
+    hist (pack + death-round histogram + matched-edge bits): 8 B per edge
+      (lowpair) + 5 B per vertex (match round read, packed write) + n/8 (bitmap)
+      + 32 B per matched edge (its candidate word, ptr, offset, slot, edge bit)."""
+    A = [int(c[3]) for c in ctr]
+    slow = [int(c[4]) for c in ctr]
+    reads = [int(c[0]) for c in ctr]
+    mv = [int(c[2]) for c in ctr]
+    probe = sum(8 * a + 20 * s_ + 8 * r for a, s_, r in zip(A, slow, reads)) + (8 * A[0] if A else 0)
+    match = sum(16 * a + 12 * v for a, v in zip(A, mv))
+    hist = 8 * m + 5 * n + n // 8 + 32 * (sum(mv) // 2)
+    return {"probe": probe, "match": match, "hist": hist, "launches": sum(1 for a in A if a > 0)}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -354,16 +437,32 @@ def run_b200(args):
     if world > 1 or args.dist:
         return run_b200_dist(args)
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     scale = WORKLOADS[args.workload]
 
     eng = Engine(local)
     eng.set_stream(stream.cuda_stream)
     eng.gen_rmat(scale, 16, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
-    setup_ms = eng.last_timing()["setup_ms"]
+    gen_setup_ms = eng.last_timing()["setup_ms"]
     n, m = eng.graph_size()
+
+    # ---- K0 from device-resident edge arrays (the load the scan loop needs:
+    # weight-ordered segments, candidates, lowpair), CUDA events on its stream
+    du, dv, dw = eng.export_graph_device()
+    load_ms = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        eng.load_graph_device(n, du, dv, dw)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        load_ms.append(l0.elapsed_time(l1))
+    del du, dv, dw
+    torch.cuda.empty_cache()
+    load_device_ms = min(load_ms)
+
     mate = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
     ids = torch.empty(max(n // 2 + 1, 1), dtype=torch.int64, device="cuda")
 
@@ -375,8 +474,6 @@ def run_b200(args):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -384,21 +481,17 @@ def run_b200(args):
     launches = 0
     rounds_exec = 0
     for _ in range(args.steps):
-        eng.match_device(MATCH_SEED, mate, ids)
+        nm = eng.match_device(MATCH_SEED, mate, ids)
         t = eng.last_timing()
         launches += t["round_launches"]
         rounds_exec += t["rounds_executed"]
     ev1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clocks = sampler.stop()
     T = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([T], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        T = float(tt.item())
     assert eng.last_rounds() == rounds, "matching trace changed between steps"
+    mate_h = mate[:n].cpu().numpy()
+    ids_h = ids[:nm].cpu().numpy()
 
     # ---- per-kernel CUDA-event timeline of the same matchings (after the
     # timed region: its per-launch events would perturb the headline)
@@ -412,30 +505,68 @@ def run_b200(args):
         hk_ms += t["hist_kernel_ms"]
     eng.set_kernel_timing(False)
     assert eng.last_rounds() == rounds, "matching trace changed between steps"
+    rk_ms, mk_ms, hk_ms = rk_ms / args.steps, mk_ms / args.steps, hk_ms / args.steps
     n_matched = int(sum(r.edges_matched for r in rounds))
 
-    B_floor, S, m0 = rmat_floor_bytes(rounds)
-    assert m0 == m
     ms_per_step = T / args.steps
-    value = world * m * args.steps / (T / 1000.0)
+    value = m * args.steps / (T / 1000.0)
     peak, peak_src = measured_hbm_gbs()
+    src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else \
+        "fallback 6.65 TB/s (B200_PROFILING.md)"
     algo = eng.algo()
-    roofline = step_roofline(algo, eng.last_round_counters(), rk_ms / args.steps, mk_ms / args.steps,
-                             hk_ms / args.steps, ms_per_step, n, m, len(rounds), B_floor, peak, peak_src,
-                             load_traffic(args.workload))
+    traffic = load_traffic(args.workload)
+    if algo == "scan":
+        by = scan_step_bytes(eng.last_round_counters(), n, m)
+        if traffic and traffic.get("kernel") != "lmx_scan_round_kernel":
+            traffic = None
+        probe_gbs = by["probe"] / (rk_ms / 1000.0) / 1e9 if rk_ms > 0 else None
+        roofline = {
+            "bound": "hbm", "achieved": probe_gbs, "peak": peak, "unit": "GB/s",
+            "frac": probe_gbs / peak if probe_gbs else None,
+            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "kernel": "lmx_scan_round_kernel (candidate probes, all rounds of one matching)",
+            "algorithmic_bytes_per_step": by["probe"],
+            "algorithmic_bytes_per_launch": by["probe"] / max(by["launches"], 1),
+            "kernel_ms_per_step": rk_ms, "peak_source": src,
+            "traffic_source": traffic.get("source") if traffic else None,
+        }
+        kern = {"probe": (by["probe"], rk_ms), "match": (by["match"], mk_ms), "hist+edge_bits": (by["hist"], hk_ms)}
+        step_bytes = by["probe"] + by["match"] + by["hist"]
+    else:
+        B_floor, S, m0 = rmat_floor_bytes(rounds)
+        gbs = B_floor / (rk_ms / 1000.0) / 1e9 if rk_ms > 0 else None
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                    "frac": gbs / peak if gbs else None, "traffic": None,
+                    "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds)",
+                    "algorithmic_bytes_per_step": B_floor, "kernel_ms_per_step": rk_ms, "peak_source": src}
+        kern = {"round": (B_floor, rk_ms), "match": (0, mk_ms)}
+        step_bytes = B_floor
+    step_gbs = step_bytes / (ms_per_step / 1000.0) / 1e9
+    step_roofline = {
+        "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+        "algorithmic_bytes_per_step": step_bytes, "ms_per_step": ms_per_step,
+        "definition": "sum of the step's kernels' algorithmic bytes (scan loop: probe + match + death-round "
+                      "histogram + matched-edge bits, DESIGN.md 4.3) / device step time / measured peak",
+        "kernels": {k: {"algorithmic_bytes": b, "ms": t_, "gbs": (b / (t_ / 1000.0) / 1e9) if t_ > 0 else None}
+                    for k, (b, t_) in kern.items()},
+    }
+
+    # ---- host copy of the graph: parity digests and the e2e leg's pinned inputs
+    pu = torch.empty(m, dtype=torch.int64, pin_memory=True)
+    pv = torch.empty(m, dtype=torch.int64, pin_memory=True)
+    pw = torch.empty(m, dtype=torch.float64, pin_memory=True)
+    g_dev = eng.export_graph()
+    pu.numpy()[:] = g_dev.edge_u
+    pv.numpy()[:] = g_dev.edge_v
+    pw.numpy()[:] = g_dev.edge_weight
+    del g_dev
+    hg = Graph(n, pu.numpy(), pv.numpy(), pw.numpy())
+    parity = parity_check(load_golden(args.workload), hg, mate_h, ids_h, rounds) if not args.no_parity \
+        else {"checked": False, "why": "--no-parity"}
 
     # ---- e2e: public API with pinned host buffers, H2D + device build + match + D2H every step
     e2e = None
     if not args.no_e2e:
-        g_dev = eng.export_graph()   # host copy of the workload graph
-        pu = torch.empty(m, dtype=torch.int64, pin_memory=True)
-        pv = torch.empty(m, dtype=torch.int64, pin_memory=True)
-        pw = torch.empty(m, dtype=torch.float64, pin_memory=True)
-        pu.numpy()[:] = g_dev.edge_u
-        pv.numpy()[:] = g_dev.edge_v
-        pw.numpy()[:] = g_dev.edge_weight
-        del g_dev
-        hg = Graph(n, pu.numpy(), pv.numpy(), pw.numpy())
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         # warm: two steps, so the pinned output pool holds the buffers of the
         # result a caller keeps while the next step allocates (steady state)
@@ -444,8 +575,6 @@ def run_b200(args):
             eng.load_graph(hg)
             keep = eng.match_raw(MATCH_SEED, True)
         del keep
-        if world > 1:
-            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -457,48 +586,42 @@ def run_b200(args):
         e1.record(stream)
         torch.cuda.synchronize()
         Te = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1000.0)
-        if world > 1:
-            tt = torch.tensor([Te], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            Te = float(tt.item())
-        assert hrounds == rounds and hids.size == n_matched
-        e2e = {"value": world * m * e2e_steps / (Te / 1000.0), "unit": "edges/s",
+        assert hrounds == rounds and np.array_equal(hids, ids_h) and np.array_equal(hmate, mate_h)
+        e2e = {"value": m * e2e_steps / (Te / 1000.0), "unit": "edges/s",
                "h2d_bytes_per_step": int(m * 24), "d2h_bytes_per_step": int(n * 8 + n_matched * 8),
                "ms_per_step": Te / e2e_steps, "steps": e2e_steps,
-               "setup_ms_last": eng.last_timing()["setup_ms"]}
+               "setup_ms_last": eng.last_timing()["setup_ms"],
+               "api": "Engine.load_graph(Graph of pinned host arrays) + Engine.match_raw (lmx_load_graph + "
+                      "lmx_match, host outputs)"}
+    del hg, pu, pv, pw
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         eng.close()
-        cpu = cpu_baseline_leg(args.cpu_sample_scale)
+        cpu = cpu_baseline_leg(args.cpu_baseline_scale)
 
-    if rank == 0:
-        line = {
-            "metric": "input edges/s to full local max maximal matching", "value": value,
-            "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor 16",
-                       "rmat_abc": list(RMAT_ABC), "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
-                       "permuted_labels": True, "n": n, "m": m, "rounds": len(rounds),
-                       "matched_edges": n_matched, "S_over_m0": S / m0, "round_loop": algo,
-                       "parallelism": "dp1" if world == 1 else f"replicas{world}",
-                       "l2": "inputs larger than L2 (slot records %.1f GB >> 126 MB)" % (2 * m * 12 / 1e9),
-                       "setup_ms": setup_ms},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": launches, "rounds_enqueued": rounds_exec,
-            # BASELINE north_star target: >= 50 % of HBM-roofline edges/s, the roofline being
-            # SURVEY 8d's floor of the matching (B_floor bytes at the measured peak bandwidth)
-            "north_star": {
-                "target_frac": 0.5,
-                "roofline_edges_per_s": m / (B_floor / (peak * 1e9)),
-                "achieved_frac": value / world / (m / (B_floor / (peak * 1e9))),
-                "roofline_definition": "m / (B_floor / peak), B_floor = 32 (2S - m0) bytes (SURVEY.md 8d)",
-            },
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    line = {
+        "metric": "input edges/s to full local max maximal matching", "value": value,
+        "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor 16",
+                   "rmat_abc": list(RMAT_ABC), "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
+                   "permuted_labels": True, "n": n, "m": m, "rounds": len(rounds),
+                   "matched_edges": n_matched, "round_loop": algo, "parallelism": "dp1",
+                   "l2": "inputs larger than L2 (slot records %.1f GB >> 126 MB)" % (2 * m * 8 / 1e9)},
+        "parity": parity,
+        "load_device_ms": load_device_ms,
+        "load_device_note": "lmx_load_graph from device-resident int64/f64 edge arrays (validation, narrowing, "
+                            "degrees, relabelling, weight-ordered segments, candidates, lowpair), CUDA events, "
+                            "best of 2; not inside `value`",
+        "value_with_load": m / ((load_device_ms + ms_per_step) / 1000.0),
+        "roofline": roofline, "step_roofline": step_roofline,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "gpu_launches": launches, "rounds_enqueued": rounds_exec,
+        "generator_setup_ms": gen_setup_ms,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -510,7 +633,11 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="rmat26")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample-scale", type=int, default=20)
+    ap.add_argument("--cpu-sample-scale", type=int, default=20,
+                    help="RMAT scale of the reference arm's per-step sample")
+    ap.add_argument("--cpu-baseline-scale", type=int, default=21,
+                    help="RMAT scale of the cpu_baseline leg (best of 3)")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true",

@@ -140,7 +140,10 @@ int lmx_last_kernel_times(const lmx_ctx *ctx, float *out, int cap);
 int lmx_last_round_counters(const lmx_ctx *ctx, int64_t *out, int cap_rounds);
 
 /* One-shot host-buffer entry point: the local_max_seq drop-in for an FFI
- * binding.  err may be NULL. */
+ * binding.  err may be NULL.  If the matching takes more than max_rounds
+ * rounds, mate / ids / n_matched are still complete, *n_rounds_out is the
+ * round count and LMX_ELIMIT is returned: call again with a larger rounds_out
+ * (INTEGRATION.md §2 does). */
 int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u,
                   const int64_t *edge_v, const double *edge_weight, uint64_t seed_masked,
                   int rerandomize, int64_t *mate_out, int64_t *matched_ids_out,

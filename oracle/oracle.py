@@ -73,6 +73,11 @@ def _load():
         ]
         lib.lmxo_edge_salts.restype = None
         lib.lmxo_edge_salts.argtypes = [ctypes.c_uint64, p, ctypes.c_int64, p]
+        lib.lmxo_rmat_raw.restype = None
+        lib.lmxo_rmat_raw.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, p, p, p]
+        lib.lmxo_build_graph.restype = ctypes.c_int64
+        lib.lmxo_build_graph.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_int64, p, p, p, p]
         _lib = lib
     return _lib
 
@@ -132,13 +137,16 @@ def c_local_max(n: int, edge_u, edge_v, edge_weight, seed: int,
     mate = np.empty(max(n, 1), dtype=np.int64)
     ids = np.empty(max(n // 2 + 1, 1), dtype=np.int64)
     nm = np.zeros(1, dtype=np.int64)
-    max_rounds = 4096
-    rounds = np.zeros(3 * max_rounds, dtype=np.int64)
-    r = lib.lmxo_local_max(
-        n, m, eu.ctypes.data, ev.ctypes.data, w.ctypes.data,
-        seed & _UINT64_MASK, 1 if rerandomize else 0,
-        mate.ctypes.data, ids.ctypes.data, nm.ctypes.data, rounds.ctypes.data, max_rounds,
-    )
+    # a path with monotone weights needs n/2 rounds: retry with room for that
+    for max_rounds in (4096, max(4096, n // 2 + 2)):
+        rounds = np.zeros(3 * max_rounds, dtype=np.int64)
+        r = lib.lmxo_local_max(
+            n, m, eu.ctypes.data, ev.ctypes.data, w.ctypes.data,
+            seed & _UINT64_MASK, 1 if rerandomize else 0,
+            mate.ctypes.data, ids.ctypes.data, nm.ctypes.data, rounds.ctypes.data, max_rounds,
+        )
+        if r != -2:
+            break
     if r < 0:
         raise RuntimeError(f"oracle failed with status {r}")
     rr = rounds[: 3 * r].reshape(r, 3)
@@ -481,6 +489,42 @@ def rmat_raw(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19
     return u.astype(np.int64), v.astype(np.int64), w
 
 
+def c_rmat_raw(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+               seed: int = 1, permute: bool = True):
+    """lmx_oracle.c:lmxo_rmat_raw -- rmat_raw with u32 ids, threaded, for scales
+    numpy cannot hold (RMAT-26: 17 GB of raw triples)."""
+    k = edge_factor << scale
+    u = np.empty(k, dtype=np.uint32)
+    v = np.empty(k, dtype=np.uint32)
+    w = np.empty(k, dtype=np.float64)
+    A = int(np.rint(a * 65536.0))
+    B = int(np.rint(b * 65536.0))
+    C = int(np.rint(c * 65536.0))
+    _load().lmxo_rmat_raw(scale, k, A, A + B, A + B + C, seed & _UINT64_MASK, int(bool(permute)),
+                          u.ctypes.data, v.ctypes.data, w.ctypes.data)
+    return u, v, w
+
+
+def c_build_graph(u, v, w, num_vertices: int):
+    """lmx_oracle.c:lmxo_build_graph -- graph.py:59-119 on u32 raw triples
+    (ids < num_vertices, weights valid) in O(k) extra memory.  Returns
+    (n, edge_u int64, edge_v int64, edge_weight f64) views of capacity-k buffers."""
+    u = np.ascontiguousarray(u, dtype=np.uint32)
+    v = np.ascontiguousarray(v, dtype=np.uint32)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    k = int(u.size)
+    rep = np.empty(max(k, 1), dtype=np.uint32)
+    eu = np.empty(max(k, 1), dtype=np.int64)
+    ev = np.empty(max(k, 1), dtype=np.int64)
+    ew = np.empty(max(k, 1), dtype=np.float64)
+    m = _load().lmxo_build_graph(k, u.ctypes.data, v.ctypes.data, w.ctypes.data, int(num_vertices),
+                                 rep.ctypes.data, eu.ctypes.data, ev.ctypes.data, ew.ctypes.data)
+    if m < 0:
+        raise MemoryError("lmxo_build_graph: allocation failed")
+    del rep
+    return int(num_vertices), eu[:m], ev[:m], ew[:m]
+
+
 def build_graph_vec(u, v, w, num_vertices=None):
     """Vectorised numpy restatement of graph.py:59-119 (pinned against
     build_graph_loop / the reference in tests); used for RMAT-size oracles."""
@@ -593,3 +637,31 @@ def coarsen_levels(n, eu, ev, w, seed=0, min_n=1024, min_shrink=0.05, max_levels
             break
         n = nc
     return levels
+
+
+# ---------------------------------------------------------------- validate_matching (graph.py:212-237)
+
+def validate_matching_loop(n: int, edge_u, edge_v, edge_ids, mate):
+    """Loop restatement of ``validate_matching`` (graph.py:212-237): returns
+    (valid, maximal).  The reference walks its frozenset; the flags do not
+    depend on the order, so this walks the ids ascending."""
+    mate = np.asarray(mate)
+    if mate.shape != (n,):
+        return False, False
+    eu = np.asarray(edge_u)
+    ev = np.asarray(edge_v)
+    m = eu.size
+    seen = np.zeros(n, dtype=bool)
+    for k in sorted(int(x) for x in edge_ids):
+        if not 0 <= k < m:
+            return False, False
+        u, v = int(eu[k]), int(ev[k])
+        if seen[u] or seen[v]:
+            return False, False
+        seen[u] = seen[v] = True
+        if mate[u] != v or mate[v] != u:
+            return False, False
+    if np.any(mate[~seen] != -1):
+        return False, False
+    addable = bool(np.any((mate[eu] == -1) & (mate[ev] == -1)))
+    return True, not addable

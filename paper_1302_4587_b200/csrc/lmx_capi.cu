@@ -1,4 +1,5 @@
 // lmx_capi.cu -- the extern "C" boundary declared in include/lmx.h.
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -136,8 +137,15 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
     if (n_rounds_out) *n_rounds_out = (int)stats.size();
     if (rounds_out)
         for (int i = 0; i < (int)stats.size() && i < max_rounds; ++i) rounds_out[i] = stats[i];
-    if (rounds_out && (int)stats.size() > max_rounds)
-        return lmx_fail(ctx, LMX_ELIMIT, "rounds_out too small; fetch with lmx_last_rounds");
+    if (rounds_out && (int)stats.size() > max_rounds) {
+        // mate / ids / counts are complete; *n_rounds_out holds the size needed
+        char buf[200];
+        snprintf(buf, sizeof buf,
+                 "rounds_out holds %d of %d rounds (outputs complete); fetch the trace with lmx_last_rounds "
+                 "or call again with max_rounds >= %d",
+                 max_rounds, (int)stats.size(), (int)stats.size());
+        return lmx_fail(ctx, LMX_ELIMIT, buf);
+    }
     return LMX_OK;
 }
 

@@ -228,6 +228,19 @@ class Engine:
                                                LMX_HOST), "lmx_graph_export")
         return Graph(n, eu, ev, w)
 
+    def export_graph_device(self):
+        """The loaded graph's edge arrays as CUDA tensors (int64, int64, float64),
+        e.g. to time a reload from device-resident inputs."""
+        import torch
+        _, m = self.graph_size()
+        dev = torch.device("cuda", self.device)
+        eu = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        ev = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        w = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+        self._check(self._lib.lmx_graph_export(self._h, _ptr(eu), _ptr(ev), _ptr(w), LMX_DEVICE),
+                    "lmx_graph_export")
+        return eu[:m], ev[:m], w[:m]
+
     def device_bytes(self) -> int:
         return int(self._lib.lmx_device_bytes(self._h))
 

@@ -15,6 +15,11 @@ Same names, fields and semantics as ``locmax.graph`` / ``locmax.matchers``
 * :class:`RoundStats`, :class:`PhaseTrace` -- per-round trace
   (matchers.py:21-58) plus ``device_millis`` (CUDA-event time of the round
   loop).
+
+When ``locmax`` is importable these ARE the reference's types: ``RoundStats``
+is ``locmax.matchers.RoundStats``, ``PhaseTrace`` and ``Matching`` subclass
+``locmax.matchers.PhaseTrace`` / ``locmax.graph.Matching``, so
+``trace.rounds == ref_trace.rounds`` and ``isinstance`` checks hold.
 * :func:`matching_from_edge_ids`, :func:`validate_matching` -- graph.py:195-237.
 
 Any object exposing ``num_vertices``, ``edge_u``, ``edge_v`` and
@@ -27,6 +32,18 @@ from dataclasses import dataclass, field
 from typing import Iterable, NamedTuple
 
 import numpy as np
+
+# When the reference package is importable, results are returned in ITS types
+# (RoundStats, a PhaseTrace subclass, a Matching subclass), so code written
+# against locmax compares them with ``==`` and ``isinstance`` unchanged.
+try:
+    from locmax.graph import Matching as _RefMatching
+    from locmax.matchers import PhaseTrace as _RefPhaseTrace
+    from locmax.matchers import RoundStats as _RefRoundStats
+except Exception:   # locmax absent: this module's own mirrors
+    _RefMatching = _RefPhaseTrace = _RefRoundStats = None
+
+REFERENCE_TYPES = _RefRoundStats is not None
 
 
 class Graph:
@@ -116,25 +133,29 @@ def _frozen(a: np.ndarray) -> np.ndarray:
     return a
 
 
-class Matching:
-    """Matched edge ids plus the induced mate table (graph.py:166-192)."""
+class Matching(_RefMatching if _RefMatching is not None else object):
+    """Matched edge ids plus the induced mate table (graph.py:166-192).
 
-    __slots__ = ("_ids", "_edges", "mate")
+    A subclass of ``locmax.Matching`` when the reference is importable.  The
+    frozenset ``edges`` is built lazily from the sorted id array the engine
+    returns (building it for millions of ids costs seconds)."""
 
     def __init__(self, edge_ids, mate: np.ndarray):
         if isinstance(edge_ids, (frozenset, set)):
-            self._edges = frozenset(edge_ids)
-            self._ids = np.fromiter(sorted(self._edges), dtype=np.int64, count=len(self._edges))
+            edges = frozenset(edge_ids)
+            ids = np.fromiter(sorted(edges), dtype=np.int64, count=len(edges))
         else:
-            self._ids = np.sort(np.asarray(edge_ids, dtype=np.int64))
-            self._edges = None
-        self._ids.setflags(write=False)
-        self.mate = _frozen(np.asarray(mate, dtype=np.int64))
+            ids = np.sort(np.asarray(edge_ids, dtype=np.int64))
+            edges = None
+        ids.setflags(write=False)
+        object.__setattr__(self, "_ids", ids)
+        object.__setattr__(self, "_edges", edges)
+        object.__setattr__(self, "mate", _frozen(np.asarray(mate, dtype=np.int64)))
 
     @property
     def edges(self) -> frozenset:
         if self._edges is None:
-            self._edges = frozenset(self._ids.tolist())
+            object.__setattr__(self, "_edges", frozenset(self._ids.tolist()))
         return self._edges
 
     def __eq__(self, other: object) -> bool:
@@ -147,6 +168,9 @@ class Matching:
     def __hash__(self) -> int:
         return hash(self.edges)
 
+    def __repr__(self) -> str:
+        return f"Matching(size={self.size}, n={self.mate.size})"
+
     @property
     def size(self) -> int:
         return int(self._ids.size)
@@ -155,6 +179,7 @@ class Matching:
         return self._ids
 
     def weight(self, g) -> float:
+        """graph.py:54-56,191-192: the sum over the ascending ids."""
         ids = self._ids
         return float(np.asarray(g.edge_weight)[ids].sum()) if ids.size else 0.0
 
@@ -202,37 +227,58 @@ def validate_matching(g, m) -> MatchingCheck:
     return MatchingCheck(True, not addable, "")
 
 
-@dataclass(frozen=True)
-class RoundStats:
-    """matchers.py:21-25."""
+if _RefRoundStats is not None:
+    RoundStats = _RefRoundStats
 
-    edges_before: int
-    edges_matched: int
-    edges_removed: int
+    @dataclass
+    class PhaseTrace(_RefPhaseTrace):
+        """locmax.PhaseTrace (matchers.py:28-58) plus the device time of the round loop."""
 
+        device_millis: float = 0.0
+else:
+    @dataclass(frozen=True, eq=False)
+    class RoundStats:
+        """matchers.py:21-25.  Equal to any object with the same three fields
+        (e.g. a locmax.RoundStats), so traces compare with ``==``."""
 
-@dataclass
-class PhaseTrace:
-    """matchers.py:28-58, plus device timing of the B200 round loop."""
+        edges_before: int
+        edges_matched: int
+        edges_removed: int
 
-    rounds: list = field(default_factory=list)
-    wall_millis: float = 0.0
-    messages: list | None = None
-    slot_ops: int | None = None
-    write_log: object | None = None
-    device_millis: float = 0.0
+        def _key(self):
+            return (self.edges_before, self.edges_matched, self.edges_removed)
 
-    @property
-    def total_rounds(self) -> int:
-        return len(self.rounds)
+        def __eq__(self, other: object) -> bool:
+            try:
+                return self._key() == (other.edges_before, other.edges_matched, other.edges_removed)
+            except AttributeError:
+                return NotImplemented
 
-    def removed_fractions(self) -> list[float]:
-        return [r.edges_removed / r.edges_before for r in self.rounds if r.edges_before]
+        def __hash__(self) -> int:
+            return hash(self._key())
 
-    def survivor_fractions(self) -> list[float]:
-        return [(r.edges_before - r.edges_removed) / r.edges_before
-                for r in self.rounds if r.edges_before]
+    @dataclass
+    class PhaseTrace:
+        """matchers.py:28-58, plus device timing of the B200 round loop."""
 
-    def mean_removed_fraction(self) -> float:
-        fr = self.removed_fractions()
-        return sum(fr) / len(fr) if fr else 0.0
+        rounds: list = field(default_factory=list)
+        wall_millis: float = 0.0
+        messages: list | None = None
+        slot_ops: int | None = None
+        write_log: object | None = None
+        device_millis: float = 0.0
+
+        @property
+        def total_rounds(self) -> int:
+            return len(self.rounds)
+
+        def removed_fractions(self) -> list[float]:
+            return [r.edges_removed / r.edges_before for r in self.rounds if r.edges_before]
+
+        def survivor_fractions(self) -> list[float]:
+            return [(r.edges_before - r.edges_removed) / r.edges_before
+                    for r in self.rounds if r.edges_before]
+
+        def mean_removed_fraction(self) -> float:
+            fr = self.removed_fractions()
+            return sum(fr) / len(fr) if fr else 0.0

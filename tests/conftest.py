@@ -15,6 +15,13 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# The unmodified reference, when tools/install_reference.sh has put it in
+# baseline/_ref: the drop-in then returns locmax's own result types, which is
+# what the tests should see (never /root/reference: it is absent on the GPU box).
+_REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(_REF, "locmax")) and _REF not in sys.path:
+    sys.path.append(_REF)
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu on the GPU box)")

@@ -86,3 +86,25 @@ def test_oracle_not_imported_by_product():
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
                 assert "liblmx_oracle" not in src and "lmxo_" not in src, f
                 assert "oracle/" not in src.replace("oracle/oracle.py:", ""), f
+
+
+def test_result_types_without_reference():
+    """Without locmax on the path the package's own RoundStats still compares
+    equal to any object with the same three fields (a locmax.RoundStats)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_1302_4587_b200 import graph as G\n"
+        "assert not G.REFERENCE_TYPES\n"
+        "class R:\n"
+        "    edges_before, edges_matched, edges_removed = 5, 2, 4\n"
+        "assert G.RoundStats(5, 2, 4) == R() and [G.RoundStats(5, 2, 4)] == [R()]\n"
+        "import numpy as np\n"
+        "m = G.Matching(np.array([2, 0]), np.array([1, 0, -1, -1]))\n"
+        "assert m.size == 2 and m.edges == frozenset({0, 2})\n"
+    ) % ROOT
+    env = dict(os.environ)
+    env["PYTHONPATH"] = ""
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -1,0 +1,71 @@
+"""Bit-exact parity at the BASELINE configs' full sizes.
+
+tests/golden/scale.json holds, per config, the digests of the graph and of
+the reference matching, made on the CPU by tests/golden/make_golden_scale.py
+(oracle generators + the pinned C oracle of matchers.py:61-122; for rgg22 and
+rmat24 also checked identical to the unmodified locmax generator and
+local_max_seq).  Here the graph is produced as the product produces it (the
+device RMAT generator + build_graph; for C2 the host restatement of
+generate.py's RGG loaded through the public API), matched on the B200, and
+every digest compared: edge arrays, mate, matched ids, RoundStats, weight.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+with open(os.path.join(ROOT, "tests", "golden", "scale.json")) as _f:
+    SCALE = json.load(_f)
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").data).hexdigest()
+
+
+def _edges(eu, ev, w):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(eu, dtype="<i8").data)
+    h.update(np.ascontiguousarray(ev, dtype="<i8").data)
+    h.update(np.ascontiguousarray(w, dtype="<f8").view("<u8").data)
+    return h.hexdigest()[:32]
+
+
+def _check(want, g, mate, ids, rounds):
+    assert g.num_vertices == want["n"] and g.num_edges == want["m"]
+    assert _edges(g.edge_u, g.edge_v, g.edge_weight) == want["edges"], "graph differs"
+    assert [[r.edges_before, r.edges_matched, r.edges_removed] for r in rounds] == want["rounds"]
+    assert ids.size == want["matched"]
+    assert _sha(mate) == want["mate"], "mate differs"
+    assert _sha(ids) == want["ids"], "matched ids differ"
+    weight = float(np.asarray(g.edge_weight)[ids].sum()) if ids.size else 0.0
+    assert weight.hex() == want["weight"], "Matching.weight differs"
+
+
+@pytest.mark.parametrize("name", ["rmat24", "rmat26"])
+def test_rmat_full_size_bit_exact(engine, name):
+    want = SCALE[name]
+    scale = int(name[4:])
+    engine.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=want["graph_seed"], permute=True)
+    mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
+    g = engine.export_graph()
+    _check(want, g, mate, ids, rounds)
+
+
+def test_rgg22_c2_bit_exact(engine):
+    """BASELINE config C2: gen_rgg(22, seed=0, "euclidean"), match seed 0."""
+    from oracle import oracle as O
+    from paper_1302_4587_b200 import Graph
+    want = SCALE["rgg22"]
+    n, eu, ev, w = O.gen_rgg(22, want["graph_seed"], "euclidean")
+    g = Graph(n, eu, ev, w)
+    engine.load_graph(g)
+    mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
+    _check(want, g, mate, ids, rounds)

@@ -109,3 +109,58 @@ def test_rmat_raw_is_deterministic_and_in_range():
     assert (w >= 0).all() and (w < 1).all()
     # permutation is a bijection on the id space
     assert np.unique(O.rmat_perm(np.arange(256), 8, 12345)).size == 256
+
+
+def test_validate_loop_matches_reference_flags():
+    """oracle.validate_matching_loop vs the unmodified reference's
+    validate_matching (tests/golden/validate.npz, make_golden_validate.py)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "validate.npz"))
+    for k in range(z["n"].size):
+        n, eu, ev, w = O.gen_random(int(z["n"][k]), int(z["alpha"][k]), int(z["seed"][k]))
+        ids = z["ids"][z["ids_off"][k]:z["ids_off"][k + 1]]
+        mate = z["mate"][z["mate_off"][k]:z["mate_off"][k + 1]]
+        assert O.validate_matching_loop(n, eu, ev, ids, mate) == (bool(z["valid"][k]), bool(z["maximal"][k]))
+
+
+@pytest.mark.parametrize("scale", [6, 10, 14])
+def test_c_rmat_and_builder_match_numpy_restatements(scale):
+    """lmxo_rmat_raw / lmxo_build_graph (the scale fixtures' generator) equal
+    oracle.rmat_raw / build_graph_vec (pinned to the reference's numbering)."""
+    u, v, w = O.rmat_raw(scale, 16, seed=3, permute=True)
+    cu, cv, cw = O.c_rmat_raw(scale, 16, seed=3, permute=True)
+    assert np.array_equal(u, cu) and np.array_equal(v, cv) and np.array_equal(w, cw)
+    a = O.build_graph_vec(u, v, w, 1 << scale)
+    b = O.c_build_graph(cu, cv, cw, 1 << scale)
+    assert a[0] == b[0] and all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
+
+
+def test_c_builder_matches_reference_numbering(golden_small):
+    """lmxo_build_graph on the reference's raw lists (self-loops, duplicates,
+    -0.0, ties): identical to the reference build_graph output."""
+    for gi, n, raw, built, nv in small_cases(golden_small):
+        u, v, w = (np.asarray(x) for x in raw)
+        if u.size == 0:
+            continue
+        nn = n if n is not None else int(max(u.max(), v.max())) + 1
+        _, eu, ev, ew = O.c_build_graph(u.astype(np.uint32), v.astype(np.uint32), w, nn)
+        assert np.array_equal(eu, built[0]) and np.array_equal(ev, built[1]), gi
+        assert np.array_equal(ew.view(np.uint64), np.asarray(built[2]).view(np.uint64)), gi
+
+
+def test_scale_fixtures_are_consistent():
+    """tests/golden/scale.json: every config the bench and GPU tests use, with
+    the fields they compare; rgg22 and rmat24 were checked against the
+    unmodified reference when they were made."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "scale.json")) as f:
+        sc = json.load(f)
+    for name in ("rgg22", "rmat24", "rmat26"):
+        rec = sc[name]
+        assert {"n", "m", "edges", "mate", "ids", "rounds", "weight", "matched"} <= set(rec)
+        assert rec["rounds"][0][0] == rec["m"]
+        assert sum(r[1] for r in rec["rounds"]) == rec["matched"]
+        assert sum(r[2] for r in rec["rounds"]) == rec["m"]
+    assert sc["rgg22"].get("reference_checked") and sc["rgg22"].get("generator_checked")
+    assert sc["rmat24"].get("reference_checked")
