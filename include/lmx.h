@@ -227,6 +227,16 @@ int lmx_dist_state(lmx_ctx *ctx, void **matched_bitmap, void **mate, void **edge
  * bins [0, n_rounds), bin n_rounds = outlived).
  */
 int lmx_dist_mround(lmx_ctx *ctx, void **mround_dev);
+/*
+ * The reference's boundary accounting (bsp.py:29-41 RoundMessages,
+ * :148-170), for either round loop, after lmx_dist_mround's slices are
+ * all-gathered: *hist_dev = device uint64[2 (n_rounds + 1)]: [0, n_rounds]
+ * candidate records by the last round they are sent in (one per owned
+ * vertex and receiving partition), then cut edges by death round (each once,
+ * from its lower end).  Summed over partitions, the suffix sums are
+ * RoundMessages.candidate_records and .cut_edges_surviving.
+ */
+int lmx_dist_messages(lmx_ctx *ctx, int n_rounds, void **hist_dev);
 int lmx_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
 
 /*

@@ -665,3 +665,78 @@ def validate_matching_loop(n: int, edge_u, edge_v, edge_ids, mate):
         return False, False
     addable = bool(np.any((mate[eu] == -1) & (mate[ev] == -1)))
     return True, not addable
+
+
+# ---------------------------------------------------------------- partition_graph (bsp.py:60-98)
+
+def partition_bounds(offsets, n: int, p: int) -> np.ndarray:
+    """Restatement of partition_graph's cut points (bsp.py:67-83): contiguous
+    ranges cut at the degree-prefix multiples of 2m/p, forced strictly
+    increasing, each later worker left at least one vertex."""
+    if p < 1:
+        raise ValueError("p must be >= 1")
+    if p > n:
+        raise ValueError(f"p={p} exceeds the vertex count {n}")
+    offsets = np.asarray(offsets, dtype=np.int64)
+    two_m = int(offsets[-1])
+    targets = (np.arange(1, p, dtype=np.float64) * two_m) / p
+    cuts = np.searchsorted(offsets, targets, side="left").astype(np.int64)
+    if cuts.size:
+        steps = np.arange(1, p, dtype=np.int64)
+        cuts = np.maximum.accumulate(cuts - steps) + steps
+        cuts = np.minimum(np.maximum(cuts, steps), n - p + steps)
+        return np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    return np.array([0, n], dtype=np.int64)
+
+
+def bsp_messages(n: int, edge_u, edge_v, edge_weight, p: int, seed: int, rerandomize: bool = True):
+    """Restatement of bsp_local_max's boundary accounting (bsp.py:148-199):
+    per round, (round_index, candidate_records, bytes_estimate,
+    cut_edges_surviving, status_records), over the live edge set of each round
+    -- local_max_seq's (bsp.py:113-115), replayed by numpy_local_max's loop."""
+    eu = np.asarray(edge_u, dtype=np.int64)
+    ev = np.asarray(edge_v, dtype=np.int64)
+    w = np.asarray(edge_weight, dtype=np.float64)
+    deg = np.bincount(eu, minlength=n) + np.bincount(ev, minlength=n)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(deg, out=offsets[1:])
+    bounds = partition_bounds(offsets, n, p)
+    owner = np.repeat(np.arange(p, dtype=np.int64), np.diff(bounds))
+    is_cut = owner[eu] != owner[ev]
+    cand_w = np.zeros(n, dtype=np.uint64)
+    cand_s = np.zeros(n, dtype=np.uint64)
+    cand_id = np.full(n, -1, dtype=np.int64)
+    vm = np.zeros(n, dtype=bool)
+    live = np.arange(eu.size, dtype=np.int64)
+    out = []
+    r = 0
+    while live.size:
+        cut_live = live[is_cut[live]]
+        cu, cv = eu[cut_live], ev[cut_live]
+        records = int(np.unique(cu * np.int64(p) + owner[cv]).size + np.unique(cv * np.int64(p) + owner[cu]).size)
+        out.append((r, records, records * 32, int(cut_live.size), 2 * int(cut_live.size)))
+        rs = round_seed(seed, r, rerandomize)
+        wbits = weight_bits(w[live])
+        salts = edge_salts(rs, live)
+        us, vs = eu[live], ev[live]
+        np.maximum.at(cand_w, us, wbits)
+        np.maximum.at(cand_w, vs, wbits)
+        tie_u = cand_w[us] == wbits
+        tie_v = cand_w[vs] == wbits
+        np.maximum.at(cand_s, us[tie_u], salts[tie_u])
+        np.maximum.at(cand_s, vs[tie_v], salts[tie_v])
+        tie_u &= cand_s[us] == salts
+        tie_v &= cand_s[vs] == salts
+        np.maximum.at(cand_id, us[tie_u], live[tie_u])
+        np.maximum.at(cand_id, vs[tie_v], live[tie_v])
+        won = (cand_id[us] == live) & (cand_id[vs] == live)
+        vm[us[won]] = True
+        vm[vs[won]] = True
+        alive = ~(vm[us] | vm[vs])
+        for ends in (us[alive], vs[alive]):
+            cand_w[ends] = 0
+            cand_s[ends] = 0
+            cand_id[ends] = -1
+        live = live[alive]
+        r += 1
+    return out

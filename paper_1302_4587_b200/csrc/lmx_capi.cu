@@ -264,7 +264,7 @@ int lmx_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize) {
 
 int lmx_dist_mround(lmx_ctx *ctx, void **mround_dev) {
     if (!ctx || !mround_dev) return LMX_EINVAL;
-    if (ctx->algo != 1) return lmx_fail(ctx, LMX_ESTATE, "the compacting round loop keeps no match rounds");
+    if (!ctx->mround) return lmx_fail(ctx, LMX_ESTATE, "no match rounds (load with LMX_OPT_DIST_P)");
     *mround_dev = ctx->mround;
     return LMX_OK;
 }

@@ -5,7 +5,9 @@
 //                      the device from the edge arrays)
 //   ids0    uint2[2m]  pristine slot records {nbr, id} grouped by owner, where
 //                      id is the edge id (layouts UNIFORM, GENERAL) or the
-//                      edge's weight key (layout DISTINCT, see below)
+//                      edge's weight key (layout DISTINCT, see below); the
+//                      scan loop's segments are weight-descending with
+//                      {nbr | tie flags, edge id} (lmx_scanload.cu)
 //   wk0     u32[2m]    GENERAL layout only: dense rank of the canonical weight
 //                      bits (tiebreak.py:105-113 order) of the slot's edge
 //   ids1/wk1           working copy: round 1 compacts the survivors of ids0 into
@@ -39,6 +41,11 @@
 namespace lmx {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+// scan-loop slot records {nbr | flags, edge id} (lmx_scanload.cu): the slot's
+// weight equals a neighbouring slot's in its segment / it starts such a run
+constexpr uint32_t kSlotTied = 0x80000000u;
+constexpr uint32_t kSlotRunStart = 0x40000000u;
+constexpr uint32_t kSlotNbr = 0x3FFFFFFFu;   // the scan loop needs n < 2^30
 constexpr int kBlock = 256;   // threads per block, every kernel
 constexpr int kWarps = kBlock / 32;
 
@@ -146,6 +153,7 @@ struct lmx_ctx {
     // 1 = weight-ordered scan (lmx_scan.cu; DISTINCT layout, single partition)
     int algo = 0;
     int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
+    bool scan_rejected = false;              // load time: ties too common for the scan loop
     bool dist_requested = false;             // LMX_OPT_DIST_P was set: stepped protocol
     uint32_t *mround = nullptr;              // scan: round each vertex was matched in (~0 never)
     unsigned long long *lowbeg = nullptr;    // scan (load time only): [n+1] offsets of lowpair
@@ -199,6 +207,10 @@ void lmx_free_graph(lmx_ctx *ctx);
 int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/w (+ deg0, weight stage)
 int lmx_setup_device_edges(lmx_ctx *ctx);   // deg0 + weight stage + lmx_setup_slots for built eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
+int lmx_weight_stage(lmx_ctx *ctx);
+void trace_mark(lmx_ctx *ctx, const char *what);   // LMX_TRACE_SETUP=1: K0 stage times
+// scan loop K0 (lmx_scanload.cu): owned weight-descending segments, cand0, lowpair
+int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid, unsigned long long *tied_slots);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);

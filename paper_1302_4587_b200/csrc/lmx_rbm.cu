@@ -30,7 +30,8 @@ struct RbmArgs {
     const uint32_t *deg0;
     const uint2 *ids;          // pristine slots {nbr, id}
     const uint32_t *wk;        // GENERAL layout: weight rank per slot (else null)
-    int layout;
+    const double *w;           // scan-loop slots: the edge weights (rank = canonical bits)
+    int layout;                // kUniform / kDistinct / kGeneral, or kScanSlots
     uint32_t D;
     const uint32_t *tie_rank;
     const uint32_t *eid_of_x;
@@ -45,8 +46,10 @@ struct RbmArgs {
     uint64_t rs;
 };
 
+constexpr int kScanSlots = 3;   // ids0 of the scan loop: {nbr | tie flags, edge id}
+
 struct Key {
-    uint32_t rank;
+    uint64_t rank;
     uint32_t id;
     uint32_t nbr;
     uint64_t salt;
@@ -56,14 +59,24 @@ __device__ __forceinline__ uint32_t eid_of(const RbmArgs &a, uint32_t id) {
     return a.layout == kDistinct ? a.eid_of_x[id] : id;
 }
 
-__device__ __forceinline__ uint32_t rank_of(const RbmArgs &a, uint32_t id, unsigned long long slot) {
+__device__ __forceinline__ uint64_t rank_of(const RbmArgs &a, uint32_t id, unsigned long long slot) {
     if (a.layout == kDistinct) return id < a.D ? id : a.tie_rank[id - a.D];
     if (a.layout == kGeneral) return a.wk[slot];
+    if (a.layout == kScanSlots) {   // canonical weight bits (tiebreak.py:105-113)
+        const unsigned long long b = (unsigned long long)__double_as_longlong(a.w[id]);
+        return (b << 1) == 0 ? 0ULL : b;
+    }
     return 0u;
 }
 
+__device__ __forceinline__ uint2 slot_at(const RbmArgs &a, unsigned long long i) {
+    uint2 s = a.ids[i];
+    if (a.layout == kScanSlots) s.x &= kSlotNbr;
+    return s;
+}
+
 // lexicographic (rank, salt) max; the edge id never decides (distinct salts)
-__device__ __forceinline__ void key_offer(Key &b, uint32_t rank, uint32_t id, uint32_t nbr, const RbmArgs &a) {
+__device__ __forceinline__ void key_offer(Key &b, uint64_t rank, uint32_t id, uint32_t nbr, const RbmArgs &a) {
     if (b.nbr != kNone && rank < b.rank) return;
     const uint64_t s = mix64((uint64_t)eid_of(a, id) ^ a.rs);
     if (b.nbr == kNone || rank > b.rank || s > b.salt) {
@@ -78,7 +91,7 @@ __device__ __forceinline__ Key key_warp_max(Key b) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         Key o;
-        o.rank = __shfl_xor_sync(0xffffffffu, b.rank, off);
+        o.rank = __shfl_xor_sync(0xffffffffu, (unsigned long long)b.rank, off);
         o.id = __shfl_xor_sync(0xffffffffu, b.id, off);
         o.nbr = __shfl_xor_sync(0xffffffffu, b.nbr, off);
         o.salt = __shfl_xor_sync(0xffffffffu, (unsigned long long)b.salt, off);
@@ -128,7 +141,7 @@ __global__ void __launch_bounds__(kBlock) k_rbm_propose(RbmArgs a) {
             bool alive = false;
             uint2 s = make_uint2(kNone, kNone);
             if (k < d) {
-                s = a.ids[b + k];
+                s = slot_at(a, b + k);
                 alive = !bit(a.matched, s.x);
             }
             live += __popc(__ballot_sync(0xffffffffu, alive));
@@ -166,7 +179,7 @@ __global__ void __launch_bounds__(kBlock) k_rbm_accept(RbmArgs a) {
         for (uint32_t c = 0; c < d; c += 32) {
             const uint32_t k = c + lane;
             if (k < d) {
-                const uint2 s = a.ids[b + k];
+                const uint2 s = slot_at(a, b + k);
                 if (!bit(a.matched, s.x) && bit(a.blue, s.x)) {
                     const uint2 p = a.prop[s.x];
                     if (p.x == v && p.y == s.y) key_offer(best, rank_of(a, s.y, b + k), s.y, s.x, a);
@@ -283,7 +296,8 @@ int lmx_rbm_impl(lmx_ctx *ctx, uint64_t seed_masked, int max_rounds, std::vector
             a.deg0 = ctx->deg0;
             a.ids = ctx->ids0;
             a.wk = ctx->wk0;
-            a.layout = ctx->layout;
+            a.w = ctx->w;
+            a.layout = ctx->algo == 1 ? kScanSlots : ctx->layout;
             a.D = ctx->n_distinct;
             a.tie_rank = ctx->tie_rank;
             a.eid_of_x = ctx->eid_of_x;
@@ -307,7 +321,7 @@ int lmx_rbm_impl(lmx_ctx *ctx, uint64_t seed_masked, int max_rounds, std::vector
             ma.mate = ctx->mate_target;
             ma.oldid = ctx->relabeled ? ctx->oldid : nullptr;
             ma.ebits = ctx->ebits;
-            ma.layout = ctx->layout;
+            ma.layout = ctx->algo == 1 ? kScanSlots : ctx->layout;
             ma.eid_of_x = ctx->eid_of_x;
             ma.ctr = ctx->ctr + r;
             ma.ctr_next = ctx->ctr + r + 1;

@@ -550,6 +550,8 @@ struct MatchArgs {
     const uint32_t *eid_of_x;   // DISTINCT layout: weight key -> edge id (else null)
     uint32_t lo, nl;            // owned device-id range [lo, lo + nl)
     uint32_t *remote_ok;        // [nl] the remote partner's owner confirmed the edge
+    uint32_t *mround;           // partitions: round each vertex was matched in (device ids), or null
+    int round;
     RoundCtr *ctr;        // this round
     RoundCtr *ctr_next;   // next round (list sizes)
 };
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MATCH_MINB) lmx_match_kernel(Match
                 }
                 if (mutual) {
                     atomicOr(a.matched + (gv >> 5), 1u << (gv & 31));
+                    if (a.mround) a.mround[gv] = (uint32_t)a.round;
                     if (a.oldid) a.mate[a.oldid[gv]] = (long long)a.oldid[x];
                     else a.mate[gv] = (long long)x;
                     ++matched_v;
@@ -793,10 +796,9 @@ static void launch_round(lmx_ctx *ctx, const RoundArgs &a) {
 int lmx_alloc_match_state(lmx_ctx *ctx) {
     const size_t n = (size_t)std::max<int64_t>(ctx->n, 1);          // global ids
     const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);   // owned vertices
-    // the scan loop indexes its per-vertex arrays by global id on every partition
-    const size_t nv = ctx->algo == 1 ? n : nl;
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, nv * 4, "vdeg"));
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, nv * 8, "cand"));
+    // per-vertex state of the owned vertices (local index v - lo)
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vdeg, nl * 4, "vdeg"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand, nl * 8, "cand"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->remote_ok, nl * 4, "remote_ok"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mate, n * 8, "mate"));
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->matched, ((n + 31) / 32) * 4, "matched"));
@@ -907,6 +909,8 @@ static int enqueue_match_kernel(lmx_ctx *ctx, int r) {
     ma.lo = (uint32_t)ctx->lo;
     ma.nl = (uint32_t)ctx->n_local;
     ma.remote_ok = ctx->remote_ok;
+    ma.mround = ctx->dist_p > 1 ? ctx->mround : nullptr;
+    ma.round = r;
     ma.ctr = ctx->ctr + r;
     ma.ctr_next = ctx->ctr + r + 1;
     lmx_match_kernel<<<ctx->match_blocks, kBlock, 0, ctx->stream>>>(ma);
@@ -1014,6 +1018,8 @@ int lmx_dist_begin_impl(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
     ctx->dist_rr = rerandomize;
     ctx->mate_target = ctx->mate;
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, (size_t)std::max<int64_t>(ctx->n_local, 1) * 4, ctx->stream));
+    if (ctx->mround)
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->mround, 0xFF, (size_t)std::max<int64_t>(ctx->n, 1) * 4, ctx->stream));
     LMX_TRY(begin_match(ctx));
     LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return LMX_OK;

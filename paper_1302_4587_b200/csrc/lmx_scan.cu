@@ -60,49 +60,50 @@ namespace lmx {
 constexpr int kHistBins = 256;   // death-round bins kept in shared memory (more go global)
 constexpr int kVpl = LMX_SCAN_VPL;
 
-constexpr uint32_t kTiedFlag = 0x80000000u;   // scan loop: n < 2^31
+constexpr uint32_t kTiedFlag = 0x80000000u;   // candidate word: the weight is tied at v
 constexpr uint32_t kNbrMask = 0x7FFFFFFFu;
 
-// Weight key of v's current candidate (neighbour word w != kNone).
-__device__ __forceinline__ uint32_t cand_key(uint32_t v, uint32_t w, const uint32_t *ckey, const uint32_t *ptr,
+// Edge id of the current candidate of owned vertex vl (local index; neighbour
+// word w != kNone): a tied candidate keeps it in ckey, an untied one sits at
+// slot ptr.
+__device__ __forceinline__ uint32_t cand_eid(uint32_t vl, uint32_t w, const uint32_t *ckey, const uint32_t *ptr,
                                              const unsigned long long *vbeg, const uint2 *ids) {
-    return (w & kTiedFlag) ? ckey[v] : ids[vbeg[v] + ptr[v]].y;
+    return (w & kTiedFlag) ? ckey[vl] : ids[vbeg[vl] + ptr[vl]].y;
 }
 
+// Per-vertex arrays are indexed by the local id v - lo of the owned range
+// [lo, lo + nl) (one GPU: lo = 0); lists, neighbours, the matched bitmap and
+// the match rounds use device ids.
 struct ScanArgs {
-    const unsigned long long *vbeg;
-    const uint32_t *deg0;
+    const unsigned long long *vbeg;   // [nl + 1] owned segment offsets
     uint32_t *ptr;              // first possibly-live slot of each vertex (segment offset)
     // each vertex's candidate: the neighbour word (bit 31: the weight is tied)
     // -- the probe's fast path and the match kernel read 4 bytes -- and, for a
-    // tied candidate only, its weight key; an untied candidate sits at slot
-    // ptr (cand_key() reads it there when a matched edge needs its id)
+    // tied candidate only, its edge id; an untied candidate sits at slot ptr
+    // (cand_eid() reads it there when a matched edge needs its id)
     uint32_t *cnbr, *ckey;
     const uint2 *cand0;         // round-0 candidates: the first slot of each segment
-    const uint2 *ids;           // ids0, weight-descending per segment
+    const uint2 *ids;           // ids0 {nbr | tie flags, edge id}, weight-descending per segment
     const uint32_t *matched;    // matched-vertex bitmap
     const uint32_t *alist;      // A_r
     RoundCtr *ctr;              // ctr[r]: pad[0] = |A_r|, pad[1] = grab cursor
     uint64_t rs;                // round seed (tiebreak.py:40-52)
-    uint32_t D;                 // distinct weight values; x >= D is a tied edge
-    const uint32_t *tie_rank;
-    const uint32_t *eid_of_x;
+    uint32_t lo, nl;            // owned range
     // stepped multi-GPU protocol (DIST): exchange A's records are appended by
     // the probe itself -- a candidate whose partner is owned elsewhere goes to
     // that owner's region -- so no second pass over A_r is needed
     const unsigned long long *bounds;   // p + 1 cut points (global ids)
     int p;
-    uint32_t lo, nl;
     uint32_t *cnt;                      // [p] records per destination
     uint2 *region;                      // p regions of capacity nl: {partner, edge id}
 };
 
-// Exchange-A record {x, edge id of key} to the owner of x.
-__device__ __forceinline__ void propose_record(const ScanArgs &a, uint32_t x, uint32_t key) {
+// Exchange-A record {x, edge id} to the owner of x.
+__device__ __forceinline__ void propose_record(const ScanArgs &a, uint32_t x, uint32_t eid) {
     int k = 0;
     while (k + 1 < a.p && x >= a.bounds[k + 1]) ++k;
     const uint32_t pos = atomicAdd(a.cnt + k, 1u);
-    a.region[(unsigned long long)k * a.nl + pos] = make_uint2(x, a.eid_of_x[key]);
+    a.region[(unsigned long long)k * a.nl + pos] = make_uint2(x, eid);
 }
 
 // (Measured and rejected, match kernel: an 8-bit fingerprint array of the
@@ -138,7 +139,7 @@ __device__ __forceinline__ bool advance(const ScanArgs &a, unsigned long long b,
         uint32_t live = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if ((uint32_t)j < cnt && (FIRST || !bit_set(a.matched, s[j].x))) live |= 1u << j;
+            if ((uint32_t)j < cnt && (FIRST || !bit_set(a.matched, s[j].x & kSlotNbr))) live |= 1u << j;
         if (live) {
             const int j0 = __ffs(live) - 1;
 #pragma unroll
@@ -152,19 +153,19 @@ __device__ __forceinline__ bool advance(const ScanArgs &a, unsigned long long b,
     return false;
 }
 
-// `out` (at p) is live and tied: every live slot of its run of equal weight
-// competes on the edge salt (tiebreak.py:55-80).
+// `out` (at p, the first live slot at or after ptr) is tied: every live slot
+// of the rest of its run of equal weight competes on the edge salt
+// (tiebreak.py:55-80); the run ends at an untied slot or the next run start.
 template <bool FIRST>
 __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long long b, uint32_t p, uint32_t d,
                                             uint2 &out, unsigned long long &reads) {
-    const uint32_t r0 = __ldg(a.tie_rank + (out.y - a.D));
-    uint64_t best = mix64((uint64_t)__ldg(a.eid_of_x + out.y) ^ a.rs);
+    uint64_t best = mix64((uint64_t)out.y ^ a.rs);
     for (uint32_t q = p + 1; q < d; ++q) {
         const uint2 t = a.ids[b + q];
         ++reads;
-        if (t.y < a.D || __ldg(a.tie_rank + (t.y - a.D)) != r0) break;
-        if (!FIRST && bit_set(a.matched, t.x)) continue;
-        const uint64_t s = mix64((uint64_t)__ldg(a.eid_of_x + t.y) ^ a.rs);
+        if (!(t.x & kSlotTied) || (t.x & kSlotRunStart)) break;
+        if (!FIRST && bit_set(a.matched, t.x & kSlotNbr)) continue;
+        const uint64_t s = mix64((uint64_t)t.y ^ a.rs);
         if (s > best) {
             best = s;
             out = t;
@@ -216,26 +217,27 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
         }
 #pragma unroll
         for (int it = 0; it < kVpl; ++it) {
-            if (FIRST) {
-                c[it] = v[it] != kNone ? a.cand0[v[it]] : make_uint2(kNone, kNone);
-            } else {   // the neighbour word alone: {nbr, 0} or {nbr, tied marker >= D}
-                const uint32_t w = v[it] != kNone ? a.cnbr[v[it]] : kNone;
-                c[it] = w == kNone ? make_uint2(kNone, kNone) : make_uint2(w & kNbrMask, (w >> 31) ? kNone - 1 : 0u);
+            if (FIRST) {   // the first slot {nbr | tie flags, edge id}
+                c[it] = v[it] != kNone ? a.cand0[v[it] - a.lo] : make_uint2(kNone, kNone);
+            } else {   // the neighbour word alone: {nbr | tied flag, -}
+                const uint32_t w = v[it] != kNone ? a.cnbr[v[it] - a.lo] : kNone;
+                c[it] = make_uint2(w, 0u);
             }
         }
         bool keep[kVpl];
 #pragma unroll
         for (int it = 0; it < kVpl; ++it)
-            keep[it] = c[it].x != kNone && c[it].y < a.D && (FIRST || !bit_set(a.matched, c[it].x));
+            keep[it] = c[it].x != kNone && !(c[it].x & kTiedFlag) && (FIRST || !bit_set(a.matched, c[it].x));
         uint32_t slow = 0;
 #pragma unroll
         for (int it = 0; it < kVpl; ++it) {
             if (v[it] == kNone) continue;
             if (keep[it]) {
-                if (FIRST) a.cnbr[v[it]] = c[it].x;   // not tied: flag clear; the key is slot ptr = 0
+                if (FIRST) a.cnbr[v[it] - a.lo] = c[it].x;   // not tied: no flags; the edge is slot ptr = 0
                 ++found_n;
-                if (DIST && c[it].x - a.lo >= a.nl)   // untied: round 0 carries the key, later it sits at ptr
-                    propose_record(a, c[it].x, FIRST ? c[it].y : a.ids[a.vbeg[v[it]] + a.ptr[v[it]]].y);
+                if (DIST && c[it].x - a.lo >= a.nl)   // untied: round 0 carries the edge id, later it sits at ptr
+                    propose_record(a, c[it].x,
+                                   FIRST ? c[it].y : a.ids[a.vbeg[v[it] - a.lo] + a.ptr[v[it] - a.lo]].y);
             } else {
                 slow |= 1u << it;
             }
@@ -255,22 +257,24 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
                     ck = c[it];
                 }
             }
-            const uint32_t pk = FIRST ? 0u : a.ptr[vk];
-            const unsigned long long bk = a.vbeg[vk];
+            const uint32_t vl = vk - a.lo;
+            const uint32_t pk = FIRST ? 0u : a.ptr[vl];
+            const unsigned long long bk = a.vbeg[vl];
             // the segment end sits next to its start (same sector 3 times in
-            // 4): one random gather fewer than reading deg0 (2.62 -> 2.52 ms)
-            const uint32_t dk = (uint32_t)(a.vbeg[vk + 1] - bk);
-            // a unique-weight candidate sits at ptr and is known dead: search past it;
-            // a tied one: its run starts at ptr, whose slot may be live or dead
-            uint32_t pp = (ck.x != kNone && ck.y < a.D) ? pk + 1 : pk;
+            // 4): one random gather fewer than reading a degree (2.62 -> 2.52 ms)
+            const uint32_t dk = (uint32_t)(a.vbeg[vl + 1] - bk);
+            // an untied candidate sits at ptr and is known dead: search past it;
+            // a tied one: ptr is the first slot not known dead, live or not
+            uint32_t pp = (!FIRST && ck.x != kNone && !(ck.x & kTiedFlag)) ? pk + 1 : pk;
             uint2 out = make_uint2(kNone, kNone);
             const bool found = advance<FIRST>(a, bk, pp, dk, out, reads);
-            if (found && out.y >= a.D) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
-            const bool tied = found && out.y >= a.D;
-            a.cnbr[vk] = found ? (out.x | (tied ? kTiedFlag : 0u)) : kNone;
-            if (tied) a.ckey[vk] = out.y;   // an untied candidate's key is the slot at ptr
-            if (pp != pk) a.ptr[vk] = pp;
-            if (DIST && found && out.x - a.lo >= a.nl) propose_record(a, out.x, out.y);
+            const bool tied = found && (out.x & kSlotTied);
+            if (tied) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
+            const uint32_t nbr = out.x & kSlotNbr;
+            a.cnbr[vl] = found ? (nbr | (tied ? kTiedFlag : 0u)) : kNone;
+            if (tied) a.ckey[vl] = out.y;   // an untied candidate's edge is the slot at ptr
+            if (pp != pk) a.ptr[vl] = pp;
+            if (DIST && found && nbr - a.lo >= a.nl) propose_record(a, nbr, out.y);
             found_n += found ? 1u : 0u;
             ++slow_n;
         }
@@ -314,11 +318,10 @@ struct ScanMatchArgs {
     const uint32_t *alist;        // A_r
     uint32_t *anext;              // A_{r+1}
     uint32_t *ebits;
-    const uint32_t *eid_of_x;
     RoundCtr *ctr;
     RoundCtr *ctr_next;
     int round;
-    uint32_t lo, nl;              // owned id range (single GPU: [0, n))
+    uint32_t lo, nl;              // owned id range (single GPU: [0, n)); per-vertex arrays are local
     uint32_t *remote_ok;          // [nl] cross-partition matches confirmed by exchange A
 };
 
@@ -346,14 +349,14 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
             vv[j] = i < total ? a.alist[i] : kNone;
         }
 #pragma unroll
-        for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cnbr[vv[j]] : kNone;
+        for (int j = 0; j < kItems; ++j) cc[j] = vv[j] != kNone ? a.cnbr[vv[j] - a.lo] : kNone;
         // mutual iff the partner's candidate neighbour is v: both are edges
         // between v and x that are maximal at both ends, hence the same edge
         // (also with parallel edges), so the 4-byte neighbour array suffices
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
             const uint32_t x = cc[j] != kNone ? (cc[j] & kNbrMask) : kNone;
-            px[j] = (x != kNone && x - a.lo < a.nl) ? (a.cnbr[x] & kNbrMask) : kNone;
+            px[j] = (x != kNone && x - a.lo < a.nl) ? (a.cnbr[x - a.lo] & kNbrMask) : kNone;
         }
 #pragma unroll
         for (int j = 0; j < kItems; ++j) {
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
                         else a.mate[v] = (long long)x;
                         ++matched_v;
                         if (!a.defer_ebits && v < x) {   // the lower endpoint records the edge (graph.py:195-203)
-                            const uint32_t e = a.eid_of_x[cand_key(v, cc[j], a.ckey, a.ptr, a.vbeg, a.ids)];
+                            const uint32_t e = cand_eid(v - a.lo, cc[j], a.ckey, a.ptr, a.vbeg, a.ids);
                             atomicOr(a.ebits + (e >> 5), 1u << (e & 31));
                         }
                     } else {
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 __global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long lo, unsigned long long n,
                                    const uint32_t *cnbr,
                                    const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
-                                   const uint2 *ids, const uint32_t *eid_of_x, uint32_t *ebits) {
+                                   const uint2 *ids, uint32_t *ebits) {
     // thread per vertex, LMX_EDGE_ITEMS vertices per thread per step with each
     // stage of the gather chain (word; ptr + offset; slot or key; edge id)
     // issued for all of them at once, so their latencies overlap
@@ -434,22 +437,18 @@ __global__ void lmx_scan_edge_bits(const uint32_t *matched, unsigned long long l
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const unsigned long long v = t0 + (unsigned long long)j * blockDim.x + threadIdx.x;
-            w[j] = (v < n && ((matched[v >> 5] >> (v & 31)) & 1u)) ? cnbr[v] : kNone;
+            w[j] = (v < n && ((matched[v >> 5] >> (v & 31)) & 1u)) ? cnbr[v - lo] : kNone;
         }
-        uint32_t key[K];
+        uint32_t eid[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const uint32_t v = (uint32_t)(t0 + (unsigned long long)j * blockDim.x + threadIdx.x);
-            key[j] = kNone;
-            if (w[j] != kNone && v < (w[j] & kNbrMask)) key[j] = cand_key(v, w[j], ckey, ptr, vbeg, ids);
+            eid[j] = kNone;
+            if (w[j] != kNone && v < (w[j] & kNbrMask)) eid[j] = cand_eid((uint32_t)(v - lo), w[j], ckey, ptr, vbeg, ids);
         }
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            if (key[j] != kNone) {
-                const uint32_t e = eid_of_x[key[j]];
-                atomicOr(ebits + (e >> 5), 1u << (e & 31));
-            }
-        }
+        for (int j = 0; j < K; ++j)
+            if (eid[j] != kNone) atomicOr(ebits + (eid[j] >> 5), 1u << (eid[j] & 31));
     }
 }
 
@@ -677,7 +676,7 @@ static int scan_begin(lmx_ctx *ctx) {
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->mate_target, 0xFF, n * 8, st));   // -1
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->matched, 0, (n + 31) / 32 * 4, st));
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->mround, 0xFF, n * 4, st));
-        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, n * 4, st));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, (size_t)std::max<int64_t>(ctx->n_local, 1) * 4, st));
     }
     ctx->ctr_host[0] = RoundCtr{};
     ctx->ctr_host[0].pad[0] = ctx->n_bins0[0];
@@ -691,24 +690,20 @@ static int scan_begin(lmx_ctx *ctx) {
 static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool rerandomize, bool dist = false) {
     ScanArgs a = {};
     a.vbeg = ctx->vbeg;
-    a.deg0 = ctx->deg0;
     a.ptr = ctx->vdeg;
     a.cnbr = reinterpret_cast<uint32_t *>(ctx->cand);
-    a.ckey = reinterpret_cast<uint32_t *>(ctx->cand) + ctx->n;
+    a.ckey = reinterpret_cast<uint32_t *>(ctx->cand) + std::max<int64_t>(ctx->n_local, 1);
     a.cand0 = ctx->cand0;
     a.ids = ctx->ids0;
     a.matched = ctx->matched;
     a.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
     a.ctr = ctx->ctr + r;
     a.rs = round_seed(seed_masked, (uint64_t)r, rerandomize);
-    a.D = ctx->n_distinct;
-    a.tie_rank = ctx->tie_rank;
-    a.eid_of_x = ctx->eid_of_x;
+    a.lo = (uint32_t)ctx->lo;
+    a.nl = (uint32_t)ctx->n_local;
     if (dist) {
         a.bounds = reinterpret_cast<const unsigned long long *>(reinterpret_cast<const char *>(ctx->send_cnt) + 1024);
         a.p = ctx->dist_p;
-        a.lo = (uint32_t)ctx->lo;
-        a.nl = (uint32_t)ctx->n_local;
         a.cnt = ctx->send_cnt;
         a.region = ctx->send;
         if (r == 0) lmx_scan_round_kernel<true, true><<<ctx->scan_grid[0], kBlock, 0, ctx->stream>>>(a);
@@ -729,7 +724,7 @@ static int scan_enqueue_probe(lmx_ctx *ctx, int r, uint64_t seed_masked, bool re
 static int scan_enqueue_match(lmx_ctx *ctx, int r, bool defer_ebits) {
     ScanMatchArgs ma;
     ma.cnbr = reinterpret_cast<const uint32_t *>(ctx->cand);
-    ma.ckey = reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n;
+    ma.ckey = reinterpret_cast<const uint32_t *>(ctx->cand) + std::max<int64_t>(ctx->n_local, 1);
     ma.ptr = ctx->vdeg;
     ma.vbeg = ctx->vbeg;
     ma.ids = ctx->ids0;
@@ -741,7 +736,6 @@ static int scan_enqueue_match(lmx_ctx *ctx, int r, bool defer_ebits) {
     ma.alist = r == 0 ? ctx->bins0 : ctx->lists[r & 1];
     ma.anext = ctx->lists[(r + 1) & 1];
     ma.ebits = ctx->ebits;
-    ma.eid_of_x = ctx->eid_of_x;
     ma.ctr = ctx->ctr + r;
     ma.ctr_next = ctx->ctr + r + 1;
     ma.round = r;
@@ -819,8 +813,8 @@ static int scan_edge_bits_launch(lmx_ctx *ctx, unsigned long long lo, unsigned l
                                                                    (unsigned long long)ctx->num_sms * 32);
     lmx_scan_edge_bits<<<(unsigned)blocks, kBlock, 0, ctx->stream>>>(
         ctx->matched, lo, hi, reinterpret_cast<const uint32_t *>(ctx->cand),
-        reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n, ctx->vdeg, ctx->vbeg, ctx->ids0, ctx->eid_of_x,
-        ctx->ebits);
+        reinterpret_cast<const uint32_t *>(ctx->cand) + std::max<int64_t>(ctx->n_local, 1), ctx->vdeg, ctx->vbeg,
+        ctx->ids0, ctx->ebits);
     LMX_CUDA(ctx, cudaGetLastError());
     ctx->timing.round_launches += 1;
     return LMX_OK;
@@ -975,13 +969,13 @@ namespace lmx {
 
 __global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, const uint32_t *cnbr,
                                        const uint32_t *ckey, const uint32_t *ptr, const unsigned long long *vbeg,
-                                       const uint2 *ids, const uint32_t *eid_of_x, uint32_t lo,
-                                       uint32_t *remote_ok) {
+                                       const uint2 *ids, uint32_t lo, uint32_t *remote_ok) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
         const uint2 r = rec[i];
-        const uint32_t w = cnbr[r.x];
-        if (w != kNone && eid_of_x[cand_key(r.x, w, ckey, ptr, vbeg, ids)] == r.y) remote_ok[r.x - lo] = 1u;
+        const uint32_t vl = r.x - lo;
+        const uint32_t w = cnbr[vl];
+        if (w != kNone && cand_eid(vl, w, ckey, ptr, vbeg, ids) == r.y) remote_ok[vl] = 1u;
     }
 }
 
@@ -1049,8 +1043,8 @@ int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count) {
     if (count <= 0) return LMX_OK;
     lmx_scan_accept_kernel<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
         ctx->recv, (unsigned long long)count, reinterpret_cast<const uint32_t *>(ctx->cand),
-        reinterpret_cast<const uint32_t *>(ctx->cand) + ctx->n, ctx->vdeg, ctx->vbeg, ctx->ids0, ctx->eid_of_x,
-        (uint32_t)ctx->lo, ctx->remote_ok);
+        reinterpret_cast<const uint32_t *>(ctx->cand) + std::max<int64_t>(ctx->n_local, 1), ctx->vdeg, ctx->vbeg,
+        ctx->ids0, (uint32_t)ctx->lo, ctx->remote_ok);
     LMX_CUDA(ctx, cudaGetLastError());
     ctx->timing.round_launches += 1;
     return LMX_OK;

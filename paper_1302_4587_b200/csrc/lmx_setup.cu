@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -242,43 +243,43 @@ __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long 
     }
 }
 
-// Partition cut points: first vertex whose slot offset reaches k * 2m / p,
-// rounded to a multiple of 32 and made non-decreasing.
-__global__ void k_cuts(const unsigned long long *vbeg, unsigned long long n, int p, unsigned long long *cuts) {
+// partition_graph's cut search (bsp.py:73-74): cut k = the first index whose
+// degree-prefix offset reaches k * 2m / p (numpy compares the int64 offsets
+// with the float64 targets as float64, side="left").
+__global__ void k_cuts(const unsigned long long *off, unsigned long long n, int p, unsigned long long *cuts) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const unsigned long long two_m = vbeg[n];
+    const double two_m = (double)off[n];
     cuts[0] = 0;
     for (int k = 1; k < p; ++k) {
-        const unsigned long long target = (unsigned long long)((double)k * (double)two_m / (double)p);
-        unsigned long long lo = 0, hi = n;   // lower_bound over vbeg[0..n]
+        const double target = ((double)k * two_m) / (double)p;
+        unsigned long long lo = 0, hi = n + 1;   // lower_bound over off[0..n]
         while (lo < hi) {
             const unsigned long long mid = (lo + hi) / 2;
-            if (vbeg[mid] < target) lo = mid + 1;
+            if ((double)off[mid] < target) lo = mid + 1;
             else hi = mid;
         }
-        unsigned long long c = (lo + 16) / 32 * 32;
-        if (c > n) c = n;
-        if (c < cuts[k - 1]) c = cuts[k - 1];
-        cuts[k] = c;
+        cuts[k] = lo;
     }
     cuts[p] = n;
 }
 
-__global__ void k_slice_local(const unsigned long long *vbeg, const uint32_t *deg, unsigned long long lo,
-                              unsigned long long nl, unsigned long long base, unsigned long long *vl,
-                              uint32_t *dl) {
+// Owned degrees (device ids [lo, lo + nl)) -> to be scanned into local offsets.
+__global__ void k_slice_local(const uint32_t *deg, unsigned long long lo, unsigned long long nl,
+                              unsigned long long *vl) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nl; i += stride) {
-        vl[i] = vbeg[lo + i] - base;
-        if (i < nl) dl[i] = deg[lo + i];
-    }
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nl; i += stride)
+        vl[i] = i < nl ? deg[lo + i] : 0ULL;
 }
 
-// relabelling helpers: sort key = ~degree (stable -> descending degree, ascending id)
-__global__ void k_relabel_keys(const uint32_t *deg, unsigned long long n, uint32_t *key, uint32_t *val) {
+// relabelling helpers: sort key = (partition of v) << 32 | ~degree, stable ->
+// inside each partition's range: descending degree, ascending id
+__global__ void k_relabel_keys(const uint32_t *deg, unsigned long long n, const unsigned long long *bounds, int p,
+                               unsigned long long *key, uint32_t *val) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        key[i] = ~deg[i];
+        unsigned long long part = 0;
+        while ((int)part + 1 < p && i >= bounds[part + 1]) ++part;
+        key[i] = (part << 32) | (unsigned long long)(~deg[i]);
         val[i] = (uint32_t)i;
     }
 }
@@ -382,172 +383,9 @@ struct HasEdge {
     __device__ bool operator()(uint32_t v) const { return deg[v] > 0; }
 };
 
-// Scan loop slot stream: the edges in descending weight order (sorted
-// position j = m-1-i), two slot records each, keyed by their owner.  x is the
-// DISTINCT weight key of the sorted position (rank, or D + tie index).
-// Endpoints in device ids, packed per edge (one random 8-byte gather below
-// instead of two 4-byte ones; the relabel lookups run in edge order here).
-__global__ void k_pack_endpoints(const uint32_t *eu, const uint32_t *ev, const uint32_t *newid,
-                                 unsigned long long m, uint2 *euv) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        uint32_t a = eu[e], b = ev[e];
-        if (newid) {
-            a = newid[a];
-            b = newid[b];
-        }
-        euv[e] = make_uint2(a, b);
-    }
-}
-
-// 4 edges per thread per step: the gathers of the step are in flight together.
-__global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
-                              const uint32_t *tidx, uint32_t D, unsigned long long m, const uint2 *euv,
-                              uint32_t *okey, uint2 *sval) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < m;
-         i0 += 4 * stride) {
-        uint32_t e[4], x[4];
-        uint2 p[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const unsigned long long i = i0 + k * stride;
-            if (i < m) {
-                const unsigned long long j = m - 1 - i;
-                e[k] = eid_sorted[j];
-                x[k] = tied[j] ? D + tidx[j] : rank[j];
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (i0 + k * stride < m) p[k] = euv[e[k]];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const unsigned long long i = i0 + k * stride;
-            if (i < m) {
-                okey[2 * i] = p[k].x;
-                sval[2 * i] = make_uint2(p[k].y, x[k]);
-                okey[2 * i + 1] = p[k].y;
-                sval[2 * i + 1] = make_uint2(p[k].x, x[k]);
-            }
-        }
-    }
-}
-
-// lowpair: every edge once as {owner v, neighbour u} with u < v, in slot order
-// (so grouped by v up to block interleaving).
-__global__ void k_low_select(const uint32_t *owner, const uint2 *ids, unsigned long long slots, uint32_t lo,
-                             uint32_t hi, uint2 *lowpair, unsigned long long *count) {
-    __shared__ uint32_t s_cnt[kWarps];
-    __shared__ unsigned long long s_base;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t lt;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    for (unsigned long long i0 = (unsigned long long)blockIdx.x * kBlock; i0 < slots;
-         i0 += (unsigned long long)gridDim.x * kBlock) {
-        const unsigned long long i = i0 + tid;
-        uint32_t v = 0, u = 0;
-        bool take = false;
-        if (i < slots) {
-            v = owner[i];
-            u = ids[i].x;
-            take = u < v && v >= lo && v < hi;   // a partition counts the edges of its own higher ends
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, take);
-        if (lane == 0) s_cnt[warp] = __popc(bal);
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
-            s_base = t ? atomicAdd(count, (unsigned long long)t) : 0ULL;
-        }
-        __syncthreads();
-        unsigned long long pos = s_base;
-        for (int w = 0; w < warp; ++w) pos += s_cnt[w];
-        if (take) lowpair[pos + __popc(bal & lt)] = make_uint2(v, u);
-        __syncthreads();
-    }
-}
-
-__global__ void k_cand0(const unsigned long long *vbeg, const uint32_t *deg, const uint2 *ids,
-                        unsigned long long n, uint2 *cand0) {
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long v = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
-        cand0[v] = deg[v] ? ids[vbeg[v]] : make_uint2(kNone, kNone);
-}
-
 }  // namespace lmx
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work);
-static void trace_mark(lmx_ctx *ctx, const char *what);
-
-// Scan loop slots (lmx_scan.cu): ids0 with every vertex segment in descending
-// weight order, built by a stable radix sort by owner of the weight-descending
-// slot stream (no scatter, no per-segment sort), plus lowpair and cand0.
-// eid_sorted / rank / tied / tidx: the weight-key stage's sorted arrays.
-static int build_scan_slots(lmx_ctx *ctx, const uint32_t *eid_sorted, const uint32_t *rank, const uint32_t *tied,
-                            const uint32_t *tidx, const uint32_t *newid) {
-    cudaStream_t st = ctx->stream;
-    const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m, slots = 2 * m;
-    uint32_t *okey = nullptr, *okey2 = nullptr;
-    uint2 *sval = nullptr;
-    void *tmp = nullptr;
-    size_t tmp_bytes = 0;
-    int bits = 1;
-    while (bits < 32 && (1ULL << bits) < n) ++bits;
-    int rc = LMX_OK;
-    do {
-        if ((rc = lmx_alloc(ctx, (void **)&okey, slots * 4, "owner keys")) != LMX_OK) break;
-        if ((rc = lmx_alloc(ctx, (void **)&okey2, slots * 4, "owner keys out")) != LMX_OK) break;
-        if ((rc = lmx_alloc(ctx, (void **)&sval, slots * 8, "slot stream")) != LMX_OK) break;
-        // the packed endpoints borrow the owner-key output buffer (same size)
-        uint2 *euv = reinterpret_cast<uint2 *>(okey2);
-        k_pack_endpoints<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, newid, m, euv);
-        k_desc_stream<<<grid_for(ctx, m), kBlock, 0, st>>>(eid_sorted, rank, tied, tidx, ctx->n_distinct, m, euv,
-                                                          okey, sval);
-        cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess)
-            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots,
-                                                0, bits, st);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
-        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
-        trace_mark(ctx, "  slot stream");
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots, 0, bits,
-                                            st);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
-        trace_mark(ctx, "  owner sort");
-        lmx_free(ctx, (void **)&sval, slots * 8);
-        lmx_free(ctx, &tmp, tmp_bytes);
-        // lowpair: each edge once, from its higher-id end
-        unsigned long long *cnt = nullptr;
-        if ((rc = lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(m, 1) * 8, "lowpair")) !=
-            LMX_OK)
-            break;
-        if ((rc = lmx_alloc(ctx, (void **)&cnt, 8, "lowpair count")) != LMX_OK) break;
-        e = cudaMemsetAsync(cnt, 0, 8, st);
-        if (e == cudaSuccess) {
-            k_low_select<<<ctx->num_sms * 8, kBlock, 0, st>>>(okey2, ctx->ids0, slots, (uint32_t)ctx->lo,
-                                                             (uint32_t)ctx->hi, ctx->lowpair, cnt);
-            e = cudaGetLastError();
-        }
-        unsigned long long got = 0;
-        if (e == cudaSuccess) e = cudaMemcpyAsync(&got, cnt, 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        lmx_free(ctx, (void **)&cnt, 8);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "lowpair"); break; }
-        if (got > m || (ctx->dist_p == 1 && got != m)) {
-            rc = lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count");
-            break;
-        }
-        ctx->lowpair_n = got;
-    } while (0);
-    cudaStreamSynchronize(st);
-    lmx_free(ctx, (void **)&okey, slots * 4);
-    lmx_free(ctx, (void **)&okey2, slots * 4);
-    lmx_free(ctx, (void **)&sval, slots * 8);
-    lmx_free(ctx, &tmp, tmp_bytes);
-    return rc;
-}
 
 static int grid_for(lmx_ctx *ctx, unsigned long long work) {
     unsigned long long b = (work + kBlock - 1) / kBlock;
@@ -559,7 +397,7 @@ static int grid_for(lmx_ctx *ctx, unsigned long long work) {
 
 // Build vbeg / ids0 / wk0 / deg0 / hubs0 from ctx->eu, ev, w (K0).
 // LMX_TRACE_SETUP=1: synchronise and print the wall time of each K0 stage.
-static void trace_mark(lmx_ctx *ctx, const char *what) {
+void trace_mark(lmx_ctx *ctx, const char *what) {
     static const bool on = getenv("LMX_TRACE_SETUP") != nullptr;
     static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
     if (!on) return;
@@ -575,7 +413,7 @@ static void trace_mark(lmx_ctx *ctx, const char *what) {
 // choice, dense ranks and tie indices, and the round-loop algorithm.  Leaves
 // ctx->ws_kofe (weight key per edge; compacting loop) or ctx->ws_{rank, eid,
 // tied, tidx} (sorted-position arrays; scan loop) for lmx_setup_slots.
-static int weight_stage(lmx_ctx *ctx) {
+int lmx_weight_stage(lmx_ctx *ctx) {
     const unsigned long long m = (unsigned long long)ctx->m;
     cudaStream_t st = ctx->stream;
     uint32_t *kofe = nullptr;
@@ -595,6 +433,16 @@ static int weight_stage(lmx_ctx *ctx) {
         uniform = got[0] == got[1];
     }
     ctx->layout = kUniform;
+    // The weight-ordered scan loop needs no global weight order (lmx_scanload.cu
+    // sorts each segment): take it tentatively; lmx_setup_slots falls back to the
+    // compacting loop (and comes back here with scan_rejected) if ties are common.
+    if (m && !uniform && ctx->force_algo != 0 && !ctx->scan_rejected && ctx->force_layout == -1 &&
+        ctx->n < (1LL << 30)) {
+        ctx->algo = 1;
+        ctx->layout = kDistinct;
+        ctx->ws_kofe = nullptr;
+        return LMX_OK;
+    }
     if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
         unsigned long long *keys = nullptr, *keys2 = nullptr;
         uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
@@ -653,20 +501,6 @@ static int weight_stage(lmx_ctx *ctx) {
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
-            // round-loop algorithm: the weight-ordered scan needs (almost) distinct
-            // weights (a fixed key order); partitions keep the global segments
-            if (distinct && ctx->force_algo != 0 && ctx->n < (1LL << 31)) {   // (bit 31 of a candidate word is a flag)
-                ctx->algo = 1;
-                lmx_free(ctx, (void **)&keys, m * 8);
-                lmx_free(ctx, (void **)&keys2, m * 8);
-                lmx_free(ctx, &tmp, tmp_bytes);
-                // kept for the slot build (lmx_setup_slots: needs the relabelling)
-                ctx->ws_rank = vals;
-                ctx->ws_eid = vals2;
-                ctx->ws_tied = tied;
-                ctx->ws_tidx = tidx;
-                vals = vals2 = tied = tidx = nullptr;
-            }
         } while (0);
         cudaStreamSynchronize(st);
         lmx_free(ctx, (void **)&keys, m * 8);
@@ -680,7 +514,6 @@ static int weight_stage(lmx_ctx *ctx) {
             lmx_free(ctx, (void **)&kofe, m * 4);
             return rc;
         }
-        if (ctx->algo == 1) lmx_free(ctx, (void **)&kofe, m * 4);   // the scan build derives x itself
     }
     ctx->ws_kofe = kofe;
     return LMX_OK;
@@ -696,7 +529,7 @@ int lmx_setup_device_edges(lmx_ctx *ctx) {
         k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
         LMX_CUDA(ctx, cudaGetLastError());
     }
-    LMX_TRY(weight_stage(ctx));
+    LMX_TRY(lmx_weight_stage(ctx));
     return lmx_setup_slots(ctx);
 }
 
@@ -709,16 +542,73 @@ void lmx_free_weight_stage(lmx_ctx *ctx) {
     lmx_free(ctx, (void **)&ctx->ws_tidx, m4);
 }
 
+// Partition cut points of bsp.py:60-98 (partition_graph) on the caller-id
+// degree prefix: cut k = searchsorted(offsets, k * 2m / p, side="left") as
+// numpy compares int64 offsets with float64 targets; the host then forces
+// them strictly increasing and leaves each later worker a vertex (:78-81).
+static int partition_bounds(lmx_ctx *ctx, std::vector<int64_t> &bounds) {
+    const int p = ctx->dist_p;
+    const unsigned long long n = (unsigned long long)ctx->n;
+    bounds.assign(2, 0);
+    bounds[1] = (int64_t)n;
+    if (p <= 1) return LMX_OK;
+    if ((unsigned long long)p > n) return lmx_fail(ctx, LMX_EINVAL, "p exceeds the vertex count");
+    cudaStream_t st = ctx->stream;
+    unsigned long long *off = nullptr, *cuts = nullptr;
+    LMX_TRY(lmx_alloc(ctx, (void **)&off, (n + 1) * 8, "partition offsets"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&cuts, (size_t)(p + 1) * 8, "cuts"));
+    k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(ctx->deg0, off, n);
+    size_t tmp = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp, off, off, (long long)(n + 1), st);
+    void *t = nullptr;
+    if (e == cudaSuccess) {
+        int rc = lmx_alloc(ctx, &t, tmp, "scan tmp");
+        if (rc != LMX_OK) return rc;
+        e = cub::DeviceScan::ExclusiveSum(t, tmp, off, off, (long long)(n + 1), st);
+    }
+    std::vector<unsigned long long> hc((size_t)p + 1, 0);
+    if (e == cudaSuccess) {
+        k_cuts<<<1, 64, 0, st>>>(off, n, p, cuts);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cuts, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    lmx_free(ctx, &t, tmp);
+    lmx_free(ctx, (void **)&off, (n + 1) * 8);
+    lmx_free(ctx, (void **)&cuts, (size_t)(p + 1) * 8);
+    LMX_CUDA(ctx, e);
+    // bsp.py:78-81: cuts = max.accumulate(cuts - steps) + steps; clip to [steps, n - p + steps]
+    std::vector<long long> c((size_t)p - 1);
+    long long run = LLONG_MIN;
+    for (int k = 1; k < p; ++k) {
+        const long long step = k;
+        run = std::max(run, (long long)hc[(size_t)k] - step);
+        long long x = run + step;
+        x = std::min(std::max(x, step), (long long)n - p + step);
+        c[(size_t)k - 1] = x;
+    }
+    bounds.assign((size_t)p + 1, 0);
+    for (int k = 1; k < p; ++k) bounds[(size_t)k] = c[(size_t)k - 1];
+    bounds[(size_t)p] = (int64_t)n;
+    return LMX_OK;
+}
+
+// vbeg / ids0 / deg0 (device ids) / bins0 / match state from ctx->eu, ev, w
+// (caller ids; deg0 counted by the conversion).  DESIGN.md §3.
 int lmx_setup_slots(lmx_ctx *ctx) {
     trace_mark(ctx, "edges on device");
     const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
-    unsigned long long slots = 2 * m;   // becomes the owned slot count below
     cudaStream_t st = ctx->stream;
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (n + 1) * 8, "vbeg"));   // deg0: counted at conversion
-    // degree-descending relabelling of skewed graphs: hubs get
-    // the low ids, so the matched bitmap and candidate lookups that follow
-    // the skew hit a small, cache-resident id range, and equal-bucket
-    // vertices become contiguous in memory.
+    // 1D vertex partition (bsp.py:60-98), caller ids; single GPU: [0, n)
+    LMX_TRY(partition_bounds(ctx, ctx->bounds));
+    ctx->lo = (unsigned long long)ctx->bounds[(size_t)ctx->dist_rank];
+    ctx->hi = (unsigned long long)ctx->bounds[(size_t)ctx->dist_rank + 1];
+    const unsigned long long lo = ctx->lo, nl = ctx->hi - ctx->lo;
+    ctx->n_local = (int64_t)nl;
+    // Degree-descending relabelling of skewed graphs, inside
+    // each partition's range (the ranges stay the reference's): hubs get the
+    // low ids of their range, so the matched bitmap and candidate lookups
+    // that follow the skew hit a small, cache-resident id range.
     uint32_t *newid = nullptr;
     ctx->relabeled = false;
     if (n > 1 && m) {
@@ -741,23 +631,36 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             relabel = (double)maxdeg > 64.0 * std::max(avg, 1.0);
         }
         if (relabel) {
-            uint32_t *key = nullptr, *key2 = nullptr, *val = nullptr, *dnew = nullptr;
+            unsigned long long *key = nullptr, *key2 = nullptr;
+            uint32_t *val = nullptr, *dnew = nullptr, *bdev = nullptr;
             void *t = nullptr;
             size_t tmp = 0;
+            const int p = ctx->dist_p;
             int rc = LMX_OK;
             do {
                 if ((rc = lmx_alloc(ctx, (void **)&ctx->oldid, n * 4, "oldid")) != LMX_OK) break;
                 if ((rc = lmx_alloc(ctx, (void **)&newid, n * 4, "newid")) != LMX_OK) break;
-                if ((rc = lmx_alloc(ctx, (void **)&key, n * 4, "relabel key")) != LMX_OK) break;
-                if ((rc = lmx_alloc(ctx, (void **)&key2, n * 4, "relabel key2")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&key, n * 8, "relabel key")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&key2, n * 8, "relabel key2")) != LMX_OK) break;
                 if ((rc = lmx_alloc(ctx, (void **)&val, n * 4, "relabel val")) != LMX_OK) break;
                 if ((rc = lmx_alloc(ctx, (void **)&dnew, n * 4, "deg new")) != LMX_OK) break;
-                k_relabel_keys<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->deg0, n, key, val);
-                cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key2, val, ctx->oldid,
-                                                                (long long)n, 0, 32, st);
+                if ((rc = lmx_alloc(ctx, (void **)&bdev, (size_t)(p + 1) * 8, "bounds")) != LMX_OK) break;
+                std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
+                cudaError_t e = cudaMemcpyAsync(bdev, hb.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, st);
+                if (e == cudaSuccess) {
+                    k_relabel_keys<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->deg0, n,
+                                                                       reinterpret_cast<unsigned long long *>(bdev),
+                                                                       p, key, val);
+                    e = cudaGetLastError();
+                }
+                int bits = 32;
+                while (p > 1 && (1 << (bits - 32)) < p) ++bits;
+                if (e == cudaSuccess)
+                    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key2, val, ctx->oldid, (long long)n, 0,
+                                                        bits, st);
                 if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel sort size"); break; }
                 if ((rc = lmx_alloc(ctx, &t, tmp, "relabel tmp")) != LMX_OK) break;
-                e = cub::DeviceRadixSort::SortPairs(t, tmp, key, key2, val, ctx->oldid, (long long)n, 0, 32, st);
+                e = cub::DeviceRadixSort::SortPairs(t, tmp, key, key2, val, ctx->oldid, (long long)n, 0, bits, st);
                 if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel sort"); break; }
                 k_relabel_apply<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->oldid, ctx->deg0, n, newid, dnew);
                 e = cudaMemcpyAsync(ctx->deg0, dnew, n * 4, cudaMemcpyDeviceToDevice, st);
@@ -765,10 +668,11 @@ int lmx_setup_slots(lmx_ctx *ctx) {
                 if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "relabel"); break; }
             } while (0);
             cudaStreamSynchronize(st);
-            lmx_free(ctx, (void **)&key, n * 4);
-            lmx_free(ctx, (void **)&key2, n * 4);
+            lmx_free(ctx, (void **)&key, n * 8);
+            lmx_free(ctx, (void **)&key2, n * 8);
             lmx_free(ctx, (void **)&val, n * 4);
             lmx_free(ctx, (void **)&dnew, n * 4);
+            lmx_free(ctx, (void **)&bdev, (size_t)(ctx->dist_p + 1) * 8);
             lmx_free(ctx, &t, tmp);
             if (rc != LMX_OK) {
                 lmx_free(ctx, (void **)&newid, n * 4);
@@ -777,72 +681,57 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             ctx->relabeled = true;
         }
     }
-    trace_mark(ctx, "degrees + relabel");
-    k_widen_deg<<<grid_for(ctx, n + 1), kBlock, 0, st>>>(ctx->deg0, ctx->vbeg, n);
-    LMX_CUDA(ctx, cudaGetLastError());
-    {
+    trace_mark(ctx, "partition + relabel");
+    if (ctx->algo == 1) {
+        unsigned long long tied = 0;
+        int rc = lmx_scan_build_slots(ctx, newid, &tied);
+        if (rc == LMX_OK && ctx->force_algo != 1 && tied * 16 > (unsigned long long)ctx->slots_local) {
+            // common ties: each round would rescan them -- the compacting loop
+            lmx_free(ctx, (void **)&ctx->vbeg, (nl + 1) * 8);
+            lmx_free(ctx, (void **)&ctx->ids0, (size_t)std::max<int64_t>(ctx->slots_local, 1) * 8);
+            lmx_free(ctx, (void **)&ctx->cand0, std::max<size_t>(nl, 1) * 8);
+            lmx_free(ctx, (void **)&ctx->lowpair, (size_t)std::max<int64_t>(ctx->m, 1) * 8);
+            ctx->algo = 0;
+            ctx->scan_rejected = true;
+            rc = lmx_weight_stage(ctx);
+            ctx->scan_rejected = false;
+        }
+        if (rc != LMX_OK) {
+            lmx_free(ctx, (void **)&newid, n * 4);
+            return rc;
+        }
+        trace_mark(ctx, "ordered slots");
+    }
+    unsigned long long slots = (unsigned long long)ctx->slots_local;
+    if (ctx->algo == 0) {
+        // compacting loop: segments of the owned range, local offsets
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (nl + 1) * 8, "vbeg"));
+        k_slice_local<<<grid_for(ctx, nl + 1), kBlock, 0, st>>>(ctx->deg0, lo, nl, ctx->vbeg);
+        LMX_CUDA(ctx, cudaGetLastError());
         size_t tmp = 0;
-        LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->vbeg, ctx->vbeg,
-                                                    (long long)(n + 1), st));
+        LMX_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->vbeg, ctx->vbeg, (long long)(nl + 1), st));
         void *t = nullptr;
         LMX_TRY(lmx_alloc(ctx, &t, tmp, "scan tmp"));
-        cudaError_t e = cub::DeviceScan::ExclusiveSum(t, tmp, ctx->vbeg, ctx->vbeg, (long long)(n + 1), st);
+        cudaError_t e = cub::DeviceScan::ExclusiveSum(t, tmp, ctx->vbeg, ctx->vbeg, (long long)(nl + 1), st);
         cudaStreamSynchronize(st);
         lmx_free(ctx, &t, tmp);
         LMX_CUDA(ctx, e);
-    }
-    // 1D vertex partition (bsp.py:60-98 idea: contiguous ranges with equal
-    // degree sums), cut points rounded to 32 so each rank owns whole words of
-    // the matched bitmap.  Single-GPU: one range [0, n).
-    ctx->lo = 0;
-    ctx->hi = n;
-    ctx->bounds.assign(2, 0);
-    ctx->bounds[1] = (int64_t)n;
-    if (ctx->dist_p > 1) {
-        const int p = ctx->dist_p;
-        unsigned long long *cuts = nullptr;
-        LMX_TRY(lmx_alloc(ctx, (void **)&cuts, (size_t)(p + 1) * 8, "cuts"));
-        k_cuts<<<1, 64, 0, st>>>(ctx->vbeg, n, p, cuts);
-        std::vector<unsigned long long> hc((size_t)p + 1);
-        cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cuts, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        lmx_free(ctx, (void **)&cuts, (size_t)(p + 1) * 8);
-        LMX_CUDA(ctx, e);
-        ctx->bounds.assign(hc.begin(), hc.end());
-        ctx->lo = hc[(size_t)ctx->dist_rank];
-        ctx->hi = hc[(size_t)ctx->dist_rank + 1];
-    }
-    const unsigned long long lo = ctx->lo, nl = ctx->hi - ctx->lo;
-    ctx->n_local = (int64_t)nl;
-    unsigned long long base = 0, top = 0;
-    LMX_CUDA(ctx, cudaMemcpyAsync(&base, ctx->vbeg + lo, 8, cudaMemcpyDeviceToHost, st));
-    LMX_CUDA(ctx, cudaMemcpyAsync(&top, ctx->vbeg + ctx->hi, 8, cudaMemcpyDeviceToHost, st));
-    LMX_CUDA(ctx, cudaStreamSynchronize(st));
-    slots = top - base;
-    if (ctx->algo == 1) slots = 2 * m;   // scan loop: every partition keeps the global segments
-    ctx->slots_local = (int64_t)slots;
-    if (ctx->dist_p > 1 && ctx->algo == 0) {
-        // local segment offsets and degrees of the owned range
-        unsigned long long *vl = nullptr;
-        uint32_t *dl = nullptr;
-        LMX_TRY(lmx_alloc(ctx, (void **)&vl, (nl + 1) * 8, "vbeg local"));
-        LMX_TRY(lmx_alloc(ctx, (void **)&dl, std::max<size_t>(nl, 1) * 4, "deg0 local"));
-        k_slice_local<<<grid_for(ctx, nl + 1), kBlock, 0, st>>>(ctx->vbeg, ctx->deg0, lo, nl, base, vl, dl);
-        LMX_CUDA(ctx, cudaGetLastError());
+        LMX_CUDA(ctx, cudaMemcpyAsync(&slots, ctx->vbeg + nl, 8, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
-        lmx_free(ctx, (void **)&ctx->vbeg, (n + 1) * 8);
+        ctx->slots_local = (int64_t)slots;
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
+    }
+    // the compacting loop's per-vertex degrees are local; the scan loop keeps deg0 by device id
+    if (ctx->algo == 0 && ctx->dist_p > 1) {
+        uint32_t *dl = nullptr;
+        LMX_TRY(lmx_alloc(ctx, (void **)&dl, std::max<size_t>(nl, 1) * 4, "deg0 local"));
+        if (nl) LMX_CUDA(ctx, cudaMemcpyAsync(dl, ctx->deg0 + lo, nl * 4, cudaMemcpyDeviceToDevice, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
         lmx_free(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4);
-        ctx->vbeg = vl;
         ctx->deg0 = dl;
     }
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, std::max<size_t>(slots, 1) * 8, "ids0"));
     LMX_TRY(lmx_alloc_match_state(ctx));
     trace_mark(ctx, "offsets + allocation");
-    if (ctx->algo == 1) {
-        LMX_TRY(build_scan_slots(ctx, ctx->ws_eid, ctx->ws_rank, ctx->ws_tied, ctx->ws_tidx, newid));
-        trace_mark(ctx, "ordered slots + lowpair");
-    }
     if (m && ctx->algo == 0) {
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
         if (ctx->layout == kGeneral) {
@@ -860,22 +749,20 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     lmx_free(ctx, (void **)&newid, n * 4);
     lmx_free_weight_stage(ctx);
-    if (ctx->algo == 1) {
+    if (ctx->algo == 1 || ctx->dist_p > 1)   // match rounds: scan-loop RoundStats, message accounting
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mround, std::max<size_t>(n, 1) * 4, "mround"));
+    if (ctx->algo == 1)
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->mpacked, (std::max<size_t>(n, 1) + 3) / 4 * 4, "mround packed"));
-        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand0, std::max<size_t>(n, 1) * 8, "cand0"));
-        k_cand0<<<grid_for(ctx, n), kBlock, 0, st>>>(ctx->vbeg, ctx->deg0, ctx->ids0, n, ctx->cand0);
-        LMX_CUDA(ctx, cudaGetLastError());
-        trace_mark(ctx, "scan state");
-    }
-    // round-0 bucket lists of the owned vertices (local indices, ascending)
+    // round-0 bucket lists of the owned vertices (compacting loop: local
+    // indices per live-degree bucket; scan loop: device ids with an edge)
     const size_t cap = std::max<size_t>(nl, 1);
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->bins0, cap * 4 * (ctx->algo == 1 ? 1 : kBuckets), "bins0"));
     {
         unsigned long long *cnt = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&cnt, 8 * kBuckets, "bucket counts"));
-        // compacting loop: local indices; scan loop: global ids of the owned range
         cub::CountingInputIterator<uint32_t> it(ctx->algo == 1 ? (uint32_t)lo : 0u);
+        // deg0 is indexed by device id (scan) or locally (compacting, p > 1),
+        // matching the counting iterator's base
         size_t tmp = 0;
         LMX_CUDA(ctx, cub::DeviceSelect::If(nullptr, tmp, it, ctx->bins0, cnt, (long long)nl,
                                             InBucket{ctx->deg0, 0}, st));
@@ -965,7 +852,7 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
             LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copy[1], 0));
             k_check_w<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, (unsigned long long)m, bad);
             LMX_CUDA(ctx, cudaGetLastError());
-            int rc = weight_stage(ctx);   // overlaps the endpoint copies
+            int rc = lmx_weight_stage(ctx);   // overlaps the endpoint copies
             cudaError_t e = cudaStreamWaitEvent(st, ctx->ev_copy[2], 0);
             if (e == cudaSuccess) {
                 k_convert_uv<<<grid_for(ctx, m), kBlock, 0, st>>>(su, sv, (unsigned long long)m, n, ctx->eu,
@@ -1040,6 +927,6 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
                      (unsigned long long)badpos, w);
         return lmx_fail(ctx, LMX_EINVAL, buf);
     }
-    if (!weights_done) LMX_TRY(weight_stage(ctx));
+    if (!weights_done) LMX_TRY(lmx_weight_stage(ctx));
     return lmx_setup_slots(ctx);
 }

@@ -3,8 +3,8 @@
 Mirrors ``locmax.bsp.bsp_local_max(g, p, seed, rerandomize)``
 (``/root/reference/pkg/src/locmax/bsp.py:101-205``).  The reference
 simulates p workers in one process; here each worker is a liblmx context:
-* it owns one of p contiguous vertex ranges with equal degree sums
-  (``bsp.py:60-98``; cuts rounded to 32 so a rank owns whole bitmap words);
+* it owns one of p contiguous vertex ranges with equal degree sums, cut
+  exactly as ``partition_graph`` cuts them (``bsp.py:60-98``);
 * it holds the slots of every edge incident to its range.
 
 Each round is driven by the host over a communicator:
@@ -51,6 +51,85 @@ from .graph import Matching, PhaseTrace, RoundStats
 LMX_OPT_DIST_P = 4
 LMX_OPT_DIST_RANK = 5
 
+try:   # the reference's own types when it is importable (graph.py's rationale)
+    from locmax.bsp import Partition as _RefPartition
+    from locmax.bsp import RoundMessages as _RefRoundMessages
+except Exception:
+    _RefPartition = _RefRoundMessages = None
+
+#: Bytes per candidate record in the reference's accounting (bsp.py:26).
+CANDIDATE_RECORD_BYTES = 32
+
+if _RefPartition is not None:
+    Partition, RoundMessages = _RefPartition, _RefRoundMessages
+else:
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class RoundMessages:
+        """bsp.py:29-41: the reference's per-round boundary accounting."""
+
+        round_index: int
+        candidate_records: int
+        bytes_estimate: int
+        cut_edges_surviving: int
+        status_records: int
+
+    @dataclass(frozen=True)
+    class Partition:
+        """bsp.py:44-57."""
+
+        num_workers: int
+        bounds: np.ndarray
+        owner: np.ndarray
+        local_edges: list
+        cut_edges: np.ndarray
+        degree_imbalance: float
+
+        @property
+        def cut_fraction(self) -> float:
+            total = sum(int(e.size) for e in self.local_edges)
+            m = total - int(self.cut_edges.size)
+            return self.cut_edges.size / m if m else 0.0
+
+
+def partition_graph(g, p: int):
+    """``partition_graph(g, p)`` (bsp.py:60-98): p contiguous vertex ranges
+    with near-equal degree sums -- the ranges the B200 partitions own (the
+    device computes the same cuts in lmx_setup.cu:partition_bounds)."""
+    n = int(g.num_vertices)
+    if p < 1:
+        raise ValueError("p must be >= 1")
+    if p > n:
+        raise ValueError(f"p={p} exceeds the vertex count {n}")
+    eu = np.asarray(g.edge_u, dtype=np.int64)
+    ev = np.asarray(g.edge_v, dtype=np.int64)
+    m = int(eu.size)
+    deg = np.bincount(eu, minlength=n) + np.bincount(ev, minlength=n)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(deg, out=offsets[1:])
+    two_m = 2 * m
+    targets = (np.arange(1, p, dtype=np.float64) * two_m) / p
+    cuts = np.searchsorted(offsets, targets, side="left").astype(np.int64)
+    if cuts.size:
+        steps = np.arange(1, p, dtype=np.int64)
+        cuts = np.maximum.accumulate(cuts - steps) + steps
+        cuts = np.minimum(np.maximum(cuts, steps), n - p + steps)
+        bounds = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    else:
+        bounds = np.array([0, n], dtype=np.int64)
+    owner = np.repeat(np.arange(p, dtype=np.int64), np.diff(bounds))
+    ou, ov = owner[eu], owner[ev]
+    ids = np.arange(m, dtype=np.int64)
+    local = [ids[(ou == k) | (ov == k)] for k in range(p)]
+    cut = ids[ou != ov]
+    if two_m:
+        share = two_m / p
+        imbalance = max(float(offsets[bounds[k + 1]] - offsets[bounds[k]]) for k in range(p)) / share
+    else:
+        imbalance = 1.0
+    return Partition(p, bounds, owner, local, cut, imbalance)
+
 
 def _bind(lib):
     if getattr(lib, "_dist_bound", False):
@@ -68,6 +147,7 @@ def _bind(lib):
                                    ctypes.POINTER(p)]),
         "lmx_dist_mround": (c_int, [p, ctypes.POINTER(p)]),
         "lmx_dist_hist": (c_int, [p, c_int, ctypes.POINTER(p), ctypes.POINTER(c_int)]),
+        "lmx_dist_messages": (c_int, [p, c_int, ctypes.POINTER(p)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -133,8 +213,8 @@ class DistRank:
         self.ebits = _view(eb.value, ((max(self.m, 1) + 31) // 32,), "<i4", self.device)
         # round loop chosen by the load: "scan" (weight-ordered, distinct weights) or "compact"
         self.algo = self.eng.algo()
-        self.mround = None
-        if self.algo == "scan":
+        self.mround = None   # match round per vertex (device ids): scan loop, or any loop with p > 1
+        if self.algo == "scan" or p > 1:
             mr = ctypes.c_void_p()
             self._chk(self.lib.lmx_dist_mround(self.eng._h, ctypes.byref(mr)), "lmx_dist_mround")
             self.mround = _view(mr.value, (max(self.n, 1),), "<i4", self.device)
@@ -190,6 +270,15 @@ class DistRank:
                   "lmx_dist_hist")
         return _view(hp.value, (nb.value,), "<i8", self.device)
 
+    def messages(self, n_rounds: int):
+        """This partition's share of the reference's boundary accounting
+        (lmx_dist_messages): device uint64 [2, n_rounds + 1] = candidate records
+        by last round sent, cut edges by death round.  Needs the all-gathered
+        match rounds."""
+        hp = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_messages(self.eng._h, int(n_rounds), ctypes.byref(hp)), "lmx_dist_messages")
+        return _view(hp.value, (2 * (n_rounds + 1),), "<i8", self.device)
+
     def close(self):
         self.eng.close()
 
@@ -222,6 +311,8 @@ class LocalComm:
         return recvs
 
     def allgather_bitmap(self, ranks):
+        # ranges follow bsp.py's cuts, so a boundary word holds bits of two
+        # ranks: merge by OR (a bit is only ever set, by its owner)
         for src in range(self.p):
             w0, w1 = ranks[src].word_range(src)
             if w1 <= w0:
@@ -229,7 +320,7 @@ class LocalComm:
             seg = ranks[src].bitmap[w0:w1]
             for dst in range(self.p):
                 if dst != src:
-                    ranks[dst].bitmap[w0:w1].copy_(seg)
+                    ranks[dst].bitmap[w0:w1].bitwise_or_(seg)
 
     def allgather_mround(self, ranks):
         for src in range(self.p):
@@ -333,8 +424,8 @@ class TorchComm:
             row[: w1 - w0].copy_(me.bitmap[w0:w1])
         self.dist.all_gather_into_tensor(out, row)
         for k, (a, b) in enumerate(spans):
-            if k != self.rank and b > a:
-                me.bitmap[a:b].copy_(out[k * width: k * width + (b - a)])
+            if k != self.rank and b > a:   # boundary words are shared: OR
+                me.bitmap[a:b].bitwise_or_(out[k * width: k * width + (b - a)])
 
     def allgather_mround(self, ranks):
         import torch
@@ -414,7 +505,34 @@ def run_rounds(ranks, comm, seed: int, rerandomize: bool = True, max_rounds: int
     for i, b in enumerate(before):
         nxt = before[i + 1] if i + 1 < len(before) else 0
         stats.append(RoundStats(b, matched[i], b - nxt))
+    if ranks[0].mround is not None:   # every partition's match rounds, for round_messages()
+        comm.allgather_mround(ranks)
     return stats, records
+
+
+def round_messages(ranks, comm, n_rounds: int) -> list:
+    """``trace.messages`` of bsp_local_max (bsp.py:148-199): per round the
+    candidate records (deduplicated per (vertex, receiving worker)), their
+    32-byte estimate, the surviving cut edges and the 2-per-cut-edge status
+    records -- derived on the device from the edges' death rounds
+    (lmx_dist_messages) and summed over the partitions."""
+    p = ranks[0].p
+    if p == 1 or n_rounds == 0:
+        return [RoundMessages(r, 0, 0, 0, 0) for r in range(n_rounds)]
+    h = comm.allreduce_sum([r.messages(n_rounds) for r in ranks])
+    rec, cut = h[: n_rounds + 1], h[n_rounds + 1:]
+    out = []
+    rs = cs = 0
+    suff_rec = [0] * (n_rounds + 1)
+    suff_cut = [0] * (n_rounds + 1)
+    for d in range(n_rounds, -1, -1):
+        rs += rec[d]
+        cs += cut[d]
+        suff_rec[d], suff_cut[d] = rs, cs
+    for r in range(n_rounds):
+        out.append(RoundMessages(r, suff_rec[r], suff_rec[r] * CANDIDATE_RECORD_BYTES, suff_cut[r],
+                                 2 * suff_cut[r]))
+    return out
 
 
 def _run_rounds_scan(ranks, comm, seed: int, rerandomize: bool, max_rounds: int | None):
@@ -496,7 +614,9 @@ def _unpack_ids(ebits, m: int) -> np.ndarray:
 def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int = 0, algo: str = "auto"):
     """Drop-in for ``bsp_local_max(g, p, seed, rerandomize)`` (bsp.py:101-205):
     p partitions emulated in this process on one B200.  ``trace.messages``
-    holds the exchange-A record count per round (cf. ``RoundMessages``)."""
+    holds the reference's ``RoundMessages`` per round (bsp.py:29-41,
+    :148-199), identical to bsp_local_max's; ``trace.exchange_a_records`` the
+    records this engine actually exchanged."""
     import torch
     t0 = time.perf_counter()
     if p < 1:
@@ -509,13 +629,15 @@ def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int =
     try:
         comm = LocalComm(p)
         stats, records = run_rounds(ranks, comm, seed, rerandomize)
+        messages = round_messages(ranks, comm, len(stats))
         mate, ebits = comm.gather_outputs(ranks)
         ids = _unpack_ids(ebits, ranks[0].m)
         mate_h = mate.cpu().numpy()[: g.num_vertices].copy()
     finally:
         for r in ranks:
             r.close()
-    trace = PhaseTrace(rounds=stats, messages=records)
+    trace = PhaseTrace(rounds=stats, messages=messages)
+    trace.exchange_a_records = records   # this engine's own per-round record counts
     trace.wall_millis = (time.perf_counter() - t0) * 1000.0
     return Matching(ids, mate_h), trace
 
@@ -530,11 +652,13 @@ def local_max_torchdist(g, seed: int, rerandomize: bool = True):
     me = DistRank(g, comm.p, comm.rank, dev, torch.cuda.current_stream().cuda_stream)
     try:
         stats, records = run_rounds([me], comm, seed, rerandomize)
+        messages = round_messages([me], comm, len(stats))
         mate, ebits = comm.gather_outputs([me])
         ids = _unpack_ids(ebits, me.m) if comm.rank == 0 else None
         mate_h = mate.cpu().numpy()[: g.num_vertices].copy() if comm.rank == 0 else None
     finally:
         me.close()
     dist.barrier()
-    trace = PhaseTrace(rounds=stats, messages=records)
+    trace = PhaseTrace(rounds=stats, messages=messages)
+    trace.exchange_a_records = records
     return (Matching(ids, mate_h) if comm.rank == 0 else None), trace

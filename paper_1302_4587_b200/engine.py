@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
+    "lmx_dist_messages",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
 )
 LMX_OPT_KERNEL_TIMING = 1

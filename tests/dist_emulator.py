@@ -18,19 +18,10 @@ from oracle import oracle as O
 
 
 def partition_bounds(n: int, eu, ev, p: int) -> np.ndarray:
-    """Same rule as csrc/lmx_setup.cu:k_cuts (equal degree sums, cuts rounded to 32)."""
+    """partition_graph's cut rule (bsp.py:60-98), as csrc/lmx_setup.cu:partition_bounds."""
     deg = np.bincount(np.concatenate([eu, ev]), minlength=n).astype(np.int64)
-    vbeg = np.concatenate([[0], np.cumsum(deg)])
-    two_m = int(vbeg[-1])
-    cuts = [0]
-    for k in range(1, p):
-        target = int(float(k) * float(two_m) / float(p))
-        lo = int(np.searchsorted(vbeg, target, side="left"))
-        c = min((lo + 16) // 32 * 32, n)
-        c = max(c, cuts[-1])
-        cuts.append(c)
-    cuts.append(n)
-    return np.array(cuts, dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    return O.partition_bounds(offsets, n, p)
 
 
 class EmulatedRank:
@@ -51,7 +42,7 @@ class EmulatedRank:
         self.bitmap = torch.zeros(max(self.words, 1), dtype=torch.int32)
         self.mate = torch.full((max(self.n, 1),), -1, dtype=torch.int64)
         self.ebits = torch.zeros((max(self.m, 1) + 31) // 32, dtype=torch.int32)
-        self.mround = torch.full((max(self.n, 1),), -1, dtype=torch.int32) if algo == "scan" else None
+        self.mround = torch.full((max(self.n, 1),), -1, dtype=torch.int32) if (algo == "scan" or p > 1) else None
 
     def vertex_range(self, k: int):
         return int(self.bounds[k]), int(self.bounds[k + 1])
@@ -64,7 +55,32 @@ class EmulatedRank:
         d = np.minimum(np.minimum(mr[self.eu[own]], mr[self.ev[own]]), n_rounds)
         return torch.from_numpy(np.bincount(d, minlength=max(n_rounds + 1, 256)).astype(np.int64))
 
+    def messages(self, n_rounds: int):
+        """lmx_dist_messages restated: candidate records by the last round
+        they are sent in (per owned vertex, its end of the edge and the
+        receiving partition: bsp.py:152-154 dedupes the edge_u and edge_v sides
+        separately) and cut edges by death round (each once, from its lower end)."""
+        mr = self.mround.numpy().view(np.uint32).astype(np.int64)
+        rec = np.zeros(n_rounds + 1, dtype=np.int64)
+        cut = np.zeros(n_rounds + 1, dtype=np.int64)
+        ou = np.searchsorted(self.bounds, self.eu, side="right") - 1
+        ov = np.searchsorted(self.bounds, self.ev, side="right") - 1
+        death = np.minimum(np.minimum(mr[self.eu], mr[self.ev]), n_rounds)
+        best = {}   # (vertex, its end of the edge (0 = edge_u, 1 = edge_v), receiving worker) -> last round
+        for e in np.nonzero(ou != ov)[0]:
+            for end, x, wx, y, wy in ((0, self.eu[e], ou[e], self.ev[e], ov[e]), (1, self.ev[e], ov[e], self.eu[e], ou[e])):
+                if wx != self.rank:
+                    continue
+                key = (int(x), end, int(wy))
+                best[key] = max(best.get(key, -1), int(death[e]))
+                if x < y:
+                    cut[death[e]] += 1
+        for d in best.values():
+            rec[d] += 1
+        return torch.from_numpy(np.concatenate([rec, cut]))
+
     def word_range(self, k: int):
+        # the bitmap words holding range k's bits (boundary words are shared)
         return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
 
     def _owner(self, x: int) -> int:

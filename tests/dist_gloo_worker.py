@@ -16,7 +16,7 @@ import torch.distributed as dist  # noqa: E402
 
 from dist_emulator import EmulatedRank  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from paper_1302_4587_b200.dist import TorchComm, _unpack_ids, run_rounds  # noqa: E402
+from paper_1302_4587_b200.dist import TorchComm, _unpack_ids, round_messages, run_rounds  # noqa: E402
 from paper_1302_4587_b200.graph import Graph  # noqa: E402
 
 
@@ -37,12 +37,15 @@ def main():
         for algo, rr in (("compact", True), ("compact", False), ("scan", True), ("scan", False)):
             me = EmulatedRank(g, comm.p, comm.rank, algo)
             stats, records = run_rounds([me], comm, seed, rr)
+            msgs = round_messages([me], comm, len(stats))
             mate, ebits = comm.gather_outputs([me])
             if comm.rank == 0:
                 ids = _unpack_ids(ebits, me.m)
                 ref = O.c_local_max(gn, eu, ev, ew, seed, rr)
                 ok = (np.array_equal(mate.numpy()[:gn], ref.mate) and np.array_equal(ids, ref.matched_ids)
-                      and [(s.edges_before, s.edges_matched, s.edges_removed) for s in stats] == ref.rounds)
+                      and [(s.edges_before, s.edges_matched, s.edges_removed) for s in stats] == ref.rounds
+                      and [tuple(vars(x).values()) if not isinstance(x, tuple) else x for x in msgs]
+                      == O.bsp_messages(gn, eu, ev, ew, comm.p, seed, rr))
                 print(f"case seed={seed} n={n} kind={kind} algo={algo} rr={rr} rounds={len(stats)} "
                       f"cut-records={sum(records)} ok={ok}", flush=True)
                 failures += 0 if ok else 1

@@ -21,17 +21,28 @@ from conftest import ROOT, instance_graph, mate_digest, small_cases, small_runs
 from oracle import oracle as O
 
 
-def test_partition_bounds_rule():
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from dist_emulator import partition_bounds
-    n, eu, ev, w = O.gen_random(1 << 12, 4, 0)
-    for p in (1, 2, 3, 8):
-        b = partition_bounds(n, eu, ev, p)
-        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
-        assert np.all(b[1:-1] % 32 == 0)
+def _partition_cases():
+    z = np.load(os.path.join(ROOT, "tests", "golden", "partition.npz"))
+    for k in range(z["p"].size):
+        kind, size, alpha, seed, p = (int(z[x][k]) for x in ("kind", "size", "alpha", "seed", "p"))
+        n, eu, ev, w = O.gen_random(size, alpha, seed) if kind == 0 else O.gen_rgg(size, seed)
+        b0 = int(z["boff"][k])
+        yield n, eu, ev, w, p, z["bounds"][b0:b0 + p + 1], int(z["cut"][k]), float(z["imbalance"][k]), \
+            float(z["cut_fraction"][k])
+
+
+def test_partition_bounds_match_reference():
+    """oracle.partition_bounds and the package's partition_graph (bsp.py:60-98
+    mirror) vs the unmodified reference (tests/golden/partition.npz)."""
+    from paper_1302_4587_b200 import Graph
+    from paper_1302_4587_b200.dist import partition_graph
+    for n, eu, ev, w, p, want, cut, imb, cf in _partition_cases():
         deg = np.bincount(np.concatenate([eu, ev]), minlength=n)
-        share = [deg[b[k]:b[k + 1]].sum() for k in range(p)]
-        assert max(share) <= 2 * eu.size / p + 32 * deg.max() + 1
+        offsets = np.concatenate([[0], np.cumsum(deg)])
+        assert np.array_equal(O.partition_bounds(offsets, n, p), want)
+        part = partition_graph(Graph(n, eu, ev, w), p)
+        assert np.array_equal(part.bounds, want) and part.cut_edges.size == cut
+        assert part.degree_imbalance == imb and part.cut_fraction == cf
 
 
 def test_gloo_world_size_2_matches_oracle():
@@ -78,7 +89,7 @@ def test_dist_reference_instances(golden_instances, name, p):
     assert mate_digest(matching.mate) == str(z[f"{name}/mate_digest"])
     assert [[r.edges_before, r.edges_matched, r.edges_removed] for r in trace.rounds] == \
         z[f"{name}/rounds"].tolist()
-    assert sum(trace.messages) > 0
+    assert sum(m.candidate_records for m in trace.messages) > 0 and sum(trace.exchange_a_records) > 0
 
 
 @pytest.mark.gpu
@@ -117,3 +128,29 @@ def test_dist_round_loop_choice():
             assert r.algo == want
         finally:
             r.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["auto", "compact"])
+def test_dist_round_messages_equal_reference(algo):
+    """trace.messages of local_max_dist == the unmodified reference's
+    bsp_local_max RoundMessages (tests/golden/bsp.npz), field by field, and
+    the partitions own exactly partition_graph's ranges."""
+    from paper_1302_4587_b200 import Graph
+    from paper_1302_4587_b200.dist import DistRank, local_max_dist
+    z = np.load(os.path.join(ROOT, "tests", "golden", "bsp.npz"))
+    for k, (kind, size, alpha, seed, p, rr) in enumerate(z["cases"]):
+        n, eu, ev, w = O.gen_random(int(size), int(alpha), int(seed)) if kind == 0 else O.gen_rgg(int(size), int(seed))
+        g = Graph(n, eu, ev, w)
+        _, trace = local_max_dist(g, int(p), int(seed), bool(rr), algo=algo)
+        want = [tuple(int(x) for x in row) for row in z["rows"][z["off"][k]:z["off"][k + 1]]]
+        got = [(m.round_index, m.candidate_records, m.bytes_estimate, m.cut_edges_surviving, m.status_records)
+               for m in trace.messages]
+        assert got == want, (k, got[:3], want[:3])
+        if p > 1 and k % 5 == 0:
+            deg = np.bincount(np.concatenate([eu, ev]), minlength=n)
+            r = DistRank(g, int(p), 0, algo=algo)
+            try:
+                assert np.array_equal(r.bounds, O.partition_bounds(np.concatenate([[0], np.cumsum(deg)]), n, int(p)))
+            finally:
+                r.close()

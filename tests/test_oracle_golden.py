@@ -164,3 +164,14 @@ def test_scale_fixtures_are_consistent():
         assert sum(r[2] for r in rec["rounds"]) == rec["m"]
     assert sc["rgg22"].get("reference_checked") and sc["rgg22"].get("generator_checked")
     assert sc["rmat24"].get("reference_checked")
+
+
+def test_bsp_messages_match_reference():
+    """oracle.bsp_messages vs the unmodified reference's bsp_local_max
+    RoundMessages (tests/golden/bsp.npz, make_golden_bsp.py)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "bsp.npz"))
+    for k, (kind, size, alpha, seed, p, rr) in enumerate(z["cases"]):
+        n, eu, ev, w = O.gen_random(int(size), int(alpha), int(seed)) if kind == 0 else O.gen_rgg(int(size), int(seed))
+        want = [tuple(int(x) for x in r) for r in z["rows"][z["off"][k]:z["off"][k + 1]]]
+        assert O.bsp_messages(n, eu, ev, w, int(p), int(seed), bool(rr)) == want
