@@ -210,7 +210,7 @@ int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_weight_stage(lmx_ctx *ctx);
 void trace_mark(lmx_ctx *ctx, const char *what);   // LMX_TRACE_SETUP=1: K0 stage times
 // scan loop K0 (lmx_scanload.cu): owned weight-descending segments, cand0, lowpair
-int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid, unsigned long long *tied_slots);
+int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);

@@ -433,16 +433,6 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         uniform = got[0] == got[1];
     }
     ctx->layout = kUniform;
-    // The weight-ordered scan loop needs no global weight order (lmx_scanload.cu
-    // sorts each segment): take it tentatively; lmx_setup_slots falls back to the
-    // compacting loop (and comes back here with scan_rejected) if ties are common.
-    if (m && !uniform && ctx->force_algo != 0 && !ctx->scan_rejected && ctx->force_layout == -1 &&
-        ctx->n < (1LL << 30)) {
-        ctx->algo = 1;
-        ctx->layout = kDistinct;
-        ctx->ws_kofe = nullptr;
-        return LMX_OK;
-    }
     if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
         unsigned long long *keys = nullptr, *keys2 = nullptr;
         uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
@@ -496,6 +486,19 @@ int lmx_weight_stage(lmx_ctx *ctx) {
                                     "tie_rank")) != LMX_OK)
                     break;
             }
+            // round-loop algorithm: the weight-ordered scan loop needs (almost)
+            // distinct weights -- a tied run is rescanned every round -- and
+            // n < 2^30 (slot flag bits); it keeps the descending order itself
+            // (eid by sorted position + global tie flags) for lmx_scan_build_slots
+            if (distinct && ctx->force_algo != 0 && !ctx->scan_rejected && ctx->n < (1LL << 30)) {
+                ctx->algo = 1;
+                lmx_free(ctx, (void **)&ctx->eid_of_x, (D + T) * 4);
+                lmx_free(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4);
+                ctx->ws_eid = vals2;
+                ctx->ws_tied = tied;
+                vals2 = tied = nullptr;
+                break;
+            }
             k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
                                                            (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
             e = cudaGetLastError();
@@ -514,6 +517,7 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             lmx_free(ctx, (void **)&kofe, m * 4);
             return rc;
         }
+        if (ctx->algo == 1) lmx_free(ctx, (void **)&kofe, m * 4);
     }
     ctx->ws_kofe = kofe;
     return LMX_OK;
@@ -683,19 +687,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     }
     trace_mark(ctx, "partition + relabel");
     if (ctx->algo == 1) {
-        unsigned long long tied = 0;
-        int rc = lmx_scan_build_slots(ctx, newid, &tied);
-        if (rc == LMX_OK && ctx->force_algo != 1 && tied * 16 > (unsigned long long)ctx->slots_local) {
-            // common ties: each round would rescan them -- the compacting loop
-            lmx_free(ctx, (void **)&ctx->vbeg, (nl + 1) * 8);
-            lmx_free(ctx, (void **)&ctx->ids0, (size_t)std::max<int64_t>(ctx->slots_local, 1) * 8);
-            lmx_free(ctx, (void **)&ctx->cand0, std::max<size_t>(nl, 1) * 8);
-            lmx_free(ctx, (void **)&ctx->lowpair, (size_t)std::max<int64_t>(ctx->m, 1) * 8);
-            ctx->algo = 0;
-            ctx->scan_rejected = true;
-            rc = lmx_weight_stage(ctx);
-            ctx->scan_rejected = false;
-        }
+        int rc = lmx_scan_build_slots(ctx, newid);
         if (rc != LMX_OK) {
             lmx_free(ctx, (void **)&newid, n * 4);
             return rc;
