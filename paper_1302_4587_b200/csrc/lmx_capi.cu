@@ -72,6 +72,8 @@ void lmx_destroy(lmx_ctx *ctx) {
     ctx->live.clear();
     if (ctx->ctr) cudaFree(ctx->ctr);
     if (ctx->ctr_host) cudaFreeHost(ctx->ctr_host);
+    if (ctx->loop_aux) cudaFree(ctx->loop_aux);
+    if (ctx->loop_host) cudaFreeHost(ctx->loop_host);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);

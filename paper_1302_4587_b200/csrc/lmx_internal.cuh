@@ -98,10 +98,13 @@ struct lmx_ctx {
     int num_sms = 148;
     int round_grid[3][3] = {};   // persistent grid of each round-kernel instance [MODE][LAYOUT]
     int match_blocks = 0;
-    int scan_grid[2] = {0, 0};   // scan round kernel grids (round 0, rounds >= 1)
+    int scan_grid[3] = {0, 0, 0};   // scan probe grids (round 0, rounds >= 1 one-phase, two-phase)
     int scan_last_rounds = -1;   // rounds of this context's last scan-loop matching (-1: none yet); a
                                  // hint for the first batch only, kept across loads (results never depend on it)
     int scan_match_grid = 0;
+    int scan_loop_grid = 0;      // persistent cooperative round loop (0: not available)
+    uint32_t *loop_aux = nullptr;        // device: [0] round count, then u64 stamps [2 ctr_cap + 2]
+    uint32_t *loop_host = nullptr;       // pinned mirror
     std::string err;
 
     // graph
@@ -214,6 +217,7 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid);
 int lmx_configure_grids(lmx_ctx *ctx);
 int lmx_scan_configure_grids(lmx_ctx *ctx);
 int lmx_ensure_ctr(lmx_ctx *ctx, int need);
+inline size_t lmx_loop_aux_bytes(int cap) { return 8 + 8 * (2 * (size_t)cap + 4); }
 // the stepped multi-GPU protocol on the scan loop (lmx_scan.cu)
 int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize);
 int lmx_scan_dist_round(lmx_ctx *ctx);

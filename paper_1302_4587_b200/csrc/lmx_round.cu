@@ -836,6 +836,12 @@ int lmx_ensure_ctr(lmx_ctx *ctx, int need) {
     ctx->ctr = nc;
     ctx->ctr_host = nh;
     ctx->ctr_cap = ncap;
+    // the persistent scan loop's round count + per-phase stamps
+    if (ctx->loop_aux) cudaFree(ctx->loop_aux);
+    if (ctx->loop_host) cudaFreeHost(ctx->loop_host);
+    ctx->loop_aux = ctx->loop_host = nullptr;
+    LMX_CUDA(ctx, cudaMalloc(&ctx->loop_aux, lmx_loop_aux_bytes(ncap)));
+    LMX_CUDA(ctx, cudaMallocHost(&ctx->loop_host, lmx_loop_aux_bytes(ncap)));
     return LMX_OK;
 }
 

@@ -26,9 +26,11 @@
 // Kernels: lmx_scan_round_kernel (candidate probe of A_r, thread per vertex),
 // lmx_scan_match_kernel (mutual candidates -> bitmap, mate, mround, edge bit;
 // appends A_{r+1}), lmx_scan_hist_kernel (death-round histogram).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "lmx_internal.cuh"
@@ -179,8 +181,7 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 // neighbour is unmatched and its weight unique, so most vertices read 12
 // bytes (list, cand) plus one bitmap bit and write nothing.
 template <bool FIRST, bool DIST>
-__global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
-    __shared__ unsigned long long s_red[3][kWarps];
+__device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long (&s_red)[3][kWarps]) {
     const uint32_t na = a.ctr->pad[0];
     if (na == 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -305,6 +306,12 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(S
     }
 }
 
+template <bool FIRST, bool DIST>
+__global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
+    __shared__ unsigned long long s_red[3][kWarps];
+    probe_body<FIRST, DIST>(a, s_red);
+}
+
 struct ScanMatchArgs {
     bool defer_ebits;             // single GPU: edge bits set after the loop (lmx_scan_edge_bits)
     const uint32_t *cnbr, *ckey;
@@ -325,15 +332,13 @@ struct ScanMatchArgs {
     uint32_t *remote_ok;          // [nl] cross-partition matches confirmed by exchange A
 };
 
-__global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_kernel(ScanMatchArgs a) {
-    __shared__ uint32_t s_cnt[kWarps];
-    __shared__ uint32_t s_base;
+template <int kItems>
+__device__ __forceinline__ void match_body(const ScanMatchArgs &a, uint32_t (&s_cnt)[kWarps], uint32_t &s_base) {
     const uint32_t total = a.ctr->pad[0];
     if (total == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = lanemask_lt_u32();
     unsigned long long matched_v = 0;
-    constexpr int kItems = LMX_SCAN_MATCH_ITEMS;
     const uint32_t tile = kBlock * kItems;
     for (uint32_t t0 = blockIdx.x * tile; t0 < total; t0 += gridDim.x * tile) {
         uint32_t vv[kItems];
@@ -411,6 +416,76 @@ __global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_ke
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) matched_v += __shfl_xor_sync(0xffffffffu, matched_v, off);
     if (lane == 0 && matched_v) atomicAdd(&a.ctr->matched_v, matched_v);
+}
+
+__global__ void __launch_bounds__(kBlock, LMX_SCAN_MATCH_MINB) lmx_scan_match_kernel(ScanMatchArgs a) {
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ uint32_t s_base;
+    match_body<LMX_SCAN_MATCH_ITEMS>(a, s_cnt, s_base);
+}
+
+// ---- the whole round loop in one persistent cooperative kernel -------------
+// Rounds r0 .. r_end-1 of probe -> grid barrier -> match -> grid barrier,
+// ending at the first round that finds no candidate (matchers.py:87-90).
+// One launch per matching instead of two per round: no launch gaps, no
+// per-kernel tails, no host round trip to learn the round count (the death
+// histogram reads it from `result`).  Block 0 stamps %globaltimer after each
+// barrier, so the per-round probe / match times come out of the same launch.
+#ifndef LMX_LOOP_MINB
+#define LMX_LOOP_MINB 4
+#endif
+#ifndef LMX_LOOP_MATCH_ITEMS
+#define LMX_LOOP_MATCH_ITEMS 8
+#endif
+
+struct LoopArgs {
+    ScanArgs p;               // probe arguments (alist, ctr, rs set per round)
+    ScanMatchArgs mt;         // match arguments (lists, ctr, round set per round)
+    const uint32_t *bins0;    // A_0
+    uint32_t *lists[2];       // A_r ping-pong
+    RoundCtr *ctr;
+    uint64_t seed_mix;        // mix64(seed), tiebreak.py:40-52
+    int rerandomize;
+    int r0, r_end;
+    uint32_t *result;         // [0]: the round count (r_end if not reached)
+    unsigned long long *stamps;   // [2 r_end + 1]: globaltimer at round start / after probe / after match
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(kBlock, LMX_LOOP_MINB) lmx_scan_loop_kernel(LoopArgs L) {
+    __shared__ unsigned long long s_red[3][kWarps];
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ uint32_t s_base;
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const bool stamp = L.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+    int r = L.r0;
+    if (stamp) L.stamps[2 * r] = globaltimer();
+    for (; r < L.r_end; ++r) {
+        ScanArgs a = L.p;
+        a.alist = r == 0 ? L.bins0 : L.lists[r & 1];
+        a.ctr = L.ctr + r;
+        a.rs = mix64(L.seed_mix ^ (L.rerandomize ? (uint64_t)r : 0ULL));
+        if (r == 0) probe_body<true, false>(a, s_red);
+        else probe_body<false, false>(a, s_red);
+        grid.sync();
+        if (stamp) L.stamps[2 * r + 1] = globaltimer();
+        if (L.ctr[r].live_slots == 0) break;   // no candidate anywhere: m_r = 0
+        ScanMatchArgs ma = L.mt;
+        ma.alist = a.alist;
+        ma.anext = L.lists[(r + 1) & 1];
+        ma.ctr = L.ctr + r;
+        ma.ctr_next = L.ctr + r + 1;
+        ma.round = r;
+        match_body<LMX_LOOP_MATCH_ITEMS>(ma, s_cnt, s_base);
+        grid.sync();
+        if (stamp) L.stamps[2 * r + 2] = globaltimer();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *L.result = (uint32_t)r;
 }
 
 // Matched-edge bits after the loop (graph.py:195-203: the lower endpoint
@@ -654,7 +729,11 @@ static int hist_hub_launch(lmx_ctx *ctx, unsigned long long mm, uint32_t R, cons
 }
 
 int lmx_scan_configure_grids(lmx_ctx *ctx) {
-    int occ0 = 0, occ1 = 0, occm = 0;
+    int occ0 = 0, occ1 = 0, occm = 0, occl = 0;
+    LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occl, lmx_scan_loop_kernel, kBlock, 0));
+    int coop = 0;
+    LMX_CUDA(ctx, cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+    ctx->scan_loop_grid = coop ? ctx->num_sms * std::max(occl, 1) : 0;
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, lmx_scan_round_kernel<true, false>, kBlock, 0));
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, lmx_scan_round_kernel<false, false>, kBlock, 0));
     LMX_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occm, lmx_scan_match_kernel, kBlock, 0));
@@ -820,8 +899,160 @@ static int scan_edge_bits_launch(lmx_ctx *ctx, unsigned long long lo, unsigned l
     return LMX_OK;
 }
 
+// Device histogram for a round count held on the device (R_dev): 4-bit
+// packed match rounds, which are exact for R < 15 (the caller reruns with the
+// right width once it knows R).
+static int scan_hist_launch_dev(lmx_ctx *ctx, const uint32_t *R_dev) {
+    cudaStream_t st = ctx->stream;
+    const size_t nbins = kHistBins;
+    if (ctx->hist_cap < nbins) {
+        lmx_free(ctx, (void **)&ctx->hist, (ctx->hist_cap + 1) * 8);
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->hist, (nbins + 1) * 8, "death histogram"));
+        ctx->hist_cap = nbins;
+    }
+    LMX_CUDA(ctx, cudaMemsetAsync(ctx->hist, 0, nbins * 8, st));
+    if (ctx->lowpair_n == 0) return LMX_OK;
+    lmx_pack_mround<4><<<ctx->num_sms * 8, kBlock, 0, st>>>(ctx->mround, (unsigned long long)ctx->n, ctx->mpacked);
+    LMX_TRY(hist_hub_launch<4>(ctx, ctx->lowpair_n, 0u, R_dev));
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 2;
+    return LMX_OK;
+}
+
+// The persistent round loop (lmx_scan_loop_kernel): one cooperative launch
+// for all rounds, then the histogram and the matched-edge bits, one
+// synchronisation.  Diagnostics (per-round probe / match times) come from the
+// kernel's globaltimer stamps.
+static int run_rounds_loop(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
+                           std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
+    cudaStream_t st = ctx->stream;
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
+    LMX_TRY(scan_begin(ctx));
+    int r0 = 0, n_rounds = -1;
+    std::vector<unsigned long long> hist;
+    uint32_t R = 0;
+    while (n_rounds < 0) {
+        const int r_end = ctx->ctr_cap - 2;
+        uint32_t *result = ctx->loop_aux;   // (reallocated when the counters grow)
+        unsigned long long *stamps = reinterpret_cast<unsigned long long *>(ctx->loop_aux + 2);
+        LoopArgs L;
+        L.p = ScanArgs{};
+        L.p.vbeg = ctx->vbeg;
+        L.p.ptr = ctx->vdeg;
+        L.p.cnbr = reinterpret_cast<uint32_t *>(ctx->cand);
+        L.p.ckey = reinterpret_cast<uint32_t *>(ctx->cand) + std::max<int64_t>(ctx->n_local, 1);
+        L.p.cand0 = ctx->cand0;
+        L.p.ids = ctx->ids0;
+        L.p.matched = ctx->matched;
+        L.p.lo = (uint32_t)ctx->lo;
+        L.p.nl = (uint32_t)ctx->n_local;
+        L.mt.defer_ebits = true;
+        L.mt.cnbr = L.p.cnbr;
+        L.mt.ckey = L.p.ckey;
+        L.mt.ptr = ctx->vdeg;
+        L.mt.vbeg = ctx->vbeg;
+        L.mt.ids = ctx->ids0;
+        L.mt.matched = ctx->matched;
+        L.mt.mround = ctx->mround;
+        L.mt.mate = ctx->mate_target;
+        L.mt.oldid = ctx->relabeled ? ctx->oldid : nullptr;
+        L.mt.ebits = ctx->ebits;
+        L.mt.lo = (uint32_t)ctx->lo;
+        L.mt.nl = (uint32_t)ctx->n_local;
+        L.mt.remote_ok = ctx->remote_ok;
+        L.bins0 = ctx->bins0;
+        L.lists[0] = ctx->lists[0];
+        L.lists[1] = ctx->lists[1];
+        L.ctr = ctx->ctr;
+        L.seed_mix = mix64(seed_masked);
+        L.rerandomize = rerandomize ? 1 : 0;
+        L.r0 = r0;
+        L.r_end = r_end;
+        L.result = result;
+        L.stamps = stamps;
+        void *args[] = {&L};
+        LMX_CUDA(ctx, cudaLaunchCooperativeKernel((const void *)lmx_scan_loop_kernel, dim3(ctx->scan_loop_grid),
+                                                  dim3(kBlock), args, 0, st));
+        ctx->timing.round_launches += 1;
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, st));
+        LMX_TRY(scan_hist_launch_dev(ctx, result));
+        LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));
+        hist.assign(kHistBins, 0);
+        LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)ctx->ctr_cap,
+                                      cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaMemcpyAsync(ctx->loop_host, ctx->loop_aux, lmx_loop_aux_bytes(ctx->ctr_cap),
+                                      cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, kHistBins * 8, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        R = ctx->loop_host[0];
+        if ((int)R < r_end) {
+            n_rounds = (int)R;
+        } else {   // more rounds than the counters hold: grow them and continue
+            r0 = (int)R;
+            LMX_TRY(lmx_ensure_ctr(ctx, 2 * ctx->ctr_cap));
+        }
+    }
+    if (n_rounds >= 15) {   // the 4-bit histogram saturated: recount at the right width
+        LMX_TRY(scan_hist_launch(ctx, n_rounds));
+        const size_t nbins = std::max<size_t>((size_t)n_rounds + 1, kHistBins);
+        hist.assign(nbins, 0);
+        LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, nbins * 8, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+    }
+    ctx->scan_last_rounds = n_rounds;
+    ctx->timing.rounds_executed = n_rounds + (n_rounds < ctx->ctr_cap ? 1 : 0);
+    // per-round times from the stamps (ns): probe r = [2r, 2r+1], match r = [2r+1, 2r+2]
+    ctx->kernel_ms.clear();
+    ctx->timing.round_kernel_ms = ctx->timing.match_kernel_ms = 0;
+    const unsigned long long *hs = reinterpret_cast<const unsigned long long *>(ctx->loop_host + 2);
+    for (int r = r0 == 0 ? 0 : r0; r <= n_rounds && r < ctx->ctr_cap - 2; ++r) {
+        const float pm = (float)((double)(hs[2 * r + 1] - hs[2 * r]) * 1e-6);
+        const float mm = r < n_rounds ? (float)((double)(hs[2 * r + 2] - hs[2 * r + 1]) * 1e-6) : 0.f;
+        ctx->kernel_ms.push_back(pm);
+        ctx->kernel_ms.push_back(mm);
+        ctx->timing.round_kernel_ms += pm;
+        ctx->timing.match_kernel_ms += mm;
+    }
+    float hms = 0.f;
+    cudaEventElapsedTime(&hms, ctx->ev2, ctx->ev1);
+    ctx->timing.hist_kernel_ms = hms;
+    unsigned long long total = 0;
+    for (size_t i = 0; i < hist.size(); ++i) total += hist[i];
+    if (total != (unsigned long long)ctx->m) return lmx_fail(ctx, LMX_ECUDA, "internal: death histogram size");
+    for (size_t i = (size_t)n_rounds; i < hist.size(); ++i)
+        if (hist[i]) return lmx_fail(ctx, LMX_ECUDA, "internal: an edge outlived the round loop");
+    long long live = ctx->m;
+    unsigned long long total_matched_v = 0;
+    ctx->timing.slot_reads = 0;
+    for (int i = 0; i < n_rounds; ++i) {
+        const RoundCtr &c = ctx->ctr_host[i];
+        if (c.matched_v & 1ULL) return lmx_fail(ctx, LMX_ECUDA, "internal: odd matched-vertex count");
+        if (live <= 0) return lmx_fail(ctx, LMX_ECUDA, "internal: a round without live edges");
+        lmx_round_stats sr;
+        sr.edges_before = live;
+        sr.edges_matched = (int64_t)(c.matched_v / 2);
+        sr.edges_removed = (int64_t)hist[(size_t)i];
+        stats.push_back(sr);
+        live -= (long long)hist[(size_t)i];
+        total_matched_v += c.matched_v;
+        ctx->timing.slot_reads += (int64_t)c.slot_reads;
+    }
+    n_matched = total_matched_v / 2;
+    return LMX_OK;
+}
+
 int lmx_run_rounds_scan(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                         std::vector<lmx_round_stats> &stats, unsigned long long &n_matched) {
+    static const bool stepped = getenv("LMX_SCAN_STEPPED") != nullptr;   // A/B: one launch per kernel
+    if (!stepped && ctx->m > 0 && ctx->scan_loop_grid > 0) {
+        stats.clear();
+        n_matched = 0;
+        ctx->timing.round_launches = 0;
+        LMX_TRY(lmx_ensure_ctr(ctx, 64));
+        return run_rounds_loop(ctx, seed_masked, rerandomize, stats, n_matched);
+    }
     stats.clear();
     n_matched = 0;
     ctx->timing.round_launches = 0;

@@ -27,7 +27,7 @@ for spec in "$@"; do
         -c $(cat /tmp/var_${name}_$f.src) -o /tmp/var_${name}_$f.o -Xptxas -v 2> /tmp/var_${name}_$f.ptxas || exit 1
     done &&
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/build/variants/liblmx_$name.so \
-      $objs $OBJ/lmx_setup.o $OBJ/lmx_capi.o $OBJ/lmx_build.o $OBJ/lmx_coarsen.o $OBJ/lmx_validate.o $OBJ/lmx_rbm.o -cudart static ) &
+      $objs $(ls $OBJ/*.o | grep -v -F -e /lmx_round.o -e /lmx_scan.o) -cudart static ) &
 done
 wait
 ls $ROOT/build/variants
