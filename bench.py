@@ -36,9 +36,22 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: RMAT scale, edge factor; Graph500 (a, b, c) = (.57, .19, .19), U[0,1) weights
-    "rmat26": 26, "rmat25": 25, "rmat24": 24, "rmat22": 22, "rmat20": 20, "rmat16": 16,
+    # name: (family, scale, edge factor).  rmat: Graph500 (a, b, c) = (.57, .19, .19),
+    # U[0,1) weights, permuted labels.  er: uniform raw pairs (the C1 family,
+    # BASELINE config C1 at 256x), unit weights.
+    "rmat26": ("rmat", 26, 16), "rmat25": ("rmat", 25, 16), "rmat24": ("rmat", 24, 16),
+    "rmat22": ("rmat", 22, 16), "rmat20": ("rmat", 20, 16), "rmat16": ("rmat", 16, 16),
+    "er24unit": ("er", 24, 4), "er20unit": ("er", 20, 4),
 }
+
+
+def generate(eng, workload: str):
+    fam, scale, ef = WORKLOADS[workload]
+    if fam == "rmat":
+        eng.gen_rmat(scale, ef, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
+        return f"RMAT scale {scale} edge factor {ef}"
+    eng.gen_er(scale, ef, seed=GRAPH_SEED, unit=True)
+    return f"random graph 2^{scale} vertices, {ef} * 2^{scale} uniform raw pairs, unit weights (C1 family)"
 RMAT_ABC = (0.57, 0.19, 0.19)
 GRAPH_SEED = 1
 MATCH_SEED = 1
@@ -124,12 +137,16 @@ def rmat_floor_bytes(rounds):
     return 32 * (2 * S - m0), S, m0
 
 
-def cpu_sample_graph(scale: int):
-    """RMAT sample of the same recipe, generated on the host by the oracle's C
+def cpu_sample_graph(scale: int, family: str = "rmat", ef: int = 16):
+    """A sample of the same recipe, generated on the host by the oracle's C
     restatement of the device generator + build_graph (test infrastructure,
     used here only to make the CPU arm's input)."""
     from oracle import oracle as O
-    u, v, w = O.c_rmat_raw(scale, 16, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
+    if family == "er":
+        u, v, w = O.c_rmat_raw(scale, ef, 0.25, 0.25, 0.25, seed=GRAPH_SEED, permute=False)
+        w[:] = 1.0
+    else:
+        u, v, w = O.c_rmat_raw(scale, ef, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
     return O.c_build_graph(u, v, w, 1 << scale)
 
 
@@ -186,7 +203,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     scale = args.cpu_sample_scale
-    n, eu, ev, w = cpu_sample_graph(scale)
+    fam, _, ef = WORKLOADS[args.workload]
+    n, eu, ev, w = cpu_sample_graph(scale, fam, ef)
     m = int(eu.size)
     ref = import_reference()
     if ref is not None:
@@ -208,7 +226,9 @@ def run_reference(args):
     dt = sum(times)
     value = m * args.steps / dt
     rounds = len(res[1].rounds) if kind == "reference" else len(res.rounds)
-    sample = (f"RMAT-{scale} ef16 (a,b,c)={RMAT_ABC} graph seed {GRAPH_SEED} permuted, n={n}, m={m}; "
+    recipe = f"RMAT-{scale} ef{ef} (a,b,c)={RMAT_ABC} graph seed {GRAPH_SEED} permuted" if fam == "rmat" else \
+        f"random graph 2^{scale}, {ef} * 2^{scale} uniform pairs, unit weights, graph seed {GRAPH_SEED}"
+    sample = (f"{recipe}, n={n}, m={m}; "
               f"{args.steps} timed calls of {what}, match seed {MATCH_SEED}; 1 of {os.cpu_count()} host "
               f"cores ({cpu_model()}); the path is single-threaded numpy")
     line = {
@@ -216,8 +236,8 @@ def run_reference(args):
         "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1000 / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"rmat{scale}-sample-of-{args.workload}", "scale": scale,
-                   "edge_factor": 16, "rmat_abc": list(RMAT_ABC), "n": n, "m": m,
+        "config": {"workload": f"{fam}{scale}-sample-of-{args.workload}", "scale": scale,
+                   "edge_factor": ef, "n": n, "m": m,
                    "rounds": rounds, "parallelism": "1 host core"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": kind, "sample": sample,
                          "best_s": min(times), "cpu_model": cpu_model()},
@@ -227,12 +247,12 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline_leg(scale: int, reps: int = 3):
+def cpu_baseline_leg(scale: int, reps: int = 3, family: str = "rmat", ef: int = 16):
     """The reference's local_max_seq (baseline/_ref; else the oracle's numpy
     port) on a bounded RMAT sample, best of `reps`, and the
     GPU result on the same sample checked identical to it."""
     from paper_1302_4587_b200 import Engine, Graph
-    n, eu, ev, w = cpu_sample_graph(scale)
+    n, eu, ev, w = cpu_sample_graph(scale, family, ef)
     ref = import_reference()
     if ref is not None:
         lg, lm = ref
@@ -265,7 +285,7 @@ def cpu_baseline_leg(scale: int, reps: int = 3):
         "the oracle's numpy port of local_max_seq (baseline/_ref not installed)"
     return {
         "value": eu.size / best, "unit": "edges/s", "cores": 1, "kind": kind,
-        "sample": (f"RMAT-{scale} ef16 same recipe (n={n}, m={eu.size}); best of {reps} calls of {what}; "
+        "sample": (f"{family}-{scale} ef{ef} same recipe (n={n}, m={eu.size}); best of {reps} calls of {what}; "
                    f"1 of {os.cpu_count()} host cores used ({cpu_model()}); GPU result identical on this "
                    f"sample: {same}"),
         "best_s": best, "cpu_model": cpu_model(), "parity_on_sample": same,
@@ -300,9 +320,11 @@ def run_b200_dist(args):
     comm = TorchComm()
     comm.bind_device(dev)
     stream = torch.cuda.current_stream()
-    scale = WORKLOADS[args.workload]
+    fam, scale, ef = WORKLOADS[args.workload]
+    if fam != "rmat":
+        raise SystemExit("the partitioned bench runs the RMAT workloads")
     me = DistRank(None, world, rank, local, stream.cuda_stream,
-                  rmat=dict(scale=scale, edge_factor=16, a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2],
+                  rmat=dict(scale=scale, edge_factor=ef, a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2],
                             seed=GRAPH_SEED, permute=True))
     n, m = me.n, me.m
     for _ in range(args.warmup):
@@ -438,11 +460,11 @@ def run_b200(args):
         return run_b200_dist(args)
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    scale = WORKLOADS[args.workload]
+    fam, scale, ef = WORKLOADS[args.workload]
 
     eng = Engine(local)
     eng.set_stream(stream.cuda_stream)
-    eng.gen_rmat(scale, 16, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
+    graph_desc = generate(eng, args.workload)
     gen_setup_ms = eng.last_timing()["setup_ms"]
     n, m = eng.graph_size()
 
@@ -533,14 +555,28 @@ def run_b200(args):
         kern = {"probe": (by["probe"], rk_ms), "match": (by["match"], mk_ms), "hist+edge_bits": (by["hist"], hk_ms)}
         step_bytes = by["probe"] + by["match"] + by["hist"]
     else:
-        B_floor, S, m0 = rmat_floor_bytes(rounds)
-        gbs = B_floor / (rk_ms / 1000.0) / 1e9 if rk_ms > 0 else None
+        # compacting loop, 8-byte slots {nbr, id} (UNIFORM / DISTINCT layouts):
+        # every live slot read once and every surviving slot written once per
+        # round, 16 (m_r + m_{r+1}) bytes; the match kernel 16 B per listed
+        # vertex (list, own and partner candidate, survivor append) + 12 B per
+        # matched vertex, listed vertices ~ live vertices <= live slots
+        S = sum(r.edges_before for r in rounds)
+        m0 = rounds[0].edges_before if rounds else 0
+        B_round = 16 * (2 * S - m0)
+        ctr = eng.last_round_counters()
+        listed = int(sum(int(sum(c[3:8])) for c in ctr))
+        mv = int(sum(int(c[2]) for c in ctr))
+        B_match = 16 * listed + 12 * mv
+        gbs = B_round / (rk_ms / 1000.0) / 1e9 if rk_ms > 0 else None
         roofline = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
-                    "frac": gbs / peak if gbs else None, "traffic": None,
-                    "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds)",
-                    "algorithmic_bytes_per_step": B_floor, "kernel_ms_per_step": rk_ms, "peak_source": src}
-        kern = {"round": (B_floor, rk_ms), "match": (0, mk_ms)}
-        step_bytes = B_floor
+                    "frac": gbs / peak if gbs else None,
+                    "traffic": traffic.get("bytes_per_launch") if traffic and traffic.get("kernel") ==
+                    "lmx_round_kernel" else None,
+                    "kernel": "lmx_round_kernel (fused kill+compact+argmax, all rounds; 8-byte slots)",
+                    "algorithmic_bytes_per_step": B_round, "kernel_ms_per_step": rk_ms, "peak_source": src,
+                    "byte_model": "16 (2 S - m0), S = sum_r m_r: each live slot (8 B) read, each survivor written"}
+        kern = {"round": (B_round, rk_ms), "match": (B_match, mk_ms)}
+        step_bytes = B_round + B_match
     step_gbs = step_bytes / (ms_per_step / 1000.0) / 1e9
     step_roofline = {
         "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
@@ -598,16 +634,17 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline:
         eng.close()
-        cpu = cpu_baseline_leg(args.cpu_baseline_scale)
+        cpu = cpu_baseline_leg(args.cpu_baseline_scale, family=fam, ef=ef)
 
     line = {
         "metric": "input edges/s to full local max maximal matching", "value": value,
         "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor 16",
-                   "rmat_abc": list(RMAT_ABC), "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
-                   "permuted_labels": True, "n": n, "m": m, "rounds": len(rounds),
+        "config": {"workload": args.workload, "graph": graph_desc,
+                   "rmat_abc": list(RMAT_ABC) if fam == "rmat" else [0.25, 0.25, 0.25],
+                   "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
+                   "permuted_labels": fam == "rmat", "n": n, "m": m, "rounds": len(rounds),
                    "matched_edges": n_matched, "round_loop": algo, "parallelism": "dp1",
                    "l2": "inputs larger than L2 (slot records %.1f GB >> 126 MB)" % (2 * m * 8 / 1e9)},
         "parity": parity,

@@ -169,6 +169,13 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
 int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                  uint64_t seed, int permute);
 
+/* G(n, m)-style random graph, the C1 family at scale (generate.py:48-89 idea;
+ * BASELINE config C1 is n = 2^16, m = 4n, unit weights): edge_factor * 2^scale
+ * uniform raw pairs (the RMAT generator with a = b = c = d = 1/4, no
+ * relabelling), weights 1.0 if unit_weights else U[0,1), then build_graph
+ * semantics.  Loads the result. */
+int lmx_gen_er(lmx_ctx *ctx, int scale, int edge_factor, uint64_t seed, int unit_weights);
+
 /* Raw RMAT triples only (no build), for oracle parity of the generator. */
 int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                      uint64_t seed, int permute, int64_t *u_out, int64_t *v_out,

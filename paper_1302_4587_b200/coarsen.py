@@ -40,6 +40,7 @@ class Level:
     rounds: list = field(default_factory=list)
     mate: np.ndarray | None = None        # host copy when keep_mates=True
     match_ms: float = 0.0                 # device round loop of this level
+    stage_ms: dict = field(default_factory=dict)   # profile=True: synchronised stage times
 
 
 def _bind(lib):
@@ -77,7 +78,8 @@ def mesh(side: int, seed: int = 0, engine: Engine | None = None):
 
 
 def coarsen(n: int, eu, ev, w, seed: int = 0, min_n: int = 1024, min_shrink: float = 0.05,
-            max_levels: int = 64, keep_mates: bool = False, engine: Engine | None = None):
+            max_levels: int = 64, keep_mates: bool = False, engine: Engine | None = None,
+            profile: bool = False):
     """Coarsen the device graph (eu, ev int64 / w float64 CUDA tensors).
 
     Returns ``(levels, (n_coarse, m_coarse))``.  ``levels[i]`` describes the
@@ -89,30 +91,54 @@ def coarsen(n: int, eu, ev, w, seed: int = 0, min_n: int = 1024, min_shrink: flo
     lib = eng._lib
     dev = eu.device
     c = torch.ones(n, dtype=torch.float64, device=dev)
+    c0 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)   # node weights, ping-pong with buf["cc"]
     levels = []
+    marks = {}
+
+    def mark(name):
+        if profile:
+            torch.cuda.synchronize()
+            marks[name] = time.perf_counter()
+
+    # Level-0-sized buffers, reused by every level (coarse graphs only shrink):
+    # one allocation set per call instead of one per level
+    m0, n0 = int(eu.numel()), n
+    buf = {k: torch.empty(max(sz, 1), dtype=dt, device=dev) for k, sz, dt in (
+        ("r", m0, torch.float64), ("mate", n0, torch.int64), ("ids", n0 // 2 + 1, torch.int64),
+        ("cid", n0, torch.int64), ("cc", n0, torch.float64))}
+    side = [{k: torch.empty(max(m0, 1), dtype=dt, device=dev) for k, dt in
+             (("eu", torch.int64), ("ev", torch.int64), ("w", torch.float64))} for _ in range(2)]
     for lvl in range(max_levels):
+        mark("start")
         m = int(eu.numel())
-        r = torch.empty(m, dtype=torch.float64, device=dev)
+        r = buf["r"][:m]
         _chk(eng, lib.lmx_ratings(eng._h, m, eu.data_ptr(), ev.data_ptr(), w.data_ptr(), c.data_ptr(),
                                   r.data_ptr()), "lmx_ratings")
+        mark("ratings")
         eng.load_graph_device(n, eu, ev, r)
-        mate = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-        ids = torch.empty(max(n // 2 + 1, 1), dtype=torch.int64, device=dev)
+        mark("load")
+        mate = buf["mate"][: max(n, 1)]
+        ids = buf["ids"][: max(n // 2 + 1, 1)]
         matched = eng.match_device(seed + lvl, mate, ids)
+        mark("match")
         lev = Level(n, m, matched, eng.last_rounds(), match_ms=eng.last_timing()["rounds_ms"])
         if keep_mates:
             lev.mate = mate[:n].cpu().numpy()
         levels.append(lev)
-        cid = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-        ceu = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
-        cev = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
-        cw = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
-        cc = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        out = side[lvl & 1]
+        cid = buf["cid"][: max(n, 1)]
+        ceu, cev, cw = out["eu"], out["ev"], out["w"]
+        cc = (buf["cc"] if lvl % 2 == 0 else c0)[: max(n, 1)]
         nc = ctypes.c_int64()
         mc = ctypes.c_int64()
         _chk(eng, lib.lmx_contract(eng._h, n, m, eu.data_ptr(), ev.data_ptr(), w.data_ptr(), c.data_ptr(),
                                    mate.data_ptr(), cid.data_ptr(), ctypes.byref(nc), ctypes.byref(mc),
                                    ceu.data_ptr(), cev.data_ptr(), cw.data_ptr(), cc.data_ptr()), "lmx_contract")
+        mark("contract")
+        if profile:
+            names = ["start", "ratings", "load", "match", "contract"]
+            lev.stage_ms = {b: (marks[b] - marks[a]) * 1e3 for a, b in zip(names, names[1:])}
+            lev.stage_ms["algo"] = {"scan": 1.0, "compact": 0.0}[eng.algo()]
         shrink_ok = (n - nc.value) >= min_shrink * n
         n, eu, ev, w, c = nc.value, ceu[: mc.value], cev[: mc.value], cw[: mc.value], cc[: nc.value]
         if n < min_n or not shrink_ok:

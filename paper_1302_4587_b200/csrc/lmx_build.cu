@@ -184,6 +184,12 @@ __global__ void k_emit(const unsigned long long *key, const uint32_t *idx, unsig
     }
 }
 
+__global__ void k_fill_ones(double *w, unsigned long long k) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride)
+        w[i] = 1.0;
+}
+
 __global__ void k_export(const uint32_t *eu, const uint32_t *ev, unsigned long long m, long long *u,
                          long long *v) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -351,6 +357,37 @@ int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, d
     LMX_CUDA(ctx, cudaGetLastError());
     LMX_TRY(build_from_raw(ctx, ru, rv, rw, k, 1LL << scale));
     lmx_flush_cache(ctx);   // the raw-build temporaries will not be reused
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->timing.setup_ms = ms;
+    return LMX_OK;
+}
+
+// G(n, m)-style random graph (the C1 family, generate.py:48-89, scaled up):
+// k = edge_factor * 2^scale uniform raw pairs from the RMAT generator with
+// a = b = c = d = 1/4, weights 1.0 (unit) or the generator's U[0,1), then
+// build_graph semantics (self-loops dropped, duplicates collapsed).
+int lmx_gen_er(lmx_ctx *ctx, int scale, int edge_factor, uint64_t seed, int unit_weights) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    LMX_TRY(rmat_check(ctx, scale, edge_factor, 0.25, 0.25, 0.25));
+    const unsigned long long k = (unsigned long long)edge_factor << scale;
+    const RmatParams p = rmat_params(scale, 0.25, 0.25, 0.25, seed, 0);
+    lmx_free_graph(ctx);
+    uint32_t *ru = nullptr, *rv = nullptr;
+    double *rw = nullptr;
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ru, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rv, k * 4));
+    LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&rw, k * 8));
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    k_rmat_raw<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(p, k, ru, rv, rw);
+    if (unit_weights) k_fill_ones<<<bgrid(ctx, k), kBlock, 0, ctx->stream>>>(rw, k);
+    LMX_CUDA(ctx, cudaGetLastError());
+    LMX_TRY(build_from_raw(ctx, ru, rv, rw, k, 1LL << scale));
+    lmx_flush_cache(ctx);
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
     float ms = 0.f;

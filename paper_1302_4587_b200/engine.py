@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times", "lmx_last_round_counters",
     "lmx_local_max",
-    "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_graph_size",
+    "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_gen_er", "lmx_graph_size",
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH):
                                      ctypes.c_double, u64, c_int]),
             "lmx_gen_rmat_raw": (c_int, [p, c_int, c_int, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, u64, c_int, p, p, p, c_int]),
+            "lmx_gen_er": (c_int, [p, c_int, c_int, u64, c_int]),
             "lmx_graph_size": (c_int, [p, p, p]),
             "lmx_graph_export": (c_int, [p, p, p, p, c_int]),
             "lmx_device_bytes": (i64, [p]),
@@ -202,6 +203,12 @@ class Engine:
                  c: float = 0.19, seed: int = 1, permute: bool = True) -> None:
         self._check(self._lib.lmx_gen_rmat(self._h, scale, edge_factor, a, b, c, seed & _UINT64_MASK,
                                            int(permute)), "lmx_gen_rmat")
+
+    def gen_er(self, scale: int, edge_factor: int = 4, seed: int = 1, unit: bool = True) -> None:
+        """Random graph of the C1 family at scale: edge_factor * 2^scale uniform
+        raw pairs, unit (or U[0,1)) weights, build_graph semantics (lmx_gen_er)."""
+        self._check(self._lib.lmx_gen_er(self._h, scale, edge_factor, seed & _UINT64_MASK, int(bool(unit))),
+                    "lmx_gen_er")
 
     def gen_rmat_raw(self, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
                      c: float = 0.19, seed: int = 1, permute: bool = True):

@@ -29,6 +29,8 @@ Configs (BASELINE.json configs / north_star):
   rgg22   C2: gen_rgg(22, seed=0, "euclidean") (generate.py:113-143), match seed 0
   rmat24  C3: RMAT scale 24 ef 16 (.57,.19,.19), graph seed 1, permuted; match seed 1
   rmat26  N*: RMAT scale 26, same recipe (the bench workload)
+  er24unit C1 family at 256x: 4 * 2^24 uniform raw pairs (the RMAT generator
+          with a = b = c = 1/4, no relabelling), unit weights; seed 1
 """
 
 from __future__ import annotations
@@ -118,6 +120,21 @@ def make_rmat(scale, ref):
     return rec
 
 
+def make_er24unit(ref):
+    t0 = time.time()
+    u, v, w = O.c_rmat_raw(24, 4, 0.25, 0.25, 0.25, seed=1, permute=False)
+    w[:] = 1.0
+    n, eu, ev, ew = O.c_build_graph(u, v, w, 1 << 24)
+    del u, v, w
+    gc.collect()
+    print(f"er24unit: generated + built in {time.time() - t0:.1f}s", flush=True)
+    rec, res = summarise("er24unit", n, eu, ev, ew, 1, graph_seed=1, permuted=False,
+                         recipe="4 * 2^24 uniform pairs (RMAT a=b=c=1/4), unit weights")
+    if ref:
+        check_reference("er24unit", n, eu, ev, ew, 1, rec, res)
+    return rec
+
+
 def make_rgg22(ref):
     t0 = time.time()
     n, eu, ev, w = O.gen_rgg(22, 0, "euclidean")
@@ -153,6 +170,8 @@ def main():
     for name in args.configs.split(","):
         if name == "rgg22":
             out[name] = make_rgg22(bool(args.reference))
+        elif name == "er24unit":
+            out[name] = make_er24unit(bool(args.reference))
         elif name.startswith("rmat"):
             out[name] = make_rmat(int(name[4:]), bool(args.reference))
         else:

@@ -69,3 +69,14 @@ def test_rgg22_c2_bit_exact(engine):
     engine.load_graph(g)
     mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
     _check(want, g, mate, ids, rounds)
+
+
+def test_er24_unit_weights_bit_exact(engine):
+    """The C1 family at 256x (bench workload er24unit): unit weights, so the
+    salts decide every round -- the compacting loop; pinned to the unmodified
+    local_max_seq when the fixture was made."""
+    want = SCALE["er24unit"]
+    engine.gen_er(24, 4, seed=want["graph_seed"], unit=True)
+    assert engine.algo() == "compact" and engine.layout() == "uniform"
+    mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
+    _check(want, engine.export_graph(), mate, ids, rounds)

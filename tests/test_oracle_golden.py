@@ -156,14 +156,14 @@ def test_scale_fixtures_are_consistent():
     import os
     with open(os.path.join(os.path.dirname(__file__), "golden", "scale.json")) as f:
         sc = json.load(f)
-    for name in ("rgg22", "rmat24", "rmat26"):
+    for name in ("rgg22", "rmat24", "rmat26", "er24unit"):
         rec = sc[name]
         assert {"n", "m", "edges", "mate", "ids", "rounds", "weight", "matched"} <= set(rec)
         assert rec["rounds"][0][0] == rec["m"]
         assert sum(r[1] for r in rec["rounds"]) == rec["matched"]
         assert sum(r[2] for r in rec["rounds"]) == rec["m"]
     assert sc["rgg22"].get("reference_checked") and sc["rgg22"].get("generator_checked")
-    assert sc["rmat24"].get("reference_checked")
+    assert sc["rmat24"].get("reference_checked") and sc["er24unit"].get("reference_checked")
 
 
 def test_bsp_messages_match_reference():
