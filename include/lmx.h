@@ -176,6 +176,16 @@ int lmx_gen_rmat(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, d
  * semantics.  Loads the result. */
 int lmx_gen_er(lmx_ctx *ctx, int scale, int edge_factor, uint64_t seed, int unit_weights);
 
+/* gen_rgg(x, seed, weight_mode) (generate.py:113-143, radius_edges_grid
+ * :146-197, _morton_order :97-110) on the device, the identical edge list:
+ * 2^x points from numpy's PCG64 whose initial 128-bit state and increment
+ * (default_rng(seed).bit_generator.state) the caller passes in halves;
+ * radius = rgg_threshold(n) (generate.py:92-94, computed by the caller);
+ * weight_random 0: Euclidean distances, 1: the next rng.random(m) draws.
+ * Loads the result. */
+int lmx_gen_rgg(lmx_ctx *ctx, int x, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                double radius, int weight_random);
+
 /* Raw RMAT triples only (no build), for oracle parity of the generator. */
 int lmx_gen_rmat_raw(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                      uint64_t seed, int permute, int64_t *u_out, int64_t *v_out,

@@ -9,7 +9,7 @@ point ``local_max_b200`` (the ``local_max_seq`` contract,
 ``csrc/`` behind the C ABI in ``include/lmx.h``.
 """
 
-from .builders import build_graph, gen_rmat
+from .builders import build_graph, gen_rgg, gen_rmat
 from .engine import (Engine, RbmDidNotConverge, default_engine, load_library, local_max_b200, pram_local_max_b200,
                      rbm_b200, run_matcher)
 from .graph import (
@@ -28,7 +28,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Engine", "Graph", "Matching", "MatchingCheck", "PhaseTrace", "RoundStats",
-    "build_graph", "default_engine", "gen_rmat", "load_library", "local_max", "local_max_b200",
+    "build_graph", "default_engine", "gen_rgg", "gen_rmat", "load_library", "local_max", "local_max_b200",
     "matching_from_edge_ids", "run_matcher", "validate_matching", "rbm_b200", "RbmDidNotConverge",
     "pram_local_max_b200",
 ]

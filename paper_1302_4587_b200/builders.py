@@ -45,3 +45,13 @@ def gen_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19
     eng = engine or default_engine(0)
     eng.gen_rmat(scale, edge_factor, a, b, c, seed, permute)
     return eng.export_graph() if export else None
+
+
+def gen_rgg(x: int, seed: int, weight_mode: str = "euclidean", engine: Engine | None = None,
+            export: bool = True) -> Graph | None:
+    """``locmax.gen_rgg`` (generate.py:113-143) on the device -- the identical
+    graph (points, Morton numbering, edge order, weights).  Loads it into
+    ``engine``; optionally exports it to host."""
+    eng = engine or default_engine(0)
+    eng.gen_rgg(x, seed, weight_mode)
+    return eng.export_graph() if export else None

@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "lmx_abi_version", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_set_stream",
     "lmx_load_graph", "lmx_match", "lmx_last_timing", "lmx_last_rounds", "lmx_last_kernel_times", "lmx_last_round_counters",
     "lmx_local_max",
-    "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_gen_er", "lmx_graph_size",
+    "lmx_build_graph", "lmx_gen_rmat", "lmx_gen_rmat_raw", "lmx_gen_er", "lmx_gen_rgg", "lmx_graph_size",
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_gen_rmat_raw": (c_int, [p, c_int, c_int, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, u64, c_int, p, p, p, c_int]),
             "lmx_gen_er": (c_int, [p, c_int, c_int, u64, c_int]),
+            "lmx_gen_rgg": (c_int, [p, c_int, u64, u64, u64, u64, ctypes.c_double, c_int]),
             "lmx_graph_size": (c_int, [p, p, p]),
             "lmx_graph_export": (c_int, [p, p, p, p, c_int]),
             "lmx_device_bytes": (i64, [p]),
@@ -209,6 +210,24 @@ class Engine:
         raw pairs, unit (or U[0,1)) weights, build_graph semantics (lmx_gen_er)."""
         self._check(self._lib.lmx_gen_er(self._h, scale, edge_factor, seed & _UINT64_MASK, int(bool(unit))),
                     "lmx_gen_er")
+
+    def gen_rgg(self, x: int, seed: int, weight_mode: str = "euclidean") -> None:
+        """``gen_rgg(x, seed, weight_mode)`` (generate.py:113-143) on the device:
+        the identical graph.  numpy's SeedSequence supplies the PCG64 start
+        state (a few integers); every draw, the Morton order, the grid sweep
+        and the distances run on the GPU (lmx_gen_rgg)."""
+        import math
+        if x < 2:
+            raise ValueError("x must be >= 2")
+        if weight_mode not in ("euclidean", "random"):
+            raise ValueError(f"weight_mode must be euclidean or random, got {weight_mode!r}")
+        st = np.random.default_rng(seed).bit_generator.state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        n = 1 << x
+        radius = 0.55 * math.sqrt(math.log(n) / n)   # rgg_threshold, generate.py:92-94
+        m64 = (1 << 64) - 1
+        self._check(self._lib.lmx_gen_rgg(self._h, x, s >> 64, s & m64, inc >> 64, inc & m64, radius,
+                                          int(weight_mode == "random")), "lmx_gen_rgg")
 
     def gen_rmat_raw(self, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
                      c: float = 0.19, seed: int = 1, permute: bool = True):

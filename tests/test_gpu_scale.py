@@ -80,3 +80,28 @@ def test_er24_unit_weights_bit_exact(engine):
     assert engine.algo() == "compact" and engine.layout() == "uniform"
     mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
     _check(want, engine.export_graph(), mate, ids, rounds)
+
+
+@pytest.mark.parametrize("name,x,seed,mode", [("rgg-x16-euclidean-s0", 16, 0, "euclidean"),
+                                               ("rgg-x12-random-s3", 12, 3, "random")])
+def test_device_rgg_generator_equals_reference(engine, golden_instances, name, x, seed, mode):
+    """lmx_gen_rgg reproduces the unmodified reference's gen_rgg graph (the
+    reference's edge-array digest in tests/golden/instances.npz) and its
+    matching."""
+    from conftest import edges_digest, mate_digest
+    z = golden_instances
+    engine.gen_rgg(x, seed, mode)
+    g = engine.export_graph()
+    assert g.num_vertices == int(z[f"{name}/n"]) and g.num_edges == int(z[f"{name}/m"])
+    assert edges_digest(g.edge_u, g.edge_v, g.edge_weight) == str(z[f"{name}/edges_sha"])
+    mate, ids, rounds = engine.match_raw(int(z[f"{name}/seed"]), bool(z[f"{name}/rerandomize"]))
+    assert mate_digest(mate) == str(z[f"{name}/mate_digest"])
+
+
+def test_device_rgg22_c2(engine):
+    """BASELINE config C2 built on the device: the graph the reference's
+    gen_rgg(22, 0) builds (scale.json, generator_checked), and its matching."""
+    want = SCALE["rgg22"]
+    engine.gen_rgg(22, want["graph_seed"], "euclidean")
+    mate, ids, rounds = engine.match_raw(want["seed"], want["rerandomize"])
+    _check(want, engine.export_graph(), mate, ids, rounds)

@@ -1,6 +1,6 @@
 """Per-round kernel durations and device counters of one match on an RMAT graph.
 
-usage: python tools/round_profile.py [scale] [auto|compact|scan]
+usage: python tools/round_profile.py [scale] [auto|compact|scan] [rmat|er]
 """
 import os
 import sys
@@ -14,7 +14,10 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 eng = Engine(0)
 if len(sys.argv) > 2:
     eng.set_algo(sys.argv[2])
-eng.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
+if len(sys.argv) > 3 and sys.argv[3] == "er":
+    eng.gen_er(scale, 4, seed=1, unit=True)
+else:
+    eng.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
 n, m = eng.graph_size()
 setup_ms = eng.last_timing()["setup_ms"]
 mate = torch.empty(n, dtype=torch.int64, device="cuda")
