@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .engine import LMX_OK, Engine, _raise
+from .engine import LMX_OK, Engine, _raise, default_engine
 
 
 @dataclass
@@ -65,7 +65,7 @@ def _chk(eng, rc, what):
 def mesh(side: int, seed: int = 0, engine: Engine | None = None):
     """side x side jittered-grid triangulation on the device: (n, eu, ev, w) CUDA tensors."""
     import torch
-    eng = engine or Engine(0)
+    eng = engine or default_engine(0)
     _bind(eng._lib)
     m_cap = (side - 1) * (3 * side - 1)
     eu = torch.empty(m_cap, dtype=torch.int64, device="cuda")
@@ -86,7 +86,7 @@ def coarsen(n: int, eu, ev, w, seed: int = 0, min_n: int = 1024, min_shrink: flo
     matching of level i; the last contraction's result is the coarsest graph.
     """
     import torch
-    eng = engine or Engine(0)
+    eng = engine or default_engine(0)
     _bind(eng._lib)
     lib = eng._lib
     dev = eu.device
@@ -108,6 +108,7 @@ def coarsen(n: int, eu, ev, w, seed: int = 0, min_n: int = 1024, min_shrink: flo
         ("cid", n0, torch.int64), ("cc", n0, torch.float64))}
     side = [{k: torch.empty(max(m0, 1), dtype=dt, device=dev) for k, dt in
              (("eu", torch.int64), ("ev", torch.int64), ("w", torch.float64))} for _ in range(2)]
+    torch.cuda.synchronize(dev)   # the buffers above come from torch's stream; the engine runs on its own
     for lvl in range(max_levels):
         mark("start")
         m = int(eu.numel())
@@ -148,7 +149,9 @@ def coarsen(n: int, eu, ev, w, seed: int = 0, min_n: int = 1024, min_shrink: flo
 
 def coarsen_mesh(side: int = 4096, seed: int = 0, **kw):
     """Config C4: coarsen the side x side mesh (2^24 vertices at side 4096)."""
-    eng = kw.pop("engine", None) or Engine(0)
+    # the process-wide engine (as local_max_b200 uses): its device block cache
+    # serves every level's buffers after the first call
+    eng = kw.pop("engine", None) or default_engine(0)
     t0 = time.perf_counter()
     n, eu, ev, w = mesh(side, seed, eng)
     levels, final = coarsen(n, eu, ev, w, seed=seed, engine=eng, **kw)

@@ -1,13 +1,14 @@
-"""Run every BASELINE.json config through the B200 engine: device time per
-matching, round loop used, and parity with the oracle where the CPU side
-finishes in seconds.  Writes one JSON object (profiles/r1_configs.json).
+"""Every BASELINE.json config through the B200 engine: device time per
+matching, round loop used, parity with the reference digests.  Writes one
+JSON object to stdout (profiles/r2_configs.json).
 
-C1 ER n=2^16 avg degree 8, unit weights   -> parity vs oracle (C restatement)
-C2 RGG n=2^22, Euclidean weights          -> parity vs oracle (C restatement)
-C3 RMAT-24 ef16, random weights           -> device timing, validate on GPU
-C4 mesh 2^24 coarsening                   -> levels, end-to-end time
-(N* RMAT-26 is bench.py's workload; C5 RMAT-28 needs 8 GPUs.)
+C1  ER n=2^16 avg degree 8, unit weights (gen_random(2^16, 4, 0)) -> vs oracle
+C2  RGG n=2^22, Euclidean weights, seed 0, DEVICE generator -> scale.json digests
+C3  RMAT-24 ef16 -> scale.json digests (pinned to the unmodified local_max_seq)
+C4  mesh 2^24 coarsening -> levels, end-to-end (cold and warm)
+(N* RMAT-26 is bench.py's workload; C5 RMAT-28 needs 2-8 GPUs.)
 """
+import hashlib
 import json
 import os
 import sys
@@ -15,73 +16,91 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_1302_4587_b200 import Engine, Graph  # noqa: E402
 from paper_1302_4587_b200.coarsen import coarsen_mesh  # noqa: E402
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCALE = json.load(open(os.path.join(ROOT, "tests", "golden", "scale.json")))
 
-def timed_match(eng, g, seed, reps=5):
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").data).hexdigest()
+
+
+def best_device_ms(eng, seed, rr=True, reps=5):
+    n, _ = eng.graph_size()
+    mate = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    ids = torch.empty(max(n // 2 + 1, 1), dtype=torch.int64, device="cuda")
     best = None
     for _ in range(reps):
-        m, tr = eng.match(g, seed, True)
-        best = tr.device_millis if best is None else min(best, tr.device_millis)
-    return m, tr, best
+        eng.match_device(seed, mate, ids, rr)
+        t = eng.last_timing()["rounds_ms"]
+        best = t if best is None else min(best, t)
+    return best
+
+
+def digest_check(eng, want):
+    mate, ids, rounds = eng.match_raw(want["seed"], want["rerandomize"])
+    return (sha(mate) == want["mate"] and sha(ids) == want["ids"]
+            and [[r.edges_before, r.edges_matched, r.edges_removed] for r in rounds] == want["rounds"])
 
 
 def main():
     out = {}
     eng = Engine(0)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
     # C1
-    n, eu, ev, w = O.gen_random(1 << 16, 4, 1, unit=True)
+    n, eu, ev, w = O.gen_random(1 << 16, 4, 0, unit=True)
     g = Graph(n, eu, ev, w)
     eng.load_graph(g)
-    m, tr, ms = timed_match(eng, g, 1)
-    ref = O.c_local_max(n, eu, ev, w, 1, True)
+    ms = best_device_ms(eng, 0)
+    mate, ids, rounds = eng.match_raw(0, True)
+    ref = O.c_local_max(n, eu, ev, w, 0, True)
     out["C1_er16_unit"] = {"n": n, "m": int(eu.size), "layout": eng.layout(), "round_loop": eng.algo(),
-                           "rounds": len(tr.rounds), "device_ms": ms,
-                           "parity": bool(np.array_equal(np.asarray(m.mate), ref.mate))}
-    print(out["C1_er16_unit"], flush=True)
-    # C2
+                           "rounds": len(rounds), "device_ms": ms,
+                           "parity": bool(np.array_equal(mate, ref.mate))}
+    print(out["C1_er16_unit"], file=sys.stderr, flush=True)
+    # C2 on the device generator
+    want = SCALE["rgg22"]
+    torch.cuda.synchronize()
     t = time.perf_counter()
-    n, eu, ev, w = O.gen_rgg(22, 1)
-    gen_s = time.perf_counter() - t
-    g = Graph(n, eu, ev, w)
-    eng.load_graph(g)
-    setup = eng.last_timing()["setup_ms"]
-    m, tr, ms = timed_match(eng, g, 1)
-    t = time.perf_counter()
-    ref = O.c_local_max(n, eu, ev, w, 1, True)
-    cpu_s = time.perf_counter() - t
-    out["C2_rgg22"] = {"n": n, "m": int(eu.size), "layout": eng.layout(), "round_loop": eng.algo(),
-                       "rounds": len(tr.rounds), "device_ms": ms, "setup_ms": setup,
-                       "edges_per_s": eu.size / (ms / 1e3), "host_generation_s": gen_s,
-                       "oracle_c_s": cpu_s, "parity": bool(np.array_equal(np.asarray(m.mate), ref.mate)) and
-                       [(r.edges_before, r.edges_matched, r.edges_removed) for r in tr.rounds] == ref.rounds}
-    print(out["C2_rgg22"], flush=True)
+    eng.gen_rgg(22, want["graph_seed"], "euclidean")
+    torch.cuda.synchronize()
+    gen_ms = (time.perf_counter() - t) * 1e3
+    n, m = eng.graph_size()
+    ms = best_device_ms(eng, want["seed"])
+    out["C2_rgg22_seed0"] = {"n": n, "m": m, "layout": eng.layout(), "round_loop": eng.algo(),
+                             "device_ms": ms, "edges_per_s": m / (ms / 1e3), "device_generation_ms": gen_ms,
+                             "parity_vs_reference_digests": digest_check(eng, want)}
+    print(out["C2_rgg22_seed0"], file=sys.stderr, flush=True)
     # C3
-    eng.gen_rmat(24, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
-    gr = eng.export_graph()
-    m, tr, ms = timed_match(eng, gr, 1)
-    chk, weight = eng.validate(m)
-    out["C3_rmat24"] = {"n": gr.num_vertices, "m": int(np.asarray(gr.edge_u).size), "layout": eng.layout(),
-                        "round_loop": eng.algo(), "relabeled": eng.relabeled(), "rounds": len(tr.rounds),
-                        "device_ms": ms, "edges_per_s": np.asarray(gr.edge_u).size / (ms / 1e3),
-                        "valid": chk.valid, "maximal": chk.maximal, "weight": weight}
-    print(out["C3_rmat24"], flush=True)
-    del gr
+    want = SCALE["rmat24"]
+    eng.gen_rmat(24, 16, 0.57, 0.19, 0.19, seed=want["graph_seed"], permute=True)
+    n, m = eng.graph_size()
+    ms = best_device_ms(eng, want["seed"])
+    out["C3_rmat24"] = {"n": n, "m": m, "layout": eng.layout(), "round_loop": eng.algo(),
+                        "relabeled": eng.relabeled(), "device_ms": ms, "edges_per_s": m / (ms / 1e3),
+                        "parity_vs_reference_digests": digest_check(eng, want)}
+    print(out["C3_rmat24"], file=sys.stderr, flush=True)
     eng.close()
-    # C4
-    levels, final, total_ms = coarsen_mesh(4096, 0)
+    # C4: cold (first call in the process: device allocations) and warm (the
+    # process-wide engine's block cache holds the level buffers)
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        levels, final, ms = coarsen_mesh(4096, 0)
+        torch.cuda.synchronize()
+        times.append(ms)
     out["C4_mesh4096_coarsening"] = {
-        "levels": len(levels), "final": list(final), "end_to_end_ms": total_ms,
+        "levels": len(levels), "final": list(final), "end_to_end_ms_cold": times[0],
+        "end_to_end_ms_warm": min(times[1:]),
         "level0": {"n": levels[0].n, "m": levels[0].m, "matched": levels[0].matched,
                    "rounds": len(levels[0].rounds), "match_ms": levels[0].match_ms},
         "match_ms_all_levels": sum(lv.match_ms for lv in levels)}
-    print(out["C4_mesh4096_coarsening"], flush=True)
-    path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/configs.json"
-    with open(path, "w") as f:
-        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
