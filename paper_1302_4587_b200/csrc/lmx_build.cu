@@ -493,6 +493,7 @@ int lmx_build_graph(lmx_ctx *ctx, int64_t k, const int64_t *u, const int64_t *v,
 
 int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edge_weight, int out_where) {
     if (!ctx) return LMX_EINVAL;
+    if (ctx->dist_local) return lmx_fail(ctx, LMX_ESTATE, "a partition holds only its local edges");
     cudaSetDevice(ctx->device);
     const unsigned long long m = (unsigned long long)ctx->m;
     if (m == 0) return LMX_OK;

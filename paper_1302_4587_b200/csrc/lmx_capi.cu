@@ -346,6 +346,7 @@ int lmx_rbm(lmx_ctx *ctx, uint64_t seed_masked, int64_t *mate_out, int64_t *matc
 
 int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t n_ids, int where,
                  int *valid, int *maximal, double *weight, char *detail, size_t detail_len) {
+    if (ctx && ctx->dist_local) return lmx_fail(ctx, LMX_ESTATE, "validate needs the whole graph (not a partition)");
     if (!ctx) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
     ctx->err.clear();

@@ -28,8 +28,7 @@ constexpr int kMaxP = 64;
 __global__ void __launch_bounds__(kBlock) k_dist_messages(const unsigned long long *vbeg, const uint2 *ids,
                                                           unsigned long long nl, uint32_t lo, uint32_t nbr_mask,
                                                           const uint32_t *mround, const unsigned long long *bounds,
-                                                          int p, int rank, uint32_t R, const uint32_t *eu,
-                                                          const uint32_t *oldid, const uint32_t *eid_of_x,
+                                                          int p, int rank, uint32_t R, const uint32_t *side_bits,
                                                           unsigned long long *rec,
                                                           unsigned long long *cut) {
     __shared__ unsigned long long s_b[kMaxP + 1];
@@ -43,7 +42,6 @@ __global__ void __launch_bounds__(kBlock) k_dist_messages(const unsigned long lo
         for (int w = lane; w < 2 * p; w += 32) s_D[warp][w] = -1;
         __syncwarp();
         const uint32_t x = lo + (uint32_t)v;
-        const uint32_t xc = oldid ? oldid[x] : x;   // caller id: which end of the edge x is
         const uint32_t mx = mround[x];
         for (unsigned long long i = vbeg[v] + lane; i < vbeg[v + 1]; i += 32) {
             const uint2 sl = ids[i];
@@ -52,8 +50,7 @@ __global__ void __launch_bounds__(kBlock) k_dist_messages(const unsigned long lo
             while (w + 1 < p && y >= s_b[w + 1]) ++w;
             if (w == rank) continue;
             const uint32_t d = min(min(mx, mround[y]), R);
-            const uint32_t e = eid_of_x ? eid_of_x[sl.y] : sl.y;
-            const int side = eu[e] == xc ? 0 : 1;
+            const int side = (side_bits[i >> 5] >> (i & 31)) & 1u;   // x is the edge's u (0) or v (1) end
             atomicMax(&s_D[warp][side * p + w], (int)d);
             if (x < y) atomicAdd(cut + d, 1ULL);
         }
@@ -69,7 +66,8 @@ __global__ void __launch_bounds__(kBlock) k_dist_messages(const unsigned long lo
 extern "C" int lmx_dist_messages(lmx_ctx *ctx, int n_rounds, void **hist_dev) {
     if (!ctx || !hist_dev || n_rounds < 0) return LMX_EINVAL;
     cudaSetDevice(ctx->device);
-    if (!ctx->mround || !ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no partitioned matching to account");
+    if (!ctx->mround || !ctx->vbeg || !ctx->slot_side)
+        return lmx_fail(ctx, LMX_ESTATE, "no partitioned matching to account");
     if (ctx->dist_p > kMaxP) return lmx_fail(ctx, LMX_ELIMIT, "message accounting supports p <= 64");
     const size_t nb = (size_t)n_rounds + 1;
     const size_t need = 2 * nb;
@@ -90,8 +88,7 @@ extern "C" int lmx_dist_messages(lmx_ctx *ctx, int n_rounds, void **hist_dev) {
     if (nl) {
         k_dist_messages<<<ctx->num_sms * 8, kBlock, 0, st>>>(
             ctx->vbeg, ctx->ids0, nl, (uint32_t)ctx->lo, ctx->algo == 1 ? kSlotNbr : 0xFFFFFFFFu, ctx->mround, bounds,
-            ctx->dist_p, ctx->dist_rank, (uint32_t)n_rounds, ctx->eu, ctx->relabeled ? ctx->oldid : nullptr,
-            (ctx->algo == 0 && ctx->layout == kDistinct) ? ctx->eid_of_x : nullptr, ctx->hist, ctx->hist + nb);
+            ctx->dist_p, ctx->dist_rank, (uint32_t)n_rounds, ctx->slot_side, ctx->hist, ctx->hist + nb);
         LMX_CUDA(ctx, cudaGetLastError());
     }
     LMX_CUDA(ctx, cudaStreamSynchronize(st));

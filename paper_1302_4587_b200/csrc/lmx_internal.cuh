@@ -157,6 +157,13 @@ struct lmx_ctx {
     int algo = 0;
     int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
     bool scan_rejected = false;              // load time: ties too common for the scan loop
+    // partitions (dist_p > 1): after the cut search, eu/ev/w hold only the edges
+    // incident to the owned range ("local edges", caller ids), geid their global ids
+    bool dist_local = false;
+    int64_t m_local = 0;
+    uint32_t *geid = nullptr;                // local edge -> global edge id (null: identity)
+    int w_uniform = -1;                      // all weights equal (global; decided before the filter)
+    uint32_t *slot_side = nullptr;           // partitions: bit per owned slot, 1 = the owner is the edge's v end
     bool dist_requested = false;             // LMX_OPT_DIST_P was set: stepped protocol
     uint32_t *mround = nullptr;              // scan: round each vertex was matched in (~0 never)
     unsigned long long *lowbeg = nullptr;    // scan (load time only): [n+1] offsets of lowpair
@@ -211,6 +218,8 @@ int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/
 int lmx_setup_device_edges(lmx_ctx *ctx);   // deg0 + weight stage + lmx_setup_slots for built eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_weight_stage(lmx_ctx *ctx);
+// edges held in ctx->eu / ev / w (all of them, or a partition's local edges)
+inline int64_t lmx_edges(const lmx_ctx *ctx) { return ctx->dist_local ? ctx->m_local : ctx->m; }
 void trace_mark(lmx_ctx *ctx, const char *what);   // LMX_TRACE_SETUP=1: K0 stage times
 // scan loop K0 (lmx_scanload.cu): owned weight-descending segments, cand0, lowpair
 int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid);

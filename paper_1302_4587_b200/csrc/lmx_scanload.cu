@@ -85,12 +85,12 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, 
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const unsigned long long i = i0 + k * stride;
-            if (i < m) {
+            if (i < m) {   // bit 30 marks, until the post pass, the slot of the edge's v end
                 const uint32_t oa = p[k].x - lo, ob = p[k].y - lo;
                 okey[2 * i] = oa < nl ? oa : nl;
                 sval[2 * i] = make_uint2(p[k].y | t[k], e[k]);
                 okey[2 * i + 1] = ob < nl ? ob : nl;
-                sval[2 * i + 1] = make_uint2(p[k].x | t[k], e[k]);
+                sval[2 * i + 1] = make_uint2(p[k].x | t[k] | kSlotRunStart, e[k]);
             }
         }
     }
@@ -99,7 +99,9 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, 
 // Tie flags, cand0 and lowpair over the owner-sorted slots (see header).
 __global__ void __launch_bounds__(kBlock) k_scan_post(const uint32_t *owner, uint2 *ids, const double *w,
                                                       unsigned long long S, uint32_t lo, uint2 *cand0,
-                                                      uint2 *lowpair, unsigned long long *counts) {
+                                                      uint2 *lowpair, unsigned long long *counts,
+                                                      const uint32_t *geid, uint32_t *side,
+                                                      const uint2 *sorted_vals) {
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ unsigned long long s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -114,22 +116,25 @@ __global__ void __launch_bounds__(kBlock) k_scan_post(const uint32_t *owner, uin
         if (i < S) {
             const uint32_t o = owner[i];
             const bool head = i == 0 || owner[i - 1] != o;
-            uint2 x = ids[i];
+            uint2 x = sorted_vals[i];
             nbr = x.x & kSlotNbr;
+            if (side && (x.x & kSlotRunStart)) atomicOr(side + (i >> 5), 1u << (i & 31));
             uint32_t flags = 0;
             if (x.x & kSlotTied) {   // the weight occurs more than once: compare with the neighbours
                 const unsigned long long k = canon_bits2(w[x.y]);
-                const bool prev = !head && (ids[i - 1].x & kSlotTied) && canon_bits2(w[ids[i - 1].y]) == k;
-                const bool next = i + 1 < S && owner[i + 1] == o && (ids[i + 1].x & kSlotTied) &&
-                                  canon_bits2(w[ids[i + 1].y]) == k;
+                const bool prev = !head && (sorted_vals[i - 1].x & kSlotTied) &&
+                                  canon_bits2(w[sorted_vals[i - 1].y]) == k;
+                const bool next = i + 1 < S && owner[i + 1] == o && (sorted_vals[i + 1].x & kSlotTied) &&
+                                  canon_bits2(w[sorted_vals[i + 1].y]) == k;
                 if (prev || next) flags = kSlotTied | (prev ? 0u : kSlotRunStart);
                 tied_n += (prev || next) ? 1u : 0u;
             }
             x.x = nbr | flags;
+            if (geid) x.y = geid[x.y];   // local edge index -> the global edge id (salts, outputs)
             if (head) cand0[o] = x;
             vdev = o + lo;
             emit = nbr < vdev;
-            ids[i].x = x.x;
+            ids[i] = x;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, emit);
         if (lane == 0) s_cnt[warp] = __popc(bal);
@@ -165,7 +170,8 @@ static int lgrid(lmx_ctx *ctx, unsigned long long work) {
 // end).  newid: caller id -> device id, or null.
 int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     cudaStream_t st = ctx->stream;
-    const unsigned long long m = (unsigned long long)ctx->m, lo = ctx->lo, nl = ctx->hi - ctx->lo;
+    // the edges held: all of them, or a partition's local edges (global ids in ctx->geid)
+    const unsigned long long m = (unsigned long long)lmx_edges(ctx), lo = ctx->lo, nl = ctx->hi - ctx->lo;
     const unsigned long long slots2 = 2 * m;
     // 1. owned segment offsets
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->vbeg, (nl + 1) * 8, "vbeg"));
@@ -186,10 +192,12 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     ctx->slots_local = (int64_t)S;
     const size_t S1 = std::max<unsigned long long>(S, 1), M2 = std::max<unsigned long long>(slots2, 1);
-    // the sort's value output is ids0: the whole stream (2m) on a partition, its owned prefix kept
-    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, (ctx->dist_p == 1 ? S1 : M2) * 8, "ids0"));
+    // one GPU: the sort writes ids0 and the post pass works in place; a
+    // partition sorts its whole local stream (2 m_local, non-owned slots last)
+    // into a scratch buffer and the post pass writes the owned prefix into ids0
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, S1 * 8, "ids0"));
     uint32_t *okey = nullptr, *okey2 = nullptr;
-    uint2 *sval = nullptr;
+    uint2 *sval = nullptr, *sorted = nullptr;
     unsigned long long *cnt = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -200,6 +208,8 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
         if ((rc = lmx_alloc(ctx, (void **)&okey, M2 * 4, "owner keys")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&okey2, M2 * 4, "owner keys out")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&sval, M2 * 8, "slot stream")) != LMX_OK) break;
+        if (ctx->dist_p > 1 && (rc = lmx_alloc(ctx, (void **)&sorted, M2 * 8, "sorted stream")) != LMX_OK) break;
+        uint2 *sort_out = ctx->dist_p > 1 ? sorted : ctx->ids0;
         if ((rc = lmx_alloc(ctx, (void **)&cnt, 16, "counts")) != LMX_OK) break;
         cudaError_t e = cudaMemsetAsync(cnt, 0, 16, st);
         if (m && e == cudaSuccess) {
@@ -213,11 +223,11 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "slot stream"); break; }
         trace_mark(ctx, "  scan: slot stream");
         if (m) {
-            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2,
+            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, sort_out, (long long)slots2,
                                                 0, bits, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
             if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2, 0,
+            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, sort_out, (long long)slots2, 0,
                                                 bits, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
             trace_mark(ctx, "  scan: owner sort");
@@ -225,15 +235,6 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
         lmx_free(ctx, (void **)&sval, M2 * 8);
         lmx_free(ctx, (void **)&okey, M2 * 4);
         lmx_free(ctx, &tmp, tmp_bytes);
-        if (ctx->dist_p > 1) {   // keep the owned prefix only
-            uint2 *own = nullptr;
-            if ((rc = lmx_alloc(ctx, (void **)&own, S1 * 8, "ids0 owned")) != LMX_OK) break;
-            if (S) e = cudaMemcpyAsync(own, ctx->ids0, S * 8, cudaMemcpyDeviceToDevice, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "ids0 trim"); break; }
-            lmx_free(ctx, (void **)&ctx->ids0, M2 * 8);
-            ctx->ids0 = own;
-        }
         // 4. flags, cand0, lowpair over the owned prefix [0, S)
         if ((rc = lmx_alloc(ctx, (void **)&ctx->cand0, std::max<unsigned long long>(nl, 1) * 8, "cand0")) != LMX_OK)
             break;
@@ -241,9 +242,13 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
                             "lowpair")) != LMX_OK)
             break;
         e = cudaMemsetAsync(ctx->cand0, 0xFF, std::max<unsigned long long>(nl, 1) * 8, st);
+        if (ctx->dist_p > 1 && e == cudaSuccess) {   // which end of its edge each owned slot is (RoundMessages)
+            if ((rc = lmx_alloc(ctx, (void **)&ctx->slot_side, (S1 + 31) / 32 * 4, "slot side")) != LMX_OK) break;
+            e = cudaMemsetAsync(ctx->slot_side, 0, (S1 + 31) / 32 * 4, st);
+        }
         if (e == cudaSuccess && S) {
             k_scan_post<<<lgrid(ctx, S), kBlock, 0, st>>>(okey2, ctx->ids0, ctx->w, S, (uint32_t)lo, ctx->cand0,
-                                                         ctx->lowpair, cnt);
+                                                         ctx->lowpair, cnt, ctx->geid, ctx->slot_side, sort_out);
             e = cudaGetLastError();
         }
         unsigned long long hc[2] = {0, 0};
@@ -258,6 +263,7 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     lmx_free(ctx, (void **)&okey, M2 * 4);
     lmx_free(ctx, (void **)&okey2, M2 * 4);
     lmx_free(ctx, (void **)&sval, M2 * 8);
+    lmx_free(ctx, (void **)&sorted, M2 * 8);
     lmx_free(ctx, (void **)&cnt, 16);
     lmx_free(ctx, &tmp, tmp_bytes);
     return rc;

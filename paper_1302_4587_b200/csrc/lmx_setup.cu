@@ -121,13 +121,17 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->cand0,    (void **)&ctx->ws_kofe,     (void **)&ctx->ws_rank,
                      (void **)&ctx->ws_eid,   (void **)&ctx->ws_tied,     (void **)&ctx->ws_tidx,
                      (void **)&ctx->rbm_prop, (void **)&ctx->rbm_acc,     (void **)&ctx->rbm_blue,
-                     (void **)&ctx->rbm_list[0], (void **)&ctx->rbm_list[1], (void **)&ctx->rbm_list0};
+                     (void **)&ctx->rbm_list[0], (void **)&ctx->rbm_list[1], (void **)&ctx->rbm_list0,
+                     (void **)&ctx->geid,     (void **)&ctx->slot_side};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
     }
     ctx->dev_bytes = 0;
     ctx->n = ctx->m = 0;
+    ctx->dist_local = false;
+    ctx->m_local = 0;
+    ctx->w_uniform = -1;
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
@@ -219,7 +223,7 @@ __global__ void k_widen_deg(const uint32_t *deg, unsigned long long *out, unsign
 __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long long m,
                           const unsigned long long *vbeg, const uint32_t *newid, unsigned long long lo,
                           unsigned long long hi, uint32_t *fill, uint2 *ids, const uint32_t *kofe, bool distinct,
-                          uint32_t *wk) {
+                          uint32_t *wk, const uint32_t *geid, uint32_t *side) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += stride) {
@@ -229,7 +233,7 @@ __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long 
             b = newid[b];
         }
         const uint32_t key = kofe ? kofe[e] : 0u;
-        const uint32_t id = distinct ? key : (uint32_t)e;
+        const uint32_t id = distinct ? key : (geid ? geid[e] : (uint32_t)e);   // global edge id
         if (a >= lo && a < hi) {
             const unsigned long long pa = vbeg[a - lo] + atomicAdd(fill + (a - lo), 1u);
             ids[pa] = make_uint2(b, id);
@@ -239,6 +243,7 @@ __global__ void k_scatter(const uint32_t *eu, const uint32_t *ev, unsigned long 
             const unsigned long long pb = vbeg[b - lo] + atomicAdd(fill + (b - lo), 1u);
             ids[pb] = make_uint2(a, id);
             if (wk) wk[pb] = key;
+            if (side) atomicOr(side + (pb >> 5), 1u << (pb & 31));   // this owner is the edge's v end
         }
     }
 }
@@ -342,7 +347,7 @@ __global__ void k_tied(const unsigned long long *sorted, unsigned long long m, u
 // GENERAL: rank per edge.  DISTINCT: weight key x per edge plus the maps back.
 __global__ void k_keys_out(const uint32_t *rank, const uint32_t *tie_idx, const uint32_t *tied,
                            const uint32_t *eid, unsigned long long m, int distinct, uint32_t D,
-                           uint32_t *key_of_eid, uint32_t *eid_of_x, uint32_t *tie_rank) {
+                           uint32_t *key_of_eid, uint32_t *eid_of_x, uint32_t *tie_rank, const uint32_t *geid) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += stride) {
@@ -359,7 +364,7 @@ __global__ void k_keys_out(const uint32_t *rank, const uint32_t *tie_idx, const 
             x = rank[i];
         }
         key_of_eid[e] = x;
-        eid_of_x[x] = e;
+        eid_of_x[x] = geid ? geid[e] : e;   // the global edge id (salts, outputs)
     }
 }
 
@@ -414,12 +419,14 @@ void trace_mark(lmx_ctx *ctx, const char *what) {
 // ctx->ws_kofe (weight key per edge; compacting loop) or ctx->ws_{rank, eid,
 // tied, tidx} (sorted-position arrays; scan loop) for lmx_setup_slots.
 int lmx_weight_stage(lmx_ctx *ctx) {
-    const unsigned long long m = (unsigned long long)ctx->m;
+    const unsigned long long m = (unsigned long long)lmx_edges(ctx);
     cudaStream_t st = ctx->stream;
     uint32_t *kofe = nullptr;
     // weight key layout
     bool uniform = true;
-    if (m) {
+    if (ctx->dist_local) {
+        uniform = ctx->w_uniform != 0;   // decided on ALL edges: every partition takes the same loop
+    } else if (m) {
         unsigned long long *mm = nullptr;
         LMX_TRY(lmx_alloc(ctx, (void **)&mm, 16, "minmax"));
         unsigned long long init[2] = {~0ULL, 0ULL};
@@ -431,6 +438,12 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
         lmx_free(ctx, (void **)&mm, 16);
         uniform = got[0] == got[1];
+    }
+    if (ctx->dist_p > 1 && !ctx->dist_local) {
+        // a partition sorts its local edges only: lmx_setup_slots comes back
+        // after the cut search and the filter
+        ctx->w_uniform = uniform ? 1 : 0;
+        return LMX_OK;
     }
     ctx->layout = kUniform;
     if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
@@ -472,7 +485,8 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank readback"); break; }
             const unsigned long long D = (unsigned long long)last_rank + 1;
             const unsigned long long T = (unsigned long long)last_tidx + last_tied;
-            bool distinct = (T <= m / 16) && (D + T < 0xFFFFFFFFULL);
+            // partitions: the choice must agree across them, and T is local -> distinct
+            bool distinct = (T <= m / 16 || ctx->dist_p > 1) && (D + T < 0xFFFFFFFFULL);
             if (ctx->force_layout == kDistinct) distinct = D + T < 0xFFFFFFFFULL;
             if (ctx->force_layout == kGeneral) distinct = false;
             ctx->layout = distinct ? kDistinct : kGeneral;
@@ -500,7 +514,8 @@ int lmx_weight_stage(lmx_ctx *ctx) {
                 break;
             }
             k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
-                                                           (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank);
+                                                           (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank,
+                                                           ctx->geid);
             e = cudaGetLastError();
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "weight keys"); break; }
@@ -597,6 +612,84 @@ static int partition_bounds(lmx_ctx *ctx, std::vector<int64_t> &bounds) {
     return LMX_OK;
 }
 
+__global__ void k_local_flags(const uint32_t *eu, const uint32_t *ev, unsigned long long m, uint32_t lo, uint32_t nl,
+                              uint32_t *flag) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
+        flag[e] = (eu[e] - lo < nl || ev[e] - lo < nl) ? 1u : 0u;
+}
+
+__global__ void k_gather_local(const uint32_t *geid, unsigned long long k, const uint32_t *eu, const uint32_t *ev,
+                               const double *w, uint32_t *eu2, uint32_t *ev2, double *w2) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint32_t e = geid[i];
+        eu2[i] = eu[e];
+        ev2[i] = ev[e];
+        w2[i] = w[e];
+    }
+}
+
+// A partition keeps the edges incident to its range (bsp.py:86-90
+// local_edges), in edge order, with their global ids: everything after this
+// (weight sort, slot stream, owner sort) is sized by the local edges.
+static int filter_local_edges(lmx_ctx *ctx) {
+    cudaStream_t st = ctx->stream;
+    const unsigned long long m = (unsigned long long)ctx->m;
+    const uint32_t lo = (uint32_t)ctx->lo, nl = (uint32_t)(ctx->hi - ctx->lo);
+    const size_t m1 = std::max<unsigned long long>(m, 1);
+    uint32_t *flag = nullptr, *geid = nullptr, *eu2 = nullptr, *ev2 = nullptr;
+    double *w2 = nullptr;
+    unsigned long long *cnt = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = LMX_OK;
+    unsigned long long k = 0;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&flag, m1 * 4, "local flags")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&geid, m1 * 4, "local edge ids")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&cnt, 8, "local count")) != LMX_OK) break;
+        k_local_flags<<<grid_for(ctx, m1), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, lo, nl, flag);
+        cub::CountingInputIterator<uint32_t> it(0u);
+        cudaError_t e = cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, geid, cnt, (long long)m, st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "filter sizing"); break; }
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "filter tmp")) != LMX_OK) break;
+        e = cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, geid, cnt, (long long)m, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "filter"); break; }
+        const size_t k1 = std::max<unsigned long long>(k, 1);
+        if ((rc = lmx_alloc(ctx, (void **)&eu2, k1 * 4, "local edge_u")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ev2, k1 * 4, "local edge_v")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&w2, k1 * 8, "local edge_weight")) != LMX_OK) break;
+        if (k) k_gather_local<<<grid_for(ctx, k), kBlock, 0, st>>>(geid, k, ctx->eu, ctx->ev, ctx->w, eu2, ev2, w2);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "local gather"); break; }
+    } while (0);
+    lmx_free(ctx, (void **)&flag, m1 * 4);
+    lmx_free(ctx, (void **)&cnt, 8);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    if (rc != LMX_OK) {
+        lmx_free(ctx, (void **)&geid, m1 * 4);
+        lmx_free(ctx, (void **)&eu2, m1 * 4);
+        lmx_free(ctx, (void **)&ev2, m1 * 4);
+        lmx_free(ctx, (void **)&w2, m1 * 8);
+        return rc;
+    }
+    lmx_free(ctx, (void **)&ctx->eu, m1 * 4);
+    lmx_free(ctx, (void **)&ctx->ev, m1 * 4);
+    lmx_free(ctx, (void **)&ctx->w, m1 * 8);
+    ctx->eu = eu2;
+    ctx->ev = ev2;
+    ctx->w = w2;
+    ctx->geid = geid;
+    ctx->m_local = (int64_t)k;
+    ctx->dist_local = true;
+    lmx_flush_cache(ctx);   // the global arrays' blocks are not reused
+    return LMX_OK;
+}
+
 // vbeg / ids0 / deg0 (device ids) / bins0 / match state from ctx->eu, ev, w
 // (caller ids; deg0 counted by the conversion).  DESIGN.md §3.
 int lmx_setup_slots(lmx_ctx *ctx) {
@@ -609,6 +702,12 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     ctx->hi = (unsigned long long)ctx->bounds[(size_t)ctx->dist_rank + 1];
     const unsigned long long lo = ctx->lo, nl = ctx->hi - ctx->lo;
     ctx->n_local = (int64_t)nl;
+    if (ctx->dist_p > 1 && !ctx->dist_local) {   // keep the local edges, then their weight stage
+        LMX_TRY(filter_local_edges(ctx));
+        LMX_TRY(lmx_weight_stage(ctx));
+        trace_mark(ctx, "local edges + weight stage");
+    }
+    const unsigned long long me = (unsigned long long)lmx_edges(ctx);   // edges held
     // Degree-descending relabelling of skewed graphs, inside
     // each partition's range (the ranges stay the reference's): hubs get the
     // low ids of their range, so the matched bitmap and candidate lookups
@@ -724,17 +823,21 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     }
     LMX_TRY(lmx_alloc_match_state(ctx));
     trace_mark(ctx, "offsets + allocation");
-    if (m && ctx->algo == 0) {
+    if (me && ctx->algo == 0) {
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
+        if (ctx->dist_p > 1) {
+            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->slot_side, (std::max<size_t>(slots, 1) + 31) / 32 * 4, "slot side"));
+            LMX_CUDA(ctx, cudaMemsetAsync(ctx->slot_side, 0, (std::max<size_t>(slots, 1) + 31) / 32 * 4, st));
+        }
         if (ctx->layout == kGeneral) {
             LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0"));
             LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1"));
         }
         // fill counters reuse vdeg (local)
         LMX_CUDA(ctx, cudaMemsetAsync(ctx->vdeg, 0, std::max<size_t>(nl, 1) * 4, st));
-        k_scatter<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->vbeg, newid, lo, ctx->hi,
-                                                      ctx->vdeg, ctx->ids0, ctx->ws_kofe,
-                                                      ctx->layout == kDistinct, ctx->wk0);
+        k_scatter<<<grid_for(ctx, me), kBlock, 0, st>>>(ctx->eu, ctx->ev, me, ctx->vbeg, newid, lo, ctx->hi,
+                                                       ctx->vdeg, ctx->ids0, ctx->ws_kofe,
+                                                       ctx->layout == kDistinct, ctx->wk0, ctx->geid, ctx->slot_side);
         LMX_CUDA(ctx, cudaGetLastError());
         trace_mark(ctx, "slot scatter");
     }

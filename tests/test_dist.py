@@ -154,3 +154,23 @@ def test_dist_round_messages_equal_reference(algo):
                 assert np.array_equal(r.bounds, O.partition_bounds(np.concatenate([[0], np.cumsum(deg)]), n, int(p)))
             finally:
                 r.close()
+
+
+@pytest.mark.gpu
+def test_partition_memory_shrinks_with_p():
+    """A partition keeps its local edges and owned slots only: device bytes per
+    rank fall roughly as 1/p (global bitmaps and per-vertex arrays aside)."""
+    from paper_1302_4587_b200 import Engine
+    from paper_1302_4587_b200.dist import DistRank
+    eng = Engine(0)
+    eng.gen_rmat(20, 16, seed=3)
+    g = eng.export_graph()
+    eng.close()
+    per = {}
+    for p in (1, 2, 4):
+        r = DistRank(g, p, p - 1)
+        try:
+            per[p] = r.eng.device_bytes()
+        finally:
+            r.close()
+    assert per[2] < 0.8 * per[1] and per[4] < 0.65 * per[1], per
