@@ -446,6 +446,11 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         return LMX_OK;
     }
     ctx->layout = kUniform;
+    if (ctx->dist_local && m == 0 && !uniform && ctx->force_algo != 0 && ctx->n < (1LL << 30)) {
+        ctx->algo = 1;   // a partition without local edges still runs the loop its peers run
+        ctx->layout = kDistinct;
+        return LMX_OK;
+    }
     if (m && (!uniform || (ctx->force_layout != -1 && ctx->force_layout != kUniform))) {
         unsigned long long *keys = nullptr, *keys2 = nullptr;
         uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr, *tidx = nullptr;
@@ -823,12 +828,12 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     }
     LMX_TRY(lmx_alloc_match_state(ctx));
     trace_mark(ctx, "offsets + allocation");
+    if (ctx->algo == 0 && ctx->dist_p > 1) {   // which end of its edge each owned slot is (RoundMessages)
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->slot_side, (std::max<size_t>(slots, 1) + 31) / 32 * 4, "slot side"));
+        LMX_CUDA(ctx, cudaMemsetAsync(ctx->slot_side, 0, (std::max<size_t>(slots, 1) + 31) / 32 * 4, st));
+    }
     if (me && ctx->algo == 0) {
         LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids1, std::max<size_t>(slots, 1) * 8, "ids1"));
-        if (ctx->dist_p > 1) {
-            LMX_TRY(lmx_alloc(ctx, (void **)&ctx->slot_side, (std::max<size_t>(slots, 1) + 31) / 32 * 4, "slot side"));
-            LMX_CUDA(ctx, cudaMemsetAsync(ctx->slot_side, 0, (std::max<size_t>(slots, 1) + 31) / 32 * 4, st));
-        }
         if (ctx->layout == kGeneral) {
             LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk0, slots * 4, "wk0"));
             LMX_TRY(lmx_alloc(ctx, (void **)&ctx->wk1, slots * 4, "wk1"));
