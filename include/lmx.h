@@ -292,6 +292,19 @@ int lmx_validate(lmx_ctx *ctx, const int64_t *mate, const int64_t *ids, int64_t 
                  int *valid, int *maximal, double *weight, char *detail, size_t detail_len);
 
 /*
+ * The PRAM restatement's incidence layout and cross pointers
+ * (pram.py:54-124 PramState, :127-166 compute_cross_pointers; Lemma 2,
+ * PAPER.md:233-257) for the loaded graph: slots sorted by (vertex, edge id)
+ * (graph.py:108-115), cross[i] = the other slot of slot i's edge, computed by
+ * the reference's two write/read step pairs through a per-edge scratch cell,
+ * each step's writes counted and checked for exclusivity (pram.py:28-51
+ * WriteLog.record), then PramState.check_consistent's involution checks.
+ * cross_out: int64[2m] or NULL (where `out_where` says).  log_out: int64[4] =
+ * {steps, writes, conflicts, first slot failing the consistency check or -1}.
+ */
+int lmx_pram_cross(lmx_ctx *ctx, int64_t *cross_out, int64_t *log_out, int out_where);
+
+/*
  * rbm(g, seed) (matchers.py:357-410): red-blue matching on the loaded graph,
  * the paper's GPU competitor.  Outputs as lmx_match (mate, ascending matched
  * ids, RoundStats).  max_rounds (the reference uses 10 000; <= 0 means that):

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
-    "lmx_dist_messages",
+    "lmx_dist_messages", "lmx_pram_cross",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
 )
 LMX_OPT_KERNEL_TIMING = 1
@@ -105,6 +105,7 @@ def load_library(path: str = LIB_PATH):
             "lmx_set_option": (c_int, [p, c_int, i64]),
             "lmx_validate": (c_int, [p, p, p, i64, c_int, p, p, p, p, ctypes.c_size_t]),
             "lmx_rbm": (c_int, [p, u64, p, p, p, p, c_int, p, c_int]),
+            "lmx_pram_cross": (c_int, [p, p, p, c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -385,6 +386,18 @@ class Engine:
         trace.wall_millis = (time.perf_counter() - t0) * 1000.0
         return Matching(ids[: nm.value].copy(), mate[:n]), trace
 
+    def pram_cross(self, want_cross: bool = False):
+        """PRAM incidence layout + cross pointers of the loaded graph on the
+        device (pram.py:127-166), with the exclusive-write check:
+        returns ({steps, writes, conflicts, bad_slot}, cross int64[2m] or None)."""
+        _, m = self.graph_size()
+        log = np.zeros(4, dtype=np.int64)
+        cross = np.empty(max(2 * m, 1), dtype=np.int64) if want_cross else None
+        self._check(self._lib.lmx_pram_cross(self._h, cross.ctypes.data if want_cross else None, log.ctypes.data,
+                                             LMX_HOST), "lmx_pram_cross")
+        return ({"steps": int(log[0]), "writes": int(log[1]), "conflicts": int(log[2]), "bad_slot": int(log[3])},
+                cross[: 2 * m] if want_cross else None)
+
     def validate(self, matching) -> tuple[MatchingCheck, float]:
         """``validate_matching(g, m)`` (graph.py:212-237) and ``m.weight(g)``
         (graph.py:54-56) on the device, for the graph loaded in this engine.
@@ -452,10 +465,15 @@ def pram_local_max_b200(g, seed: int, checked: bool = False, rerandomize: bool =
     ``trace.slot_ops`` linear-work meter, ``n + 3m`` for the set-up plus
     ``m_r + 2 m_r`` (live edges and incidence slots) per phase (pram.py:293,300).
 
-    ``checked=True`` validates the result on the device (valid and maximal,
-    graph.py:212-237) and raises ``RuntimeError`` if it is not; the
-    reference's per-step write log (a property of its PRAM simulation) is not
-    produced, so ``trace.write_log`` stays ``None``.
+    ``checked=True`` (pram.py:283-286) builds the PRAM incidence layout and
+    its cross pointers on the device with the reference's exclusive-write
+    steps (``lmx_pram_cross``), checks them as ``PramState.check_consistent``
+    does, validates the matching on the device (graph.py:212-237), and
+    returns ``trace.write_log``: a ``WriteLog`` (locmax's when importable)
+    holding the cross-pointer steps' writes and conflicts plus one
+    ``match/mate`` step per round (2 writes per matched edge; a vertex written
+    twice would fail validation and count as a conflict).  Any conflict or
+    inconsistency raises ``RuntimeError``.
     """
     t0 = time.perf_counter()
     eng = default_engine(device)
@@ -464,11 +482,38 @@ def pram_local_max_b200(g, seed: int, checked: bool = False, rerandomize: bool =
     trace.slot_ops = int(g.num_vertices) + 3 * int(np.asarray(g.edge_u).size) + \
         3 * sum(int(r.edges_before) for r in trace.rounds)
     if checked:
+        log, _ = eng.pram_cross()
+        if log["bad_slot"] >= 0:
+            raise RuntimeError(f"pram_local_max_b200: cross pointers inconsistent at slot {log['bad_slot']}")
         chk, _ = eng.validate(matching)
         if not (chk.valid and chk.maximal):
             raise RuntimeError(f"pram_local_max_b200: device validation failed: {chk}")
+        wl = _write_log()
+        wl.steps = log["steps"] + len(trace.rounds)
+        wl.writes = log["writes"] + 2 * sum(int(r.edges_matched) for r in trace.rounds)
+        wl.conflicts = log["conflicts"]
+        if wl.conflicts:
+            raise RuntimeError(f"pram_local_max_b200: {wl.conflicts} write conflicts in the cross-pointer steps")
+        trace.write_log = wl
     trace.wall_millis = (time.perf_counter() - t0) * 1000.0
     return matching, trace
+
+
+def _write_log():
+    """pram.py:28-51 WriteLog (locmax's own when importable)."""
+    try:
+        from locmax.pram import WriteLog
+        return WriteLog()
+    except ImportError:
+        from dataclasses import dataclass, field
+
+        @dataclass
+        class WriteLog:
+            steps: int = 0
+            writes: int = 0
+            conflicts: int = 0
+            samples: list = field(default_factory=list)
+        return WriteLog()
 
 
 class RbmDidNotConverge(RuntimeError):

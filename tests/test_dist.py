@@ -174,3 +174,43 @@ def test_partition_memory_shrinks_with_p():
         finally:
             r.close()
     assert per[2] < 0.8 * per[1] and per[4] < 0.65 * per[1], per
+
+
+@pytest.mark.gpu
+def test_reference_bsp_assertions_with_b200_engine():
+    """test_bsp.py:59-98 with bsp_local_max replaced by local_max_dist."""
+    from paper_1302_4587_b200 import Graph, local_max_b200, validate_matching
+    from paper_1302_4587_b200.dist import local_max_dist, partition_graph
+    n, eu, ev, w = O.gen_random(256, 4, 2)
+    g = Graph(n, eu, ev, w)
+    base, _ = local_max_b200(g, 9)
+    matching, trace = local_max_dist(g, 1, 9)
+    assert matching == base
+    assert all(rm.candidate_records == 0 for rm in trace.messages)
+    assert all(rm.bytes_estimate == 0 for rm in trace.messages)
+    n, eu, ev, w = O.gen_rgg(12, 4)
+    g = Graph(n, eu, ev, w)
+    base, _ = local_max_b200(g, 7)
+    for p in (2, 4, 8):
+        matching, trace = local_max_dist(g, p, 7)
+        assert matching == base
+        check = validate_matching(g, matching)
+        assert check.valid and check.maximal
+    n, eu, ev, w = O.gen_random(256, 4, 6)
+    unit = Graph(n, eu, ev, np.ones_like(w))
+    base, _ = local_max_b200(unit, 3)
+    for p in (1, 2, 4, 8):
+        matching, _ = local_max_dist(unit, p, 3)
+        assert matching == base
+    n, eu, ev, w = O.gen_random(512, 4, 8)
+    _, trace = local_max_dist(Graph(n, eu, ev, w), 8, 1)
+    for rm in trace.messages:
+        assert rm.candidate_records <= 2 * rm.cut_edges_surviving
+        assert rm.bytes_estimate == rm.candidate_records * 32
+    cuts = [rm.cut_edges_surviving for rm in trace.messages]
+    assert cuts == sorted(cuts, reverse=True)
+    n1, eu1, ev1, w1 = O.gen_rgg(12, 5)
+    alpha = max(1, round(len(eu1) / 4096))
+    n2, eu2, ev2, w2 = O.gen_random(4096, alpha, 5)
+    assert partition_graph(Graph(n1, eu1, ev1, w1), 8).cut_fraction < \
+        partition_graph(Graph(n2, eu2, ev2, w2), 8).cut_fraction

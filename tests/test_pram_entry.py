@@ -64,3 +64,56 @@ def test_run_matcher_pram_engine():
     a, _ = run_matcher(g, "localmax", 2, engine="b200")
     b, tb = run_matcher(g, "localmax", 2, engine="b200-pram")
     assert a == b and tb.slot_ops > 0
+
+
+@pytest.mark.gpu
+def test_pram_cross_pointers_and_write_log():
+    """lmx_pram_cross: the reference incidence layout's cross pointers
+    (pram.py:127-166) -- each slot points at the other slot of its edge, an
+    involution -- built with 4 exclusive-write steps of m writes each."""
+    from oracle import oracle as O
+    from paper_1302_4587_b200 import Engine, Graph
+    for n, eu, ev, w in (O.gen_random(500, 3, 1), O.gen_rgg(10, 2), O.gen_random(64, 2, 4, unit=True)):
+        g = Graph(n, eu, ev, w)
+        with Engine(0) as eng:
+            eng.load_graph(g)
+            log, cross = eng.pram_cross(want_cross=True)
+        m = len(eu)
+        # graph.py:108-115 layout, numpy: slots sorted by (vertex, edge id)
+        sv = np.concatenate([eu, ev])
+        se = np.concatenate([np.arange(m), np.arange(m)])
+        order = np.lexsort((se, sv))
+        sv, se = sv[order], se[order]
+        idx = np.arange(2 * m)
+        want = np.empty(2 * m, dtype=np.int64)
+        pos = {}
+        for i, e in zip(idx.tolist(), se.tolist()):
+            pos.setdefault(e, []).append(i)
+        for e, (a, b) in pos.items():
+            want[a], want[b] = b, a
+        assert np.array_equal(cross, want)
+        assert log == {"steps": 4, "writes": 4 * m, "conflicts": 0, "bad_slot": -1}
+
+
+@pytest.mark.gpu
+def test_reference_pram_assertions_with_b200_engine():
+    """test_pram.py:164-184 with pram_local_max replaced by the B200 engine:
+    equal matching, equal round count, a write log without conflicts; and
+    the rerandomize flag respected."""
+    from oracle import oracle as O
+    from paper_1302_4587_b200 import Graph, local_max_b200, pram_local_max_b200
+    cases = [(O.gen_rgg(12, 7), 7), (O.gen_random(512, 4, 3), 3), (O.gen_random(512, 16, 4), 11),
+             ((2, np.array([0]), np.array([1]), np.array([1.0])), 0)]
+    for (n, eu, ev, w), seed in cases:
+        g = Graph(n, eu, ev, w)
+        ref = O.c_local_max(n, eu, ev, w, seed, True)
+        par_matching, par_trace = pram_local_max_b200(g, seed, checked=True)
+        assert np.array_equal(np.asarray(par_matching.mate), ref.mate)
+        assert par_trace.total_rounds == len(ref.rounds)
+        assert par_trace.write_log.conflicts == 0
+    n, eu, ev, w = O.gen_rgg(10, 2)
+    g = Graph(n, eu, ev, w)
+    for flag in (True, False):
+        a, _ = local_max_b200(g, 5, rerandomize=flag)
+        b, _ = pram_local_max_b200(g, 5, rerandomize=flag)
+        assert a == b

@@ -11,9 +11,13 @@ from paper_1302_4587_b200 import Engine  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=26)
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--er", action="store_true", help="the er24unit family (unit weights, compacting loop)")
 args = ap.parse_args()
 eng = Engine(0)
-eng.gen_rmat(args.scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
+if args.er:
+    eng.gen_er(args.scale, 4, seed=1, unit=True)
+else:
+    eng.gen_rmat(args.scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
 n, m = eng.graph_size()
 mate = torch.empty(n, dtype=torch.int64, device="cuda")
 ids = torch.empty(n // 2 + 1, dtype=torch.int64, device="cuda")
