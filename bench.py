@@ -323,9 +323,15 @@ def run_b200_dist(args):
     fam, scale, ef = WORKLOADS[args.workload]
     if fam != "rmat":
         raise SystemExit("the partitioned bench runs the RMAT workloads")
-    me = DistRank(None, world, rank, local, stream.cuda_stream,
-                  rmat=dict(scale=scale, edge_factor=ef, a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2],
-                            seed=GRAPH_SEED, permute=True))
+    if world > 1:
+        # the distributed builder: no rank ever holds the whole graph (config C5)
+        from paper_1302_4587_b200.dist import build_rmat_distributed
+        me = DistRank(None, world, rank, local, stream.cuda_stream, defer=True)
+        build_rmat_distributed([me], comm, scale, ef, *RMAT_ABC, GRAPH_SEED, True)
+    else:
+        me = DistRank(None, world, rank, local, stream.cuda_stream,
+                      rmat=dict(scale=scale, edge_factor=ef, a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2],
+                                seed=GRAPH_SEED, permute=True))
     n, m = me.n, me.m
     for _ in range(args.warmup):
         rounds, _ = run_rounds([me], comm, MATCH_SEED, True)
@@ -362,8 +368,10 @@ def run_b200_dist(args):
             "value": m * args.steps / (T / 1000.0), "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor 16",
+            "config": {"workload": args.workload, "graph": f"RMAT scale {scale} edge factor {ef}",
                        "n": n, "m": m, "rounds": len(rounds), "parallelism": f"1d-vertex-partition{world}",
+                       "build": "distributed (lmx_dist_rmat_*)" if world > 1 else "whole graph per rank",
+                       "rank0_device_bytes": me.eng.device_bytes(),
                        "exchange_a_records": int(sum(records)),
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": step_bytes / (ms_per_step / 1000.0) / 1e9 if step_bytes else None,

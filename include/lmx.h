@@ -87,6 +87,8 @@ typedef struct {
 #define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
 #define LMX_QUERY_RELABELED 101 /* lmx_set_option returns 1 if the loaded graph is relabelled */
 #define LMX_QUERY_ALGO 102      /* lmx_set_option returns the loaded graph's round loop (0 / 1) */
+#define LMX_QUERY_PEAK_BYTES 103 /* lmx_set_option returns the context's device-memory high-water mark
+                                    in MiB (allocations through the context); value != 0 resets it */
 
 int lmx_abi_version(void);
 
@@ -254,6 +256,36 @@ int lmx_dist_mround(lmx_ctx *ctx, void **mround_dev);
  * RoundMessages.candidate_records and .cut_edges_surviving.
  */
 int lmx_dist_messages(lmx_ctx *ctx, int n_rounds, void **hist_dev);
+
+/*
+ * Distributed RMAT build: no rank ever holds the whole graph (config C5).
+ * With LMX_OPT_DIST_P = p > 1 and LMX_OPT_DIST_RANK set:
+ *   lmx_dist_rmat_build   every rank generates the raw stream (lmx_gen_rmat's
+ *                         recipe) and keeps the triples whose lower end lies in
+ *                         [rank n / p, (rank + 1) n / p); parallel pairs are
+ *                         collapsed as graph.py:94-100 does; out: the bitmap of
+ *                         first-occurrence raw positions (*words u32 words), the
+ *                         degree contributions (u32[n], caller ids) and the
+ *                         weight-bit min / max (u64[2]), all on the device
+ *   (host: sum the bitmaps -- the bit sets are disjoint -- and the degrees
+ *    over the ranks, in place; min / max of the weight bits)
+ *   lmx_dist_rmat_route   global edge ids (graph.py's first-occurrence order),
+ *                         partition_graph's cuts on the summed degrees, and this
+ *                         rank's pairs packed by destination: 24-byte records
+ *                         {edge id, u, v, pad, weight} to the owners of u and v;
+ *                         counts_out: int64[p]; m_out: the global edge count
+ *   (host: all-to-all-v of the records)
+ *   lmx_dist_rmat_recv_buffer / lmx_dist_rmat_finish   the received records are
+ *                         the rank's local edges (bsp.py:86-90); ordered by edge
+ *                         id, then the partition's K0.  w_uniform: all weights
+ *                         equal over the whole graph.
+ * The resulting partition equals the one lmx_gen_rmat + LMX_OPT_DIST_P loads.
+ */
+int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                        int permute, void **bits_dev, int64_t *words_out, void **deg_dev, void **minmax_dev);
+int lmx_dist_rmat_route(lmx_ctx *ctx, void **send_dev, int64_t *counts_out, int64_t *m_out);
+int lmx_dist_rmat_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_dev);
+int lmx_dist_rmat_finish(lmx_ctx *ctx, int w_uniform);
 int lmx_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
 
 /*

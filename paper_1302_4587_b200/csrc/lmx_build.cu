@@ -57,33 +57,185 @@ __host__ __device__ __forceinline__ uint32_t rmat_perm(uint32_t x, const RmatPar
     return (uint32_t)y;
 }
 
+// Raw triple i of the stream (see the file header).
+__device__ __forceinline__ void rmat_one(const RmatParams &p, unsigned long long i, uint32_t &u, uint32_t &v,
+                                         double &w) {
+    uint32_t a = 0, b = 0;
+    uint64_t h = 0;
+    for (int l = 0; l < p.scale; ++l) {
+        if ((l & 3) == 0) h = mix64(p.s0 ^ (i * 16ULL + (unsigned long long)(l >> 2)));
+        const uint32_t x = (uint32_t)((h >> (16 * (l & 3))) & 0xFFFFu);
+        const uint32_t bit = 1u << (p.scale - 1 - l);
+        if (x < p.A) {
+        } else if (x < p.AB) {
+            b |= bit;
+        } else if (x < p.ABC) {
+            a |= bit;
+        } else {
+            a |= bit;
+            b |= bit;
+        }
+    }
+    if (p.permute) {
+        a = rmat_perm(a, p);
+        b = rmat_perm(b, p);
+    }
+    u = a;
+    v = b;
+    w = (double)(mix64(p.s1 ^ i) >> 11) * (1.0 / 9007199254740992.0);
+}
+
 __global__ void k_rmat_raw(RmatParams p, unsigned long long k, uint32_t *u, uint32_t *v, double *w) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
-         i += stride) {
+         i += stride)
+        rmat_one(p, i, u[i], v[i], w[i]);
+}
+
+// ---- distributed build (a partition generates the whole raw stream and keeps
+// the triples whose LOWER endpoint falls in its build range) -------------------
+// Pass 0 counts, pass 1 appends {u, v, w, raw position} (block-aggregated).
+template <bool WRITE>
+__global__ void __launch_bounds__(kBlock) k_rmat_keep(RmatParams p, unsigned long long k, uint32_t blo,
+                                                      uint32_t bhi, unsigned long long *cursor, uint32_t *ku,
+                                                      uint32_t *kv, double *kw, uint32_t *kpos) {
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ unsigned long long s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * kBlock; i0 < k;
+         i0 += (unsigned long long)gridDim.x * kBlock) {
+        const unsigned long long i = i0 + tid;
         uint32_t a = 0, b = 0;
-        uint64_t h = 0;
-        for (int l = 0; l < p.scale; ++l) {
-            if ((l & 3) == 0) h = mix64(p.s0 ^ (i * 16ULL + (unsigned long long)(l >> 2)));
-            const uint32_t x = (uint32_t)((h >> (16 * (l & 3))) & 0xFFFFu);
-            const uint32_t bit = 1u << (p.scale - 1 - l);
-            if (x < p.A) {
-            } else if (x < p.AB) {
-                b |= bit;
-            } else if (x < p.ABC) {
-                a |= bit;
-            } else {
-                a |= bit;
-                b |= bit;
+        double w = 0;
+        bool keep = false;
+        if (i < k) {
+            rmat_one(p, i, a, b, w);
+            const uint32_t lo = a < b ? a : b;
+            keep = a != b && lo >= blo && lo < bhi;   // self-loops dropped (graph.py:89-91)
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_cnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int q = 0; q < kWarps; ++q) t += s_cnt[q];
+            s_base = t ? atomicAdd(cursor, (unsigned long long)t) : 0ULL;
+        }
+        __syncthreads();
+        if (WRITE && keep) {
+            unsigned long long pos = s_base;
+            for (int q = 0; q < warp; ++q) pos += s_cnt[q];
+            pos += __popc(bal & lt);
+            ku[pos] = a;
+            kv[pos] = b;
+            kw[pos] = w;
+            kpos[pos] = (uint32_t)i;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_pair_keys_local(const uint32_t *u, const uint32_t *v, unsigned long long k, int bits,
+                                  unsigned long long *key, uint32_t *idx) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const unsigned long long a = u[i], b = v[i];
+        key[i] = ((a < b ? a : b) << bits) | (a < b ? b : a);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// One thread per run of equal pairs: the first occurrence (smallest raw
+// position) numbers the pair; the kept occurrence is the heaviest, the
+// earliest of equal weights (graph.py:94-100) -- kept order is arbitrary here,
+// so positions decide explicitly.  Sets the first-occurrence bit (global raw
+// position) and counts the pair into both endpoints' degrees.
+__global__ void k_runs_dist(const unsigned long long *key, const uint32_t *idx, unsigned long long k,
+                            const uint32_t *u, const uint32_t *v, const double *w, const uint32_t *pos,
+                            uint32_t *first_bits, uint32_t *deg, uint32_t *pf, uint32_t *pu, uint32_t *pv,
+                            double *pw, unsigned long long *npairs) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const unsigned long long kk = key[i];
+        if (i > 0 && key[i - 1] == kk) continue;
+        uint32_t best = idx[i], first = pos[idx[i]];
+        double bw = w[best];
+        uint32_t bp = first;
+        for (unsigned long long j = i + 1; j < k && key[j] == kk; ++j) {
+            const uint32_t c = idx[j];
+            const uint32_t cp = pos[c];
+            const double cw = w[c];
+            first = cp < first ? cp : first;
+            if (cw > bw || (cw == bw && cp < bp)) {
+                bw = cw;
+                best = c;
+                bp = cp;
             }
         }
-        if (p.permute) {
-            a = rmat_perm(a, p);
-            b = rmat_perm(b, p);
+        atomicOr(first_bits + (first >> 5), 1u << (first & 31));
+        atomicAdd(deg + u[best], 1u);
+        atomicAdd(deg + v[best], 1u);
+        const unsigned long long q = atomicAdd(npairs, 1ULL);
+        pf[q] = first;
+        pu[q] = u[best];
+        pv[q] = v[best];
+        pw[q] = bw;
+    }
+}
+
+__global__ void k_word_popc(const uint32_t *bits, unsigned long long words, unsigned long long *cnt) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= words; i += stride)
+        cnt[i] = i < words ? (unsigned long long)__popc(bits[i]) : 0ULL;
+}
+
+// Records {eid, u, v, w} to the owners of u and v (once if the same):
+// pass 0 counts per destination, pass 1 writes into its region.
+struct DistRec {
+    uint32_t eid, u, v, pad;
+    double w;
+};
+
+template <bool WRITE>
+__global__ void k_route(const uint32_t *pf, const uint32_t *pu, const uint32_t *pv, const double *pw,
+                        unsigned long long np, const uint32_t *first_bits, const unsigned long long *word_prefix,
+                        const unsigned long long *bounds, int p, unsigned long long *cnt,
+                        const unsigned long long *region, DistRec *out) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+        const uint32_t f = pf[i];
+        const uint32_t below = first_bits[f >> 5] & ((1u << (f & 31)) - 1u);
+        const uint32_t eid = (uint32_t)(word_prefix[f >> 5] + (unsigned long long)__popc(below));
+        int ou = 0, ov = 0;
+        while (ou + 1 < p && pu[i] >= bounds[ou + 1]) ++ou;
+        while (ov + 1 < p && pv[i] >= bounds[ov + 1]) ++ov;
+        for (int t = 0; t < (ou == ov ? 1 : 2); ++t) {
+            const int d = t == 0 ? ou : ov;
+            const unsigned long long q = atomicAdd(cnt + d, 1ULL);
+            if (WRITE) {
+                DistRec r;
+                r.eid = eid;
+                r.u = pu[i];
+                r.v = pv[i];
+                r.pad = 0;
+                r.w = pw[i];
+                out[region[d] + q] = r;
+            }
         }
-        u[i] = a;
-        v[i] = b;
-        w[i] = (double)(mix64(p.s1 ^ i) >> 11) * (1.0 / 9007199254740992.0);
+    }
+}
+
+__global__ void k_rec_unpack(const DistRec *rec, const uint32_t *idx, unsigned long long k, uint32_t *eu,
+                             uint32_t *ev, double *w, uint32_t *geid) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        const DistRec r = rec[idx ? idx[i] : i];
+        eu[i] = r.u;
+        ev[i] = r.v;
+        w[i] = r.w;
+        geid[i] = r.eid;
     }
 }
 
@@ -519,6 +671,272 @@ int lmx_graph_export(lmx_ctx *ctx, int64_t *edge_u, int64_t *edge_v, double *edg
         lmx_dfree(ctx, lv);
     }
     LMX_CUDA(ctx, e);
+    return LMX_OK;
+}
+
+}  // extern "C"
+
+// ---- distributed RMAT build (C ABI, see include/lmx.h) ---------------------
+
+namespace lmx {
+__global__ void k_pair_minmax(const double *w, unsigned long long k, unsigned long long *mm) {
+    unsigned long long lo = ~0ULL, hi = 0;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(w[i]);
+        b = (b << 1) == 0 ? 0ULL : b;
+        lo = b < lo ? b : lo;
+        hi = b > hi ? b : hi;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, off);
+        const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+}  // namespace lmx
+
+extern "C" {
+
+// Phase 1: generate the whole raw stream, keep the triples whose lower end is
+// in this rank's build range [rank n / p, (rank + 1) n / p), collapse parallel
+// pairs (graph.py:94-100) and record each pair's first raw position.
+int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                        int permute, void **bits_dev, int64_t *words_out, void **deg_dev, void **minmax_dev) {
+    if (!ctx || !bits_dev || !words_out || !deg_dev || !minmax_dev) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (ctx->dist_p < 2) return lmx_fail(ctx, LMX_ESTATE, "set LMX_OPT_DIST_P > 1 first");
+    LMX_TRY(rmat_check(ctx, scale, edge_factor, a, b, c));
+    const unsigned long long n = 1ULL << scale, k = (unsigned long long)edge_factor << scale;
+    const RmatParams P = rmat_params(scale, a, b, c, seed, permute);
+    const int p = ctx->dist_p, rank = ctx->dist_rank;
+    const uint32_t blo = (uint32_t)(n * (unsigned long long)rank / (unsigned long long)p);
+    const uint32_t bhi = (uint32_t)(n * (unsigned long long)(rank + 1) / (unsigned long long)p);
+    lmx_free_graph(ctx);
+    ctx->n = (int64_t)n;
+    cudaStream_t st = ctx->stream;
+    unsigned long long *cursor = nullptr, *key = nullptr, *key2 = nullptr;
+    uint32_t *ku = nullptr, *kv = nullptr, *kpos = nullptr, *idx = nullptr, *idx2 = nullptr;
+    double *kw = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    unsigned long long K = 0;
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&cursor, 16, "keep cursor")) != LMX_OK) break;
+        e = cudaMemsetAsync(cursor, 0, 16, st);
+        if (e != cudaSuccess) break;
+        k_rmat_keep<false><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, blo, bhi, cursor, nullptr, nullptr, nullptr,
+                                                            nullptr);
+        e = cudaMemcpyAsync(&K, cursor, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) break;
+        const size_t K1 = std::max<unsigned long long>(K, 1);
+        if ((rc = lmx_alloc(ctx, (void **)&ku, K1 * 4, "kept u")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&kv, K1 * 4, "kept v")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&kw, K1 * 8, "kept w")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&kpos, K1 * 4, "kept pos")) != LMX_OK) break;
+        e = cudaMemsetAsync(cursor, 0, 16, st);
+        if (e != cudaSuccess) break;
+        k_rmat_keep<true><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, blo, bhi, cursor, ku, kv, kw, kpos);
+        // group the kept triples by pair
+        const int bits = bits_for(n);
+        if ((rc = lmx_alloc(ctx, (void **)&key, K1 * 8, "pair keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&key2, K1 * 8, "pair keys2")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&idx, K1 * 4, "pair idx")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&idx2, K1 * 4, "pair idx2")) != LMX_OK) break;
+        k_pair_keys_local<<<bgrid(ctx, K1), kBlock, 0, st>>>(ku, kv, K, bits, key, idx);
+        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, (long long)K, 0, 2 * bits, st);
+        if (e != cudaSuccess) break;
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "pair sort tmp")) != LMX_OK) break;
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, (long long)K, 0, 2 * bits, st);
+        if (e != cudaSuccess) break;
+        lmx_free(ctx, (void **)&key, K1 * 8);
+        lmx_free(ctx, (void **)&idx, K1 * 4);
+        lmx_free(ctx, &tmp, tmp_bytes);
+        // pairs, first-occurrence bits, degree contributions
+        ctx->db_words = (k + 31) / 32;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_bits, ctx->db_words * 4, "first-occurrence bits")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->deg0, n * 4, "deg0")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_pf, K1 * 4, "pairs first")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_pu, K1 * 4, "pairs u")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_pv, K1 * 4, "pairs v")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_pw, K1 * 8, "pairs w")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->db_minmax, 16, "pair minmax")) != LMX_OK) break;
+        ctx->db_cap = K1;
+        e = cudaMemsetAsync(ctx->db_bits, 0, ctx->db_words * 4, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(ctx->deg0, 0, n * 4, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(cursor, 0, 16, st);
+        unsigned long long mm0[2] = {~0ULL, 0ULL};
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->db_minmax, mm0, 16, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) break;
+        if (K)
+            k_runs_dist<<<bgrid(ctx, K), kBlock, 0, st>>>(key2, idx2, K, ku, kv, kw, kpos, ctx->db_bits, ctx->deg0,
+                                                         ctx->db_pf, ctx->db_pu, ctx->db_pv, ctx->db_pw, cursor);
+        e = cudaMemcpyAsync(&ctx->db_np, cursor, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) break;
+        if (ctx->db_np)
+            k_pair_minmax<<<bgrid(ctx, ctx->db_np), kBlock, 0, st>>>(ctx->db_pw, ctx->db_np, ctx->db_minmax);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    } while (0);
+    const size_t K1 = std::max<unsigned long long>(K, 1);
+    lmx_free(ctx, (void **)&cursor, 16);
+    lmx_free(ctx, (void **)&key, K1 * 8);
+    lmx_free(ctx, (void **)&key2, K1 * 8);
+    lmx_free(ctx, (void **)&idx, K1 * 4);
+    lmx_free(ctx, (void **)&idx2, K1 * 4);
+    lmx_free(ctx, (void **)&ku, K1 * 4);
+    lmx_free(ctx, (void **)&kv, K1 * 4);
+    lmx_free(ctx, (void **)&kw, K1 * 8);
+    lmx_free(ctx, (void **)&kpos, K1 * 4);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, e);
+    *bits_dev = ctx->db_bits;
+    *words_out = (int64_t)ctx->db_words;
+    *deg_dev = ctx->deg0;
+    *minmax_dev = ctx->db_minmax;
+    return LMX_OK;
+}
+
+// Phase 2 (after the bitmap and the degrees are summed over the ranks): the
+// global edge ids (first occurrences numbered in raw order, graph.py:94-98),
+// partition_graph's cuts on the global degrees, and the records of this
+// rank's pairs packed by destination (the owners of both ends).
+int lmx_dist_rmat_route(lmx_ctx *ctx, void **send_dev, int64_t *counts_out, int64_t *m_out) {
+    if (!ctx || !send_dev || !counts_out || !m_out) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (!ctx->db_bits) return lmx_fail(ctx, LMX_ESTATE, "lmx_dist_rmat_build first");
+    cudaStream_t st = ctx->stream;
+    const int p = ctx->dist_p;
+    const unsigned long long W = ctx->db_words, np = ctx->db_np;
+    unsigned long long *prefix = nullptr, *cnt = nullptr, *region = nullptr, *bdev = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    unsigned long long m = 0;
+    std::vector<unsigned long long> hc((size_t)p, 0), hr((size_t)p + 1, 0);
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&prefix, (W + 1) * 8, "word prefix")) != LMX_OK) break;
+        k_word_popc<<<bgrid(ctx, W + 1), kBlock, 0, st>>>(ctx->db_bits, W, prefix);
+        e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, prefix, prefix, (long long)(W + 1), st);
+        if (e != cudaSuccess) break;
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "prefix tmp")) != LMX_OK) break;
+        e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, prefix, prefix, (long long)(W + 1), st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&m, prefix + W, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) break;
+        if (m >= 0xFFFFFFFFULL) { rc = lmx_fail(ctx, LMX_ELIMIT, "m exceeds the 32-bit edge id range"); break; }
+        ctx->m = (int64_t)m;
+        if ((rc = lmx_partition_bounds(ctx, ctx->bounds)) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&bdev, (size_t)(p + 1) * 8, "bounds")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&cnt, (size_t)p * 8, "route counts")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&region, (size_t)(p + 1) * 8, "route regions")) != LMX_OK) break;
+        std::vector<unsigned long long> hb(ctx->bounds.begin(), ctx->bounds.end());
+        e = cudaMemcpyAsync(bdev, hb.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)p * 8, st);
+        if (e != cudaSuccess) break;
+        if (np)
+            k_route<false><<<bgrid(ctx, np), kBlock, 0, st>>>(ctx->db_pf, ctx->db_pu, ctx->db_pv, ctx->db_pw, np,
+                                                             ctx->db_bits, prefix, bdev, p, cnt, nullptr, nullptr);
+        e = cudaMemcpyAsync(hc.data(), cnt, (size_t)p * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) break;
+        for (int q = 0; q < p; ++q) hr[(size_t)q + 1] = hr[(size_t)q] + hc[(size_t)q];
+        ctx->db_send_n = hr[(size_t)p];
+        if ((rc = lmx_alloc(ctx, &ctx->db_send, std::max<unsigned long long>(ctx->db_send_n, 1) * sizeof(DistRec),
+                            "route records")) != LMX_OK)
+            break;
+        e = cudaMemcpyAsync(region, hr.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)p * 8, st);
+        if (e != cudaSuccess) break;
+        if (np)
+            k_route<true><<<bgrid(ctx, np), kBlock, 0, st>>>(ctx->db_pf, ctx->db_pu, ctx->db_pv, ctx->db_pw, np,
+                                                            ctx->db_bits, prefix, bdev, p, cnt, region,
+                                                            reinterpret_cast<DistRec *>(ctx->db_send));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    } while (0);
+    lmx_free(ctx, (void **)&prefix, (W + 1) * 8);
+    lmx_free(ctx, (void **)&cnt, (size_t)p * 8);
+    lmx_free(ctx, (void **)&region, (size_t)(p + 1) * 8);
+    lmx_free(ctx, (void **)&bdev, (size_t)(p + 1) * 8);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, e);
+    // the build's pair arrays and bitmap are no longer needed
+    lmx_free(ctx, (void **)&ctx->db_bits, W * 4);
+    lmx_free(ctx, (void **)&ctx->db_pf, ctx->db_cap * 4);
+    lmx_free(ctx, (void **)&ctx->db_pu, ctx->db_cap * 4);
+    lmx_free(ctx, (void **)&ctx->db_pv, ctx->db_cap * 4);
+    lmx_free(ctx, (void **)&ctx->db_pw, ctx->db_cap * 8);
+    for (int q = 0; q < p; ++q) counts_out[q] = (int64_t)hc[(size_t)q];
+    *send_dev = ctx->db_send;
+    *m_out = (int64_t)m;
+    return LMX_OK;
+}
+
+int lmx_dist_rmat_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_dev) {
+    if (!ctx || !recv_dev || count < 0) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    lmx_free(ctx, &ctx->db_recv, std::max<unsigned long long>(ctx->db_recv_n, 1) * sizeof(DistRec));
+    ctx->db_recv_n = (unsigned long long)count;
+    LMX_TRY(lmx_alloc(ctx, &ctx->db_recv, std::max<unsigned long long>(ctx->db_recv_n, 1) * sizeof(DistRec),
+                      "received records"));
+    *recv_dev = ctx->db_recv;
+    return LMX_OK;
+}
+
+// Phase 3: the received records are this rank's local edges (bsp.py:86-90),
+// in arrival order (slots carry the global edge ids, so the local order is
+// free); then the partition's K0.
+int lmx_dist_rmat_finish(lmx_ctx *ctx, int w_uniform) {
+    if (!ctx) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (!ctx->db_recv) return lmx_fail(ctx, LMX_ESTATE, "lmx_dist_rmat_recv_buffer first");
+    cudaStream_t st = ctx->stream;
+    const unsigned long long k = ctx->db_recv_n;
+    const size_t k1 = std::max<unsigned long long>(k, 1);
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, st));
+    lmx_free(ctx, &ctx->db_send, std::max<unsigned long long>(ctx->db_send_n, 1) * sizeof(DistRec));
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->eu, k1 * 4, "local edge_u")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->ev, k1 * 4, "local edge_v")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->w, k1 * 8, "local edge_weight")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&ctx->geid, k1 * 4, "local edge ids")) != LMX_OK) break;
+        if (k) {
+            k_rec_unpack<<<bgrid(ctx, k), kBlock, 0, st>>>(reinterpret_cast<const DistRec *>(ctx->db_recv), nullptr,
+                                                          k, ctx->eu, ctx->ev, ctx->w, ctx->geid);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    } while (0);
+    lmx_free(ctx, &ctx->db_recv, k1 * sizeof(DistRec));
+    lmx_free(ctx, (void **)&ctx->db_minmax, 16);
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, e);
+    ctx->m_local = (int64_t)k;
+    ctx->dist_local = true;
+    ctx->w_uniform = w_uniform ? 1 : 0;
+    LMX_TRY(lmx_weight_stage(ctx));   // on the local edges
+    LMX_TRY(lmx_setup_slots(ctx));
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
+    LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->timing.setup_ms = ms;
     return LMX_OK;
 }
 

@@ -193,6 +193,11 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
     if (option == LMX_QUERY_LAYOUT) return ctx->layout;
     if (option == LMX_QUERY_RELABELED) return ctx->relabeled ? 1 : 0;
     if (option == LMX_QUERY_ALGO) return ctx->algo;
+    if (option == LMX_QUERY_PEAK_BYTES) {   // in MiB (the return is an int); value != 0 resets the mark
+        const int r = (int)(ctx->peak_bytes >> 20);
+        if (value) ctx->peak_bytes = ctx->dev_bytes;
+        return r;
+    }
     return lmx_fail(ctx, LMX_EINVAL, "unknown option");
 }
 

@@ -141,6 +141,7 @@ struct lmx_ctx {
     void *sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
     int64_t dev_bytes = 0;
+    int64_t peak_bytes = 0;                  // high-water mark of dev_bytes (LMX_QUERY_PEAK_BYTES)
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     lmx_timing timing{};
@@ -164,6 +165,15 @@ struct lmx_ctx {
     uint32_t *geid = nullptr;                // local edge -> global edge id (null: identity)
     int w_uniform = -1;                      // all weights equal (global; decided before the filter)
     uint32_t *slot_side = nullptr;           // partitions: bit per owned slot, 1 = the owner is the edge's v end
+    // distributed RMAT build state (lmx_dist_rmat_*; freed by lmx_dist_rmat_finish)
+    uint32_t *db_bits = nullptr;             // first-occurrence bitmap over the raw positions
+    unsigned long long db_words = 0;
+    uint32_t *db_pf = nullptr, *db_pu = nullptr, *db_pv = nullptr;   // this rank's built pairs
+    double *db_pw = nullptr;
+    unsigned long long db_np = 0, db_cap = 0;
+    unsigned long long *db_minmax = nullptr; // weight bits min / max of the rank's pairs
+    void *db_send = nullptr, *db_recv = nullptr;
+    unsigned long long db_send_n = 0, db_recv_n = 0;
     bool dist_requested = false;             // LMX_OPT_DIST_P was set: stepped protocol
     uint32_t *mround = nullptr;              // scan: round each vertex was matched in (~0 never)
     unsigned long long *lowbeg = nullptr;    // scan (load time only): [n+1] offsets of lowpair
@@ -218,6 +228,7 @@ int lmx_setup_slots(lmx_ctx *ctx);   // builds vbeg/ids0/(wk0)/bins0 from eu/ev/
 int lmx_setup_device_edges(lmx_ctx *ctx);   // deg0 + weight stage + lmx_setup_slots for built eu/ev/w
 int lmx_alloc_match_state(lmx_ctx *ctx);
 int lmx_weight_stage(lmx_ctx *ctx);
+int lmx_partition_bounds(lmx_ctx *ctx, std::vector<int64_t> &bounds);   // bsp.py:60-98 on ctx->deg0
 // edges held in ctx->eu / ev / w (all of them, or a partition's local edges)
 inline int64_t lmx_edges(const lmx_ctx *ctx) { return ctx->dist_local ? ctx->m_local : ctx->m; }
 void trace_mark(lmx_ctx *ctx, const char *what);   // LMX_TRACE_SETUP=1: K0 stage times

@@ -100,8 +100,7 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, 
 __global__ void __launch_bounds__(kBlock) k_scan_post(const uint32_t *owner, uint2 *ids, const double *w,
                                                       unsigned long long S, uint32_t lo, uint2 *cand0,
                                                       uint2 *lowpair, unsigned long long *counts,
-                                                      const uint32_t *geid, uint32_t *side,
-                                                      const uint2 *sorted_vals) {
+                                                      uint32_t *side) {
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ unsigned long long s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -116,25 +115,26 @@ __global__ void __launch_bounds__(kBlock) k_scan_post(const uint32_t *owner, uin
         if (i < S) {
             const uint32_t o = owner[i];
             const bool head = i == 0 || owner[i - 1] != o;
-            uint2 x = sorted_vals[i];
+            uint2 x = ids[i];
             nbr = x.x & kSlotNbr;
             if (side && (x.x & kSlotRunStart)) atomicOr(side + (i >> 5), 1u << (i & 31));
             uint32_t flags = 0;
             if (x.x & kSlotTied) {   // the weight occurs more than once: compare with the neighbours
                 const unsigned long long k = canon_bits2(w[x.y]);
-                const bool prev = !head && (sorted_vals[i - 1].x & kSlotTied) &&
-                                  canon_bits2(w[sorted_vals[i - 1].y]) == k;
-                const bool next = i + 1 < S && owner[i + 1] == o && (sorted_vals[i + 1].x & kSlotTied) &&
-                                  canon_bits2(w[sorted_vals[i + 1].y]) == k;
+                // (in place: a neighbour may already hold its final flags, but its
+                // tied bit only clears when its weight differs from both
+                // neighbours', and .y -- the local edge -- is not rewritten here)
+                const bool prev = !head && (ids[i - 1].x & kSlotTied) && canon_bits2(w[ids[i - 1].y]) == k;
+                const bool next = i + 1 < S && owner[i + 1] == o && (ids[i + 1].x & kSlotTied) &&
+                                  canon_bits2(w[ids[i + 1].y]) == k;
                 if (prev || next) flags = kSlotTied | (prev ? 0u : kSlotRunStart);
                 tied_n += (prev || next) ? 1u : 0u;
             }
             x.x = nbr | flags;
-            if (geid) x.y = geid[x.y];   // local edge index -> the global edge id (salts, outputs)
             if (head) cand0[o] = x;
             vdev = o + lo;
             emit = nbr < vdev;
-            ids[i] = x;
+            ids[i].x = x.x;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, emit);
         if (lane == 0) s_cnt[warp] = __popc(bal);
@@ -155,6 +155,27 @@ __global__ void __launch_bounds__(kBlock) k_scan_post(const uint32_t *owner, uin
     for (int off = 16; off > 0; off >>= 1) tied_n += __shfl_xor_sync(0xffffffffu, tied_n, off);
     if (lane == 0 && tied_n) atomicAdd(counts, tied_n);
 }
+
+// A partition's slots and round-0 candidates name local edges until here:
+// to the global edge ids (salts, exchange records, outputs).
+__global__ void k_to_global_eid(uint2 *ids, unsigned long long S, uint2 *cand0, unsigned long long nl,
+                                const uint32_t *geid) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < S + nl; i += stride) {
+        if (i < S) ids[i].y = geid[ids[i].y];
+        else if (cand0[i - S].x != kNone) cand0[i - S].y = geid[cand0[i - S].y];
+    }
+}
+
+struct OwnedKey {
+    uint32_t nl;
+    __host__ __device__ __forceinline__ bool operator()(const uint32_t &k) const { return k < nl; }
+};
+
+struct OwnedFlag {
+    uint32_t nl;
+    __host__ __device__ __forceinline__ char operator()(const uint32_t &k) const { return k < nl ? 1 : 0; }
+};
 
 }  // namespace lmx
 
@@ -192,12 +213,12 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     ctx->slots_local = (int64_t)S;
     const size_t S1 = std::max<unsigned long long>(S, 1), M2 = std::max<unsigned long long>(slots2, 1);
-    // one GPU: the sort writes ids0 and the post pass works in place; a
-    // partition sorts its whole local stream (2 m_local, non-owned slots last)
-    // into a scratch buffer and the post pass writes the owned prefix into ids0
+    // one GPU: the stream is sorted straight into ids0; a partition first
+    // selects its owned slots (weight order kept), then sorts those
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->ids0, S1 * 8, "ids0"));
     uint32_t *okey = nullptr, *okey2 = nullptr;
     uint2 *sval = nullptr, *sorted = nullptr;
+    const bool part = ctx->dist_p > 1;
     unsigned long long *cnt = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -208,8 +229,6 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
         if ((rc = lmx_alloc(ctx, (void **)&okey, M2 * 4, "owner keys")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&okey2, M2 * 4, "owner keys out")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&sval, M2 * 8, "slot stream")) != LMX_OK) break;
-        if (ctx->dist_p > 1 && (rc = lmx_alloc(ctx, (void **)&sorted, M2 * 8, "sorted stream")) != LMX_OK) break;
-        uint2 *sort_out = ctx->dist_p > 1 ? sorted : ctx->ids0;
         if ((rc = lmx_alloc(ctx, (void **)&cnt, 16, "counts")) != LMX_OK) break;
         cudaError_t e = cudaMemsetAsync(cnt, 0, 16, st);
         if (m && e == cudaSuccess) {
@@ -222,18 +241,56 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
         }
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "slot stream"); break; }
         trace_mark(ctx, "  scan: slot stream");
-        if (m) {
-            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, sort_out, (long long)slots2,
+        const uint32_t *owner = okey2;   // owner of each sorted slot, for the post pass
+        if (m && !part) {
+            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2,
                                                 0, bits, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
             if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, sort_out, (long long)slots2, 0,
+            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2, 0,
                                                 bits, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
             trace_mark(ctx, "  scan: owner sort");
+        } else if (m) {
+            // the owned slots, weight order kept: keys -> okey2, values -> ids0
+            unsigned long long *nsel = nullptr;
+            if ((rc = lmx_alloc(ctx, (void **)&nsel, 8, "selected")) != LMX_OK) break;
+            cub::TransformInputIterator<char, OwnedFlag, const uint32_t *> flags(okey, OwnedFlag{(uint32_t)nl});
+            size_t t1 = 0, t2 = 0;
+            e = cub::DeviceSelect::If(nullptr, t1, okey, okey2, nsel, (long long)slots2, OwnedKey{(uint32_t)nl}, st);
+            if (e == cudaSuccess)
+                e = cub::DeviceSelect::Flagged(nullptr, t2, sval, flags, ctx->ids0, nsel, (long long)slots2, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "select sizing"); break; }
+            tmp_bytes = std::max(t1, t2);
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "select tmp")) != LMX_OK) break;
+            e = cub::DeviceSelect::If(tmp, t1, okey, okey2, nsel, (long long)slots2, OwnedKey{(uint32_t)nl}, st);
+            if (e == cudaSuccess)
+                e = cub::DeviceSelect::Flagged(tmp, t2, sval, flags, ctx->ids0, nsel, (long long)slots2, st);
+            unsigned long long got = 0;
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&got, nsel, 8, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            lmx_free(ctx, (void **)&nsel, 8);
+            lmx_free(ctx, &tmp, tmp_bytes);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owned select"); break; }
+            if (got != S) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: owned slot count"); break; }
+            lmx_free(ctx, (void **)&sval, M2 * 8);
+            // stable sort of the S owned slots by owner: okey2 -> okey, ids0 -> sorted
+            if ((rc = lmx_alloc(ctx, (void **)&sorted, S1 * 8, "sorted slots")) != LMX_OK) break;
+            tmp_bytes = 0;
+            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey2, okey, ctx->ids0, sorted, (long long)S, 0,
+                                                bits, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
+            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey2, okey, ctx->ids0, sorted, (long long)S, 0,
+                                                bits, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
+            lmx_free(ctx, (void **)&ctx->ids0, S1 * 8);
+            ctx->ids0 = sorted;
+            sorted = nullptr;
+            owner = okey;
+            trace_mark(ctx, "  scan: owned select + owner sort");
         }
         lmx_free(ctx, (void **)&sval, M2 * 8);
-        lmx_free(ctx, (void **)&okey, M2 * 4);
         lmx_free(ctx, &tmp, tmp_bytes);
         // 4. flags, cand0, lowpair over the owned prefix [0, S)
         if ((rc = lmx_alloc(ctx, (void **)&ctx->cand0, std::max<unsigned long long>(nl, 1) * 8, "cand0")) != LMX_OK)
@@ -247,8 +304,12 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
             e = cudaMemsetAsync(ctx->slot_side, 0, (S1 + 31) / 32 * 4, st);
         }
         if (e == cudaSuccess && S) {
-            k_scan_post<<<lgrid(ctx, S), kBlock, 0, st>>>(okey2, ctx->ids0, ctx->w, S, (uint32_t)lo, ctx->cand0,
-                                                         ctx->lowpair, cnt, ctx->geid, ctx->slot_side, sort_out);
+            k_scan_post<<<lgrid(ctx, S), kBlock, 0, st>>>(owner, ctx->ids0, ctx->w, S, (uint32_t)lo, ctx->cand0,
+                                                         ctx->lowpair, cnt, ctx->slot_side);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess && ctx->geid && S + nl) {
+            k_to_global_eid<<<lgrid(ctx, S + nl), kBlock, 0, st>>>(ctx->ids0, S, ctx->cand0, nl, ctx->geid);
             e = cudaGetLastError();
         }
         unsigned long long hc[2] = {0, 0};
@@ -263,7 +324,7 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     lmx_free(ctx, (void **)&okey, M2 * 4);
     lmx_free(ctx, (void **)&okey2, M2 * 4);
     lmx_free(ctx, (void **)&sval, M2 * 8);
-    lmx_free(ctx, (void **)&sorted, M2 * 8);
+    lmx_free(ctx, (void **)&sorted, S1 * 8);
     lmx_free(ctx, (void **)&cnt, 16);
     lmx_free(ctx, &tmp, tmp_bytes);
     return rc;

@@ -95,6 +95,7 @@ int lmx_alloc(lmx_ctx *ctx, void **p, size_t bytes, const char *what) {
                             ": " + cudaGetErrorString(e));
     }
     ctx->dev_bytes += (int64_t)bytes;
+    ctx->peak_bytes = std::max(ctx->peak_bytes, ctx->dev_bytes);
     return LMX_OK;
 }
 
@@ -122,7 +123,10 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->ws_eid,   (void **)&ctx->ws_tied,     (void **)&ctx->ws_tidx,
                      (void **)&ctx->rbm_prop, (void **)&ctx->rbm_acc,     (void **)&ctx->rbm_blue,
                      (void **)&ctx->rbm_list[0], (void **)&ctx->rbm_list[1], (void **)&ctx->rbm_list0,
-                     (void **)&ctx->geid,     (void **)&ctx->slot_side};
+                     (void **)&ctx->geid,     (void **)&ctx->slot_side,
+                     (void **)&ctx->db_bits,  (void **)&ctx->db_pf,       (void **)&ctx->db_pu,
+                     (void **)&ctx->db_pv,    (void **)&ctx->db_pw,       (void **)&ctx->db_minmax,
+                     (void **)&ctx->db_send,  (void **)&ctx->db_recv};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -132,6 +136,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->dist_local = false;
     ctx->m_local = 0;
     ctx->w_uniform = -1;
+    ctx->db_words = ctx->db_np = ctx->db_cap = ctx->db_send_n = ctx->db_recv_n = 0;
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
@@ -570,7 +575,7 @@ void lmx_free_weight_stage(lmx_ctx *ctx) {
 // degree prefix: cut k = searchsorted(offsets, k * 2m / p, side="left") as
 // numpy compares int64 offsets with float64 targets; the host then forces
 // them strictly increasing and leaves each later worker a vertex (:78-81).
-static int partition_bounds(lmx_ctx *ctx, std::vector<int64_t> &bounds) {
+int lmx_partition_bounds(lmx_ctx *ctx, std::vector<int64_t> &bounds) {
     const int p = ctx->dist_p;
     const unsigned long long n = (unsigned long long)ctx->n;
     bounds.assign(2, 0);
@@ -702,7 +707,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     const unsigned long long n = (unsigned long long)ctx->n, m = (unsigned long long)ctx->m;
     cudaStream_t st = ctx->stream;
     // 1D vertex partition (bsp.py:60-98), caller ids; single GPU: [0, n)
-    LMX_TRY(partition_bounds(ctx, ctx->bounds));
+    LMX_TRY(lmx_partition_bounds(ctx, ctx->bounds));
     ctx->lo = (unsigned long long)ctx->bounds[(size_t)ctx->dist_rank];
     ctx->hi = (unsigned long long)ctx->bounds[(size_t)ctx->dist_rank + 1];
     const unsigned long long lo = ctx->lo, nl = ctx->hi - ctx->lo;

@@ -148,6 +148,12 @@ def _bind(lib):
         "lmx_dist_mround": (c_int, [p, ctypes.POINTER(p)]),
         "lmx_dist_hist": (c_int, [p, c_int, ctypes.POINTER(p), ctypes.POINTER(c_int)]),
         "lmx_dist_messages": (c_int, [p, c_int, ctypes.POINTER(p)]),
+        "lmx_dist_rmat_build": (c_int, [p, c_int, c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, u64,
+                                        c_int, ctypes.POINTER(p), ctypes.POINTER(i64), ctypes.POINTER(p),
+                                        ctypes.POINTER(p)]),
+        "lmx_dist_rmat_route": (c_int, [p, ctypes.POINTER(p), p, ctypes.POINTER(i64)]),
+        "lmx_dist_rmat_recv_buffer": (c_int, [p, i64, ctypes.POINTER(p)]),
+        "lmx_dist_rmat_finish": (c_int, [p, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -176,12 +182,13 @@ class DistRank:
     """One partition: a liblmx context loaded with LMX_OPT_DIST_P / RANK."""
 
     def __init__(self, g, p: int, rank: int, device: int = 0, stream=None, rmat: dict | None = None,
-                 algo: str = "auto"):
+                 algo: str = "auto", defer: bool = False):
         """Load partition `rank` of `p` from a host graph `g`, or, with
         ``rmat=dict(scale=..., edge_factor=..., seed=...)``, from the device
         RMAT generator (every rank generates the same graph and keeps its part).
         ``algo`` picks the round loop as ``Engine.set_algo`` does ("auto":
-        the scan loop when the weights are distinct)."""
+        the scan loop when the weights are distinct).  ``defer=True`` only
+        creates the context: ``build_rmat_distributed`` then loads it."""
         import torch
         self.eng = Engine(device)
         self.lib = self.eng._lib
@@ -195,10 +202,16 @@ class DistRank:
         self._opt(LMX_OPT_DIST_P, p)
         self._opt(LMX_OPT_DIST_RANK, rank)
         self.eng.set_algo(algo)
+        if defer:
+            return
         if rmat is not None:
             self.eng.gen_rmat(**rmat)
         else:
             self.eng.load_graph(g)
+        self._after_load()
+
+    def _after_load(self):
+        p, rank = self.p, self.rank
         self.n, self.m = self.eng.graph_size()
         b = np.zeros(p + 1, dtype=np.int64)
         self._chk(self.lib.lmx_dist_bounds(self.eng._h, b.ctypes.data), "lmx_dist_bounds")
@@ -283,6 +296,53 @@ class DistRank:
         self.eng.close()
 
 
+def build_rmat_distributed(ranks, comm, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+                           c: float = 0.19, seed: int = 1, permute: bool = True):
+    """Load the local partitions ``ranks`` (created with ``defer=True``) with the
+    RMAT graph of ``lmx_gen_rmat``'s recipe WITHOUT any rank holding the whole
+    graph (config C5): each rank builds the pairs whose lower end is in its
+    build range, the first-occurrence bitmaps and the degrees are summed over
+    the ranks (the global edge ids and partition_graph's cuts follow), and
+    every pair is sent to the owners of its ends (all-to-all-v)."""
+    import torch
+    bits, degs, mms = [], [], []
+    for r in ranks:
+        bp, dp, mp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        words = ctypes.c_int64()
+        r._chk(r.lib.lmx_dist_rmat_build(r.eng._h, scale, edge_factor, a, b, c, seed & ((1 << 64) - 1),
+                                         int(permute), ctypes.byref(bp), ctypes.byref(words), ctypes.byref(dp),
+                                         ctypes.byref(mp)), "lmx_dist_rmat_build")
+        bits.append(_view(bp.value, (max(words.value, 1),), "<i4", r.device))
+        degs.append(_view(dp.value, (1 << scale,), "<i4", r.device))
+        mms.append(_view(mp.value, (2,), "<i8", r.device))
+    # disjoint bit sets: an int32 sum is their OR; degree contributions add
+    comm.allreduce_sum_(ranks, bits)
+    comm.allreduce_sum_(ranks, degs)
+    lo = comm.allreduce_min_u64(ranks, [m_[0:1] for m_ in mms])
+    hi = comm.allreduce_max_u64(ranks, [m_[1:2] for m_ in mms])
+    uniform = int(lo == hi)
+    sends = []
+    for r in ranks:
+        sp = ctypes.c_void_p()
+        counts = np.zeros(r.p, dtype=np.int64)
+        mtot = ctypes.c_int64()
+        r._chk(r.lib.lmx_dist_rmat_route(r.eng._h, ctypes.byref(sp), counts.ctypes.data, ctypes.byref(mtot)),
+               "lmx_dist_rmat_route")
+        total = int(counts.sum())
+        sends.append((_view(sp.value, (max(total, 1), 6), "<i4", r.device), counts))
+    recvs = comm.alltoallv_records(ranks, sends, 6, lambda r, cnt: _recv_records(r, cnt))
+    for r, cnt in zip(ranks, recvs):
+        r._chk(r.lib.lmx_dist_rmat_finish(r.eng._h, uniform), "lmx_dist_rmat_finish")
+        r._after_load()
+    torch.cuda.synchronize()
+
+
+def _recv_records(r, count: int):
+    rp = ctypes.c_void_p()
+    r._chk(r.lib.lmx_dist_rmat_recv_buffer(r.eng._h, int(count), ctypes.byref(rp)), "lmx_dist_rmat_recv_buffer")
+    return _view(rp.value, (max(int(count), 1), 6), "<i4", r.device)
+
+
 class LocalComm:
     """All p partitions in this process (one GPU): collectives are device copies."""
 
@@ -334,6 +394,36 @@ class LocalComm:
 
     def allreduce_sum(self, values):
         return [sum(col) for col in zip(*(v.tolist() for v in values))]
+
+    def allreduce_sum_(self, ranks, tensors):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        for t in tensors:
+            t.copy_(total)
+
+    def allreduce_min_u64(self, ranks, tensors):
+        return min(int(t.item()) & ((1 << 64) - 1) for t in tensors)
+
+    def allreduce_max_u64(self, ranks, tensors):
+        return max(int(t.item()) & ((1 << 64) - 1) for t in tensors)
+
+    def alltoallv_records(self, ranks, sends, width, recv_buffer):
+        """sends[k] = (records [*, width] int32 packed by destination, int64 counts[p])."""
+        import torch
+        counts_h = [c.tolist() if hasattr(c, "tolist") else list(c) for _, c in sends]
+        out = []
+        for dst in range(self.p):
+            parts = []
+            for src in range(self.p):
+                off = int(sum(counts_h[src][:dst]))
+                parts.append(sends[src][0][off: off + int(counts_h[src][dst])])
+            total = sum(int(x.shape[0]) for x in parts)
+            buf = recv_buffer(ranks[dst], total)
+            if total:
+                buf[:total].copy_(torch.cat(parts, dim=0))
+            out.append(total)
+        return out
 
     def gather_outputs(self, ranks):
         import torch
@@ -447,6 +537,39 @@ class TorchComm:
         t = vals.clone()   # device int64[k]
         self.dist.all_reduce(t)
         return [int(x) for x in t.tolist()]
+
+    def allreduce_sum_(self, ranks, tensors):
+        (t,) = tensors
+        self.dist.all_reduce(t)
+
+    def _u64_extreme(self, tensors, op):
+        import torch
+        (t,) = tensors
+        # u64 weight bits of non-negative doubles stay below 2^63: int64 compare is exact
+        x = t.clone()
+        self.dist.all_reduce(x, op=op)
+        return int(x.item()) & ((1 << 64) - 1)
+
+    def allreduce_min_u64(self, ranks, tensors):
+        return self._u64_extreme(tensors, self.dist.ReduceOp.MIN)
+
+    def allreduce_max_u64(self, ranks, tensors):
+        return self._u64_extreme(tensors, self.dist.ReduceOp.MAX)
+
+    def alltoallv_records(self, ranks, sends, width, recv_buffer):
+        import torch
+        (me,), ((send, counts),) = ranks, sends
+        dev = me.device
+        sc = torch.as_tensor(np.asarray(counts), dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc)
+        scounts, rcounts = [int(x) for x in sc.tolist()], [int(x) for x in rc.tolist()]
+        total = sum(rcounts)
+        recv = recv_buffer(me, total)
+        flat_in = send[: sum(scounts)].reshape(-1)
+        flat_out = recv[:total].reshape(-1) if total else torch.empty(0, dtype=torch.int32, device=dev)
+        self.dist.all_to_all_single(flat_out, flat_in, [width * c for c in rcounts], [width * c for c in scounts])
+        return [total]
 
     def gather_outputs(self, ranks):
         (me,) = ranks
@@ -640,6 +763,34 @@ def local_max_dist(g, p: int, seed: int, rerandomize: bool = True, device: int =
     trace.exchange_a_records = records   # this engine's own per-round record counts
     trace.wall_millis = (time.perf_counter() - t0) * 1000.0
     return Matching(ids, mate_h), trace
+
+
+def local_max_dist_rmat(p: int, scale: int, seed: int, rerandomize: bool = True, edge_factor: int = 16,
+                        a: float = 0.57, b: float = 0.19, c: float = 0.19, graph_seed: int = 1,
+                        permute: bool = True, device: int = 0):
+    """p partitions in this process, built by the distributed RMAT builder
+    (no rank ever holds the whole graph), then the bsp_local_max protocol.
+    Returns (Matching, PhaseTrace, per-rank (device bytes after the load,
+    high-water mark during it))."""
+    import torch
+    torch.cuda.set_device(device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    ranks = [DistRank(None, p, k, device, stream, defer=True) for k in range(p)]
+    try:
+        comm = LocalComm(p)
+        build_rmat_distributed(ranks, comm, scale, edge_factor, a, b, c, graph_seed, permute)
+        dev_bytes = [(r.eng.device_bytes(), r.eng.peak_device_bytes()) for r in ranks]
+        stats, records = run_rounds(ranks, comm, seed, rerandomize)
+        messages = round_messages(ranks, comm, len(stats))
+        mate, ebits = comm.gather_outputs(ranks)
+        ids = _unpack_ids(ebits, ranks[0].m)
+        mate_h = mate.cpu().numpy()[: ranks[0].n].copy()
+    finally:
+        for r in ranks:
+            r.close()
+    trace = PhaseTrace(rounds=stats, messages=messages)
+    trace.exchange_a_records = records
+    return Matching(ids, mate_h), trace, dev_bytes
 
 
 def local_max_torchdist(g, seed: int, rerandomize: bool = True):

@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = (
     "lmx_graph_export", "lmx_device_bytes", "lmx_set_option", "lmx_validate", "lmx_rbm",
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
-    "lmx_dist_messages", "lmx_pram_cross",
+    "lmx_dist_messages", "lmx_pram_cross", "lmx_dist_rmat_build", "lmx_dist_rmat_route",
+    "lmx_dist_rmat_recv_buffer", "lmx_dist_rmat_finish",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
 )
 LMX_OPT_KERNEL_TIMING = 1
@@ -268,6 +269,10 @@ class Engine:
         self._check(self._lib.lmx_graph_export(self._h, _ptr(eu), _ptr(ev), _ptr(w), LMX_DEVICE),
                     "lmx_graph_export")
         return eu[:m], ev[:m], w[:m]
+
+    def peak_device_bytes(self, reset: bool = False) -> int:
+        """High-water mark of the context's device allocations (LMX_QUERY_PEAK_BYTES)."""
+        return int(self._lib.lmx_set_option(self._h, 103, int(reset))) << 20
 
     def device_bytes(self) -> int:
         return int(self._lib.lmx_device_bytes(self._h))

@@ -49,6 +49,28 @@ def main():
                 print(f"case seed={seed} n={n} kind={kind} algo={algo} rr={rr} rounds={len(stats)} "
                       f"cut-records={sum(records)} ok={ok}", flush=True)
                 failures += 0 if ok else 1
+    # the distributed builder's collectives (TorchComm side) on CPU tensors
+    class _R:
+        device = torch.device("cpu")
+    me = _R()
+    t = torch.tensor([1 << (3 * comm.rank), 7 + comm.rank], dtype=torch.int32)
+    comm.allreduce_sum_([me], [t])
+    lo = comm.allreduce_min_u64([me], [torch.tensor([100 + comm.rank], dtype=torch.int64)])
+    hi = comm.allreduce_max_u64([me], [torch.tensor([100 + comm.rank], dtype=torch.int64)])
+    # rank k sends k + 1 records of width 6 to every rank
+    counts = np.array([comm.rank + 1] * comm.p, dtype=np.int64)
+    send = torch.arange(int(counts.sum()) * 6, dtype=torch.int32).reshape(-1, 6) + 1000 * comm.rank
+    box = {}
+
+    def recv_buffer(r, cnt):
+        box["buf"] = torch.zeros((max(cnt, 1), 6), dtype=torch.int32)
+        return box["buf"]
+    (got,) = comm.alltoallv_records([me], [(send, counts)], 6, recv_buffer)
+    want_total = sum(k + 1 for k in range(comm.p))
+    ok = (t.tolist() == [1 + 8, 7 + 8] and lo == 100 and hi == 100 + comm.p - 1 and got == want_total
+          and int(box["buf"][0, 0]) == 6 * (comm.rank * 1))
+    print(f"collectives rank={comm.rank} ok={ok}", flush=True)
+    failures += 0 if ok else 1
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(1 if failures else 0)

@@ -53,7 +53,7 @@ def test_gloo_world_size_2_matches_oracle():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
-    assert out.count("ok=True") == 16 and "algo=scan" in out, out[-4000:]
+    assert out.count("ok=True") == 18 and "algo=scan" in out, out[-4000:]
 
 
 @pytest.mark.gpu
@@ -214,3 +214,22 @@ def test_reference_bsp_assertions_with_b200_engine():
     n2, eu2, ev2, w2 = O.gen_random(4096, alpha, 5)
     assert partition_graph(Graph(n1, eu1, ev1, w1), 8).cut_fraction < \
         partition_graph(Graph(n2, eu2, ev2, w2), 8).cut_fraction
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("scale,permute", [(12, True), (15, True), (14, False)])
+def test_distributed_rmat_build_equals_single_gpu(engine, p, scale, permute):
+    """The distributed builder (every rank keeps the pairs of its build range,
+    bitmaps + degrees summed, records routed to the owners) gives the same
+    graph: the matching, RoundStats and edge count equal the single-GPU run on
+    lmx_gen_rmat's graph."""
+    from paper_1302_4587_b200.dist import local_max_dist_rmat
+    engine.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=3, permute=permute)
+    n, m = engine.graph_size()
+    mate, ids, rounds = engine.match_raw(5, True)
+    matching, trace, dev_bytes = local_max_dist_rmat(p, scale, 5, True, graph_seed=3, permute=permute)
+    assert np.array_equal(np.asarray(matching.mate), mate)
+    assert np.array_equal(matching.sorted_edge_ids(), ids)
+    assert trace.rounds == rounds and rounds[0].edges_before == m
+    assert len(dev_bytes) == p
