@@ -639,7 +639,10 @@ def run_b200(args):
         Te = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1000.0)
         assert hrounds == rounds and np.array_equal(hids, ids_h) and np.array_equal(hmate, mate_h)
         e2e = {"value": m * e2e_steps / (Te / 1000.0), "unit": "edges/s",
-               "h2d_bytes_per_step": int(m * 24), "d2h_bytes_per_step": int(n * 8 + n_matched * 8),
+               "h2d_bytes_per_step": int(m * 16), "d2h_bytes_per_step": int(n * 8 + n_matched * 8),
+               "h2d_note": "host arrays read: m*24 B (int64 u, v, f64 w); crossing the link: m*16 B -- the "
+                           "endpoints are range-checked and narrowed to u32 by host threads into a pinned "
+                           "staging ring (csrc/lmx_hostload.cpp, lmx_setup.cu load_host_narrowed)",
                "ms_per_step": Te / e2e_steps, "steps": e2e_steps,
                "setup_ms_last": eng.last_timing()["setup_ms"],
                "api": "Engine.load_graph(Graph of pinned host arrays) + Engine.match_raw (lmx_load_graph + "

@@ -81,6 +81,10 @@ void lmx_destroy(lmx_ctx *ctx) {
     for (cudaEvent_t e : ctx->ev_copy)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (cudaEvent_t e : ctx->stage_ev) cudaEventDestroy(e);
+    if (ctx->ev_deg) cudaEventDestroy(ctx->ev_deg);
+    if (ctx->deg_stream) cudaStreamDestroy(ctx->deg_stream);
+    if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -192,6 +192,12 @@ struct lmx_ctx {
     uint32_t *ws_rank = nullptr, *ws_eid = nullptr, *ws_tied = nullptr, *ws_tidx = nullptr;   // by sorted position
     cudaStream_t copy_stream = nullptr;      // pinned-host loads: copy engine stream
     cudaEvent_t ev_copy[3] = {nullptr, nullptr, nullptr};
+    // host loads: pinned staging ring of the narrowing workers (kept across loads)
+    void *stage_host = nullptr;
+    size_t stage_bytes = 0;
+    std::vector<cudaEvent_t> stage_ev;       // one per ring slot
+    cudaStream_t deg_stream = nullptr;       // per-block degree counts behind the copies
+    cudaEvent_t ev_deg = nullptr;
     unsigned long long *hist = nullptr;      // scan: death-round histogram
     size_t hist_cap = 0;
 

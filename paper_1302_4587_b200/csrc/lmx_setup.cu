@@ -15,11 +15,15 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
 
 #include "lmx_internal.cuh"
 
@@ -479,6 +483,7 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
             e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort"); break; }
+            trace_mark(ctx, "  weight sort");
             // dense rank of the weight value (vals reused)
             k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
             e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
@@ -897,6 +902,162 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     return LMX_OK;
 }
 
+// Host-memory loads.  The int64 endpoint arrays are narrowed to u32 (and
+// range-checked) by a pool of host threads into a pinned staging ring and the
+// copy engine moves the narrowed blocks: 8 instead of 16 bytes per edge cross
+// the host link, which is what bounds the load from host memory.  The weights
+// go first (directly when they are page-locked) so the weight-key stage runs
+// on the device while the endpoint blocks are still arriving; each block's
+// degree counts run on a third stream right behind its copy.
+bool lmx_narrow_block(const int64_t *u, const int64_t *v, size_t k, uint64_t n, uint32_t *ou, uint32_t *ov);
+
+namespace {
+
+int load_threads() {
+    const char *env = getenv("LMX_LOAD_THREADS");
+    int t = env ? atoi(env) : (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(t, 64));
+}
+
+}  // namespace
+
+// Fills ctx->eu/ev/w/deg0 from host arrays; *host_bad = the first edge whose
+// endpoints fail check_uv (or ~0); device-side weight checks go to `bad`.
+// *weights_done: the weight-key stage already ran (page-locked weights).
+static int load_host_narrowed(lmx_ctx *ctx, const int64_t *edge_u, const int64_t *edge_v, const double *edge_weight,
+                              unsigned long long *bad, unsigned long long *host_bad, bool *weights_done) {
+    const unsigned long long m = (unsigned long long)ctx->m;
+    const uint64_t n = (uint64_t)ctx->n;
+    cudaStream_t st = ctx->stream;
+    bool w_pinned = !getenv("LMX_NO_ZEROCOPY");
+    if (w_pinned) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, edge_weight) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            w_pinned = false;
+        }
+    }
+    const auto t_start = std::chrono::steady_clock::now();
+    const int T = load_threads();
+    const int R = getenv("LMX_LOAD_RING") ? std::max(2, atoi(getenv("LMX_LOAD_RING"))) : 4;
+    unsigned long long B = std::max<unsigned long long>(1ULL << 14, (m + 4ULL * T - 1) / (4ULL * T));
+    B = std::min<unsigned long long>(B, 1ULL << 20);
+    const size_t slot_bytes = (size_t)B * (w_pinned ? 8 : 16);
+    const size_t ring = slot_bytes * T * R;
+    if (ctx->stage_bytes < ring) {
+        if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
+        ctx->stage_host = nullptr;
+        ctx->stage_bytes = 0;
+        LMX_CUDA(ctx, cudaHostAlloc(&ctx->stage_host, ring, cudaHostAllocPortable));
+        ctx->stage_bytes = ring;
+    }
+    while (ctx->stage_ev.size() < (size_t)T * R) {
+        cudaEvent_t e;
+        LMX_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->stage_ev.push_back(e);
+    }
+    if (!ctx->copy_stream) {
+        LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t &e : ctx->ev_copy) LMX_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if (!ctx->deg_stream) {
+        LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->deg_stream, cudaStreamNonBlocking));
+        LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_deg, cudaEventDisableTiming));
+    }
+    cudaStream_t cs = ctx->copy_stream, ds = ctx->deg_stream;
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[0], st));   // allocations / memsets before the copies
+    LMX_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_copy[0], 0));
+    LMX_CUDA(ctx, cudaStreamWaitEvent(ds, ctx->ev_copy[0], 0));
+    if (w_pinned) {
+        LMX_CUDA(ctx, cudaMemcpyAsync(ctx->w, edge_weight, (size_t)m * 8, cudaMemcpyHostToDevice, cs));
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[1], cs));
+        LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copy[1], 0));
+        k_check_w<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, bad);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    const unsigned long long nblocks = (m + B - 1) / B;
+    std::atomic<unsigned long long> first_bad{~0ULL}, next_block{0};
+    std::mutex err_mu;
+    cudaError_t werr = cudaSuccess;
+    auto worker = [&](int t) {
+        cudaError_t e = cudaSetDevice(ctx->device);
+        char *mine = (char *)ctx->stage_host + (size_t)t * R * slot_bytes;
+        for (unsigned long long it = 0; e == cudaSuccess; ++it) {
+            const unsigned long long b = next_block.fetch_add(1);
+            if (b >= nblocks) break;
+            const int j = (int)(it % R);
+            cudaEvent_t ev = ctx->stage_ev[(size_t)t * R + j];
+            if (it >= (unsigned long long)R && (e = cudaEventSynchronize(ev)) != cudaSuccess) break;
+            const unsigned long long off = b * B, k = std::min<unsigned long long>(B, m - off);
+            uint32_t *su = (uint32_t *)(mine + (size_t)j * slot_bytes), *sv = su + B;
+            if (lmx_narrow_block(edge_u + off, edge_v + off, k, n, su, sv)) {
+                for (unsigned long long i = 0; i < k; ++i) {
+                    const uint64_t a = (uint64_t)edge_u[off + i], c = (uint64_t)edge_v[off + i];
+                    if (a >= n || c >= n || a == c) {
+                        unsigned long long cur = first_bad.load();
+                        while (off + i < cur && !first_bad.compare_exchange_weak(cur, off + i)) {
+                        }
+                        break;
+                    }
+                }
+            }
+            e = cudaMemcpyAsync(ctx->eu + off, su, k * 4, cudaMemcpyHostToDevice, cs);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->ev + off, sv, k * 4, cudaMemcpyHostToDevice, cs);
+            if (e == cudaSuccess && !w_pinned) {
+                double *sw = (double *)(sv + B);
+                memcpy(sw, edge_weight + off, k * 8);
+                e = cudaMemcpyAsync(ctx->w + off, sw, k * 8, cudaMemcpyHostToDevice, cs);
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(ds, ev, 0);
+            if (e == cudaSuccess) {
+                k_degrees<<<grid_for(ctx, k), kBlock, 0, ds>>>(ctx->eu + off, ctx->ev + off, k, ctx->deg0);
+                e = cudaGetLastError();
+            }
+        }
+        if (e != cudaSuccess) {
+            std::lock_guard<std::mutex> g(err_mu);
+            if (werr == cudaSuccess) werr = e;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) pool.emplace_back(worker, t);
+    int rc = LMX_OK;
+    if (w_pinned) {   // the weight-key stage overlaps the endpoint copies
+        rc = lmx_weight_stage(ctx);
+        *weights_done = true;
+    }
+    for (std::thread &th : pool) th.join();
+    const auto t_join = std::chrono::steady_clock::now();
+    if (rc != LMX_OK || werr != cudaSuccess) {   // no copy may still read the ring
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(ds);
+    }
+    if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, werr);
+    if (!w_pinned) {
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[1], cs));
+        LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copy[1], 0));
+        k_check_w<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, bad);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev_deg, ds));
+    LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_deg, 0));
+    LMX_CUDA(ctx, cudaEventRecord(ctx->ev_copy[2], cs));
+    LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_copy[2], 0));
+    *host_bad = first_bad.load();
+    if (getenv("LMX_TRACE_SETUP")) {
+        LMX_CUDA(ctx, cudaStreamSynchronize(st));
+        const auto t_end = std::chrono::steady_clock::now();
+        fprintf(stderr, "[lmx setup] host load: %d threads, blocks of %llu edges, weights %s; workers done %.1f ms, "
+                "copies + degrees done %.1f ms\n", T, B, w_pinned ? "page-locked" : "staged",
+                std::chrono::duration<double, std::milli>(t_join - t_start).count(),
+                std::chrono::duration<double, std::milli>(t_end - t_start).count());
+        trace_mark(ctx, "host narrow + copies");
+    }
+    return LMX_OK;
+}
+
 // lmx_load_graph: validate + narrow the edge arrays, then K0.
 int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, const int64_t *edge_v,
                    const double *edge_weight, int where) {
@@ -935,7 +1096,10 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
         }
     }
     bool weights_done = false;
-    if (m > 0) {
+    unsigned long long host_bad = ~0ULL;
+    if (m > 0 && where == LMX_HOST && !getenv("LMX_LOAD_LEGACY")) {
+        LMX_TRY(load_host_narrowed(ctx, edge_u, edge_v, edge_weight, bad, &host_bad, &weights_done));
+    } else if (m > 0) {
         if (pinned) {
             if (!ctx->copy_stream) {
                 LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
@@ -1003,10 +1167,12 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
             LMX_CUDA(ctx, e);
         }
     }
+    trace_mark(ctx, "convert + degrees");
     unsigned long long badpos = 0;
     LMX_CUDA(ctx, cudaMemcpyAsync(&badpos, bad, 8, cudaMemcpyDeviceToHost, st));
     LMX_CUDA(ctx, cudaStreamSynchronize(st));
     lmx_free(ctx, (void **)&bad, 8);
+    badpos = std::min(badpos, host_bad);
     if (badpos != ~0ULL) {
         int64_t u = 0, v = 0;
         double w = 0;
@@ -1033,5 +1199,6 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
         return lmx_fail(ctx, LMX_EINVAL, buf);
     }
     if (!weights_done) LMX_TRY(lmx_weight_stage(ctx));
+    trace_mark(ctx, "weight stage");
     return lmx_setup_slots(ctx);
 }
