@@ -940,8 +940,10 @@ static int load_host_narrowed(lmx_ctx *ctx, const int64_t *edge_u, const int64_t
     const auto t_start = std::chrono::steady_clock::now();
     const int T = load_threads();
     const int R = getenv("LMX_LOAD_RING") ? std::max(2, atoi(getenv("LMX_LOAD_RING"))) : 4;
-    unsigned long long B = std::max<unsigned long long>(1ULL << 14, (m + 4ULL * T - 1) / (4ULL * T));
-    B = std::min<unsigned long long>(B, 1ULL << 20);
+    const unsigned long long bmax = getenv("LMX_LOAD_BLOCK") ? std::max(1ULL << 12, strtoull(getenv("LMX_LOAD_BLOCK"), 0, 10))
+                                                             : (1ULL << 19);
+    unsigned long long B = std::max<unsigned long long>(1ULL << 12, (m + 4ULL * T - 1) / (4ULL * T));
+    B = (std::min<unsigned long long>(B, bmax) + 7) & ~7ULL;   // 32-byte aligned slot halves
     const size_t slot_bytes = (size_t)B * (w_pinned ? 8 : 16);
     const size_t ring = slot_bytes * T * R;
     if (ctx->stage_bytes < ring) {

@@ -36,21 +36,23 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(f"torch H2D int64 {m * 8 / (time.perf_counter() - t) / 1e9:.1f} GB/s", file=sys.stderr)
 del d
-configs = [(os.cpu_count(), 4), (os.cpu_count(), 16), (max(1, os.cpu_count() - 2), 8), (8, 8), (0, 0)]
+configs = [(os.cpu_count(), 4, 1 << 18), (os.cpu_count(), 8, 1 << 18), (os.cpu_count(), 4, 1 << 19),
+           (os.cpu_count(), 4, 1 << 20), (0, 0, 0)]
 if len(sys.argv) > 2:
     configs = [tuple(int(x) for x in c.split(",")) for c in sys.argv[2:]]
-for th, ring in configs:
-    for k in ("LMX_LOAD_THREADS", "LMX_LOAD_RING", "LMX_LOAD_LEGACY"):
+for th, ring, block in configs:
+    for k in ("LMX_LOAD_THREADS", "LMX_LOAD_RING", "LMX_LOAD_LEGACY", "LMX_LOAD_BLOCK"):
         os.environ.pop(k, None)
     if th:
         os.environ["LMX_LOAD_THREADS"] = str(th)
         os.environ["LMX_LOAD_RING"] = str(ring)
+        os.environ["LMX_LOAD_BLOCK"] = str(block)
     else:
         os.environ["LMX_LOAD_LEGACY"] = "1"
     for rep in range(2):
         torch.cuda.synchronize()
         t = time.perf_counter()
-        print(f"--- threads {th or 'legacy'} ring {ring} rep {rep}", file=sys.stderr, flush=True)
+        print(f"--- threads {th or 'legacy'} ring {ring} block {block} rep {rep}", file=sys.stderr, flush=True)
         eng.load_graph(g)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
