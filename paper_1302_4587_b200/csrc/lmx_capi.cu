@@ -84,6 +84,8 @@ void lmx_destroy(lmx_ctx *ctx) {
     for (cudaEvent_t e : ctx->stage_ev) cudaEventDestroy(e);
     if (ctx->ev_deg) cudaEventDestroy(ctx->ev_deg);
     if (ctx->deg_stream) cudaStreamDestroy(ctx->deg_stream);
+    if (ctx->ev_load) cudaEventDestroy(ctx->ev_load);
+    if (ctx->load_stream) cudaStreamDestroy(ctx->load_stream);
     if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -116,8 +118,23 @@ int lmx_load_graph(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
     cudaSetDevice(ctx->device);
     ctx->err.clear();
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    // The load runs on the engine's own non-blocking stream, ordered after the
+    // caller's prior work and before its later work: a caller stream that is
+    // the legacy default stream would otherwise serialise against the copy
+    // and degree streams of a host load.
+    if (!ctx->load_stream) {
+        LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->load_stream, cudaStreamNonBlocking));
+        LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_load, cudaEventDisableTiming));
+    }
+    cudaStream_t user = ctx->stream;
+    LMX_CUDA(ctx, cudaStreamWaitEvent(ctx->load_stream, ctx->ev0, 0));
+    ctx->stream = ctx->load_stream;
     int rc = lmx_load_edges(ctx, n, m, edge_u, edge_v, edge_weight, where);
+    cudaError_t e = cudaEventRecord(ctx->ev_load, ctx->load_stream);
+    ctx->stream = user;
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, ctx->ev_load, 0);
     if (rc != LMX_OK) return rc;
+    LMX_CUDA(ctx, e);
     LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     LMX_CUDA(ctx, cudaEventSynchronize(ctx->ev1));
     float ms = 0.f;

@@ -197,6 +197,8 @@ struct lmx_ctx {
     size_t stage_bytes = 0;
     std::vector<cudaEvent_t> stage_ev;       // one per ring slot
     cudaStream_t deg_stream = nullptr;       // per-block degree counts behind the copies
+    cudaStream_t load_stream = nullptr;      // lmx_load_graph runs here (ordered with the caller's stream)
+    cudaEvent_t ev_load = nullptr;
     cudaEvent_t ev_deg = nullptr;
     unsigned long long *hist = nullptr;      // scan: death-round histogram
     size_t hist_cap = 0;

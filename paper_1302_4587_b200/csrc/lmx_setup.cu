@@ -909,7 +909,8 @@ int lmx_setup_slots(lmx_ctx *ctx) {
 // go first (directly when they are page-locked) so the weight-key stage runs
 // on the device while the endpoint blocks are still arriving; each block's
 // degree counts run on a third stream right behind its copy.
-bool lmx_narrow_block(const int64_t *u, const int64_t *v, size_t k, uint64_t n, uint32_t *ou, uint32_t *ov);
+bool lmx_narrow_block(const int64_t *u, const int64_t *v, size_t k, uint64_t n, uint32_t *ou, uint32_t *ov,
+                      bool streaming);
 
 namespace {
 
@@ -945,6 +946,7 @@ static int load_host_narrowed(lmx_ctx *ctx, const int64_t *edge_u, const int64_t
     unsigned long long B = std::max<unsigned long long>(1ULL << 12, (m + 4ULL * T - 1) / (4ULL * T));
     B = (std::min<unsigned long long>(B, bmax) + 7) & ~7ULL;   // 32-byte aligned slot halves
     const size_t slot_bytes = (size_t)B * (w_pinned ? 8 : 16);
+    const bool streaming = getenv("LMX_LOAD_NT") ? atoi(getenv("LMX_LOAD_NT")) != 0 : true;
     const size_t ring = slot_bytes * T * R;
     if (ctx->stage_bytes < ring) {
         if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
@@ -992,7 +994,8 @@ static int load_host_narrowed(lmx_ctx *ctx, const int64_t *edge_u, const int64_t
             if (it >= (unsigned long long)R && (e = cudaEventSynchronize(ev)) != cudaSuccess) break;
             const unsigned long long off = b * B, k = std::min<unsigned long long>(B, m - off);
             uint32_t *su = (uint32_t *)(mine + (size_t)j * slot_bytes), *sv = su + B;
-            if (lmx_narrow_block(edge_u + off, edge_v + off, k, n, su, sv)) {
+            const bool block_bad = lmx_narrow_block(edge_u + off, edge_v + off, k, n, su, sv, streaming);
+            if (block_bad) {
                 for (unsigned long long i = 0; i < k; ++i) {
                     const uint64_t a = (uint64_t)edge_u[off + i], c = (uint64_t)edge_v[off + i];
                     if (a >= n || c >= n || a == c) {
@@ -1012,7 +1015,7 @@ static int load_host_narrowed(lmx_ctx *ctx, const int64_t *edge_u, const int64_t
             }
             if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(ds, ev, 0);
-            if (e == cudaSuccess) {
+            if (e == cudaSuccess && !block_bad) {   // (a failing load never reads the degrees)
                 k_degrees<<<grid_for(ctx, k), kBlock, 0, ds>>>(ctx->eu + off, ctx->ev + off, k, ctx->deg0);
                 e = cudaGetLastError();
             }

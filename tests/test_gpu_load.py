@@ -93,6 +93,10 @@ def test_first_bad_edge_reported(engine, pinned, monkeypatch):
     eu[early] = good_u
     with pytest.raises(ValueError, match=f"edge {late}: vertex id out of range"):
         engine.load_graph(graph(eu, ev, w))
+    eu2 = eu.copy()
+    eu2[7] = -1                                           # negative id: nothing may touch deg[-1]
+    with pytest.raises(ValueError, match="edge 7: vertex id out of range"):
+        engine.load_graph(graph(eu2, ev, w))
     w2 = w.copy()
     w2[5] = -1.0
     with pytest.raises(ValueError, match="edge 5: weight"):

@@ -6,7 +6,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["LMX_TRACE_SETUP"] = "1"
+if not os.environ.get("TRACE_OFF"):
+    os.environ["LMX_TRACE_SETUP"] = "1"
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -14,6 +15,8 @@ from paper_1302_4587_b200 import Engine, Graph  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 eng = Engine(0)
+if os.environ.get("TRACE_TORCH_STREAM"):
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)   # as bench.py does
 eng.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
 g0 = eng.export_graph()
 n, m = g0.num_vertices, len(g0.edge_u)
@@ -36,23 +39,23 @@ for _ in range(2):
     torch.cuda.synchronize()
     print(f"torch H2D int64 {m * 8 / (time.perf_counter() - t) / 1e9:.1f} GB/s", file=sys.stderr)
 del d
-configs = [(os.cpu_count(), 4, 1 << 18), (os.cpu_count(), 8, 1 << 18), (os.cpu_count(), 4, 1 << 19),
-           (os.cpu_count(), 4, 1 << 20), (0, 0, 0)]
+configs = [(os.cpu_count(), 4, 1 << 19, 1), (0, 0, 0, 0)]
 if len(sys.argv) > 2:
     configs = [tuple(int(x) for x in c.split(",")) for c in sys.argv[2:]]
-for th, ring, block in configs:
-    for k in ("LMX_LOAD_THREADS", "LMX_LOAD_RING", "LMX_LOAD_LEGACY", "LMX_LOAD_BLOCK"):
+for th, ring, block, nt in configs:
+    for k in ("LMX_LOAD_THREADS", "LMX_LOAD_RING", "LMX_LOAD_LEGACY", "LMX_LOAD_BLOCK", "LMX_LOAD_NT"):
         os.environ.pop(k, None)
     if th:
         os.environ["LMX_LOAD_THREADS"] = str(th)
         os.environ["LMX_LOAD_RING"] = str(ring)
         os.environ["LMX_LOAD_BLOCK"] = str(block)
+        os.environ["LMX_LOAD_NT"] = str(nt)
     else:
         os.environ["LMX_LOAD_LEGACY"] = "1"
-    for rep in range(2):
+    for rep in range(3):
         torch.cuda.synchronize()
         t = time.perf_counter()
-        print(f"--- threads {th or 'legacy'} ring {ring} block {block} rep {rep}", file=sys.stderr, flush=True)
+        print(f"--- threads {th or 'legacy'} ring {ring} block {block} nt {nt} rep {rep}", file=sys.stderr, flush=True)
         eng.load_graph(g)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
