@@ -84,9 +84,17 @@ typedef struct {
 #define LMX_OPT_ALGO 6          /* round loop of the next load: -1 auto, 0 compacting rounds,
                                    1 weight-ordered scan (taken only for the distinct layout on a
                                    context without LMX_OPT_DIST_P; results are identical) */
+#define LMX_OPT_STATIC_ORDER 7  /* rerandomize=False: 1 = the next load lays graphs with tied weights
+                                   out in the fixed total order (weight, salt) of the seed given by
+                                   LMX_OPT_STATIC_SEED (tiebreak.py:40-59: with rerandomize off every
+                                   round's salts are round 0's), so the weight-ordered scan loop
+                                   serves them; such a graph then only matches with that seed and
+                                   rerandomize=0 (LMX_ESTATE otherwise).  0 = off (default) */
+#define LMX_OPT_STATIC_SEED 8   /* the masked seed (uint64 bits as int64) for LMX_OPT_STATIC_ORDER */
 #define LMX_QUERY_LAYOUT 100    /* lmx_set_option returns the loaded graph's layout */
 #define LMX_QUERY_RELABELED 101 /* lmx_set_option returns 1 if the loaded graph is relabelled */
 #define LMX_QUERY_ALGO 102      /* lmx_set_option returns the loaded graph's round loop (0 / 1) */
+#define LMX_QUERY_STATIC 104    /* lmx_set_option returns 1 if the loaded graph has the static order */
 #define LMX_QUERY_PEAK_BYTES 103 /* lmx_set_option returns the context's device-memory high-water mark
                                     in MiB (allocations through the context); value != 0 resets it */
 

@@ -152,6 +152,11 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
     if (!ctx->vbeg) return lmx_fail(ctx, LMX_ESTATE, "no graph loaded (call lmx_load_graph first)");
     std::vector<lmx_round_stats> &stats = ctx->rounds;
     unsigned long long nm = 0;
+    if (ctx->static_layout && (rerandomize || lmx::round_seed(seed_masked, 0, false) != ctx->static_rs)) {
+        return lmx_fail(ctx, LMX_ESTATE, "the loaded graph is laid out for the fixed salt order of one seed "
+                                         "(LMX_OPT_STATIC_ORDER): it matches only that seed with rerandomize=0; "
+                                         "reload for this call");
+    }
     ctx->mate_target = (out_where == LMX_DEVICE && mate_out) ? (long long *)mate_out : ctx->mate;
     if (ctx->algo == 1) LMX_TRY(lmx_run_rounds_scan(ctx, seed_masked, rerandomize != 0, stats, nm));
     else LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
@@ -211,6 +216,16 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
         ctx->dist_rank = (int)value;
         return LMX_OK;
     }
+    if (option == LMX_OPT_STATIC_ORDER) {
+        if (value < 0 || value > 1) return lmx_fail(ctx, LMX_EINVAL, "static order must be 0 or 1");
+        ctx->static_order = value != 0;
+        return LMX_OK;
+    }
+    if (option == LMX_OPT_STATIC_SEED) {
+        ctx->static_seed = (uint64_t)value;
+        return LMX_OK;
+    }
+    if (option == LMX_QUERY_STATIC) return ctx->static_layout ? 1 : 0;
     if (option == LMX_QUERY_LAYOUT) return ctx->layout;
     if (option == LMX_QUERY_RELABELED) return ctx->relabeled ? 1 : 0;
     if (option == LMX_QUERY_ALGO) return ctx->algo;
@@ -262,6 +277,10 @@ int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const
                   int max_rounds, int *n_rounds_out, char *err, size_t errlen) {
     lmx_ctx *ctx = nullptr;
     int rc = lmx_create(device, &ctx);
+    if (rc == LMX_OK && !rerandomize) {   // one seed, fixed salts: the static order serves tied weights
+        ctx->static_order = true;
+        ctx->static_seed = seed_masked;
+    }
     if (rc == LMX_OK) rc = lmx_load_graph(ctx, n, m, edge_u, edge_v, edge_weight, LMX_HOST);
     if (rc == LMX_OK)
         rc = lmx_match(ctx, seed_masked, rerandomize, mate_out, matched_ids_out, n_matched_out, rounds_out,

@@ -158,6 +158,13 @@ struct lmx_ctx {
     int algo = 0;
     int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
     bool scan_rejected = false;              // load time: ties too common for the scan loop
+    // rerandomize=False (salts fixed for the run): a load may lay tie-heavy
+    // weights out in the total order (weight, salt of round 0) of one seed,
+    // which the scan loop then matches with no tie handling
+    bool static_order = false;               // option: lay out for static_seed
+    uint64_t static_seed = 0;                // masked seed of the next load
+    bool static_layout = false;              // the loaded graph is laid out so
+    uint64_t static_rs = 0;                  // ... for this round-0 seed
     // partitions (dist_p > 1): after the cut search, eu/ev/w hold only the edges
     // incident to the owned range ("local edges", caller ids), geid their global ids
     bool dist_local = false;

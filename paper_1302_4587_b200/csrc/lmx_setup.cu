@@ -145,6 +145,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;
     ctx->algo = 0;
+    ctx->static_layout = false;
     ctx->hist_cap = 0;
     ctx->send_cap = ctx->recv_cap = 0;
     ctx->n_local = ctx->slots_local = 0;
@@ -338,6 +339,23 @@ __global__ void k_keys(const double *w, unsigned long long m, unsigned long long
     }
 }
 
+// static order: the round-0 salt of every edge (tiebreak.py:54-58), then the
+// canonical weight bits in salt order (for the stable weight pass)
+__global__ void k_salt_keys(unsigned long long m, uint64_t rs, unsigned long long *keys, uint32_t *vals) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        keys[e] = mix64((uint64_t)e ^ rs);
+        vals[e] = (uint32_t)e;
+    }
+}
+
+__global__ void k_weight_keys_of(const double *w, const uint32_t *eid, unsigned long long m,
+                                 unsigned long long *keys) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+        keys[i] = canon_bits(w[eid[i]]);
+}
+
 __global__ void k_heads(const unsigned long long *sorted, unsigned long long m, uint32_t *flag) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
@@ -422,6 +440,66 @@ void trace_mark(lmx_ctx *ctx, const char *what) {
     last = now;
 }
 
+// Static order (LMX_OPT_STATIC_ORDER, rerandomize=False): eids sorted by the
+// strict total order (weight, round-0 salt) -- salts are a bijection of the
+// edge id, so there are no ties -- for the scan loop's weight-ordered
+// segments (ws_eid, ascending; ws_tied all zero).  Uniform weights: the salt
+// alone.  Otherwise a stable weight pass over the salt order.
+static int static_order_stage(lmx_ctx *ctx, bool uniform) {
+    const unsigned long long m = (unsigned long long)ctx->m;
+    cudaStream_t st = ctx->stream;
+    const uint64_t rs = round_seed(ctx->static_seed, 0, false);
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    uint32_t *vals = nullptr, *vals2 = nullptr, *tied = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "static keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "static keys2")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "static vals")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "static vals2")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "static tied")) != LMX_OK) break;
+        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
+        if (e != cudaSuccess) break;
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "static sort tmp")) != LMX_OK) break;
+        k_salt_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(m, rs, keys, vals);
+        size_t t1 = tmp_bytes;
+        e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
+        if (e != cudaSuccess) break;
+        if (!uniform) {   // stable: equal weights keep the salt order
+            k_weight_keys_of<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, vals2, m, keys);
+            t1 = tmp_bytes;
+            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals2, vals, (long long)m, 0, 64, st);
+            if (e != cudaSuccess) break;
+            std::swap(vals, vals2);
+        }
+        e = cudaMemsetAsync(tied, 0, m * 4, st);
+        if (e != cudaSuccess) break;
+        ctx->ws_eid = vals2;
+        ctx->ws_tied = tied;
+        vals2 = tied = nullptr;
+    } while (0);
+    if (e != cudaSuccess && rc == LMX_OK) rc = lmx_cuda_check(ctx, e, "static order sort");
+    cudaStreamSynchronize(st);
+    lmx_free(ctx, (void **)&keys, m * 8);
+    lmx_free(ctx, (void **)&keys2, m * 8);
+    lmx_free(ctx, (void **)&vals, m * 4);
+    lmx_free(ctx, (void **)&vals2, m * 4);
+    lmx_free(ctx, (void **)&tied, m * 4);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    if (rc != LMX_OK) return rc;
+    ctx->algo = 1;
+    ctx->layout = kDistinct;
+    ctx->n_distinct = (uint32_t)m;
+    ctx->n_tied = 0;
+    ctx->static_layout = true;
+    ctx->static_rs = rs;
+    trace_mark(ctx, "  static order sort");
+    return LMX_OK;
+}
+
 // Weight keys (tiebreak.py:105-113 order) from ctx->w alone, so a pinned-host
 // load can run it while the endpoint arrays are still in flight: layout
 // choice, dense ranks and tie indices, and the round-loop algorithm.  Leaves
@@ -455,6 +533,9 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         return LMX_OK;
     }
     ctx->layout = kUniform;
+    const bool want_static = ctx->static_order && !ctx->dist_local && ctx->dist_p <= 1 && m &&
+                             ctx->force_algo != 0 && ctx->n < (1LL << 30) && ctx->force_layout == -1;
+    if (want_static && uniform) return static_order_stage(ctx, true);
     if (ctx->dist_local && m == 0 && !uniform && ctx->force_algo != 0 && ctx->n < (1LL << 30)) {
         ctx->algo = 1;   // a partition without local edges still runs the loop its peers run
         ctx->layout = kDistinct;
@@ -466,6 +547,7 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         void *tmp = nullptr;
         size_t tmp_bytes = 0;
         int rc = LMX_OK;
+        bool static_pending = false;
         do {
             if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
@@ -504,6 +586,10 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             bool distinct = (T <= m / 16 || ctx->dist_p > 1) && (D + T < 0xFFFFFFFFULL);
             if (ctx->force_layout == kDistinct) distinct = D + T < 0xFFFFFFFFULL;
             if (ctx->force_layout == kGeneral) distinct = false;
+            if (want_static && !distinct) {   // tie-heavy: the static order instead (after the frees)
+                static_pending = true;
+                break;
+            }
             ctx->layout = distinct ? kDistinct : kGeneral;
             ctx->n_distinct = (uint32_t)D;
             ctx->n_tied = (uint32_t)T;
@@ -547,6 +633,7 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             lmx_free(ctx, (void **)&kofe, m * 4);
             return rc;
         }
+        if (static_pending) return static_order_stage(ctx, false);
         if (ctx->algo == 1) lmx_free(ctx, (void **)&kofe, m * 4);
     }
     ctx->ws_kofe = kofe;

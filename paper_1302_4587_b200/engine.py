@@ -44,6 +44,9 @@ LMX_OPT_KERNEL_TIMING = 1
 LMX_OPT_LAYOUT = 2
 LMX_OPT_RELABEL = 3
 LMX_OPT_ALGO = 6
+LMX_OPT_STATIC_ORDER = 7
+LMX_OPT_STATIC_SEED = 8
+LMX_QUERY_STATIC = 104
 LMX_QUERY_LAYOUT = 100
 LMX_QUERY_RELABELED = 101
 LMX_QUERY_ALGO = 102
@@ -360,6 +363,22 @@ class Engine:
         code = self._lib.lmx_set_option(self._h, LMX_QUERY_LAYOUT, 0)
         return {v: k for k, v in self.LAYOUTS.items()}[code]
 
+    def set_static_order(self, seed: int | None) -> None:
+        """rerandomize=False fast path (LMX_OPT_STATIC_ORDER): the next load lays
+        graphs with tied weights out in the fixed (weight, salt) order of
+        ``seed`` so the weight-ordered scan loop serves them; the loaded graph
+        then matches only ``seed`` with rerandomize=False.  None = off."""
+        if seed is not None:
+            bits = int(seed) & 0xFFFFFFFFFFFFFFFF
+            val = bits - (1 << 64) if bits >= (1 << 63) else bits
+            self._check(self._lib.lmx_set_option(self._h, LMX_OPT_STATIC_SEED, val), "lmx_set_option")
+        self._check(self._lib.lmx_set_option(self._h, LMX_OPT_STATIC_ORDER, int(seed is not None)),
+                    "lmx_set_option")
+
+    def static_order(self) -> bool:
+        """True if the loaded graph has the static (weight, salt) layout."""
+        return bool(self._lib.lmx_set_option(self._h, LMX_QUERY_STATIC, 0))
+
     def set_kernel_timing(self, on: bool = True) -> None:
         """Record a CUDA event after every round / match kernel (per-kernel durations)."""
         self._check(self._lib.lmx_set_option(self._h, LMX_OPT_KERNEL_TIMING, int(on)), "lmx_set_option")
@@ -456,7 +475,13 @@ def local_max_b200(g, seed: int, rerandomize: bool = True, device: int = 0) -> t
     """
     t0 = time.perf_counter()
     eng = default_engine(device)
-    eng.load_graph(g)
+    # with rerandomize off the salts are fixed for the run: tied weights get
+    # the static (weight, salt) layout and the scan loop (LMX_OPT_STATIC_ORDER)
+    eng.set_static_order(None if rerandomize else seed)
+    try:
+        eng.load_graph(g)
+    finally:
+        eng.set_static_order(None)
     matching, trace = eng.match(g, seed, rerandomize)
     trace.wall_millis = (time.perf_counter() - t0) * 1000.0
     return matching, trace
