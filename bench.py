@@ -42,11 +42,22 @@ WORKLOADS = {
     "rmat26": ("rmat", 26, 16), "rmat25": ("rmat", 25, 16), "rmat24": ("rmat", 24, 16),
     "rmat22": ("rmat", 22, 16), "rmat20": ("rmat", 20, 16), "rmat16": ("rmat", 16, 16),
     "er24unit": ("er", 24, 4), "er20unit": ("er", 20, 4),
+    # rerandomize=False (the salts fixed for the run): the static (weight, salt)
+    # layout serves unit weights on the scan loop (LMX_OPT_STATIC_ORDER)
+    "er24unit-norr": ("er", 24, 4, False),
 }
 
 
+def wl(name: str):
+    """(family, scale, edge factor, rerandomize) of a workload."""
+    spec = WORKLOADS[name]
+    return spec[0], spec[1], spec[2], (spec[3] if len(spec) > 3 else True)
+
+
 def generate(eng, workload: str):
-    fam, scale, ef = WORKLOADS[workload]
+    fam, scale, ef, rr = wl(workload)
+    if not rr:   # the layout for the fixed salts of the match seed
+        eng.set_static_order(MATCH_SEED)
     if fam == "rmat":
         eng.gen_rmat(scale, ef, *RMAT_ABC, seed=GRAPH_SEED, permute=True)
         return f"RMAT scale {scale} edge factor {ef}"
@@ -203,18 +214,18 @@ def run_reference(args):
     if rank != 0:
         return 0
     scale = args.cpu_sample_scale
-    fam, _, ef = WORKLOADS[args.workload]
+    fam, _, ef, RR = wl(args.workload)
     n, eu, ev, w = cpu_sample_graph(scale, fam, ef)
     m = int(eu.size)
     ref = import_reference()
     if ref is not None:
         lg, lm = ref
         g = reference_graph(lg, n, eu, ev, w)
-        run = lambda: lm.local_max_seq(g, MATCH_SEED, True)   # noqa: E731
+        run = lambda: lm.local_max_seq(g, MATCH_SEED, RR)   # noqa: E731
         kind, what = "reference", "locmax.local_max_seq (unmodified reference, baseline/_ref)"
     else:
         from oracle import oracle as O
-        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)   # noqa: E731
+        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, RR)   # noqa: E731
         kind, what = "port", "oracle numpy port of local_max_seq (baseline/_ref not installed)"
     for _ in range(args.warmup):
         run()
@@ -247,7 +258,7 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline_leg(scale: int, reps: int = 3, family: str = "rmat", ef: int = 16):
+def cpu_baseline_leg(scale: int, reps: int = 3, family: str = "rmat", ef: int = 16, RR: bool = True):
     """The reference's local_max_seq (baseline/_ref; else the oracle's numpy
     port) on a bounded RMAT sample, best of `reps`, and the
     GPU result on the same sample checked identical to it."""
@@ -258,11 +269,11 @@ def cpu_baseline_leg(scale: int, reps: int = 3, family: str = "rmat", ef: int = 
         lg, lm = ref
         g = reference_graph(lg, n, eu, ev, w)
         kind = "reference"
-        run = lambda: lm.local_max_seq(g, MATCH_SEED, True)   # noqa: E731
+        run = lambda: lm.local_max_seq(g, MATCH_SEED, RR)   # noqa: E731
     else:
         from oracle import oracle as O
         kind = "port"
-        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, True)   # noqa: E731
+        run = lambda: O.numpy_local_max(n, eu, ev, w, MATCH_SEED, RR)   # noqa: E731
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -278,7 +289,7 @@ def cpu_baseline_leg(scale: int, reps: int = 3, family: str = "rmat", ef: int = 
         ref_mate, ref_ids, ref_rounds = res.mate, res.matched_ids, res.rounds
     with Engine(0) as eng:
         eng.load_graph(Graph(n, eu, ev, w))
-        mate, ids, rounds = eng.match_raw(MATCH_SEED, True)
+        mate, ids, rounds = eng.match_raw(MATCH_SEED, RR)
     same = bool(np.array_equal(mate, ref_mate) and np.array_equal(ids, ref_ids)
                 and [(r.edges_before, r.edges_matched, r.edges_removed) for r in rounds] == ref_rounds)
     what = "locmax.local_max_seq (unmodified reference, baseline/_ref)" if kind == "reference" else \
@@ -320,7 +331,7 @@ def run_b200_dist(args):
     comm = TorchComm()
     comm.bind_device(dev)
     stream = torch.cuda.current_stream()
-    fam, scale, ef = WORKLOADS[args.workload]
+    fam, scale, ef, RR = wl(args.workload)
     if fam != "rmat":
         raise SystemExit("the partitioned bench runs the RMAT workloads")
     if world > 1:
@@ -468,7 +479,7 @@ def run_b200(args):
         return run_b200_dist(args)
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    fam, scale, ef = WORKLOADS[args.workload]
+    fam, scale, ef, RR = wl(args.workload)
 
     eng = Engine(local)
     eng.set_stream(stream.cuda_stream)
@@ -497,7 +508,7 @@ def run_b200(args):
     ids = torch.empty(max(n // 2 + 1, 1), dtype=torch.int64, device="cuda")
 
     for _ in range(args.warmup):
-        eng.match_device(MATCH_SEED, mate, ids)
+        eng.match_device(MATCH_SEED, mate, ids, RR)
     rounds = eng.last_rounds()
 
     # ---- timed region: K full matchings from HBM-resident slots
@@ -511,7 +522,7 @@ def run_b200(args):
     launches = 0
     rounds_exec = 0
     for _ in range(args.steps):
-        nm = eng.match_device(MATCH_SEED, mate, ids)
+        nm = eng.match_device(MATCH_SEED, mate, ids, RR)
         t = eng.last_timing()
         launches += t["round_launches"]
         rounds_exec += t["rounds_executed"]
@@ -528,7 +539,7 @@ def run_b200(args):
     eng.set_kernel_timing(True)
     rk_ms = mk_ms = hk_ms = 0.0
     for _ in range(args.steps):
-        eng.match_device(MATCH_SEED, mate, ids)
+        eng.match_device(MATCH_SEED, mate, ids, RR)
         t = eng.last_timing()
         rk_ms += t["round_kernel_ms"]
         mk_ms += t["match_kernel_ms"]
@@ -624,7 +635,7 @@ def run_b200(args):
         keep = None
         for _ in range(2):
             eng.load_graph(hg)
-            keep = eng.match_raw(MATCH_SEED, True)
+            keep = eng.match_raw(MATCH_SEED, RR)
         del keep
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -633,7 +644,7 @@ def run_b200(args):
         e0.record(stream)
         for _ in range(e2e_steps):
             eng.load_graph(hg)
-            hmate, hids, hrounds = eng.match_raw(MATCH_SEED, True)
+            hmate, hids, hrounds = eng.match_raw(MATCH_SEED, RR)
         e1.record(stream)
         torch.cuda.synchronize()
         Te = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1000.0)
@@ -652,7 +663,7 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline:
         eng.close()
-        cpu = cpu_baseline_leg(args.cpu_baseline_scale, family=fam, ef=ef)
+        cpu = cpu_baseline_leg(args.cpu_baseline_scale, family=fam, ef=ef, RR=RR)
 
     line = {
         "metric": "input edges/s to full local max maximal matching", "value": value,
@@ -661,7 +672,8 @@ def run_b200(args):
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.workload, "graph": graph_desc,
                    "rmat_abc": list(RMAT_ABC) if fam == "rmat" else [0.25, 0.25, 0.25],
-                   "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED,
+                   "graph_seed": GRAPH_SEED, "match_seed": MATCH_SEED, "rerandomize": RR,
+                   "static_order": eng.static_order(),
                    "permuted_labels": fam == "rmat", "n": n, "m": m, "rounds": len(rounds),
                    "matched_edges": n_matched, "round_loop": algo, "parallelism": "dp1",
                    "l2": "inputs larger than L2 (slot records %.1f GB >> 126 MB)" % (2 * m * 8 / 1e9)},

@@ -31,6 +31,7 @@ Configs (BASELINE.json configs / north_star):
   rmat26  N*: RMAT scale 26, same recipe (the bench workload)
   er24unit C1 family at 256x: 4 * 2^24 uniform raw pairs (the RMAT generator
           with a = b = c = 1/4, no relabelling), unit weights; seed 1
+  er24unit-norr  the same graph and seed, rerandomize=False
 """
 
 from __future__ import annotations
@@ -85,7 +86,7 @@ def summarise(name, n, eu, ev, w, seed, rerandomize=True, **extra):
     return rec, res
 
 
-def check_reference(name, n, eu, ev, w, seed, rec, res):
+def check_reference(name, n, eu, ev, w, seed, rec, res, rerandomize=True):
     """Run the unmodified locmax.local_max_seq on the same arrays."""
     from locmax.graph import Graph
     from locmax.matchers import local_max_seq
@@ -93,7 +94,7 @@ def check_reference(name, n, eu, ev, w, seed, rec, res):
     g = Graph(int(n), np.zeros(n + 1, dtype=np.int64), empty, empty,
               np.asarray(eu, dtype=np.int64), np.asarray(ev, dtype=np.int64), np.asarray(w, dtype=np.float64))
     t0 = time.time()
-    mm, tr = local_max_seq(g, seed, True)
+    mm, tr = local_max_seq(g, seed, rerandomize)
     dt = time.time() - t0
     ids = np.array(sorted(mm.edges), dtype=np.int64)
     same = (np.array_equal(np.asarray(mm.mate), res.mate) and np.array_equal(ids, res.matched_ids)
@@ -120,18 +121,19 @@ def make_rmat(scale, ref):
     return rec
 
 
-def make_er24unit(ref):
+def make_er24unit(ref, rerandomize=True):
     t0 = time.time()
     u, v, w = O.c_rmat_raw(24, 4, 0.25, 0.25, 0.25, seed=1, permute=False)
     w[:] = 1.0
     n, eu, ev, ew = O.c_build_graph(u, v, w, 1 << 24)
     del u, v, w
     gc.collect()
-    print(f"er24unit: generated + built in {time.time() - t0:.1f}s", flush=True)
-    rec, res = summarise("er24unit", n, eu, ev, ew, 1, graph_seed=1, permuted=False,
+    name = "er24unit" if rerandomize else "er24unit-norr"
+    print(f"{name}: generated + built in {time.time() - t0:.1f}s", flush=True)
+    rec, res = summarise(name, n, eu, ev, ew, 1, rerandomize, graph_seed=1, permuted=False,
                          recipe="4 * 2^24 uniform pairs (RMAT a=b=c=1/4), unit weights")
     if ref:
-        check_reference("er24unit", n, eu, ev, ew, 1, rec, res)
+        check_reference(name, n, eu, ev, ew, 1, rec, res, rerandomize)
     return rec
 
 
@@ -172,6 +174,8 @@ def main():
             out[name] = make_rgg22(bool(args.reference))
         elif name == "er24unit":
             out[name] = make_er24unit(bool(args.reference))
+        elif name == "er24unit-norr":
+            out[name] = make_er24unit(bool(args.reference), rerandomize=False)
         elif name.startswith("rmat"):
             out[name] = make_rmat(int(name[4:]), bool(args.reference))
         else:
