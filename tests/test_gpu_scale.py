@@ -82,6 +82,25 @@ def test_er24_unit_weights_bit_exact(engine):
     _check(want, engine.export_graph(), mate, ids, rounds)
 
 
+def test_er24_unit_static_order_bit_exact(engine):
+    """The same graph with rerandomize=False (er24unit-norr, pinned to the
+    unmodified local_max_seq): the static (weight, salt) layout on the scan
+    loop, and the compacting loop, both equal the reference."""
+    want = SCALE["er24unit-norr"]
+    assert want["rerandomize"] is False and want.get("reference_checked")
+    engine.set_static_order(want["seed"])
+    engine.gen_er(24, 4, seed=want["graph_seed"], unit=True)
+    engine.set_static_order(None)
+    assert engine.algo() == "scan" and engine.static_order()
+    mate, ids, rounds = engine.match_raw(want["seed"], False)
+    g = engine.export_graph()
+    _check(want, g, mate, ids, rounds)
+    engine.load_graph(g)                                   # no static order: the compacting loop
+    assert engine.algo() == "compact"
+    mate, ids, rounds = engine.match_raw(want["seed"], False)
+    _check(want, g, mate, ids, rounds)
+
+
 @pytest.mark.parametrize("name,x,seed,mode", [("rgg-x16-euclidean-s0", 16, 0, "euclidean"),
                                                ("rgg-x12-random-s3", 12, 3, "random")])
 def test_device_rgg_generator_equals_reference(engine, golden_instances, name, x, seed, mode):
