@@ -29,6 +29,7 @@
 #include <cmath>
 
 #include "lmx_internal.cuh"
+#include "lmx_sort.cuh"
 
 using namespace lmx;
 
@@ -96,8 +97,8 @@ __global__ void k_rmat_raw(RmatParams p, unsigned long long k, uint32_t *u, uint
 // the triples whose LOWER endpoint falls in its build range) -------------------
 // Pass 0 counts, pass 1 appends {u, v, w, raw position} (block-aggregated).
 template <bool WRITE>
-__global__ void __launch_bounds__(kBlock) k_rmat_keep(RmatParams p, unsigned long long k, uint32_t blo,
-                                                      uint32_t bhi, unsigned long long *cursor, uint32_t *ku,
+__global__ void __launch_bounds__(kBlock) k_rmat_keep(RmatParams p, unsigned long long k, uint32_t nparts,
+                                                      uint32_t part, unsigned long long *cursor, uint32_t *ku,
                                                       uint32_t *kv, double *kw, uint32_t *kpos) {
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ unsigned long long s_base;
@@ -113,7 +114,11 @@ __global__ void __launch_bounds__(kBlock) k_rmat_keep(RmatParams p, unsigned lon
         if (i < k) {
             rmat_one(p, i, a, b, w);
             const uint32_t lo = a < b ? a : b;
-            keep = a != b && lo >= blo && lo < bhi;   // self-loops dropped (graph.py:89-91)
+            const uint32_t hi = a < b ? b : a;
+            // the pair's build rank: a hash of the unordered pair, so every
+            // occurrence of a pair meets on one rank and the ranks get even
+            // shares whatever the id distribution (self-loops dropped, graph.py:89-91)
+            keep = a != b && (uint32_t)(mix64(((uint64_t)lo << 32) | hi) % nparts) == part;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) s_cnt[warp] = __popc(bal);
@@ -388,16 +393,15 @@ static int build_from_raw(lmx_ctx *ctx, uint32_t *ru, uint32_t *rv, double *rw, 
         if ((rc = lmx_alloc(ctx, (void **)&flag, (kk + 1) * 4, "build flags")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&kept, kk * 4, "build kept")) != LMX_OK) break;
         k_pair_keys<<<bgrid(ctx, k), kBlock, 0, st>>>(ru, rv, k, bits, key, idx);
-        size_t t1 = 0, t2 = 0;
-        cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, key, key2, idx, idx2, (long long)k, 0,
-                                                        2 * bits, st);
-        if (e == cudaSuccess)
-            e = cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, flag, (long long)(k + 1), st);
+        if ((rc = lmx_sort_pairs(ctx, &key, &key2, &idx, &idx2, (long long)k, 0, 2 * bits, st, "build sort")) !=
+            LMX_OK)
+            break;
+        size_t t2 = 0;
+        cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, t2, flag, flag, (long long)(k + 1), st);
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build sizing"); break; }
-        tmp_bytes = std::max(t1, t2);
+        tmp_bytes = t2;
         if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "build tmp")) != LMX_OK) break;
-        e = cub::DeviceRadixSort::SortPairs(tmp, t1, key, key2, idx, idx2, (long long)k, 0, 2 * bits, st);
-        if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, (kk + 1) * 4, st);
+        e = cudaMemsetAsync(flag, 0, (kk + 1) * 4, st);
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "build sort"); break; }
         k_runs<<<bgrid(ctx, k), kBlock, 0, st>>>(key2, idx2, k, sentinel, ru, rv, rw, flag, kept);
         e = cub::DeviceScan::ExclusiveSum(tmp, t2, flag, flag, (long long)(k + 1), st);
@@ -703,9 +707,9 @@ __global__ void k_pair_minmax(const double *w, unsigned long long k, unsigned lo
 
 extern "C" {
 
-// Phase 1: generate the whole raw stream, keep the triples whose lower end is
-// in this rank's build range [rank n / p, (rank + 1) n / p), collapse parallel
-// pairs (graph.py:94-100) and record each pair's first raw position.
+// Phase 1: generate the whole raw stream, keep the triples whose unordered
+// pair hashes to this rank, collapse parallel pairs (graph.py:94-100) and
+// record each pair's first raw position.
 int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
                         int permute, void **bits_dev, int64_t *words_out, void **deg_dev, void **minmax_dev) {
     if (!ctx || !bits_dev || !words_out || !deg_dev || !minmax_dev) return LMX_EINVAL;
@@ -716,8 +720,6 @@ int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, doub
     const unsigned long long n = 1ULL << scale, k = (unsigned long long)edge_factor << scale;
     const RmatParams P = rmat_params(scale, a, b, c, seed, permute);
     const int p = ctx->dist_p, rank = ctx->dist_rank;
-    const uint32_t blo = (uint32_t)(n * (unsigned long long)rank / (unsigned long long)p);
-    const uint32_t bhi = (uint32_t)(n * (unsigned long long)(rank + 1) / (unsigned long long)p);
     lmx_free_graph(ctx);
     ctx->n = (int64_t)n;
     cudaStream_t st = ctx->stream;
@@ -733,8 +735,8 @@ int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, doub
         if ((rc = lmx_alloc(ctx, (void **)&cursor, 16, "keep cursor")) != LMX_OK) break;
         e = cudaMemsetAsync(cursor, 0, 16, st);
         if (e != cudaSuccess) break;
-        k_rmat_keep<false><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, blo, bhi, cursor, nullptr, nullptr, nullptr,
-                                                            nullptr);
+        k_rmat_keep<false><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, (uint32_t)p, (uint32_t)rank, cursor, nullptr,
+                                                            nullptr, nullptr, nullptr);
         e = cudaMemcpyAsync(&K, cursor, 8, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) break;
@@ -745,7 +747,8 @@ int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, doub
         if ((rc = lmx_alloc(ctx, (void **)&kpos, K1 * 4, "kept pos")) != LMX_OK) break;
         e = cudaMemsetAsync(cursor, 0, 16, st);
         if (e != cudaSuccess) break;
-        k_rmat_keep<true><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, blo, bhi, cursor, ku, kv, kw, kpos);
+        k_rmat_keep<true><<<bgrid(ctx, k), kBlock, 0, st>>>(P, k, (uint32_t)p, (uint32_t)rank, cursor, ku, kv, kw,
+                                                           kpos);
         // group the kept triples by pair
         const int bits = bits_for(n);
         if ((rc = lmx_alloc(ctx, (void **)&key, K1 * 8, "pair keys")) != LMX_OK) break;
@@ -753,14 +756,11 @@ int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, doub
         if ((rc = lmx_alloc(ctx, (void **)&idx, K1 * 4, "pair idx")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&idx2, K1 * 4, "pair idx2")) != LMX_OK) break;
         k_pair_keys_local<<<bgrid(ctx, K1), kBlock, 0, st>>>(ku, kv, K, bits, key, idx);
-        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, (long long)K, 0, 2 * bits, st);
-        if (e != cudaSuccess) break;
-        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "pair sort tmp")) != LMX_OK) break;
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, (long long)K, 0, 2 * bits, st);
-        if (e != cudaSuccess) break;
+        if ((rc = lmx_sort_pairs(ctx, &key, &key2, &idx, &idx2, (long long)K, 0, 2 * bits, st, "pair sort")) !=
+            LMX_OK)
+            break;
         lmx_free(ctx, (void **)&key, K1 * 8);
         lmx_free(ctx, (void **)&idx, K1 * 4);
-        lmx_free(ctx, &tmp, tmp_bytes);
         // pairs, first-occurrence bits, degree contributions
         ctx->db_words = (k + 31) / 32;
         if ((rc = lmx_alloc(ctx, (void **)&ctx->db_bits, ctx->db_words * 4, "first-occurrence bits")) != LMX_OK) break;

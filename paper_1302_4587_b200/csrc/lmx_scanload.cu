@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "lmx_internal.cuh"
+#include "lmx_sort.cuh"
 
 using namespace lmx;
 
@@ -63,9 +64,15 @@ __global__ void k_pack_endpoints(const uint32_t *eu, const uint32_t *ev, const u
 
 // The slot stream in descending weight order (sorted position j = m-1-i);
 // 4 edges per thread per step, the gathers of a step in flight together.
+// Stream positions [ib, ib + cnt) of the m edges (a partition streams its
+// weight order in chunks), written from okey / sval index 0.
 __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, unsigned long long m,
-                              const uint2 *euv, uint32_t lo, uint32_t nl, uint32_t *okey, uint2 *sval) {
+                              unsigned long long ib, unsigned long long cnt, const uint2 *euv, uint32_t lo,
+                              uint32_t nl, uint32_t *okey, uint2 *sval) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    eid_sorted += m - ib - cnt;   // sorted positions j = m-1-(ib+i) for i in [0, cnt)
+    tied += m - ib - cnt;
+    m = cnt;
     for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < m;
          i0 += 4 * stride) {
         uint32_t e[4], t[4];
@@ -185,6 +192,132 @@ static int lgrid(lmx_ctx *ctx, unsigned long long work) {
     return (int)std::max<unsigned long long>(1, std::min(b, cap));
 }
 
+// 4. tie flags, cand0, lowpair over the owner-sorted slots ids0[0, S)
+// (owner[i]: local owner of slot i); partitions: slot sides, global edge ids.
+static int scan_post(lmx_ctx *ctx, const uint32_t *owner, unsigned long long S, unsigned long long *cnt) {
+    cudaStream_t st = ctx->stream;
+    const unsigned long long m = (unsigned long long)lmx_edges(ctx), lo = ctx->lo, nl = ctx->hi - ctx->lo;
+    const size_t S1 = std::max<unsigned long long>(S, 1);
+    cudaError_t e = cudaSuccess;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->cand0, std::max<unsigned long long>(nl, 1) * 8, "cand0"));
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(std::min(m, S), 1) * 8, "lowpair"));
+    e = cudaMemsetAsync(ctx->cand0, 0xFF, std::max<unsigned long long>(nl, 1) * 8, st);
+    if (ctx->dist_p > 1 && e == cudaSuccess) {   // which end of its edge each owned slot is (RoundMessages)
+        LMX_TRY(lmx_alloc(ctx, (void **)&ctx->slot_side, (S1 + 31) / 32 * 4, "slot side"));
+        e = cudaMemsetAsync(ctx->slot_side, 0, (S1 + 31) / 32 * 4, st);
+    }
+    if (e == cudaSuccess && S) {
+        k_scan_post<<<lgrid(ctx, S), kBlock, 0, st>>>(owner, ctx->ids0, ctx->w, S, (uint32_t)lo, ctx->cand0,
+                                                     ctx->lowpair, cnt, ctx->slot_side);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && ctx->geid && S + nl) {
+        k_to_global_eid<<<lgrid(ctx, S + nl), kBlock, 0, st>>>(ctx->ids0, S, ctx->cand0, nl, ctx->geid);
+        e = cudaGetLastError();
+    }
+    unsigned long long hc[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return lmx_cuda_check(ctx, e, "slot flags");
+    trace_mark(ctx, "  scan: flags + lowpair");
+    ctx->lowpair_n = hc[1];
+    if (ctx->dist_p == 1 && hc[1] != m) return lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count");
+    return LMX_OK;
+}
+
+// A partition's owned slots (weight order by owner), memory-lean: the
+// endpoints are packed (new ids) and the caller-id arrays freed -- a
+// partition never reads them again -- then the weight order is streamed in
+// chunks, each chunk's owned slots appended (a stable select keeps the
+// weight order), and the S owned slots sorted by owner.  Peak: the packed
+// endpoints + one chunk of the stream + the owned slots twice, instead of
+// the whole two-record-per-edge stream next to everything else.
+static int partition_slots(lmx_ctx *ctx, const uint32_t *newid, unsigned long long S, int bits) {
+    cudaStream_t st = ctx->stream;
+    const unsigned long long m = (unsigned long long)lmx_edges(ctx), lo = ctx->lo, nl = ctx->hi - ctx->lo;
+    const size_t S1 = std::max<unsigned long long>(S, 1);
+    const unsigned long long C = std::min<unsigned long long>(m, std::max<unsigned long long>(1ULL << 24, (m + 3) / 4));
+    uint2 *euv = nullptr, *sval = nullptr, *sorted = nullptr;
+    uint32_t *okey_c = nullptr, *okey2 = nullptr, *okey = nullptr;
+    unsigned long long *nsel = nullptr, *cnt = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&euv, m * 8, "packed endpoints")) != LMX_OK) break;
+        k_pack_endpoints<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, newid, m, euv);
+        if ((e = cudaGetLastError()) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        lmx_free(ctx, (void **)&ctx->eu, m * 4);
+        lmx_free(ctx, (void **)&ctx->ev, m * 4);
+        if ((rc = lmx_alloc(ctx, (void **)&okey2, S1 * 4, "owned keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&okey_c, 2 * C * 4, "stream chunk keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&sval, 2 * C * 8, "stream chunk")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&nsel, 8, "selected")) != LMX_OK) break;
+        cub::TransformInputIterator<char, OwnedFlag, const uint32_t *> flags(okey_c, OwnedFlag{(uint32_t)nl});
+        size_t t1 = 0, t2 = 0;
+        e = cub::DeviceSelect::If(nullptr, t1, okey_c, okey2, nsel, (long long)(2 * C), OwnedKey{(uint32_t)nl}, st);
+        if (e == cudaSuccess)
+            e = cub::DeviceSelect::Flagged(nullptr, t2, sval, flags, ctx->ids0, nsel, (long long)(2 * C), st);
+        if (e != cudaSuccess) break;
+        tmp_bytes = std::max(t1, t2);
+        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "select tmp")) != LMX_OK) break;
+        unsigned long long off = 0;
+        for (unsigned long long ib = 0; ib < m && e == cudaSuccess; ib += C) {
+            const unsigned long long k = std::min(C, m - ib);
+            k_desc_stream<<<lgrid(ctx, k), kBlock, 0, st>>>(ctx->ws_eid, ctx->ws_tied, m, ib, k, euv, (uint32_t)lo,
+                                                           (uint32_t)nl, okey_c, sval);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+            size_t a1 = t1, a2 = t2;
+            e = cub::DeviceSelect::If(tmp, a1, okey_c, okey2 + off, nsel, (long long)(2 * k), OwnedKey{(uint32_t)nl},
+                                      st);
+            if (e == cudaSuccess)
+                e = cub::DeviceSelect::Flagged(tmp, a2, sval, flags, ctx->ids0 + off, nsel, (long long)(2 * k), st);
+            unsigned long long got = 0;
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&got, nsel, 8, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            off += got;
+            if (off > S) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: owned slot count"); break; }
+        }
+        if (e != cudaSuccess || rc != LMX_OK) break;
+        if (off != S) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: owned slot count"); break; }
+        lmx_free(ctx, (void **)&euv, m * 8);
+        lmx_free(ctx, (void **)&okey_c, 2 * C * 4);
+        lmx_free(ctx, (void **)&sval, 2 * C * 8);
+        lmx_free(ctx, &tmp, tmp_bytes);
+        lmx_free(ctx, (void **)&ctx->ws_eid, m * 4);
+        lmx_free(ctx, (void **)&ctx->ws_tied, m * 4);
+        trace_mark(ctx, "  scan: chunked stream + owned select");
+        // stable sort of the S owned slots by owner: okey2 -> okey, ids0 -> sorted
+        if ((rc = lmx_alloc(ctx, (void **)&okey, S1 * 4, "owner keys")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&sorted, S1 * 8, "sorted slots")) != LMX_OK) break;
+        if ((rc = lmx_sort_pairs(ctx, &okey2, &okey, &ctx->ids0, &sorted, (long long)S, 0, bits, st,
+                                 "owner sort")) != LMX_OK)
+            break;
+        lmx_free(ctx, (void **)&ctx->ids0, S1 * 8);
+        ctx->ids0 = sorted;
+        sorted = nullptr;
+        lmx_free(ctx, (void **)&okey2, S1 * 4);
+        trace_mark(ctx, "  scan: owner sort");
+        if ((rc = lmx_alloc(ctx, (void **)&cnt, 16, "counts")) != LMX_OK) break;
+        if ((e = cudaMemsetAsync(cnt, 0, 16, st)) != cudaSuccess) break;
+        rc = scan_post(ctx, okey, S, cnt);
+    } while (0);
+    if (e != cudaSuccess && rc == LMX_OK) rc = lmx_cuda_check(ctx, e, "partition slots");
+    cudaStreamSynchronize(st);
+    lmx_free(ctx, (void **)&euv, m * 8);
+    lmx_free(ctx, (void **)&okey_c, 2 * C * 4);
+    lmx_free(ctx, (void **)&sval, 2 * C * 8);
+    lmx_free(ctx, (void **)&okey2, S1 * 4);
+    lmx_free(ctx, (void **)&okey, S1 * 4);
+    lmx_free(ctx, (void **)&sorted, S1 * 8);
+    lmx_free(ctx, (void **)&nsel, 8);
+    lmx_free(ctx, (void **)&cnt, 16);
+    lmx_free(ctx, &tmp, tmp_bytes);
+    return rc;
+}
+
 // Builds ctx->vbeg (local, n_local + 1), ctx->ids0 (owned slots, flags),
 // ctx->cand0, ctx->lowpair / lowpair_n from ctx->eu/ev/w, ctx->deg0 (device
 // ids) and the weight stage's ws_eid / ws_tied (descending order from the
@@ -225,6 +358,7 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
     int bits = 1;
     while (bits < 32 && (1ULL << bits) <= nl) ++bits;   // owner keys in [0, nl], nl = not owned
     int rc = LMX_OK;
+    if (part && m) return partition_slots(ctx, newid, S, bits);
     do {
         if ((rc = lmx_alloc(ctx, (void **)&okey, M2 * 4, "owner keys")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&okey2, M2 * 4, "owner keys out")) != LMX_OK) break;
@@ -235,90 +369,21 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
             // the packed endpoints borrow the owner-key output buffer (same size)
             uint2 *euv = reinterpret_cast<uint2 *>(okey2);
             k_pack_endpoints<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, newid, m, euv);
-            k_desc_stream<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->ws_eid, ctx->ws_tied, m, euv, (uint32_t)lo,
+            k_desc_stream<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->ws_eid, ctx->ws_tied, m, 0, m, euv, (uint32_t)lo,
                                                            (uint32_t)nl, okey, sval);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "slot stream"); break; }
         trace_mark(ctx, "  scan: slot stream");
-        const uint32_t *owner = okey2;   // owner of each sorted slot, for the post pass
-        if (m && !part) {
-            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2,
-                                                0, bits, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey, okey2, sval, ctx->ids0, (long long)slots2, 0,
-                                                bits, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
+        if (m && !part) {   // (sval and ids0 have the same size: S = 2m on one GPU)
+            if ((rc = lmx_sort_pairs(ctx, &okey, &okey2, &sval, &ctx->ids0, (long long)slots2, 0, bits, st,
+                                     "owner sort")) != LMX_OK)
+                break;
             trace_mark(ctx, "  scan: owner sort");
-        } else if (m) {
-            // the owned slots, weight order kept: keys -> okey2, values -> ids0
-            unsigned long long *nsel = nullptr;
-            if ((rc = lmx_alloc(ctx, (void **)&nsel, 8, "selected")) != LMX_OK) break;
-            cub::TransformInputIterator<char, OwnedFlag, const uint32_t *> flags(okey, OwnedFlag{(uint32_t)nl});
-            size_t t1 = 0, t2 = 0;
-            e = cub::DeviceSelect::If(nullptr, t1, okey, okey2, nsel, (long long)slots2, OwnedKey{(uint32_t)nl}, st);
-            if (e == cudaSuccess)
-                e = cub::DeviceSelect::Flagged(nullptr, t2, sval, flags, ctx->ids0, nsel, (long long)slots2, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "select sizing"); break; }
-            tmp_bytes = std::max(t1, t2);
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "select tmp")) != LMX_OK) break;
-            e = cub::DeviceSelect::If(tmp, t1, okey, okey2, nsel, (long long)slots2, OwnedKey{(uint32_t)nl}, st);
-            if (e == cudaSuccess)
-                e = cub::DeviceSelect::Flagged(tmp, t2, sval, flags, ctx->ids0, nsel, (long long)slots2, st);
-            unsigned long long got = 0;
-            if (e == cudaSuccess) e = cudaMemcpyAsync(&got, nsel, 8, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            lmx_free(ctx, (void **)&nsel, 8);
-            lmx_free(ctx, &tmp, tmp_bytes);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owned select"); break; }
-            if (got != S) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: owned slot count"); break; }
-            lmx_free(ctx, (void **)&sval, M2 * 8);
-            // stable sort of the S owned slots by owner: okey2 -> okey, ids0 -> sorted
-            if ((rc = lmx_alloc(ctx, (void **)&sorted, S1 * 8, "sorted slots")) != LMX_OK) break;
-            tmp_bytes = 0;
-            e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, okey2, okey, ctx->ids0, sorted, (long long)S, 0,
-                                                bits, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort sizing"); break; }
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "owner sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, okey2, okey, ctx->ids0, sorted, (long long)S, 0,
-                                                bits, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "owner sort"); break; }
-            lmx_free(ctx, (void **)&ctx->ids0, S1 * 8);
-            ctx->ids0 = sorted;
-            sorted = nullptr;
-            owner = okey;
-            trace_mark(ctx, "  scan: owned select + owner sort");
         }
         lmx_free(ctx, (void **)&sval, M2 * 8);
         lmx_free(ctx, &tmp, tmp_bytes);
-        // 4. flags, cand0, lowpair over the owned prefix [0, S)
-        if ((rc = lmx_alloc(ctx, (void **)&ctx->cand0, std::max<unsigned long long>(nl, 1) * 8, "cand0")) != LMX_OK)
-            break;
-        if ((rc = lmx_alloc(ctx, (void **)&ctx->lowpair, std::max<unsigned long long>(std::min(m, S), 1) * 8,
-                            "lowpair")) != LMX_OK)
-            break;
-        e = cudaMemsetAsync(ctx->cand0, 0xFF, std::max<unsigned long long>(nl, 1) * 8, st);
-        if (ctx->dist_p > 1 && e == cudaSuccess) {   // which end of its edge each owned slot is (RoundMessages)
-            if ((rc = lmx_alloc(ctx, (void **)&ctx->slot_side, (S1 + 31) / 32 * 4, "slot side")) != LMX_OK) break;
-            e = cudaMemsetAsync(ctx->slot_side, 0, (S1 + 31) / 32 * 4, st);
-        }
-        if (e == cudaSuccess && S) {
-            k_scan_post<<<lgrid(ctx, S), kBlock, 0, st>>>(owner, ctx->ids0, ctx->w, S, (uint32_t)lo, ctx->cand0,
-                                                         ctx->lowpair, cnt, ctx->slot_side);
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess && ctx->geid && S + nl) {
-            k_to_global_eid<<<lgrid(ctx, S + nl), kBlock, 0, st>>>(ctx->ids0, S, ctx->cand0, nl, ctx->geid);
-            e = cudaGetLastError();
-        }
-        unsigned long long hc[2] = {0, 0};
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "slot flags"); break; }
-        trace_mark(ctx, "  scan: flags + lowpair");
-        ctx->lowpair_n = hc[1];
-        if (ctx->dist_p == 1 && hc[1] != m) { rc = lmx_fail(ctx, LMX_ECUDA, "internal: lowpair count"); break; }
+        rc = scan_post(ctx, okey2, S, cnt);   // okey2: the owner of each sorted slot
     } while (0);
     cudaStreamSynchronize(st);
     lmx_free(ctx, (void **)&okey, M2 * 4);

@@ -26,6 +26,7 @@
 #include <thread>
 
 #include "lmx_internal.cuh"
+#include "lmx_sort.cuh"
 
 using namespace lmx;
 
@@ -168,23 +169,39 @@ __device__ __forceinline__ bool check_uv(long long a, long long b, long long n) 
 }
 __device__ __forceinline__ bool check_w(double x) { return isfinite(x) && !(x < 0.0); }
 
+// Degree count of one endpoint per lane: lanes of a warp holding the same
+// vertex add once (edge lists sorted by their first endpoint, as build_graph
+// leaves them, repeat it across neighbouring lanes).
+__device__ __forceinline__ void add_degree_grouped(uint32_t *deg, uint32_t a, bool on) {
+#ifdef LMX_DEG_PLAIN
+    if (on) atomicAdd(deg + a, 1u);
+#else
+    const uint32_t active = __activemask();
+    const uint32_t key = on ? a : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(active, key);
+    const int lane = threadIdx.x & 31;
+    if (on && (__ffs(peers) - 1) == lane) atomicAdd(deg + a, (uint32_t)__popc(peers));
+#endif
+}
+
 __global__ void k_convert(const long long *u, const long long *v, const double *w,
                           unsigned long long k, long long n, unsigned long long base, uint32_t *eu,
                           uint32_t *ev, double *wout, uint32_t *deg, unsigned long long *bad) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k;
-         i += stride) {
-        const long long a = u[i], b = v[i];
-        const double x = w[i];
-        const bool uv = check_uv(a, b, n);
-        if (!uv || !check_w(x)) atomicMin(bad, base + i);
-        eu[base + i] = (uint32_t)a;
-        ev[base + i] = (uint32_t)b;
-        wout[base + i] = x;
-        if (uv) {
-            atomicAdd(deg + a, 1u);
-            atomicAdd(deg + b, 1u);
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x; i0 < k; i0 += stride) {
+        const unsigned long long i = i0 + threadIdx.x;   // whole warps stay in the loop (match_any)
+        const bool in = i < k;
+        const long long a = in ? u[i] : 0, b = in ? v[i] : 0;
+        const double x = in ? w[i] : 0.0;
+        const bool uv = in && check_uv(a, b, n);
+        if (in) {
+            if (!uv || !check_w(x)) atomicMin(bad, base + i);
+            eu[base + i] = (uint32_t)a;
+            ev[base + i] = (uint32_t)b;
+            wout[base + i] = x;
         }
+        add_degree_grouped(deg, (uint32_t)a, uv);
+        if (uv) atomicAdd(deg + b, 1u);
     }
 }
 
@@ -213,10 +230,11 @@ __global__ void k_check_w(const double *w, unsigned long long m, unsigned long l
 
 __global__ void k_degrees(const uint32_t *eu, const uint32_t *ev, unsigned long long m, uint32_t *deg) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-         e += stride) {
-        atomicAdd(deg + eu[e], 1u);
-        atomicAdd(deg + ev[e], 1u);
+    for (unsigned long long e0 = (unsigned long long)blockIdx.x * blockDim.x; e0 < m; e0 += stride) {
+        const unsigned long long e = e0 + threadIdx.x;
+        const bool in = e < m;
+        add_degree_grouped(deg, in ? eu[e] : 0u, in);
+        if (in) atomicAdd(deg + ev[e], 1u);
     }
 }
 
@@ -435,8 +453,9 @@ void trace_mark(lmx_ctx *ctx, const char *what) {
     if (!on) return;
     cudaStreamSynchronize(ctx->stream);
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[lmx setup] %-24s %9.3f ms\n", what,
-            std::chrono::duration<double, std::milli>(now - last).count());
+    fprintf(stderr, "[lmx setup] %-24s %9.3f ms  (live %.2f GB, peak %.2f GB)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(), ctx->dev_bytes / 1e9,
+            ctx->peak_bytes / 1e9);
     last = now;
 }
 
@@ -461,18 +480,15 @@ static int static_order_stage(lmx_ctx *ctx, bool uniform) {
         if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "static vals")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "static vals2")) != LMX_OK) break;
         if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "static tied")) != LMX_OK) break;
-        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
-        if (e != cudaSuccess) break;
-        if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "static sort tmp")) != LMX_OK) break;
         k_salt_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(m, rs, keys, vals);
-        size_t t1 = tmp_bytes;
-        e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
-        if (e != cudaSuccess) break;
+        if ((rc = lmx_sort_pairs(ctx, &keys, &keys2, &vals, &vals2, (long long)m, 0, 64, st, "static salt sort")) !=
+            LMX_OK)
+            break;
         if (!uniform) {   // stable: equal weights keep the salt order
             k_weight_keys_of<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, vals2, m, keys);
-            t1 = tmp_bytes;
-            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals2, vals, (long long)m, 0, 64, st);
-            if (e != cudaSuccess) break;
+            if ((rc = lmx_sort_pairs(ctx, &keys, &keys2, &vals2, &vals, (long long)m, 0, 64, st,
+                                     "static weight sort")) != LMX_OK)
+                break;
             std::swap(vals, vals2);
         }
         e = cudaMemsetAsync(tied, 0, m * 4, st);
@@ -553,19 +569,19 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
+            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
+            if ((rc = lmx_sort_pairs(ctx, &keys, &keys2, &vals, &vals2, (long long)m, 0, 64, st, "key sort")) !=
+                LMX_OK)
+                break;
+            trace_mark(ctx, "  weight sort");
+            lmx_free(ctx, (void **)&keys, m * 8);   // the sort's scratch half
             if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&tidx, m * 4, "tie idx")) != LMX_OK) break;
-            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
-            size_t t1 = 0, t2 = 0;
-            cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, vals, vals2,
-                                                            (long long)m, 0, 64, st);
-            if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort sizing"); break; }
-            tmp_bytes = std::max(t1, t2);
-            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "sort tmp")) != LMX_OK) break;
-            e = cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys2, vals, vals2, (long long)m, 0, 64, st);
-            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "key sort"); break; }
-            trace_mark(ctx, "  weight sort");
+            size_t t2 = 0;
+            cudaError_t e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
+            if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "scan sizing"); break; }
+            tmp_bytes = t2;
+            if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "scan tmp")) != LMX_OK) break;
             // dense rank of the weight value (vals reused)
             k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
             e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
@@ -593,6 +609,17 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             ctx->layout = distinct ? kDistinct : kGeneral;
             ctx->n_distinct = (uint32_t)D;
             ctx->n_tied = (uint32_t)T;
+            // round-loop algorithm: the weight-ordered scan loop needs (almost)
+            // distinct weights -- a tied run is rescanned every round -- and
+            // n < 2^30 (slot flag bits); it keeps the descending order itself
+            // (eid by sorted position + global tie flags) for lmx_scan_build_slots
+            if (distinct && ctx->force_algo != 0 && !ctx->scan_rejected && ctx->n < (1LL << 30)) {
+                ctx->algo = 1;
+                ctx->ws_eid = vals2;
+                ctx->ws_tied = tied;
+                vals2 = tied = nullptr;
+                break;
+            }
             if ((rc = lmx_alloc(ctx, (void **)&kofe, m * 4, "key of edge")) != LMX_OK) break;
             uint32_t *key_of_eid = kofe;
             if (distinct) {
@@ -600,19 +627,6 @@ int lmx_weight_stage(lmx_ctx *ctx) {
                 if ((rc = lmx_alloc(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4,
                                     "tie_rank")) != LMX_OK)
                     break;
-            }
-            // round-loop algorithm: the weight-ordered scan loop needs (almost)
-            // distinct weights -- a tied run is rescanned every round -- and
-            // n < 2^30 (slot flag bits); it keeps the descending order itself
-            // (eid by sorted position + global tie flags) for lmx_scan_build_slots
-            if (distinct && ctx->force_algo != 0 && !ctx->scan_rejected && ctx->n < (1LL << 30)) {
-                ctx->algo = 1;
-                lmx_free(ctx, (void **)&ctx->eid_of_x, (D + T) * 4);
-                lmx_free(ctx, (void **)&ctx->tie_rank, std::max<unsigned long long>(T, 1) * 4);
-                ctx->ws_eid = vals2;
-                ctx->ws_tied = tied;
-                vals2 = tied = nullptr;
-                break;
             }
             k_keys_out<<<grid_for(ctx, m), kBlock, 0, st>>>(vals, tidx, tied, vals2, m, distinct ? 1 : 0,
                                                            (uint32_t)D, key_of_eid, ctx->eid_of_x, ctx->tie_rank,
@@ -655,7 +669,7 @@ int lmx_setup_device_edges(lmx_ctx *ctx) {
 }
 
 void lmx_free_weight_stage(lmx_ctx *ctx) {
-    const size_t m4 = (size_t)std::max<int64_t>(ctx->m, 1) * 4;
+    const size_t m4 = (size_t)std::max<int64_t>(lmx_edges(ctx), 1) * 4;   // a partition: its local edges
     lmx_free(ctx, (void **)&ctx->ws_kofe, m4);
     lmx_free(ctx, (void **)&ctx->ws_rank, m4);
     lmx_free(ctx, (void **)&ctx->ws_eid, m4);

@@ -300,8 +300,8 @@ def build_rmat_distributed(ranks, comm, scale: int, edge_factor: int = 16, a: fl
                            c: float = 0.19, seed: int = 1, permute: bool = True):
     """Load the local partitions ``ranks`` (created with ``defer=True``) with the
     RMAT graph of ``lmx_gen_rmat``'s recipe WITHOUT any rank holding the whole
-    graph (config C5): each rank builds the pairs whose lower end is in its
-    build range, the first-occurrence bitmaps and the degrees are summed over
+    graph (config C5): each rank builds the pairs that hash to it (an even
+    share whatever the ids), the first-occurrence bitmaps and the degrees are summed over
     the ranks (the global edge ids and partition_graph's cuts follow), and
     every pair is sent to the owners of its ends (all-to-all-v)."""
     import torch
