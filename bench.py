@@ -491,7 +491,9 @@ def run_b200(args):
     # weight-ordered segments, candidates, lowpair), CUDA events on its stream
     du, dv, dw = eng.export_graph_device()
     load_ms = []
-    for _ in range(2):
+    for rep in range(2):
+        if rep == 1:
+            eng.peak_device_bytes(reset=True)
         torch.cuda.synchronize()
         l0 = torch.cuda.Event(enable_timing=True)
         l1 = torch.cuda.Event(enable_timing=True)
@@ -500,6 +502,9 @@ def run_b200(args):
         l1.record(stream)
         torch.cuda.synchronize()
         load_ms.append(l0.elapsed_time(l1))
+    device_memory = {"after_load_GB": round(eng.device_bytes() / 1e9, 2),
+                     "load_peak_GB": round(eng.peak_device_bytes() / 1e9, 2),
+                     "note": "engine allocations (device edge inputs of the load excluded)"}
     del du, dv, dw
     torch.cuda.empty_cache()
     load_device_ms = min(load_ms)
@@ -683,6 +688,7 @@ def run_b200(args):
                             "degrees, relabelling, weight-ordered segments, candidates, lowpair), CUDA events, "
                             "best of 2; not inside `value`",
         "value_with_load": m / ((load_device_ms + ms_per_step) / 1000.0),
+        "device_memory": device_memory,
         "roofline": roofline, "step_roofline": step_roofline,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": launches, "rounds_enqueued": rounds_exec,
