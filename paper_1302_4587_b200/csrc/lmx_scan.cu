@@ -61,6 +61,9 @@ namespace lmx {
 
 constexpr int kHistBins = 256;   // death-round bins kept in shared memory (more go global)
 constexpr int kVpl = LMX_SCAN_VPL;
+#ifndef LMX_SLOW_BALANCE
+#define LMX_SLOW_BALANCE 1   // deal a warp's slow-path vertices round-robin to its lanes (0: each lane its own)
+#endif
 
 constexpr uint32_t kTiedFlag = 0x80000000u;   // candidate word: the weight is tied at v
 constexpr uint32_t kNbrMask = 0x7FFFFFFFu;
@@ -181,7 +184,8 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 // neighbour is unmatched and its weight unique, so most vertices read 12
 // bytes (list, cand) plus one bitmap bit and write nothing.
 template <bool FIRST, bool DIST>
-__device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long (&s_red)[3][kWarps]) {
+__device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long (&s_red)[3][kWarps],
+                                           uint32_t (*s_slowq)[32 * kVpl]) {
     const uint32_t na = a.ctr->pad[0];
     if (na == 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -244,20 +248,7 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
             }
         }
         // slow path: the candidate died (advance past dead slots) or its weight is tied
-        while (slow) {
-            const int k = __ffs(slow) - 1;
-            slow &= slow - 1;
-            uint32_t vk = 0;
-            uint2 ck = make_uint2(kNone, kNone);
-            // (fetching ptr / degree / offset for all vertices up front, before the
-            // liveness test, was measured slower: 2.82 -> 2.91 ms per step)
-#pragma unroll
-            for (int it = 0; it < kVpl; ++it) {
-                if (it == k) {
-                    vk = v[it];
-                    ck = c[it];
-                }
-            }
+        auto slow_one = [&](uint32_t vk, uint32_t ck) {
             const uint32_t vl = vk - a.lo;
             const uint32_t pk = FIRST ? 0u : a.ptr[vl];
             const unsigned long long bk = a.vbeg[vl];
@@ -266,7 +257,7 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
             const uint32_t dk = (uint32_t)(a.vbeg[vl + 1] - bk);
             // an untied candidate sits at ptr and is known dead: search past it;
             // a tied one: ptr is the first slot not known dead, live or not
-            uint32_t pp = (!FIRST && ck.x != kNone && !(ck.x & kTiedFlag)) ? pk + 1 : pk;
+            uint32_t pp = (!FIRST && ck != kNone && !(ck & kTiedFlag)) ? pk + 1 : pk;
             uint2 out = make_uint2(kNone, kNone);
             const bool found = advance<FIRST>(a, bk, pp, dk, out, reads);
             const bool tied = found && (out.x & kSlotTied);
@@ -278,7 +269,46 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
             if (DIST && found && nbr - a.lo >= a.nl) propose_record(a, nbr, out.y);
             found_n += found ? 1u : 0u;
             ++slow_n;
+        };
+#if LMX_SLOW_BALANCE
+        // the warp's slow vertices, dealt round-robin to its lanes: a lane no
+        // longer chains up to kVpl of them while its neighbours idle
+        {
+            uint32_t qn = 0;
+#pragma unroll
+            for (int it = 0; it < kVpl; ++it) {
+                const bool sl = (slow >> it) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, sl);
+                // the vertex and whether its candidate is untied (then known dead: search past ptr)
+                if (sl)
+                    s_slowq[tid >> 5][qn + __popc(bal & lanemask_lt_u32())] =
+                        v[it] | ((c[it].x != kNone && !(c[it].x & kTiedFlag)) ? 0x80000000u : 0u);
+                qn += __popc(bal);
+            }
+            __syncwarp();
+            for (uint32_t q = lane; q < qn; q += 32) {
+                const uint32_t e = s_slowq[tid >> 5][q];
+                slow_one(e & 0x7FFFFFFFu, (e >> 31) ? 0u : kNone);   // 0: an untied candidate word
+            }
+            __syncwarp();
         }
+#else
+        while (slow) {
+            const int k = __ffs(slow) - 1;
+            slow &= slow - 1;
+            uint32_t vk = 0, ck = kNone;
+            // (fetching ptr / degree / offset for all vertices up front, before the
+            // liveness test, was measured slower: 2.82 -> 2.91 ms per step)
+#pragma unroll
+            for (int it = 0; it < kVpl; ++it) {
+                if (it == k) {
+                    vk = v[it];
+                    ck = c[it].x;
+                }
+            }
+            slow_one(vk, ck);
+        }
+#endif
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -309,7 +339,8 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
 template <bool FIRST, bool DIST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
     __shared__ unsigned long long s_red[3][kWarps];
-    probe_body<FIRST, DIST>(a, s_red);
+    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl];
+    probe_body<FIRST, DIST>(a, s_red, s_slowq);
 }
 
 struct ScanMatchArgs {
@@ -461,6 +492,7 @@ __global__ void __launch_bounds__(kBlock, LMX_LOOP_MINB) lmx_scan_loop_kernel(Lo
     __shared__ unsigned long long s_red[3][kWarps];
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ uint32_t s_base;
+    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl];
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const bool stamp = L.stamps && blockIdx.x == 0 && threadIdx.x == 0;
     int r = L.r0;
@@ -470,8 +502,8 @@ __global__ void __launch_bounds__(kBlock, LMX_LOOP_MINB) lmx_scan_loop_kernel(Lo
         a.alist = r == 0 ? L.bins0 : L.lists[r & 1];
         a.ctr = L.ctr + r;
         a.rs = mix64(L.seed_mix ^ (L.rerandomize ? (uint64_t)r : 0ULL));
-        if (r == 0) probe_body<true, false>(a, s_red);
-        else probe_body<false, false>(a, s_red);
+        if (r == 0) probe_body<true, false>(a, s_red, s_slowq);
+        else probe_body<false, false>(a, s_red, s_slowq);
         grid.sync();
         if (stamp) L.stamps[2 * r + 1] = globaltimer();
         if (L.ctr[r].live_slots == 0) break;   // no candidate anywhere: m_r = 0
