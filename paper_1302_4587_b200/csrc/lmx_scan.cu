@@ -64,6 +64,9 @@ constexpr int kVpl = LMX_SCAN_VPL;
 #ifndef LMX_SLOW_BALANCE
 #define LMX_SLOW_BALANCE 1   // deal a warp's slow-path vertices round-robin to its lanes (0: each lane its own)
 #endif
+#ifndef LMX_SLOW_BATCH
+#define LMX_SLOW_BATCH 1     // chunks whose slow vertices are pooled before they are dealt
+#endif
 
 constexpr uint32_t kTiedFlag = 0x80000000u;   // candidate word: the weight is tied at v
 constexpr uint32_t kNbrMask = 0x7FFFFFFFu;
@@ -185,7 +188,7 @@ __device__ __forceinline__ void resolve_tie(const ScanArgs &a, unsigned long lon
 // bytes (list, cand) plus one bitmap bit and write nothing.
 template <bool FIRST, bool DIST>
 __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long (&s_red)[3][kWarps],
-                                           uint32_t (*s_slowq)[32 * kVpl]) {
+                                           uint32_t (*s_slowq)[32 * kVpl * LMX_SLOW_BATCH]) {
     const uint32_t na = a.ctr->pad[0];
     if (na == 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -203,6 +206,45 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
     const uint32_t nstat = FIRST ? nchunks : (uint32_t)((unsigned long long)nchunks * LMX_SCAN_STATIC_PCT / 100);
     uint32_t c = blockIdx.x * (uint32_t)kWarps + (uint32_t)(tid >> 5);
     const uint32_t cstride = gridDim.x * (uint32_t)kWarps;
+    // slow path: the candidate died (advance past dead slots) or its weight is tied
+    auto slow_one = [&](uint32_t vk, uint32_t ck) {
+        const uint32_t vl = vk - a.lo;
+        const uint32_t pk = FIRST ? 0u : a.ptr[vl];
+        const unsigned long long bk = a.vbeg[vl];
+        // the segment end sits next to its start (same sector 3 times in
+        // 4): one random gather fewer than reading a degree (2.62 -> 2.52 ms)
+        const uint32_t dk = (uint32_t)(a.vbeg[vl + 1] - bk);
+        // an untied candidate sits at ptr and is known dead: search past it;
+        // a tied one: ptr is the first slot not known dead, live or not
+        uint32_t pp = (!FIRST && ck != kNone && !(ck & kTiedFlag)) ? pk + 1 : pk;
+        uint2 out = make_uint2(kNone, kNone);
+        const bool found = advance<FIRST>(a, bk, pp, dk, out, reads);
+        const bool tied = found && (out.x & kSlotTied);
+        if (tied) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
+        const uint32_t nbr = out.x & kSlotNbr;
+        a.cnbr[vl] = found ? (nbr | (tied ? kTiedFlag : 0u)) : kNone;
+        if (tied) a.ckey[vl] = out.y;   // an untied candidate's edge is the slot at ptr
+        if (pp != pk) a.ptr[vl] = pp;
+        if (DIST && found && nbr - a.lo >= a.nl) propose_record(a, nbr, out.y);
+        found_n += found ? 1u : 0u;
+        ++slow_n;
+    };
+#if LMX_SLOW_BALANCE
+    // the warp's slow vertices of LMX_SLOW_BATCH chunks, dealt round-robin to
+    // its lanes: a lane no longer chains up to kVpl of them while its
+    // neighbours idle
+    uint32_t qn = 0, nb = 0;
+    auto drain = [&]() {
+        __syncwarp();
+        for (uint32_t q = lane; q < qn; q += 32) {
+            const uint32_t e = s_slowq[tid >> 5][q];
+            slow_one(e & 0x7FFFFFFFu, (e >> 31) ? 0u : kNone);   // 0: an untied candidate word
+        }
+        __syncwarp();
+        qn = 0;
+        nb = 0;
+    };
+#endif
     for (;;) {
         uint32_t i0 = 0;
         if (c < nstat) {
@@ -247,51 +289,18 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
                 slow |= 1u << it;
             }
         }
-        // slow path: the candidate died (advance past dead slots) or its weight is tied
-        auto slow_one = [&](uint32_t vk, uint32_t ck) {
-            const uint32_t vl = vk - a.lo;
-            const uint32_t pk = FIRST ? 0u : a.ptr[vl];
-            const unsigned long long bk = a.vbeg[vl];
-            // the segment end sits next to its start (same sector 3 times in
-            // 4): one random gather fewer than reading a degree (2.62 -> 2.52 ms)
-            const uint32_t dk = (uint32_t)(a.vbeg[vl + 1] - bk);
-            // an untied candidate sits at ptr and is known dead: search past it;
-            // a tied one: ptr is the first slot not known dead, live or not
-            uint32_t pp = (!FIRST && ck != kNone && !(ck & kTiedFlag)) ? pk + 1 : pk;
-            uint2 out = make_uint2(kNone, kNone);
-            const bool found = advance<FIRST>(a, bk, pp, dk, out, reads);
-            const bool tied = found && (out.x & kSlotTied);
-            if (tied) resolve_tie<FIRST>(a, bk, pp, dk, out, reads);
-            const uint32_t nbr = out.x & kSlotNbr;
-            a.cnbr[vl] = found ? (nbr | (tied ? kTiedFlag : 0u)) : kNone;
-            if (tied) a.ckey[vl] = out.y;   // an untied candidate's edge is the slot at ptr
-            if (pp != pk) a.ptr[vl] = pp;
-            if (DIST && found && nbr - a.lo >= a.nl) propose_record(a, nbr, out.y);
-            found_n += found ? 1u : 0u;
-            ++slow_n;
-        };
 #if LMX_SLOW_BALANCE
-        // the warp's slow vertices, dealt round-robin to its lanes: a lane no
-        // longer chains up to kVpl of them while its neighbours idle
-        {
-            uint32_t qn = 0;
 #pragma unroll
-            for (int it = 0; it < kVpl; ++it) {
-                const bool sl = (slow >> it) & 1u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, sl);
-                // the vertex and whether its candidate is untied (then known dead: search past ptr)
-                if (sl)
-                    s_slowq[tid >> 5][qn + __popc(bal & lanemask_lt_u32())] =
-                        v[it] | ((c[it].x != kNone && !(c[it].x & kTiedFlag)) ? 0x80000000u : 0u);
-                qn += __popc(bal);
-            }
-            __syncwarp();
-            for (uint32_t q = lane; q < qn; q += 32) {
-                const uint32_t e = s_slowq[tid >> 5][q];
-                slow_one(e & 0x7FFFFFFFu, (e >> 31) ? 0u : kNone);   // 0: an untied candidate word
-            }
-            __syncwarp();
+        for (int it = 0; it < kVpl; ++it) {
+            const bool sl = (slow >> it) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, sl);
+            // the vertex and whether its candidate is untied (then known dead: search past ptr)
+            if (sl)
+                s_slowq[tid >> 5][qn + __popc(bal & lanemask_lt_u32())] =
+                    v[it] | ((c[it].x != kNone && !(c[it].x & kTiedFlag)) ? 0x80000000u : 0u);
+            qn += __popc(bal);
         }
+        if (++nb == LMX_SLOW_BATCH) drain();
 #else
         while (slow) {
             const int k = __ffs(slow) - 1;
@@ -310,6 +319,9 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
         }
 #endif
     }
+#if LMX_SLOW_BALANCE
+    drain();
+#endif
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         found_n += __shfl_xor_sync(0xffffffffu, found_n, off);
@@ -339,7 +351,7 @@ __device__ __forceinline__ void probe_body(const ScanArgs &a, unsigned long long
 template <bool FIRST, bool DIST>
 __global__ void __launch_bounds__(kBlock, LMX_SCAN_MINB) lmx_scan_round_kernel(ScanArgs a) {
     __shared__ unsigned long long s_red[3][kWarps];
-    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl];
+    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl * LMX_SLOW_BATCH];
     probe_body<FIRST, DIST>(a, s_red, s_slowq);
 }
 
@@ -492,7 +504,7 @@ __global__ void __launch_bounds__(kBlock, LMX_LOOP_MINB) lmx_scan_loop_kernel(Lo
     __shared__ unsigned long long s_red[3][kWarps];
     __shared__ uint32_t s_cnt[kWarps];
     __shared__ uint32_t s_base;
-    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl];
+    __shared__ uint32_t s_slowq[LMX_SLOW_BALANCE ? kWarps : 1][32 * kVpl * LMX_SLOW_BATCH];
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const bool stamp = L.stamps && blockIdx.x == 0 && threadIdx.x == 0;
     int r = L.r0;
