@@ -260,12 +260,14 @@ int lmx_last_round_counters(const lmx_ctx *ctx, int64_t *out, int cap_rounds) {
         o[1] = (int64_t)c.live_slots;
         o[2] = (int64_t)c.matched_v;
         // scan loop: |A_r| (vertices probed), slow-path probes; compact: bucket sizes 0..4
+        // (live degree <= 4, 17..32 + 5..16 (buckets 1 and 5 together), 33..1024, block, hub)
         if (ctx->algo == 1) {
             o[3] = c.pad[0];
             o[4] = c.n[0];
             o[5] = o[6] = o[7] = 0;
         } else {
             for (int q = 0; q < 5; ++q) o[3 + q] = c.n[q];
+            o[4] += c.n[5];
         }
     }
     return k;

@@ -50,14 +50,18 @@ constexpr int kBlock = 256;   // threads per block, every kernel
 constexpr int kWarps = kBlock / 32;
 
 // live-degree buckets of the per-round vertex lists and their mappings
-constexpr int kBuckets = 5;
 //   0: d <= 4            thread per vertex
 //   1: 5 <= d <= 32      8-lane group per vertex
 //   2: 33 <= d <= 1024   warp per vertex
 //   3: 1025 <= d < 32768 block per vertex
 //   4: d >= 32768        block per vertex, scheduled first
+// compacting loop live-degree buckets: 0: <= 4 a thread per vertex,
+// 5: <= 16 a group of 4 lanes, 1: <= 32 a group of 8 lanes, 2: <= 1024 a
+// warp, 3: < 32768 a block, 4: hubs, a block each (bucket 5 is numbered last
+// so the others keep their indices)
+constexpr int kBuckets = 6;
 __host__ __device__ __forceinline__ int bucket_of(uint32_t d) {
-    return d <= 4 ? 0 : d <= 32 ? 1 : d <= 1024 ? 2 : d < 32768 ? 3 : 4;
+    return d <= 4 ? 0 : d <= 16 ? 5 : d <= 32 ? 1 : d <= 1024 ? 2 : d < 32768 ? 3 : 4;
 }
 
 enum Layout { kUniform = 0, kDistinct = 1, kGeneral = 2 };

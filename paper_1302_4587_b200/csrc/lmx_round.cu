@@ -366,6 +366,43 @@ __device__ __forceinline__ void put_result(const RoundArgs &a, int mode, uint32_
     a.cand_id[v] = (w > 0) ? b.id : kNone;
 }
 
+// Buckets 1 and 5: a group of G lanes per vertex (live degree <= 4 G), 4
+// rounds of 32 / G vertices per grab.
+template <int MODE, int L, int G>
+__device__ __forceinline__ void group_bucket(const RoundArgs &a, int q, uint32_t n, int lane,
+                                             unsigned long long &live, unsigned long long &reads) {
+    constexpr int kVpi = 32 / G, kGrab = 4 * kVpi;
+    static_assert(G >= 4 && G <= 32 && (G & (G - 1)) == 0, "a grab's vertices are one per lane");
+    for (;;) {
+        uint32_t i0 = 0;
+        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[q], (uint32_t)kGrab);
+        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        if (i0 >= n) break;
+        uint32_t mv = kNone, md = 0;
+        unsigned long long mb = 0;
+        if (lane < kGrab && i0 + lane < n) {
+            mv = a.list[q][i0 + lane];
+            md = a.vdeg[mv];
+            mb = a.vbeg[mv];
+        }
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+            const int src = it * kVpi + lane / G;
+            const uint32_t v = __shfl_sync(0xffffffffu, mv, src);
+            const uint32_t d = __shfl_sync(0xffffffffu, md, src);
+            const unsigned long long beg = __shfl_sync(0xffffffffu, mb, src);
+            Best b;
+            best_init(b);
+            const uint32_t w = group_vertex<MODE, L, G, 4>(a, beg, d, lane, b);
+            if ((lane & (G - 1)) == 0 && d) {
+                put_result(a, MODE, v, w, b);
+                live += w;
+                reads += d;
+            }
+        }
+    }
+}
+
 template <int MODE, int L>
 __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a) {
     __shared__ uint32_t s_cnt[kBlockItems][kWarps];
@@ -392,7 +429,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
 
     // phase 1: buckets 4 then 3, one block per vertex
 #pragma unroll
-    for (int q = kBuckets - 1; q >= 3; --q) {
+    for (int q = 4; q >= 3; --q) {
         for (;;) {
             if (tid == 0) s_item = atomicAdd(&a.ctr->cur[q], 1u);
             __syncthreads();
@@ -453,35 +490,9 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
     }
 
     PHASE_MARK(1);
-    // phase 3: bucket 1, 8 lanes per vertex, 16 vertices per grab
-    for (;;) {
-        uint32_t i0 = 0;
-        if (lane == 0) i0 = atomicAdd(&a.ctr->cur[1], 16u);
-        i0 = __shfl_sync(0xffffffffu, i0, 0);
-        if (i0 >= nb[1]) break;
-        uint32_t mv = kNone, md = 0;
-        unsigned long long mb = 0;
-        if (lane < 16 && i0 + lane < nb[1]) {
-            mv = a.list[1][i0 + lane];
-            md = a.vdeg[mv];
-            mb = a.vbeg[mv];
-        }
-#pragma unroll 1
-        for (int it = 0; it < 4; ++it) {
-            const int src = it * 4 + (lane >> 3);
-            const uint32_t v = __shfl_sync(0xffffffffu, mv, src);
-            const uint32_t d = __shfl_sync(0xffffffffu, md, src);
-            const unsigned long long beg = __shfl_sync(0xffffffffu, mb, src);
-            Best b;
-            best_init(b);
-            const uint32_t w = group_vertex<MODE, L, 8, 4>(a, beg, d, lane, b);
-            if ((lane & 7) == 0 && d) {
-                put_result(a, MODE, v, w, b);
-                live += w;
-                reads += d;
-            }
-        }
-    }
+    // phase 3: buckets 1 (8 lanes per vertex) and 5 (4 lanes per vertex)
+    group_bucket<MODE, L, 8>(a, 1, nb[1], lane, live, reads);
+    group_bucket<MODE, L, 4>(a, 5, nb[5], lane, live, reads);
 
     PHASE_MARK(2);
     // phase 4: bucket 0, thread per vertex, 128 vertices per grab

@@ -12,8 +12,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=26)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--er", action="store_true", help="the er24unit family (unit weights, compacting loop)")
+ap.add_argument("--compact", action="store_true", help="force the compacting loop (LMX_OPT_ALGO 0)")
 args = ap.parse_args()
 eng = Engine(0)
+if args.compact:
+    eng.set_algo("compact")
 if args.er:
     eng.gen_er(args.scale, 4, seed=1, unit=True)
 else:
