@@ -58,7 +58,8 @@ constexpr int kWarps = kBlock / 32;
 // compacting loop live-degree buckets: 0: <= 4 a thread per vertex,
 // 5: <= 16 a group of 4 lanes, 1: <= 32 a group of 8 lanes, 2: <= 1024 a
 // warp, 3: < 32768 a block, 4: hubs, a block each (bucket 5 is numbered last
-// so the others keep their indices)
+// so the others keep their indices; 2-lane groups for degree 5..8 measured
+// slower: ER-24 unit 4.2 against 3.4 ms)
 constexpr int kBuckets = 6;
 __host__ __device__ __forceinline__ int bucket_of(uint32_t d) {
     return d <= 4 ? 0 : d <= 16 ? 5 : d <= 32 ? 1 : d <= 1024 ? 2 : d < 32768 ? 3 : 4;
@@ -127,7 +128,7 @@ struct lmx_ctx {
     uint32_t *tie_rank = nullptr;            // [n_tied]
     // round-0 bucket lists (built once per graph, ascending vertex id)
     uint32_t *bins0 = nullptr;               // kBuckets regions of capacity n
-    unsigned int n_bins0[lmx::kBuckets] = {0, 0, 0, 0, 0};
+    unsigned int n_bins0[lmx::kBuckets] = {};
 
     // match state
     uint32_t *vdeg = nullptr;

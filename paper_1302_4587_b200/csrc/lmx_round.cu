@@ -371,8 +371,8 @@ __device__ __forceinline__ void put_result(const RoundArgs &a, int mode, uint32_
 template <int MODE, int L, int G>
 __device__ __forceinline__ void group_bucket(const RoundArgs &a, int q, uint32_t n, int lane,
                                              unsigned long long &live, unsigned long long &reads) {
-    constexpr int kVpi = 32 / G, kGrab = 4 * kVpi;
-    static_assert(G >= 4 && G <= 32 && (G & (G - 1)) == 0, "a grab's vertices are one per lane");
+    constexpr int kVpi = 32 / G, kIters = kVpi > 8 ? 32 / kVpi : 4, kGrab = kIters * kVpi;
+    static_assert(G >= 2 && G <= 32 && (G & (G - 1)) == 0 && kGrab <= 32, "a grab's vertices are one per lane");
     for (;;) {
         uint32_t i0 = 0;
         if (lane == 0) i0 = atomicAdd(&a.ctr->cur[q], (uint32_t)kGrab);
@@ -386,7 +386,7 @@ __device__ __forceinline__ void group_bucket(const RoundArgs &a, int q, uint32_t
             mb = a.vbeg[mv];
         }
 #pragma unroll 1
-        for (int it = 0; it < 4; ++it) {
+        for (int it = 0; it < kIters; ++it) {
             const int src = it * kVpi + lane / G;
             const uint32_t v = __shfl_sync(0xffffffffu, mv, src);
             const uint32_t d = __shfl_sync(0xffffffffu, md, src);
@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(kBlock, LMX_MINB) lmx_round_kernel(RoundArgs a
     // phase 3: buckets 1 (8 lanes per vertex) and 5 (4 lanes per vertex)
     group_bucket<MODE, L, 8>(a, 1, nb[1], lane, live, reads);
     group_bucket<MODE, L, 4>(a, 5, nb[5], lane, live, reads);
+
 
     PHASE_MARK(2);
     // phase 4: bucket 0, thread per vertex, 128 vertices per grab

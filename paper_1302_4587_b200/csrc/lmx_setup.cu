@@ -990,7 +990,7 @@ int lmx_setup_slots(lmx_ctx *ctx) {
             e = cub::DeviceSelect::If(t, tb, it, ctx->bins0 + (size_t)q * cap, cnt + q, (long long)nl,
                                       InBucket{ctx->deg0, q}, st);
         }
-        unsigned long long h[kBuckets] = {0, 0, 0, 0, 0};
+        unsigned long long h[kBuckets] = {};
         if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, 8 * kBuckets, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         lmx_free(ctx, &t, tmp);
