@@ -200,8 +200,10 @@ __global__ void k_convert(const long long *u, const long long *v, const double *
             ev[base + i] = (uint32_t)b;
             wout[base + i] = x;
         }
-        add_degree_grouped(deg, (uint32_t)a, uv);
-        if (uv) atomicAdd(deg + b, 1u);
+        if (deg) {
+            add_degree_grouped(deg, (uint32_t)a, uv);
+            if (uv) atomicAdd(deg + b, 1u);
+        }
     }
 }
 
@@ -235,6 +237,18 @@ __global__ void k_degrees(const uint32_t *eu, const uint32_t *ev, unsigned long 
         const bool in = e < m;
         add_degree_grouped(deg, in ? eu[e] : 0u, in);
         if (in) atomicAdd(deg + ev[e], 1u);
+    }
+}
+
+// Degrees of the vertices [lo, hi) only: the slice's counters stay in L2
+// (random atomics over a 256 MB array otherwise go to DRAM one sector each).
+__global__ void k_degrees_slice(const uint32_t *eu, const uint32_t *ev, unsigned long long m, uint32_t lo,
+                                uint32_t hi, uint32_t *deg) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint2 ab = make_uint2(__ldcs(eu + e), __ldcs(ev + e));
+        if (ab.x - lo < hi - lo) atomicAdd(deg + ab.x, 1u);
+        if (ab.y - lo < hi - lo) atomicAdd(deg + ab.y, 1u);
     }
 }
 
@@ -443,6 +457,26 @@ static int grid_for(lmx_ctx *ctx, unsigned long long work) {
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
+}
+
+// All degrees from device edge arrays (ids already validated): in vertex
+// slices of LMX_DEG_SLICE_MB of counters, one pass over the edges each.
+static int count_degrees(lmx_ctx *ctx, const uint32_t *eu, const uint32_t *ev, unsigned long long m,
+                         unsigned long long n, uint32_t *deg) {
+    static const long slice_mb = getenv("LMX_DEG_SLICE_MB") ? atol(getenv("LMX_DEG_SLICE_MB")) : 48;
+    if (m == 0) return LMX_OK;
+    if (slice_mb <= 0) {
+        k_degrees<<<grid_for(ctx, m), kBlock, 0, ctx->stream>>>(eu, ev, m, deg);
+        LMX_CUDA(ctx, cudaGetLastError());
+        return LMX_OK;
+    }
+    const unsigned long long per = std::max<unsigned long long>(1, ((unsigned long long)slice_mb << 20) / 4);
+    for (unsigned long long lo = 0; lo < n; lo += per) {
+        const unsigned long long hi = std::min(n, lo + per);
+        k_degrees_slice<<<grid_for(ctx, m), kBlock, 0, ctx->stream>>>(eu, ev, m, (uint32_t)lo, (uint32_t)hi, deg);
+        LMX_CUDA(ctx, cudaGetLastError());
+    }
+    return LMX_OK;
 }
 
 // Build vbeg / ids0 / wk0 / deg0 / hubs0 from ctx->eu, ev, w (K0).
@@ -661,8 +695,7 @@ int lmx_setup_device_edges(lmx_ctx *ctx) {
     LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, std::max<size_t>(n, 1) * 4, "deg0"));
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->deg0, 0, std::max<size_t>(n, 1) * 4, st));
     if (m) {
-        k_degrees<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, m, ctx->deg0);
-        LMX_CUDA(ctx, cudaGetLastError());
+        LMX_TRY(count_degrees(ctx, ctx->eu, ctx->ev, m, n, ctx->deg0));
     }
     LMX_TRY(lmx_weight_stage(ctx));
     return lmx_setup_slots(ctx);
@@ -1201,7 +1234,7 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
             }
         }
     }
-    bool weights_done = false;
+    bool weights_done = false, device_degrees = false;
     unsigned long long host_bad = ~0ULL;
     if (m > 0 && where == LMX_HOST && !getenv("LMX_LOAD_LEGACY")) {
         LMX_TRY(load_host_narrowed(ctx, edge_u, edge_v, edge_weight, bad, &host_bad, &weights_done));
@@ -1243,8 +1276,9 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
         } else if (where == LMX_DEVICE) {
             k_convert<<<grid_for(ctx, m), kBlock, 0, st>>>((const long long *)edge_u, (const long long *)edge_v,
                                                           edge_weight, (unsigned long long)m, n, 0, ctx->eu,
-                                                          ctx->ev, ctx->w, ctx->deg0, bad);
+                                                          ctx->ev, ctx->w, nullptr, bad);
             LMX_CUDA(ctx, cudaGetLastError());
+            device_degrees = true;   // counted once the ids are known valid
         } else {
             // chunked H2D through two staging buffers of int64 ids
             const unsigned long long chunk = 1ULL << 24;
@@ -1303,6 +1337,10 @@ int lmx_load_edges(lmx_ctx *ctx, int64_t n, int64_t m, const int64_t *edge_u, co
             snprintf(buf, sizeof buf, "edge %llu: weight must be finite and >= 0, got %.17g",
                      (unsigned long long)badpos, w);
         return lmx_fail(ctx, LMX_EINVAL, buf);
+    }
+    if (device_degrees) {
+        LMX_TRY(count_degrees(ctx, ctx->eu, ctx->ev, (unsigned long long)m, (unsigned long long)n, ctx->deg0));
+        trace_mark(ctx, "degrees (sliced)");
     }
     if (!weights_done) LMX_TRY(lmx_weight_stage(ctx));
     trace_mark(ctx, "weight stage");

@@ -1,5 +1,5 @@
 """K0 stage times (LMX_TRACE_SETUP=1) of lmx_load_graph from DEVICE-resident
-edge arrays (bench.py's load_device_ms).  usage: python tools/load_trace.py [scale]"""
+edge arrays (bench.py's load_device_ms).  usage: python tools/load_trace.py [scale] [rmat|er]"""
 import os
 import sys
 import time
@@ -10,9 +10,13 @@ import torch  # noqa: E402
 from paper_1302_4587_b200 import Engine  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 26
+family = sys.argv[2] if len(sys.argv) > 2 else "rmat"
 eng = Engine(0)
 eng.set_stream(torch.cuda.current_stream().cuda_stream)
-eng.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
+if family == "er":   # same m, no hubs (random weights via a U[0,1) fill of the unit graph's weights)
+    eng.gen_er(scale, 16, seed=1, unit=False)
+else:
+    eng.gen_rmat(scale, 16, 0.57, 0.19, 0.19, seed=1, permute=True)
 n, m = eng.graph_size()
 du, dv, dw = eng.export_graph_device()
 for rep in range(3):
