@@ -49,16 +49,31 @@ __global__ void k_owned_deg(const uint32_t *deg0, unsigned long long lo, unsigne
 
 // Endpoints in device ids, packed per edge (one random 8-byte gather in the
 // stream instead of two 4-byte ones; the relabel lookups run in edge order).
+// 4 edges per thread per step: their new-id gathers are in flight together.
 __global__ void k_pack_endpoints(const uint32_t *eu, const uint32_t *ev, const uint32_t *newid,
                                  unsigned long long m, uint2 *euv) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        uint32_t a = eu[e], b = ev[e];
-        if (newid) {
-            a = newid[a];
-            b = newid[b];
+    for (unsigned long long e0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < m;
+         e0 += 4 * stride) {
+        uint32_t a[4], b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long e = e0 + k * stride;
+            a[k] = e < m ? __ldcs(eu + e) : 0u;
+            b[k] = e < m ? __ldcs(ev + e) : 0u;
         }
-        euv[e] = make_uint2(a, b);
+        if (newid) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                a[k] = newid[a[k]];
+                b[k] = newid[b[k]];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long e = e0 + k * stride;
+            if (e < m) euv[e] = make_uint2(a[k], b[k]);
+        }
     }
 }
 
@@ -369,6 +384,7 @@ int lmx_scan_build_slots(lmx_ctx *ctx, const uint32_t *newid) {
             // the packed endpoints borrow the owner-key output buffer (same size)
             uint2 *euv = reinterpret_cast<uint2 *>(okey2);
             k_pack_endpoints<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->eu, ctx->ev, newid, m, euv);
+            trace_mark(ctx, "  scan: packed endpoints");
             k_desc_stream<<<lgrid(ctx, m), kBlock, 0, st>>>(ctx->ws_eid, ctx->ws_tied, m, 0, m, euv, (uint32_t)lo,
                                                            (uint32_t)nl, okey, sval);
             e = cudaGetLastError();
