@@ -81,6 +81,9 @@ __global__ void k_pack_endpoints(const uint32_t *eu, const uint32_t *ev, const u
 // 4 edges per thread per step, the gathers of a step in flight together.
 // Stream positions [ib, ib + cnt) of the m edges (a partition streams its
 // weight order in chunks), written from okey / sval index 0.
+#ifndef LMX_STREAM_ILP
+#define LMX_STREAM_ILP 4   // edges per thread per step of the slot stream
+#endif
 __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, unsigned long long m,
                               unsigned long long ib, unsigned long long cnt, const uint2 *euv, uint32_t lo,
                               uint32_t nl, uint32_t *okey, uint2 *sval) {
@@ -89,11 +92,11 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, 
     tied += m - ib - cnt;
     m = cnt;
     for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < m;
-         i0 += 4 * stride) {
-        uint32_t e[4], t[4];
-        uint2 p[4];
+         i0 += LMX_STREAM_ILP * stride) {
+        uint32_t e[LMX_STREAM_ILP], t[LMX_STREAM_ILP];
+        uint2 p[LMX_STREAM_ILP];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < LMX_STREAM_ILP; ++k) {
             const unsigned long long i = i0 + k * stride;
             if (i < m) {
                 const unsigned long long j = m - 1 - i;
@@ -102,10 +105,10 @@ __global__ void k_desc_stream(const uint32_t *eid_sorted, const uint32_t *tied, 
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < LMX_STREAM_ILP; ++k)
             if (i0 + k * stride < m) p[k] = euv[e[k]];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < LMX_STREAM_ILP; ++k) {
             const unsigned long long i = i0 + k * stride;
             if (i < m) {   // bit 30 marks, until the post pass, the slot of the edge's v end
                 const uint32_t oa = p[k].x - lo, ob = p[k].y - lo;
