@@ -388,6 +388,71 @@ __global__ void k_weight_keys_of(const double *w, const uint32_t *eid, unsigned 
         keys[i] = canon_bits(w[eid[i]]);
 }
 
+// Weight order through 32-bit keys (the 64-bit sort's 8 passes -> 4): key32 =
+// floor((w - wmin) * scale), a monotone map of the value, so different
+// key32 mean different weights and the sort by key32 leaves only the runs of
+// equal key32 to order by the exact (canonical bits, edge id) -- most of
+// them singletons for spread-out weights.  A run longer than kRunCap sets
+// `fallback` (the exact 64-bit sort then runs instead).
+constexpr uint32_t kRunCap = 64;
+
+__global__ void k_keys32(const double *w, unsigned long long m, double wmin, double scale, uint32_t *keys,
+                         uint32_t *vals) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const double t = floor((w[e] - wmin) * scale);
+        keys[e] = t >= 4294967295.0 ? 0xFFFFFFFFu : (t > 0.0 ? (uint32_t)t : 0u);
+        vals[e] = (uint32_t)e;
+    }
+}
+
+// Per run of equal key32 (its first position's thread): exact order by
+// (canonical weight bits, edge id), dense-rank heads (i > 0 and the weight
+// differs from position i - 1) and tie flags, as k_heads / k_tied give them
+// on the exactly sorted keys.
+__global__ void k_key32_runs(const uint32_t *sk, uint32_t *se, const double *w, unsigned long long m,
+                             uint32_t *head, uint32_t *tied, unsigned int *fallback) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const uint32_t k = sk[i];
+        if (i > 0 && sk[i - 1] == k) continue;   // not a run start
+        uint32_t L = 1;
+        while (i + L < m && sk[i + L] == k && L <= kRunCap) ++L;
+        if (L == 1) {
+            head[i] = i > 0 ? 1u : 0u;
+            tied[i] = 0u;
+            continue;
+        }
+        if (L > kRunCap) {
+            atomicOr(fallback, 1u);
+            continue;
+        }
+        uint32_t e[kRunCap];
+        unsigned long long f[kRunCap];
+        for (uint32_t j = 0; j < L; ++j) {
+            e[j] = se[i + j];
+            f[j] = canon_bits(w[e[j]]);
+        }
+        for (uint32_t j = 1; j < L; ++j) {   // insertion sort by (weight bits, edge id)
+            const uint32_t ej = e[j];
+            const unsigned long long fj = f[j];
+            uint32_t q = j;
+            while (q > 0 && (f[q - 1] > fj || (f[q - 1] == fj && e[q - 1] > ej))) {
+                f[q] = f[q - 1];
+                e[q] = e[q - 1];
+                --q;
+            }
+            f[q] = fj;
+            e[q] = ej;
+        }
+        for (uint32_t j = 0; j < L; ++j) {
+            se[i + j] = e[j];
+            head[i + j] = (i + j > 0 && (j == 0 || f[j] != f[j - 1])) ? 1u : 0u;
+            tied[i + j] = ((j > 0 && f[j] == f[j - 1]) || (j + 1 < L && f[j] == f[j + 1])) ? 1u : 0u;
+        }
+    }
+}
+
 __global__ void k_heads(const unsigned long long *sorted, unsigned long long m, uint32_t *flag) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
@@ -550,6 +615,61 @@ static int static_order_stage(lmx_ctx *ctx, bool uniform) {
     return LMX_OK;
 }
 
+// The 32-bit-key weight order (see k_keys32).  *exact = true when it does not
+// apply (spread too narrow, or a run of equal 32-bit keys longer than
+// kRunCap): the caller then sorts the 64-bit weight bits.
+static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, uint32_t *head, uint32_t *eids, uint32_t *tied,
+                              bool *exact) {
+    *exact = true;
+    if (getenv("LMX_EXACT_WEIGHT_SORT") || m < 2) return LMX_OK;
+    cudaStream_t st = ctx->stream;
+    unsigned long long *mm = nullptr;
+    uint32_t *k1 = nullptr, *k2 = nullptr, *v1 = nullptr;
+    unsigned int *fb = nullptr;
+    int rc = LMX_OK;
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((rc = lmx_alloc(ctx, (void **)&mm, 16, "minmax")) != LMX_OK) break;
+        unsigned long long init[2] = {~0ULL, 0ULL}, got[2] = {0, 0};
+        if ((e = cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+        k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
+        if ((e = cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        double wmin, wmax;   // canonical bits of non-negative doubles: the value's bits
+        memcpy(&wmin, &got[0], 8);
+        memcpy(&wmax, &got[1], 8);
+        const double spread = wmax - wmin;
+        const double scale = 4294967295.0 / spread;
+        if (!(spread > 1e-280) || !std::isfinite(scale)) break;   // exact sort
+        if ((rc = lmx_alloc(ctx, (void **)&k1, m * 4, "key32")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&k2, m * 4, "key32 sorted")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&v1, m * 4, "key32 vals")) != LMX_OK) break;
+        if ((rc = lmx_alloc(ctx, (void **)&fb, 4, "run fallback")) != LMX_OK) break;
+        if ((e = cudaMemsetAsync(fb, 0, 4, st)) != cudaSuccess) break;
+        k_keys32<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, wmin, scale, k1, v1);
+        uint32_t *vo = eids;
+        if ((rc = lmx_sort_pairs(ctx, &k1, &k2, &v1, &vo, (long long)m, 0, 32, st, "key32 sort")) != LMX_OK) break;
+        if (vo != eids) {   // the sorted ids ended in the scratch buffer
+            if ((e = cudaMemcpyAsync(eids, vo, m * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) break;
+            v1 = vo;
+        }
+        trace_mark(ctx, "    key32 sort");
+        k_key32_runs<<<grid_for(ctx, m), kBlock, 0, st>>>(k2, eids, ctx->w, m, head, tied, fb);
+        unsigned int hfb = 1;
+        if ((e = cudaMemcpyAsync(&hfb, fb, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        *exact = hfb != 0;
+    } while (0);
+    if (e != cudaSuccess && rc == LMX_OK) rc = lmx_cuda_check(ctx, e, "32-bit weight order");
+    cudaStreamSynchronize(st);
+    lmx_free(ctx, (void **)&mm, 16);
+    lmx_free(ctx, (void **)&k1, m * 4);
+    lmx_free(ctx, (void **)&k2, m * 4);
+    lmx_free(ctx, (void **)&v1, m * 4);
+    lmx_free(ctx, (void **)&fb, 4);
+    return rc;
+}
+
 // Weight keys (tiebreak.py:105-113 order) from ctx->w alone, so a pinned-host
 // load can run it while the endpoint arrays are still in flight: layout
 // choice, dense ranks and tie indices, and the round-loop algorithm.  Leaves
@@ -599,29 +719,35 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         int rc = LMX_OK;
         bool static_pending = false;
         do {
-            if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
-            if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals, m * 4, "sort vals")) != LMX_OK) break;
             if ((rc = lmx_alloc(ctx, (void **)&vals2, m * 4, "sort vals2")) != LMX_OK) break;
-            k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
-            if ((rc = lmx_sort_pairs(ctx, &keys, &keys2, &vals, &vals2, (long long)m, 0, 64, st, "key sort")) !=
-                LMX_OK)
-                break;
-            trace_mark(ctx, "  weight sort");
-            lmx_free(ctx, (void **)&keys, m * 8);   // the sort's scratch half
             if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
+            // vals <- dense-rank heads, vals2 <- edge ids by weight, tied <- tie flags
+            bool exact = true;
+            if ((rc = weight_order_key32(ctx, m, vals, vals2, tied, &exact)) != LMX_OK) break;
+            if (exact) {   // spread too narrow for 32-bit keys: the 64-bit sort of the weight bits
+                if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
+                if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
+                k_keys<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, keys, vals);
+                if ((rc = lmx_sort_pairs(ctx, &keys, &keys2, &vals, &vals2, (long long)m, 0, 64, st, "key sort")) !=
+                    LMX_OK)
+                    break;
+                lmx_free(ctx, (void **)&keys, m * 8);   // the sort's scratch half
+                k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
+                k_tied<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, tied);
+                lmx_free(ctx, (void **)&keys2, m * 8);
+            }
+            trace_mark(ctx, "  weight sort");
             if ((rc = lmx_alloc(ctx, (void **)&tidx, m * 4, "tie idx")) != LMX_OK) break;
             size_t t2 = 0;
             cudaError_t e = cub::DeviceScan::InclusiveSum(nullptr, t2, vals, vals, (long long)m, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "scan sizing"); break; }
             tmp_bytes = t2;
             if ((rc = lmx_alloc(ctx, &tmp, tmp_bytes, "scan tmp")) != LMX_OK) break;
-            // dense rank of the weight value (vals reused)
-            k_heads<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, vals);
+            // dense rank of the weight value (the heads in vals)
             e = cub::DeviceScan::InclusiveSum(tmp, t2, vals, vals, (long long)m, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "rank scan"); break; }
-            // tied flags and tie indices
-            k_tied<<<grid_for(ctx, m), kBlock, 0, st>>>(keys2, m, tied);
+            // tie indices
             e = cub::DeviceScan::ExclusiveSum(tmp, t2, tied, tidx, (long long)m, st);
             if (e != cudaSuccess) { rc = lmx_cuda_check(ctx, e, "tie scan"); break; }
             uint32_t last_rank = 0, last_tidx = 0, last_tied = 0;
