@@ -427,6 +427,38 @@ __global__ void k_key32_runs(const uint32_t *sk, uint32_t *se, const double *w, 
             atomicOr(fallback, 1u);
             continue;
         }
+        if (L <= 4) {   // the common short runs, in registers (odd-even transposition sort)
+            uint32_t e4[4];
+            unsigned long long f4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                e4[j] = (uint32_t)j < L ? se[i + j] : 0xFFFFFFFFu;
+                f4[j] = (uint32_t)j < L ? canon_bits(w[e4[j]]) : ~0ULL;
+            }
+#pragma unroll
+            for (int pass = 0; pass < 4; ++pass) {
+#pragma unroll
+                for (int j = pass & 1; j + 1 < 4; j += 2) {
+                    const bool sw = f4[j] > f4[j + 1] || (f4[j] == f4[j + 1] && e4[j] > e4[j + 1]);
+                    if (sw) {
+                        const unsigned long long tf = f4[j];
+                        f4[j] = f4[j + 1];
+                        f4[j + 1] = tf;
+                        const uint32_t te = e4[j];
+                        e4[j] = e4[j + 1];
+                        e4[j + 1] = te;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if ((uint32_t)j >= L) break;
+                se[i + j] = e4[j];
+                head[i + j] = (i + j > 0 && (j == 0 || f4[j] != f4[j - 1])) ? 1u : 0u;
+                tied[i + j] = ((j > 0 && f4[j] == f4[j - 1]) || ((uint32_t)j + 1 < L && f4[j] == f4[j + 1])) ? 1u : 0u;
+            }
+            continue;
+        }
         uint32_t e[kRunCap];
         unsigned long long f[kRunCap];
         for (uint32_t j = 0; j < L; ++j) {
@@ -618,8 +650,8 @@ static int static_order_stage(lmx_ctx *ctx, bool uniform) {
 // The 32-bit-key weight order (see k_keys32).  *exact = true when it does not
 // apply (spread too narrow, or a run of equal 32-bit keys longer than
 // kRunCap): the caller then sorts the 64-bit weight bits.
-static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, uint32_t *head, uint32_t *eids, uint32_t *tied,
-                              bool *exact) {
+static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, const unsigned long long *wbits, uint32_t *head,
+                              uint32_t *eids, uint32_t *tied, bool *exact) {
     *exact = true;
     if (getenv("LMX_EXACT_WEIGHT_SORT") || m < 2) return LMX_OK;
     cudaStream_t st = ctx->stream;
@@ -629,12 +661,18 @@ static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, uint32_t *head
     int rc = LMX_OK;
     cudaError_t e = cudaSuccess;
     do {
-        if ((rc = lmx_alloc(ctx, (void **)&mm, 16, "minmax")) != LMX_OK) break;
-        unsigned long long init[2] = {~0ULL, 0ULL}, got[2] = {0, 0};
-        if ((e = cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
-        k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
-        if ((e = cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        unsigned long long got[2] = {0, 0};
+        if (wbits) {   // the layout check's min / max
+            got[0] = wbits[0];
+            got[1] = wbits[1];
+        } else {
+            if ((rc = lmx_alloc(ctx, (void **)&mm, 16, "minmax")) != LMX_OK) break;
+            unsigned long long init[2] = {~0ULL, 0ULL};
+            if ((e = cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+            k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
+            if ((e = cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+        }
         double wmin, wmax;   // canonical bits of non-negative doubles: the value's bits
         memcpy(&wmin, &got[0], 8);
         memcpy(&wmax, &got[1], 8);
@@ -680,7 +718,8 @@ int lmx_weight_stage(lmx_ctx *ctx) {
     cudaStream_t st = ctx->stream;
     uint32_t *kofe = nullptr;
     // weight key layout
-    bool uniform = true;
+    bool uniform = true, have_wbits = false;
+    unsigned long long wbits[2] = {0, 0};   // min / max canonical weight bits
     if (ctx->dist_local) {
         uniform = ctx->w_uniform != 0;   // decided on ALL edges: every partition takes the same loop
     } else if (m) {
@@ -690,11 +729,11 @@ int lmx_weight_stage(lmx_ctx *ctx) {
         LMX_CUDA(ctx, cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
         k_minmax_bits<<<grid_for(ctx, m), kBlock, 0, st>>>(ctx->w, m, mm);
         LMX_CUDA(ctx, cudaGetLastError());
-        unsigned long long got[2];
-        LMX_CUDA(ctx, cudaMemcpyAsync(got, mm, 16, cudaMemcpyDeviceToHost, st));
+        LMX_CUDA(ctx, cudaMemcpyAsync(wbits, mm, 16, cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
         lmx_free(ctx, (void **)&mm, 16);
-        uniform = got[0] == got[1];
+        uniform = wbits[0] == wbits[1];
+        have_wbits = true;
     }
     if (ctx->dist_p > 1 && !ctx->dist_local) {
         // a partition sorts its local edges only: lmx_setup_slots comes back
@@ -724,7 +763,8 @@ int lmx_weight_stage(lmx_ctx *ctx) {
             if ((rc = lmx_alloc(ctx, (void **)&tied, m * 4, "tied")) != LMX_OK) break;
             // vals <- dense-rank heads, vals2 <- edge ids by weight, tied <- tie flags
             bool exact = true;
-            if ((rc = weight_order_key32(ctx, m, vals, vals2, tied, &exact)) != LMX_OK) break;
+            if ((rc = weight_order_key32(ctx, m, have_wbits ? wbits : nullptr, vals, vals2, tied, &exact)) != LMX_OK)
+                break;
             if (exact) {   // spread too narrow for 32-bit keys: the 64-bit sort of the weight bits
                 if ((rc = lmx_alloc(ctx, (void **)&keys, m * 8, "sort keys")) != LMX_OK) break;
                 if ((rc = lmx_alloc(ctx, (void **)&keys2, m * 8, "sort keys2")) != LMX_OK) break;
