@@ -85,6 +85,8 @@ void lmx_destroy(lmx_ctx *ctx) {
     if (ctx->ev_deg) cudaEventDestroy(ctx->ev_deg);
     if (ctx->deg_stream) cudaStreamDestroy(ctx->deg_stream);
     if (ctx->ev_load) cudaEventDestroy(ctx->ev_load);
+    if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->load_stream) cudaStreamDestroy(ctx->load_stream);
     if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

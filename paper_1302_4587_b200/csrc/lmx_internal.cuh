@@ -210,6 +210,8 @@ struct lmx_ctx {
     std::vector<cudaEvent_t> stage_ev;       // one per ring slot
     cudaStream_t deg_stream = nullptr;       // per-block degree counts behind the copies
     cudaStream_t load_stream = nullptr;      // lmx_load_graph runs here (ordered with the caller's stream)
+    cudaStream_t side_stream = nullptr;      // scan loop: matched-edge bits next to the histogram
+    cudaEvent_t ev_side = nullptr;
     cudaEvent_t ev_load = nullptr;
     cudaEvent_t ev_deg = nullptr;
     unsigned long long *hist = nullptr;      // scan: death-round histogram

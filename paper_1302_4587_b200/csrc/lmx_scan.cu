@@ -1062,8 +1062,25 @@ static int run_rounds_loop(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         }
         ctx->timing.round_launches += 1;
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, st));
+        // the matched-edge bits and the death-round histogram are independent:
+        // the edge bits run on a side stream next to the histogram
+        static const bool serial_tail = getenv("LMX_SERIAL_TAIL") != nullptr;
+        if (!serial_tail && !ctx->side_stream) {
+            LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+            LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
+        }
+        if (!serial_tail) {
+            LMX_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev2, 0));
+            cudaStream_t keep = ctx->stream;
+            ctx->stream = ctx->side_stream;
+            const int rc_eb = scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n);
+            ctx->stream = keep;
+            LMX_TRY(rc_eb);
+            LMX_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->side_stream));
+        }
         LMX_TRY(scan_hist_launch_dev(ctx, result));
-        LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));
+        if (serial_tail) LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));
+        else LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_side, 0));
         hist.assign(kHistBins, 0);
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)ctx->ctr_cap,
                                       cudaMemcpyDeviceToHost, st));
