@@ -292,7 +292,8 @@ class Engine:
                                         mate.ctypes.data, ids.ctypes.data, ctypes.byref(nm), None, 0,
                                         ctypes.byref(nr), LMX_HOST), "lmx_match")
         rounds = self.last_rounds()
-        return mate[:n], ids[: nm.value].copy(), rounds
+        # views of the (page-locked) output blocks: no host copy of the ids
+        return mate[:n], ids[: nm.value], rounds
 
     def match_device(self, seed: int, mate_out, ids_out, rerandomize: bool = True) -> int:
         """Device outputs (CUDA tensors int64[n] and int64[>= n/2]); returns #matched edges."""
