@@ -163,6 +163,7 @@ struct lmx_ctx {
     int algo = 0;
     int force_algo = -1;                     // -1 auto, 0 compact, 1 scan (if eligible)
     bool scan_rejected = false;              // load time: ties too common for the scan loop
+    unsigned long long key32_fallback_m = 0; // the last 32-bit-key weight order fell back at this m
     // rerandomize=False (salts fixed for the run): a load may lay tie-heavy
     // weights out in the total order (weight, salt of round 0) of one seed,
     // which the scan loop then matches with no tie handling

@@ -653,7 +653,11 @@ static int static_order_stage(lmx_ctx *ctx, bool uniform) {
 static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, const unsigned long long *wbits, uint32_t *head,
                               uint32_t *eids, uint32_t *tied, bool *exact) {
     *exact = true;
-    if (getenv("LMX_EXACT_WEIGHT_SORT") || m < 2) return LMX_OK;
+    if (getenv("LMX_EXACT_WEIGHT_SORT") || m < (1ULL << 16)) return LMX_OK;
+    // a graph no larger than one whose 32-bit keys left a long run (heavily
+    // tied weights, e.g. the levels of a coarsening) goes to the exact sort
+    // directly: the attempt would only add to its cost
+    if (ctx->key32_fallback_m && m <= ctx->key32_fallback_m) return LMX_OK;
     cudaStream_t st = ctx->stream;
     unsigned long long *mm = nullptr;
     uint32_t *k1 = nullptr, *k2 = nullptr, *v1 = nullptr;
@@ -697,6 +701,7 @@ static int weight_order_key32(lmx_ctx *ctx, unsigned long long m, const unsigned
         if ((e = cudaMemcpyAsync(&hfb, fb, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
         *exact = hfb != 0;
+        ctx->key32_fallback_m = *exact ? m : 0;
     } while (0);
     if (e != cudaSuccess && rc == LMX_OK) rc = lmx_cuda_check(ctx, e, "32-bit weight order");
     cudaStreamSynchronize(st);
