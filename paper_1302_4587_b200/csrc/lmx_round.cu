@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "lmx_internal.cuh"
@@ -985,7 +986,17 @@ int lmx_run_rounds(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
                 break;
             }
         }
+        // the next batch: as many rounds as the live slots' decay over the last
+        // round predicts (+1), 1..4 -- empty rounds past the end cost launches
         batch = 4;
+        if (n_rounds < 0 && r >= 2) {
+            const double last = (double)ctx->ctr_host[r - 1].live_slots, prev = (double)ctx->ctr_host[r - 2].live_slots;
+            if (last > 0 && prev > last) {
+                const double q = last / prev;   // per-round survival of live slots
+                const double est = std::log(std::max(last, 2.0)) / std::log(1.0 / q) + 1.0;
+                batch = std::max(1, std::min(4, (int)std::ceil(est)));
+            }
+        }
 #ifdef LMX_ONLY_BUCKET   // profiling experiments: results are meaningless, stop after one batch
         if (n_rounds < 0) n_rounds = 0;
 #endif
