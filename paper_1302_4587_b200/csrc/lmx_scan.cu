@@ -698,7 +698,10 @@ __global__ void __launch_bounds__(kBlock) lmx_scan_hist_kernel(const uint2 *lowp
 #ifndef LMX_HIST_HUB_KB
 #define LMX_HIST_HUB_KB 80   // packed match rounds of the lowest ids staged in shared memory
 #endif
-constexpr int kHistThreads = 1024;
+#ifndef LMX_HIST_THREADS
+#define LMX_HIST_THREADS 1024
+#endif
+constexpr int kHistThreads = LMX_HIST_THREADS;
 
 // The same pass, persistent (two 1024-thread blocks per SM) and software-
 // pipelined: the next step's edge pairs are loaded before this step's
