@@ -13,6 +13,7 @@ ap.add_argument("--scale", type=int, default=26)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--er", action="store_true", help="the er24unit family (unit weights, compacting loop)")
 ap.add_argument("--compact", action="store_true", help="force the compacting loop (LMX_OPT_ALGO 0)")
+ap.add_argument("--no-kt", action="store_true", help="no per-kernel timeline (persistent loops stay on)")
 args = ap.parse_args()
 eng = Engine(0)
 if args.compact:
@@ -25,7 +26,7 @@ n, m = eng.graph_size()
 mate = torch.empty(n, dtype=torch.int64, device="cuda")
 ids = torch.empty(n // 2 + 1, dtype=torch.int64, device="cuda")
 eng.match_device(1, mate, ids)
-eng.set_kernel_timing(True)
+eng.set_kernel_timing(not args.no_kt)
 best = None
 for _ in range(args.steps):
     eng.match_device(1, mate, ids)
