@@ -71,3 +71,19 @@ def test_fuzz_engine_paths_vs_oracle(engine, case, path):
     assert np.array_equal(mate, ref.mate)
     assert np.array_equal(ids, ref.matched_ids)
     assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in rounds] == ref.rounds
+
+
+@settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck))
+@given(graphs(), st.integers(2, 5), st.sampled_from(["auto", "compact"]))
+def test_fuzz_partitioned_vs_oracle(case, p, algo):
+    """bsp_local_max's p-invariance (test_bsp.py:68-87): the partitioned
+    engine (p partitions emulated on one B200) equals the sequential oracle"""
+    from paper_1302_4587_b200.dist import local_max_dist
+    n, eu, ev, w, seed, rr = case
+    if p > n:
+        return
+    ref = O.c_local_max(n, eu, ev, w, seed, rr)
+    matching, trace = local_max_dist(_graph(n, eu, ev, w), p, seed, rr, algo=algo)
+    assert np.array_equal(matching.mate, ref.mate)
+    assert np.array_equal(matching.sorted_edge_ids(), ref.matched_ids)
+    assert [(r.edges_before, r.edges_matched, r.edges_removed) for r in trace.rounds] == ref.rounds
