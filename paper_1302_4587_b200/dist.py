@@ -245,20 +245,33 @@ class DistRank:
     def round(self):
         self._chk(self.lib.lmx_dist_round(self.eng._h), "lmx_dist_round")
 
+    def _cached_view(self, ptr: int, rows: int, cols: int, typestr: str):
+        """A tensor over device memory the context owns; the per-round protocol
+        asks for the same few buffers every round, so their views are kept
+        (a view of at least `rows` rows is sliced)."""
+        cache = self.__dict__.setdefault("_view_cache", {})
+        key = (ptr, cols, typestr)
+        t = cache.get(key)
+        if t is None or t.shape[0] < rows:
+            t = _view(ptr, (rows, cols) if cols else (rows,), typestr, self.device)
+            if rows:
+                cache[key] = t
+        return t[:rows]
+
     def propose(self):
         """Exchange-A records on the device: (packed int32 [cap, 2] view, int64[p] counts).
         Nothing is synchronised; the first `counts.sum()` rows are valid."""
         cptr = ctypes.c_void_p()
         sptr = ctypes.c_void_p()
         self._chk(self.lib.lmx_dist_propose(self.eng._h, ctypes.byref(cptr), ctypes.byref(sptr)), "lmx_dist_propose")
-        counts = _view(cptr.value, (self.p,), "<i8", self.device)
-        send = _view(sptr.value, (max(self.n_local, 1), 2), "<i4", self.device)
+        counts = self._cached_view(cptr.value, self.p, 0, "<i8")
+        send = self._cached_view(sptr.value, max(self.n_local, 1), 2, "<i4")
         return send, counts
 
     def recv_buffer(self, count: int):
         ptr = ctypes.c_void_p()
         self._chk(self.lib.lmx_dist_recv_buffer(self.eng._h, int(count), ctypes.byref(ptr)), "lmx_dist_recv_buffer")
-        return _view(ptr.value, (int(count), 2), "<i4", self.device)
+        return self._cached_view(ptr.value, int(count), 2, "<i4")
 
     def accept(self, count: int):
         self._chk(self.lib.lmx_dist_accept(self.eng._h, int(count)), "lmx_dist_accept")
@@ -267,7 +280,7 @@ class DistRank:
         """Enqueue the match step; returns the round's device {live slots, matched} (int64[2] view)."""
         ptr = ctypes.c_void_p()
         self._chk(self.lib.lmx_dist_match(self.eng._h, ctypes.byref(ptr)), "lmx_dist_match")
-        return _view(ptr.value, (2,), "<i8", self.device)
+        return self._cached_view(ptr.value, 2, 0, "<i8")
 
     def word_range(self, k: int):
         return int(self.bounds[k]) // 32, (int(self.bounds[k + 1]) + 31) // 32
@@ -475,13 +488,22 @@ class TorchComm:
         import torch
         (me,), ((send, counts),) = ranks, sends
         dev = me.device
-        sc = torch.zeros((self.p, 3), dtype=torch.int64, device=dev)
-        sc[:, 0].copy_(torch.as_tensor(counts, dtype=torch.int64, device=dev))
+        bufs = getattr(self, "_stats_bufs", None)
+        if bufs is None or bufs[0].device != dev:
+            sc = torch.zeros((self.p, 3), dtype=torch.int64, device=dev)
+            both_d = torch.empty(4 * self.p, dtype=torch.int64, device=dev)   # [send counts | received rows]
+            both_h = torch.empty(4 * self.p, dtype=torch.int64, pin_memory=torch.device(dev).type == "cuda")
+            self._stats_bufs = bufs = (sc, both_d, both_h)
+        sc, both_d, both_h = bufs
+        sc[:, 0].copy_(counts)
         if prev is not None:
             sc[:, 1:].copy_(prev.reshape(1, 2).expand(self.p, 2))
-        rc = torch.empty_like(sc)
-        self.dist.all_to_all_single(rc, sc)
-        both = torch.cat([sc[:, 0], rc.reshape(-1)]).tolist()   # the one host sync of the round
+        else:
+            sc[:, 1:].zero_()
+        both_d[: self.p].copy_(counts)
+        self.dist.all_to_all_single(both_d[self.p:], sc.reshape(-1))
+        both_h.copy_(both_d)
+        both = both_h.tolist()   # (the copy above is synchronous: the one host sync of the round)
         scounts = both[: self.p]
         rows = [both[self.p + 3 * k: self.p + 3 * k + 3] for k in range(self.p)]
         rcounts = [r[0] for r in rows]
