@@ -86,6 +86,7 @@ void lmx_destroy(lmx_ctx *ctx) {
     if (ctx->deg_stream) cudaStreamDestroy(ctx->deg_stream);
     if (ctx->ev_load) cudaEventDestroy(ctx->ev_load);
     if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+    if (ctx->ev_mate) cudaEventDestroy(ctx->ev_mate);
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->load_stream) cudaStreamDestroy(ctx->load_stream);
     if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
@@ -160,6 +161,16 @@ int lmx_match(lmx_ctx *ctx, uint64_t seed_masked, int rerandomize, int64_t *mate
                                          "reload for this call");
     }
     ctx->mate_target = (out_where == LMX_DEVICE && mate_out) ? (long long *)mate_out : ctx->mate;
+    // a page-locked host mate buffer can take the mate array while the
+    // histogram and the id emission still run (scan loop)
+    ctx->mate_early = nullptr;
+    ctx->mate_early_done = false;
+    if (out_where == LMX_HOST && mate_out && ctx->n > 0) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, mate_out) == cudaSuccess && at.type == cudaMemoryTypeHost)
+            ctx->mate_early = mate_out;
+        cudaGetLastError();
+    }
     if (ctx->algo == 1) LMX_TRY(lmx_run_rounds_scan(ctx, seed_masked, rerandomize != 0, stats, nm));
     else LMX_TRY(lmx_run_rounds(ctx, seed_masked, rerandomize != 0, stats, nm));
     LMX_TRY(lmx_emit_outputs(ctx, nm, mate_out, matched_ids_out, out_where));

@@ -212,6 +212,9 @@ struct lmx_ctx {
     cudaStream_t deg_stream = nullptr;       // per-block degree counts behind the copies
     cudaStream_t load_stream = nullptr;      // lmx_load_graph runs here (ordered with the caller's stream)
     cudaStream_t side_stream = nullptr;      // scan loop: matched-edge bits next to the histogram
+    int64_t *mate_early = nullptr;           // page-locked host mate output, copied as soon as it is final
+    bool mate_early_done = false;
+    cudaEvent_t ev_mate = nullptr;
     cudaEvent_t ev_side = nullptr;
     cudaEvent_t ev_load = nullptr;
     cudaEvent_t ev_deg = nullptr;

@@ -1173,8 +1173,12 @@ int lmx_emit_outputs(lmx_ctx *ctx, unsigned long long n_matched, int64_t *mate_o
         LMX_CUDA(ctx, cudaEventRecord(ctx->ev2, ctx->stream));
         LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     } else {
-        if (mate_out && n)
+        if (ctx->mate_early_done && mate_out == ctx->mate_early)   // copied next to the histogram
+            LMX_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_mate, 0));
+        else if (mate_out && n)
             LMX_CUDA(ctx, cudaMemcpyAsync(mate_out, ctx->mate_target, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->mate_early_done = false;
+        ctx->mate_early = nullptr;
         if (ids_out && n_matched)
             LMX_CUDA(ctx, cudaMemcpyAsync(ids_out, ctx->mids, (size_t)n_matched * 8, cudaMemcpyDeviceToHost,
                                           ctx->stream));

@@ -1071,6 +1071,7 @@ static int run_rounds_loop(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
         if (!serial_tail && !ctx->side_stream) {
             LMX_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
             LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
+            LMX_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_mate, cudaEventDisableTiming));
         }
         if (!serial_tail) {
             LMX_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev2, 0));
@@ -1080,23 +1081,30 @@ static int run_rounds_loop(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize,
             ctx->stream = keep;
             LMX_TRY(rc_eb);
             LMX_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->side_stream));
+            if (ctx->mate_early && ctx->mate_target == ctx->mate) {   // final once the loop kernel is done
+                LMX_CUDA(ctx, cudaMemcpyAsync(ctx->mate_early, ctx->mate_target, (size_t)ctx->n * 8,
+                                              cudaMemcpyDeviceToHost, ctx->side_stream));
+                LMX_CUDA(ctx, cudaEventRecord(ctx->ev_mate, ctx->side_stream));
+                ctx->mate_early_done = true;
+            }
         }
         LMX_TRY(scan_hist_launch_dev(ctx, result));
         if (serial_tail) LMX_TRY(scan_edge_bits_launch(ctx, 0, (unsigned long long)ctx->n));
         else LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_side, 0));
+        LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));   // the device loop ends here (an early mate copy may go on)
         hist.assign(kHistBins, 0);
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->ctr_host, ctx->ctr, sizeof(RoundCtr) * (size_t)ctx->ctr_cap,
                                       cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaMemcpyAsync(ctx->loop_host, ctx->loop_aux, lmx_loop_aux_bytes(ctx->ctr_cap),
                                       cudaMemcpyDeviceToHost, st));
         LMX_CUDA(ctx, cudaMemcpyAsync(hist.data(), ctx->hist, kHistBins * 8, cudaMemcpyDeviceToHost, st));
-        LMX_CUDA(ctx, cudaEventRecord(ctx->ev1, st));
         LMX_CUDA(ctx, cudaStreamSynchronize(st));
         R = ctx->loop_host[0];
         if ((int)R < r_end) {
             n_rounds = (int)R;
         } else {   // more rounds than the counters hold: grow them and continue
             r0 = (int)R;
+            if (ctx->mate_early_done) LMX_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_mate, 0));   // (copied again later)
             LMX_TRY(lmx_ensure_ctr(ctx, 2 * ctx->ctr_cap));
         }
     }
