@@ -29,6 +29,10 @@ Configs (BASELINE.json configs / north_star):
   rgg22   C2: gen_rgg(22, seed=0, "euclidean") (generate.py:113-143), match seed 0
   rmat24  C3: RMAT scale 24 ef 16 (.57,.19,.19), graph seed 1, permuted; match seed 1
   rmat26  N*: RMAT scale 26, same recipe (the bench workload)
+  rmat27  RMAT scale 27, same recipe (2.1 G edges, the largest graph one B200
+          holds; ~70 GB of host memory: made on a GPU box's host, whose 196 GB
+          fit it, with `gpurun -- python tests/golden/make_golden_scale.py
+          --configs rmat27`; C oracle only)
   er24unit C1 family at 256x: 4 * 2^24 uniform raw pairs (the RMAT generator
           with a = b = c = 1/4, no relabelling), unit weights; seed 1
   er24unit-norr  the same graph and seed, rerandomize=False
