@@ -336,11 +336,12 @@ def run_b200_dist(args):
     if fam != "rmat":
         raise SystemExit("the partitioned bench runs the RMAT workloads")
     if world > 1:
-        # the distributed builder: no rank ever holds the whole graph (config C5)
+        # the distributed builder: no rank ever holds the whole graph (config C5);
+        # each rank keeps its local edges in page-locked host memory for the e2e leg
         from paper_1302_4587_b200.dist import build_rmat_distributed
         me = DistRank(None, world, rank, local, stream.cuda_stream, defer=True)
-        build_rmat_distributed([me], comm, scale, ef, *RMAT_ABC, GRAPH_SEED, True)
-    else:
+        build_rmat_distributed([me], comm, scale, ef, *RMAT_ABC, GRAPH_SEED, True, keep_records=not args.no_e2e)
+    else:   # one rank (--dist): the whole graph; the single-GPU line carries the e2e number
         me = DistRank(None, world, rank, local, stream.cuda_stream,
                       rmat=dict(scale=scale, edge_factor=ef, a=RMAT_ABC[0], b=RMAT_ABC[1], c=RMAT_ABC[2],
                                 seed=GRAPH_SEED, permute=True))
@@ -374,6 +375,47 @@ def run_b200_dist(args):
                       dtype=torch.float64)
     dist.all_reduce(tb)
     step_bytes = float(tb.item())
+    # ---- e2e at N GPUs: every step each rank copies its local edges (bsp.py:86-90,
+    # with their global ids) from page-locked host memory, loads its partition
+    # (K0), runs the matching protocol and reads its owned slice of mate back
+    e2e = None
+    if not args.no_e2e and world > 1:
+        recs, k_local = me.host_records
+        a, b = me.vertex_range(rank)
+        hmate = torch.empty(max(b - a, 1), dtype=torch.int64, pin_memory=True)
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+
+        def e2e_step():
+            me.load_local_edges(recs, k_local, me.host_degrees, m)
+            r_, _ = run_rounds([me], comm, MATCH_SEED, True)
+            if b > a:
+                hmate[: b - a].copy_(me.mate[a:b], non_blocking=True)
+            return r_
+        rounds_e = e2e_step()   # warm
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            rounds_e = e2e_step()
+        torch.cuda.synchronize()
+        te = torch.tensor([(time.perf_counter() - t0) * 1000.0, float(k_local) * 24.0 + float(n) * 4.0,
+                           float(b - a) * 8.0],
+                          device=dev, dtype=torch.float64)
+        dist.all_reduce(te[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(te[1:])
+        Te, h2d, d2h = (float(x) for x in te.tolist())
+        assert rounds_e == rounds, "e2e matching trace differs from the timed one"
+        e2e = {"value": m * e2e_steps / (Te / 1000.0), "unit": "edges/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": Te / e2e_steps, "steps": e2e_steps,
+               "api": "DistRank.load_local_edges = lmx_dist_load_local (each rank's local edges with global "
+                      "ids as 24-byte records + the global degrees u32[n], from page-locked host memory; the "
+                      "partition's K0) + run_rounds + owned mate slice D2H; wall clock, max over ranks"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # rank 0 alone, after the timed region: the reference on a bounded
+        # sample of the same recipe (the other ranks wait at the barrier below)
+        cpu = cpu_baseline_leg(args.cpu_baseline_scale, family=fam, ef=ef, RR=RR)
     if rank == 0:
         line = {
             "metric": "input edges/s to full local max maximal matching",
@@ -393,13 +435,12 @@ def run_b200_dist(args):
                          "kernel": "whole step: the scan loop's algorithmic bytes (probe + match + histogram, "
                                    "DESIGN.md 4.3; histogram share taken as m/p) summed over ranks, against all ranks' HBM",
                          "algorithmic_bytes_per_step": step_bytes},
-            "cpu_baseline": None, "e2e": None,
-            "e2e_note": "not measured on the partitioned path: every rank would need the full 25 GB host graph "
-                        "pinned; the one-GPU line carries the end-to-end number",
+            "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    dist.barrier()   # the other ranks wait for rank 0's CPU leg
     me.close()
     dist.destroy_process_group()
     return 0

@@ -294,6 +294,19 @@ int lmx_dist_rmat_build(lmx_ctx *ctx, int scale, int edge_factor, double a, doub
 int lmx_dist_rmat_route(lmx_ctx *ctx, void **send_dev, int64_t *counts_out, int64_t *m_out);
 int lmx_dist_rmat_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_dev);
 int lmx_dist_rmat_finish(lmx_ctx *ctx, int w_uniform);
+
+/* Load one partition from its local edges in HOST memory (a multi-GPU job
+ * whose ranks already hold their shares, and the multi-GPU end-to-end leg of
+ * bench.py): records = the rank's k local edges (bsp.py:86-90) as the 24-byte
+ * records lmx_dist_rmat_route produces ({edge id, u, v, pad, weight}: global
+ * edge ids and caller vertex ids); deg = the global degrees u32[n] (caller
+ * ids), from which partition_graph's cuts follow (bsp.py:60-98); m = the
+ * global edge count.  Both are copied to the device on the context's stream
+ * (page-locked memory copies at link rate), then the partition's K0 runs as
+ * in lmx_dist_rmat_finish.  Replaces the worker state setup of
+ * bsp_local_max (bsp.py:117-135) for one worker. */
+int lmx_dist_load_local(lmx_ctx *ctx, int64_t n, int64_t m, const uint32_t *deg, int64_t k, const void *records,
+                        int w_uniform);
 int lmx_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
 
 /*

@@ -897,6 +897,26 @@ int lmx_dist_rmat_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_dev) {
     return LMX_OK;
 }
 
+int lmx_dist_load_local(lmx_ctx *ctx, int64_t n, int64_t m, const uint32_t *deg, int64_t k, const void *records,
+                        int w_uniform) {
+    if (!ctx || n < 1 || m < 0 || k < 0 || k > m || !deg || (k && !records)) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    if (ctx->dist_p < 2) return lmx_fail(ctx, LMX_ESTATE, "set LMX_OPT_DIST_P > 1 first");
+    if (n > (int64_t)0xFFFFFFFEu || m > (int64_t)0xFFFFFFFEu)
+        return lmx_fail(ctx, LMX_ELIMIT, "more than 2^32 - 2 vertices or edges");
+    lmx_free_graph(ctx);
+    ctx->n = n;
+    ctx->m = m;
+    cudaStream_t st = ctx->stream;
+    LMX_TRY(lmx_alloc(ctx, (void **)&ctx->deg0, (size_t)n * 4, "global degrees"));
+    LMX_CUDA(ctx, cudaMemcpyAsync(ctx->deg0, deg, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    void *dst = nullptr;
+    LMX_TRY(lmx_dist_rmat_recv_buffer(ctx, k, &dst));
+    if (k) LMX_CUDA(ctx, cudaMemcpyAsync(dst, records, (size_t)k * sizeof(DistRec), cudaMemcpyHostToDevice, st));
+    return lmx_dist_rmat_finish(ctx, w_uniform);
+}
+
 // Phase 3: the received records are this rank's local edges (bsp.py:86-90),
 // in arrival order (slots carry the global edge ids, so the local order is
 // free); then the partition's K0.

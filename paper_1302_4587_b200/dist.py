@@ -154,6 +154,7 @@ def _bind(lib):
         "lmx_dist_rmat_route": (c_int, [p, ctypes.POINTER(p), p, ctypes.POINTER(i64)]),
         "lmx_dist_rmat_recv_buffer": (c_int, [p, i64, ctypes.POINTER(p)]),
         "lmx_dist_rmat_finish": (c_int, [p, c_int]),
+        "lmx_dist_load_local": (c_int, [p, i64, i64, p, i64, p, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -305,18 +306,34 @@ class DistRank:
         self._chk(self.lib.lmx_dist_messages(self.eng._h, int(n_rounds), ctypes.byref(hp)), "lmx_dist_messages")
         return _view(hp.value, (2 * (n_rounds + 1),), "<i8", self.device)
 
+    def load_local_edges(self, records, count: int, degrees, m: int):
+        """Load this partition from host memory (lmx_dist_load_local):
+        `records` (int32 [>= count, 6], page-locked) are its local edges with
+        their global ids, `degrees` (int32 [n], page-locked) the global degrees
+        in caller ids, `m` the global edge count -- as
+        ``build_rmat_distributed(..., keep_records=True)`` keeps them.  The
+        host-to-device copies and the partition's K0 run on the engine's stream."""
+        self._chk(self.lib.lmx_dist_load_local(self.eng._h, int(degrees.numel()), int(m), degrees.data_ptr(),
+                                               int(count), records.data_ptr() if count else None, self.w_uniform),
+                  "lmx_dist_load_local")
+        self._after_load()
+
     def close(self):
         self.eng.close()
 
 
 def build_rmat_distributed(ranks, comm, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
-                           c: float = 0.19, seed: int = 1, permute: bool = True):
+                           c: float = 0.19, seed: int = 1, permute: bool = True, keep_records: bool = False):
     """Load the local partitions ``ranks`` (created with ``defer=True``) with the
     RMAT graph of ``lmx_gen_rmat``'s recipe WITHOUT any rank holding the whole
     graph (config C5): each rank builds the pairs that hash to it (an even
     share whatever the ids), the first-occurrence bitmaps and the degrees are summed over
     the ranks (the global edge ids and partition_graph's cuts follow), and
-    every pair is sent to the owners of its ends (all-to-all-v)."""
+    every pair is sent to the owners of its ends (all-to-all-v).
+    ``keep_records=True`` also keeps each rank's received records -- its
+    local edges (bsp.py:86-90) with their global ids -- in page-locked host
+    memory (``rank.host_records``), so ``DistRank.load_local_edges`` can load
+    the partition again from the host (the multi-GPU end-to-end leg)."""
     import torch
     bits, degs, mms = [], [], []
     for r in ranks:
@@ -331,6 +348,10 @@ def build_rmat_distributed(ranks, comm, scale: int, edge_factor: int = 16, a: fl
     # disjoint bit sets: an int32 sum is their OR; degree contributions add
     comm.allreduce_sum_(ranks, bits)
     comm.allreduce_sum_(ranks, degs)
+    if keep_records:   # the global degrees (caller ids): partition_graph's cuts on a reload
+        for r, d in zip(ranks, degs):
+            r.host_degrees = torch.empty(d.shape, dtype=torch.int32, pin_memory=True)
+            r.host_degrees.copy_(d)
     lo = comm.allreduce_min_u64(ranks, [m_[0:1] for m_ in mms])
     hi = comm.allreduce_max_u64(ranks, [m_[1:2] for m_ in mms])
     uniform = int(lo == hi)
@@ -345,14 +366,25 @@ def build_rmat_distributed(ranks, comm, scale: int, edge_factor: int = 16, a: fl
         sends.append((_view(sp.value, (max(total, 1), 6), "<i4", r.device), counts))
     recvs = comm.alltoallv_records(ranks, sends, 6, lambda r, cnt: _recv_records(r, cnt))
     for r, cnt in zip(ranks, recvs):
+        r.w_uniform = uniform
+        if keep_records:
+            h = torch.empty((max(int(cnt), 1), 6), dtype=torch.int32, pin_memory=True)
+            if cnt:
+                h[:cnt].copy_(_recv_records(r, cnt, keep=True)[:cnt])
+            r.host_records = (h, int(cnt))
         r._chk(r.lib.lmx_dist_rmat_finish(r.eng._h, uniform), "lmx_dist_rmat_finish")
         r._after_load()
     torch.cuda.synchronize()
 
 
-def _recv_records(r, count: int):
+def _recv_records(r, count: int, keep: bool = False):
+    """The device buffer of `count` received build records (allocated by
+    liblmx; ``keep=True``: the one already allocated, records intact)."""
+    if keep:
+        return _view(r._recv_ptr, (max(int(count), 1), 6), "<i4", r.device)
     rp = ctypes.c_void_p()
     r._chk(r.lib.lmx_dist_rmat_recv_buffer(r.eng._h, int(count), ctypes.byref(rp)), "lmx_dist_rmat_recv_buffer")
+    r._recv_ptr = rp.value
     return _view(rp.value, (max(int(count), 1), 6), "<i4", r.device)
 
 
@@ -594,11 +626,28 @@ class TorchComm:
         return [total]
 
     def gather_outputs(self, ranks):
+        """The global mate table and matched-edge bits on every rank.  Each
+        rank writes mate only inside its owned range (relabelling stays inside
+        a range), so the owned slices are all-gathered: (p-1)/p of n int64 per
+        rank instead of an all-reduce's 2 (p-1)/p.  The edge bits are set by
+        the owner of an edge's lower end, scattered over the id space: an
+        all-reduce (disjoint bit sets: sum == or)."""
+        import torch
         (me,) = ranks
-        mate = me.mate.clone()
+        spans = [me.vertex_range(k) for k in range(self.p)]
+        width = max(max(b - a for a, b in spans), 1)
+        a, b = spans[self.rank]
+        row = torch.full((width,), -1, dtype=torch.int64, device=me.device)
+        if b > a:
+            row[: b - a].copy_(me.mate[a:b])
+        out = torch.empty(self.p * width, dtype=torch.int64, device=me.device)
+        self.dist.all_gather_into_tensor(out, row)
+        mate = torch.full_like(me.mate, -1)
+        for k, (x, y) in enumerate(spans):
+            if y > x:
+                mate[x:y].copy_(out[k * width: k * width + (y - x)])
         ebits = me.ebits.clone()
-        self.dist.all_reduce(mate, op=self.dist.ReduceOp.MAX)
-        self.dist.all_reduce(ebits)   # disjoint bit sets: sum == or
+        self.dist.all_reduce(ebits)
         return mate, ebits
 
     def bind_device(self, device):

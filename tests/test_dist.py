@@ -57,6 +57,23 @@ def test_gloo_world_size_2_matches_oracle():
 
 
 @pytest.mark.gpu
+def test_two_processes_real_partitions():
+    """Two processes, each one liblmx partition (the real kernels), through
+    TorchComm over gloo (tests/dist_gpu_worker.py): the multi-process path of
+    the NCCL runs on the one GPU of the test box.  Matchings, RoundStats and
+    RoundMessages against the C oracle; the distributed RMAT build against
+    the single-GPU engine."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29519",
+           os.path.join(ROOT, "tests", "dist_gpu_worker.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ok=True") == 18 and "ok=False" not in out and "algo=scan" in out, out[-4000:]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("algo", ["auto", "compact"])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
 def test_dist_equals_single_gpu_small(golden_small, p, algo):
@@ -233,3 +250,35 @@ def test_distributed_rmat_build_equals_single_gpu(engine, p, scale, permute):
     assert np.array_equal(matching.sorted_edge_ids(), ids)
     assert trace.rounds == rounds and rounds[0].edges_before == m
     assert len(dev_bytes) == p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 3])
+def test_partition_reload_from_host_records(p):
+    """The multi-GPU end-to-end leg (bench.py --gpus N): every partition kept
+    its local edges (with global ids) in page-locked host memory at build
+    time and loads itself again from them (DistRank.load_local_edges); the
+    matching, RoundStats and gathered mate equal the first load's."""
+    import torch
+    from paper_1302_4587_b200.dist import DistRank, LocalComm, _unpack_ids, build_rmat_distributed, run_rounds
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream(0).cuda_stream
+    ranks = [DistRank(None, p, k, 0, stream, defer=True) for k in range(p)]
+    try:
+        comm = LocalComm(p)
+        build_rmat_distributed(ranks, comm, 13, 16, 0.57, 0.19, 0.19, 7, True, keep_records=True)
+        stats0, _ = run_rounds(ranks, comm, 5, True)
+        mate0, eb0 = comm.gather_outputs(ranks)
+        mate0, ids0 = mate0.cpu().numpy().copy(), _unpack_ids(eb0, ranks[0].m)
+        for _ in range(2):
+            for r in ranks:
+                recs, k = r.host_records
+                r.load_local_edges(recs, k, r.host_degrees, r.m)
+            stats1, _ = run_rounds(ranks, comm, 5, True)
+            mate1, eb1 = comm.gather_outputs(ranks)
+            assert stats1 == stats0
+            assert np.array_equal(mate1.cpu().numpy(), mate0)
+            assert np.array_equal(_unpack_ids(eb1, ranks[0].m), ids0)
+    finally:
+        for r in ranks:
+            r.close()
