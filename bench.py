@@ -323,12 +323,17 @@ def run_b200_dist(args):
     from paper_1302_4587_b200.dist import DistRank, TorchComm, run_rounds
 
     world, rank, local = dist_env()
+    if args.backend != "nccl":   # test only: the ranks share the GPUs there are
+        local %= max(torch.cuda.device_count(), 1)
     if "RANK" not in os.environ:   # --dist without torchrun: a one-rank group
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:   # test only: every rank on one GPU, host-staged collectives (no kernel waits on another rank)
+        dist.init_process_group(args.backend)
     comm = TorchComm()
     comm.bind_device(dev)
     stream = torch.cuda.current_stream()
@@ -810,6 +815,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", help=argparse.SUPPRESS)
     ap.add_argument("--dist", action="store_true",
                     help="use the 1D-partitioned multi-GPU engine even at one rank (NCCL code path check)")
     args = ap.parse_args()

@@ -55,3 +55,25 @@ def test_b200_arm_line():
     assert c["sm_mhz"] > 0 and isinstance(c["reasons"], list)
     assert d["gpu_launches"] > 0
     assert d["device_memory"]["load_peak_GB"] >= d["device_memory"]["after_load_GB"] > 0
+
+
+@pytest.mark.gpu
+def test_two_rank_line_over_gloo():
+    """The N-GPU line (torchrun, one rank per GPU) end to end: distributed
+    RMAT build, the round protocol, the per-rank e2e leg (local edges from
+    page-locked host memory), rank 0's CPU baseline -- two ranks on the test
+    box's one GPU with gloo's host-staged collectives (--backend is test only;
+    the driver's runs use NCCL)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29537", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--backend", "gloo", "--workload", "rmat16", "--steps", "3", "--warmup", "3",
+           "--cpu-baseline-scale", "12"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, OMP_NUM_THREADS="1"))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["build"].startswith("distributed")
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["value"] > 0 and d["gpu_launches"] > 0
