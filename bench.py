@@ -735,6 +735,7 @@ def run_b200(args):
     if not args.no_e2e and load_note is not None:
         e2e = {"unavailable": "the device-input load did not fit (see load_device_note)"}
     elif not args.no_e2e:
+        eng.set_relabel(args.e2e_relabel)
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         # warm: two steps, so the pinned output pool holds the buffers of the
         # result a caller keeps while the next step allocates (steady state)
@@ -763,7 +764,8 @@ def run_b200(args):
                "ms_per_step": Te / e2e_steps, "steps": e2e_steps,
                "setup_ms_last": eng.last_timing()["setup_ms"],
                "api": "Engine.load_graph(Graph of pinned host arrays) + Engine.match_raw (lmx_load_graph + "
-                      "lmx_match, host outputs)"}
+                      "lmx_match, host outputs)",
+               "relabel": args.e2e_relabel}
     del hg, pu, pv, pw
 
     cpu = None
@@ -816,6 +818,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="nccl", help=argparse.SUPPRESS)
+    ap.add_argument("--e2e-relabel", default="once", choices=("auto", "on", "off", "once"),
+                    help="degree relabelling of the e2e leg's loads (Engine.set_relabel); each e2e step is "
+                         "one load + one matching: 'once', the one-shot entry points' choice")
     ap.add_argument("--dist", action="store_true",
                     help="use the 1D-partitioned multi-GPU engine even at one rank (NCCL code path check)")
     args = ap.parse_args()

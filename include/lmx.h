@@ -78,7 +78,11 @@ typedef struct {
 #define LMX_OPT_LAYOUT 2        /* weight-key layout of the next load: -1 auto, 0 uniform
                                    (only valid if all weights are equal), 1 distinct, 2 general */
 #define LMX_OPT_RELABEL 3       /* degree-descending vertex relabelling of the next load:
-                                   -1 auto (skewed degree distributions), 0 off, 1 on */
+                                   -1 auto (skewed degree distributions), 0 off, 1 on,
+                                   2 once: auto, except for the scan loop, for a load that
+                                   serves ONE matching (relabelling costs the scan loop's
+                                   load more than it saves one matching; lmx_local_max's
+                                   choice) */
 #define LMX_OPT_DIST_P 4        /* number of 1D vertex partitions of the next load (1 = single GPU) */
 #define LMX_OPT_DIST_RANK 5     /* which partition this context owns (set after LMX_OPT_DIST_P) */
 #define LMX_OPT_ALGO 6          /* round loop of the next load: -1 auto, 0 compacting rounds,

@@ -209,7 +209,7 @@ int lmx_set_option(lmx_ctx *ctx, int option, int64_t value) {
         return LMX_OK;
     }
     if (option == LMX_OPT_RELABEL) {
-        if (value < -1 || value > 1) return lmx_fail(ctx, LMX_EINVAL, "relabel must be -1, 0 or 1");
+        if (value < -1 || value > 2) return lmx_fail(ctx, LMX_EINVAL, "relabel must be -1, 0, 1 or 2");
         ctx->force_relabel = (int)value;
         return LMX_OK;
     }
@@ -296,6 +296,7 @@ int lmx_local_max(int device, int64_t n, int64_t m, const int64_t *edge_u, const
         ctx->static_order = true;
         ctx->static_seed = seed_masked;
     }
+    if (rc == LMX_OK) ctx->force_relabel = 2;   // one matching per load (LMX_OPT_RELABEL)
     if (rc == LMX_OK) rc = lmx_load_graph(ctx, n, m, edge_u, edge_v, edge_weight, LMX_HOST);
     if (rc == LMX_OK)
         rc = lmx_match(ctx, seed_masked, rerandomize, mate_out, matched_ids_out, n_matched_out, rounds_out,

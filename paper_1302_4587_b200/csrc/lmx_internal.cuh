@@ -155,7 +155,7 @@ struct lmx_ctx {
     std::vector<cudaEvent_t> tl_events;      // per-kernel timeline (kernel_timing)
     std::vector<float> kernel_ms;            // its durations: round, match, round, ...
     int force_layout = -1;                   // testing: force a weight-key layout
-    int force_relabel = -1;                  // -1 auto (skewed graphs), 0 off, 1 on
+    int force_relabel = -1;                  // -1 auto (skewed graphs), 0 off, 1 on, 2 once (no scan loop relabel)
     bool relabeled = false;                  // device vertex ids are degree-sorted
     uint32_t *oldid = nullptr;               // device id -> caller's vertex id
     // round-loop algorithm: 0 = compacting rounds (lmx_round.cu),

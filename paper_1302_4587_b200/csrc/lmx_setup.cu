@@ -1036,7 +1036,9 @@ int lmx_setup_slots(lmx_ctx *ctx) {
     ctx->relabeled = false;
     if (n > 1 && m) {
         bool relabel = ctx->force_relabel == 1;
-        if (ctx->force_relabel == -1) {
+        // "once": one matching per load -- the scan loop's relabelling costs
+        // its load more than it saves one matching (RMAT-26: +23 / -3.7 ms)
+        if (ctx->force_relabel == -1 || (ctx->force_relabel == 2 && ctx->algo != 1)) {
             uint32_t *mx = nullptr;
             size_t tmp = 0;
             LMX_TRY(lmx_alloc(ctx, (void **)&mx, 4, "max degree"));

@@ -342,8 +342,9 @@ class Engine:
         self._check(self._lib.lmx_set_option(self._h, LMX_OPT_LAYOUT, self.LAYOUTS[layout]), "lmx_set_option")
 
     def set_relabel(self, mode: str = "auto") -> None:
-        """Degree-descending vertex relabelling of the next load: auto / on / off."""
-        val = {"auto": -1, "off": 0, "on": 1}[mode]
+        """Degree-descending vertex relabelling of the next load: auto / on / off /
+        once (auto, except for the scan loop: a load that serves one matching)."""
+        val = {"auto": -1, "off": 0, "on": 1, "once": 2}[mode]
         self._check(self._lib.lmx_set_option(self._h, LMX_OPT_RELABEL, val), "lmx_set_option")
 
     ALGOS = {"auto": -1, "compact": 0, "scan": 1}
@@ -479,10 +480,12 @@ def local_max_b200(g, seed: int, rerandomize: bool = True, device: int = 0) -> t
     # with rerandomize off the salts are fixed for the run: tied weights get
     # the static (weight, salt) layout and the scan loop (LMX_OPT_STATIC_ORDER)
     eng.set_static_order(None if rerandomize else seed)
+    eng.set_relabel("once")   # one matching per load
     try:
         eng.load_graph(g)
     finally:
         eng.set_static_order(None)
+        eng.set_relabel("auto")
     matching, trace = eng.match(g, seed, rerandomize)
     trace.wall_millis = (time.perf_counter() - t0) * 1000.0
     return matching, trace
