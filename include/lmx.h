@@ -241,6 +241,17 @@ int lmx_dist_round(lmx_ctx *ctx);
 int lmx_dist_propose(lmx_ctx *ctx, void **counts_dev_out, void **send_dev_out);
 int lmx_dist_recv_buffer(lmx_ctx *ctx, int64_t count, void **recv_out);
 int lmx_dist_accept(lmx_ctx *ctx, int64_t count);
+/* The late rounds' exchange A without a host round trip (scan loop
+ * partitions): after lmx_dist_propose, lay the records out in p slots of
+ * `capacity` records each (destination j's records first, the rest filler
+ * the receiver's lmx_dist_accept skips), so the all-to-all has equal, host-
+ * known splits and lmx_dist_accept takes p * capacity.  capacity must bound
+ * every rank's count: the largest list size of any rank at or before this
+ * round (lists only shrink); *overflow_dev_out (u32, may be NULL) becomes
+ * nonzero if it did not.  lmx_dist_list_size: the device u32 holding this
+ * rank's list size for the next round (valid after lmx_dist_match). */
+int lmx_dist_pad(lmx_ctx *ctx, int64_t capacity, void **padded_dev_out, void **overflow_dev_out);
+int lmx_dist_list_size(lmx_ctx *ctx, void **size_dev_out);
 /* Enqueues the match step; *stats_dev_out = device {live slots, matched
  * vertices} (two uint64) of the round, for the all-reduce.  No synchronisation. */
 int lmx_dist_match(lmx_ctx *ctx, void **stats_dev_out);

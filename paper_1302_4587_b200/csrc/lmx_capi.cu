@@ -363,6 +363,21 @@ int lmx_dist_accept(lmx_ctx *ctx, int64_t count) {
     return lmx_dist_accept_impl(ctx, count);
 }
 
+int lmx_dist_pad(lmx_ctx *ctx, int64_t capacity, void **padded_dev_out, void **overflow_dev_out) {
+    if (!ctx || !padded_dev_out) return LMX_EINVAL;
+    cudaSetDevice(ctx->device);
+    if (ctx->algo != 1) return lmx_fail(ctx, LMX_ESTATE, "fixed-capacity exchange: scan loop partitions only");
+    return lmx_scan_dist_pad(ctx, capacity, padded_dev_out, overflow_dev_out);
+}
+
+int lmx_dist_list_size(lmx_ctx *ctx, void **size_dev_out) {
+    if (!ctx || !size_dev_out) return LMX_EINVAL;
+    if (ctx->algo != 1) return lmx_fail(ctx, LMX_ESTATE, "list size: scan loop partitions only");
+    if (!ctx->ctr) return lmx_fail(ctx, LMX_ESTATE, "lmx_dist_begin first");
+    *size_dev_out = &ctx->ctr[ctx->dist_round].pad[0];
+    return LMX_OK;
+}
+
 int lmx_dist_match(lmx_ctx *ctx, void **stats_dev_out) {
     if (!ctx || !stats_dev_out) return LMX_EINVAL;
     cudaSetDevice(ctx->device);

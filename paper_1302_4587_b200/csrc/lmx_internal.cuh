@@ -233,6 +233,8 @@ struct lmx_ctx {
     int64_t n_local = 0, slots_local = 0;
     std::vector<int64_t> bounds;             // p + 1 cut points
     uint32_t *remote_ok = nullptr;           // [n_local] partner owner confirmed the edge
+    uint2 *pad = nullptr;                    // fixed-capacity exchange A (late rounds): p * capacity records
+    size_t pad_cap = 0;
     uint2 *send = nullptr, *recv = nullptr;  // proposal records {global target, edge id}
     uint32_t *send_cnt = nullptr;            // [p] per destination
     size_t send_cap = 0, recv_cap = 0;
@@ -269,6 +271,7 @@ int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize);
 int lmx_scan_dist_round(lmx_ctx *ctx);
 int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev);
 int lmx_scan_dist_accept(lmx_ctx *ctx, int64_t count);
+int lmx_scan_dist_pad(lmx_ctx *ctx, int64_t C, void **padded_dev, void **overflow_dev);
 int lmx_scan_dist_match(lmx_ctx *ctx, void **stats_dev);
 int lmx_scan_dist_hist(lmx_ctx *ctx, int n_rounds, void **hist_dev, int *nbins);
 namespace lmx {

@@ -1319,13 +1319,44 @@ __global__ void lmx_scan_accept_kernel(const uint2 *rec, unsigned long long k, c
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) {
         const uint2 r = rec[i];
+        if (r.y == kNone) continue;   // the filler of a fixed-capacity exchange (lmx_scan_pad_kernel)
         const uint32_t vl = r.x - lo;
         const uint32_t w = cnbr[vl];
         if (w != kNone && cand_eid(vl, w, ckey, ptr, vbeg, ids) == r.y) remote_ok[vl] = 1u;
     }
 }
 
+// Fixed-capacity exchange A (the late rounds, no host round trip): the packed
+// records of destination j go to padded[j C, j C + count_j), the rest of its
+// C slots is filler {first vertex of j, kNone} that the receiver's accept
+// skips.  C bounds every count (no rank proposes more records than it has
+// listed vertices); a count above it sets *overflow.
+__global__ void lmx_scan_pad_kernel(const uint2 *packed, const long long *counts64, const unsigned long long *bounds,
+                                    int p, unsigned long long C, uint2 *padded, unsigned int *overflow) {
+    __shared__ unsigned long long s_off[65];
+    if (threadIdx.x == 0) {
+        unsigned long long o = 0;
+        for (int j = 0; j < p; ++j) {
+            s_off[j] = o;
+            o += (unsigned long long)counts64[j];
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)p && (unsigned long long)counts64[threadIdx.x] > C)
+        atomicOr(overflow, 1u);
+    const unsigned long long total = (unsigned long long)p * C;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int j = (int)(i / C);
+        const unsigned long long t = i - (unsigned long long)j * C;
+        padded[i] = t < (unsigned long long)counts64[j] ? packed[s_off[j] + t]
+                                                         : make_uint2((uint32_t)bounds[j], kNone);
+    }
+}
+
 }  // namespace lmx
+
+static int scan_dist_send_buffers(lmx_ctx *ctx);
 
 int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
     ctx->timing.round_launches = 0;
@@ -1335,6 +1366,8 @@ int lmx_scan_dist_begin(lmx_ctx *ctx, uint64_t seed_masked, bool rerandomize) {
     ctx->mate_target = ctx->mate;
     LMX_CUDA(ctx, cudaMemsetAsync(ctx->remote_ok, 0, (size_t)std::max<int64_t>(ctx->n_local, 1) * 4, ctx->stream));
     LMX_TRY(scan_begin(ctx));
+    LMX_TRY(scan_dist_send_buffers(ctx));
+    LMX_CUDA(ctx, cudaMemsetAsync(reinterpret_cast<char *>(ctx->send_cnt) + 768, 0, 4, ctx->stream));   // overflow
     LMX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return LMX_OK;
 }
@@ -1382,6 +1415,31 @@ int lmx_scan_dist_propose(lmx_ctx *ctx, void **counts_dev, void **packed_dev) {
     ctx->timing.round_launches += 1;
     *counts_dev = counts64;
     *packed_dev = packed;
+    return LMX_OK;
+}
+
+// The fixed-capacity exchange of the late rounds (after lmx_scan_dist_propose).
+int lmx_scan_dist_pad(lmx_ctx *ctx, int64_t C, void **padded_dev, void **overflow_dev) {
+    const int p = ctx->dist_p;
+    if (!ctx->send || !ctx->send_cnt) return lmx_fail(ctx, LMX_ESTATE, "pad before propose");
+    if (C < 1) return lmx_fail(ctx, LMX_EINVAL, "capacity must be >= 1");
+    const size_t need = (size_t)C * (size_t)p;
+    if (ctx->pad_cap < need) {
+        lmx_dfree(ctx, ctx->pad);
+        ctx->pad = nullptr;
+        LMX_CUDA(ctx, lmx_dmalloc(ctx, (void **)&ctx->pad, need * sizeof(uint2)));
+        ctx->pad_cap = need;
+    }
+    const size_t nl = (size_t)std::max<int64_t>(ctx->n_local, 1);
+    char *cb = reinterpret_cast<char *>(ctx->send_cnt);
+    unsigned int *overflow = reinterpret_cast<unsigned int *>(cb + 768);
+    lmx_scan_pad_kernel<<<ctx->num_sms * 2, kBlock, 0, ctx->stream>>>(
+        ctx->send + nl * (size_t)p, reinterpret_cast<const long long *>(cb + 256),
+        reinterpret_cast<const unsigned long long *>(cb + 1024), p, (unsigned long long)C, ctx->pad, overflow);
+    LMX_CUDA(ctx, cudaGetLastError());
+    ctx->timing.round_launches += 1;
+    *padded_dev = ctx->pad;
+    if (overflow_dev) *overflow_dev = overflow;
     return LMX_OK;
 }
 

@@ -131,7 +131,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
                      (void **)&ctx->geid,     (void **)&ctx->slot_side,
                      (void **)&ctx->db_bits,  (void **)&ctx->db_pf,       (void **)&ctx->db_pu,
                      (void **)&ctx->db_pv,    (void **)&ctx->db_pw,       (void **)&ctx->db_minmax,
-                     (void **)&ctx->db_send,  (void **)&ctx->db_recv};
+                     (void **)&ctx->db_send,  (void **)&ctx->db_recv,     (void **)&ctx->pad};
     for (void **p : ptrs) {
         lmx_dfree(ctx, *p);
         *p = nullptr;
@@ -142,6 +142,7 @@ void lmx_free_graph(lmx_ctx *ctx) {
     ctx->m_local = 0;
     ctx->w_uniform = -1;
     ctx->db_words = ctx->db_np = ctx->db_cap = ctx->db_send_n = ctx->db_recv_n = 0;
+    ctx->pad_cap = 0;
     ctx->layout = kUniform;
     ctx->n_distinct = ctx->n_tied = 0;
     ctx->relabeled = false;

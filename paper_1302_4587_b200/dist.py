@@ -41,6 +41,7 @@ Communicators:
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 
 import numpy as np
@@ -155,6 +156,8 @@ def _bind(lib):
         "lmx_dist_rmat_recv_buffer": (c_int, [p, i64, ctypes.POINTER(p)]),
         "lmx_dist_rmat_finish": (c_int, [p, c_int]),
         "lmx_dist_load_local": (c_int, [p, i64, i64, p, i64, p, c_int]),
+        "lmx_dist_pad": (c_int, [p, i64, ctypes.POINTER(p), ctypes.POINTER(p)]),
+        "lmx_dist_list_size": (c_int, [p, ctypes.POINTER(p)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -268,6 +271,22 @@ class DistRank:
         counts = self._cached_view(cptr.value, self.p, 0, "<i8")
         send = self._cached_view(sptr.value, max(self.n_local, 1), 2, "<i4")
         return send, counts
+
+    def pad(self, capacity: int):
+        """Fixed-capacity exchange A (lmx_dist_pad, after propose): int32
+        [p * capacity, 2] records, destination j's in slot j, and the device
+        overflow flag (int32 [1], nonzero if capacity did not bound a count)."""
+        pp, op = ctypes.c_void_p(), ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_pad(self.eng._h, int(capacity), ctypes.byref(pp), ctypes.byref(op)),
+                  "lmx_dist_pad")
+        return (self._cached_view(pp.value, self.p * int(capacity), 2, "<i4"),
+                self._cached_view(op.value, 1, 0, "<i4"))
+
+    def list_size(self):
+        """This rank's list size for the next round (device int32 [1]; after match)."""
+        sp = ctypes.c_void_p()
+        self._chk(self.lib.lmx_dist_list_size(self.eng._h, ctypes.byref(sp)), "lmx_dist_list_size")
+        return _view(sp.value, (1,), "<i4", self.device)
 
     def recv_buffer(self, count: int):
         ptr = ctypes.c_void_p()
@@ -596,6 +615,10 @@ class TorchComm:
         (t,) = tensors
         self.dist.all_reduce(t)
 
+    def allreduce_max_(self, ranks, tensors):
+        (t,) = tensors
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+
     def _u64_extreme(self, tensors, op):
         import torch
         (t,) = tensors
@@ -624,6 +647,20 @@ class TorchComm:
         flat_out = recv[:total].reshape(-1) if total else torch.empty(0, dtype=torch.int32, device=dev)
         self.dist.all_to_all_single(flat_out, flat_in, [width * c for c in rcounts], [width * c for c in scounts])
         return [total]
+
+    def alltoall_padded(self, ranks, padded, counts, capacity: int):
+        """Exchange A with equal, host-known splits (p slots of `capacity`
+        records; filler skipped by accept): no host round trip.  Returns the
+        slots' record total (what accept reads) and this rank's received
+        record count as a device int64 [1]."""
+        import torch
+        (me,) = ranks
+        total = self.p * int(capacity)
+        recv = me.recv_buffer(total)
+        self.dist.all_to_all_single(recv.reshape(-1), padded[:total].reshape(-1))
+        rc = torch.empty_like(counts)
+        self.dist.all_to_all_single(rc, counts)
+        return total, rc.sum().view(1)
 
     def gather_outputs(self, ranks):
         """The global mate table and matched-edge bits on every rank.  Each
@@ -764,6 +801,10 @@ def _run_rounds_scan(ranks, comm, seed: int, rerandomize: bool, max_rounds: int 
                 r.accept(cnt)
             (prev,) = [r.match().clone() for r in ranks]   # the view lives in the counter array
             comm.allgather_bitmap(ranks)
+            if (st is not None and st[0] <= _LATE_FOUND and hasattr(comm, "alltoall_padded")
+                    and all(r.algo == "scan" and hasattr(r, "pad") for r in ranks)):
+                _late_rounds(ranks, comm, prev, matched, records, max_rounds)
+                break
     else:
         while True:
             for r in ranks:
@@ -797,6 +838,65 @@ def _run_rounds_scan(ranks, comm, seed: int, rerandomize: bool, max_rounds: int 
         stats.append(RoundStats(alive, matched[i], hist[i]))
         alive -= hist[i]
     return stats, records
+
+
+#: The late rounds (global candidates found in a round at most this many)
+#: run in batches of _LATE_BATCH with fixed-capacity exchanges and one host
+#: round trip per batch instead of one per round.
+_LATE_FOUND = int(os.environ.get("LMX_DIST_LATE_FOUND", str(1 << 22)))
+_LATE_BATCH = max(1, int(os.environ.get("LMX_DIST_LATE_BATCH", "8")))
+
+
+def _late_rounds(ranks, comm, prev, matched, records, max_rounds):
+    """The tail of the round protocol (scan loop partitions, TorchComm).
+
+    The lists only shrink, so the largest list of any rank now bounds every
+    rank's exchange-A count in every later round: exchange A runs with that
+    fixed capacity per destination (lmx_dist_pad; equal all-to-all splits the
+    host knows), and a batch of rounds is enqueued with no host round trip.
+    Their statistics come back in one all-reduce per batch; rounds enqueued
+    past the end (no candidate anywhere) probe and match empty lists.
+    `prev` is the last synchronised round's pending {found, matched} (device)."""
+    import torch
+    (me,) = ranks
+    cap = me.list_size().to(torch.int64)
+    comm.allreduce_max_(ranks, [cap])
+    capacity = max(int(cap.item()), 1)
+    rows, recs = [prev], []   # per round: {found, matched} (summed over ranks) / records received here
+    first = True
+    while True:
+        for _ in range(_LATE_BATCH):
+            me.round()
+            _send, counts = me.propose()
+            padded, overflow = me.pad(capacity)
+            total, received = comm.alltoall_padded(ranks, padded, counts, capacity)
+            me.accept(total)
+            rows.append(me.match().clone())
+            recs.append(received)
+            comm.allgather_bitmap(ranks)
+        flat = torch.cat([torch.stack(rows).reshape(-1), overflow.to(torch.int64)])
+        comm.allreduce_sum_(ranks, [flat])
+        h = torch.cat([flat] + recs).tolist()   # the batch's one host round trip
+        nrow = len(rows)
+        if h[2 * nrow]:
+            raise RuntimeError("internal: exchange-A capacity exceeded")
+        rec_h = h[2 * nrow + 1:]
+        skip = 1 if first else 0   # the first batch starts with the synchronised round (its records are in)
+        for i in range(nrow):
+            found, mv = h[2 * i], h[2 * i + 1]
+            if found == 0:
+                if i < skip:
+                    records.pop()
+                return
+            if mv % 2:
+                raise RuntimeError("internal: odd global matched-vertex count")
+            matched.append(mv // 2)
+            if i >= skip:
+                records.append(int(rec_h[i - skip]))
+            if max_rounds is not None and len(matched) > max_rounds:
+                raise RuntimeError("round limit exceeded")
+        rows, recs = [], []
+        first = False
 
 
 def _unpack_ids(ebits, m: int) -> np.ndarray:

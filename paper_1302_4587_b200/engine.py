@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "lmx_dist_bounds", "lmx_dist_begin", "lmx_dist_round", "lmx_dist_propose", "lmx_dist_recv_buffer",
     "lmx_dist_accept", "lmx_dist_match", "lmx_dist_state", "lmx_dist_mround", "lmx_dist_hist",
     "lmx_dist_messages", "lmx_pram_cross", "lmx_dist_rmat_build", "lmx_dist_rmat_route",
-    "lmx_dist_rmat_recv_buffer", "lmx_dist_rmat_finish", "lmx_dist_load_local",
+    "lmx_dist_rmat_recv_buffer", "lmx_dist_rmat_finish", "lmx_dist_load_local", "lmx_dist_pad", "lmx_dist_list_size",
     "lmx_mesh_edges", "lmx_ratings", "lmx_contract",
 )
 LMX_OPT_KERNEL_TIMING = 1
