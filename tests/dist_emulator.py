@@ -125,9 +125,27 @@ class EmulatedRank:
             if not (self.lo <= x < self.hi):
                 groups[self._owner(x)].append((x, e))
         counts = torch.tensor([len(gp) for gp in groups], dtype=torch.int64)
+        self._groups = groups
         flat = [rec for gp in groups for rec in gp]
         send = torch.tensor(flat if flat else np.zeros((0, 2)), dtype=torch.int32).reshape(-1, 2)
         return send, counts
+
+    def pad(self, capacity: int):
+        """lmx_dist_pad restated: p slots of `capacity` records, filler
+        {first vertex of the slot's owner, kNone} after each slot's records."""
+        C = int(capacity)
+        out = np.zeros((self.p * C, 2), dtype=np.int64)
+        overflow = 0
+        for j, gp in enumerate(self._groups):
+            overflow |= int(len(gp) > C)
+            for t in range(C):
+                out[j * C + t] = gp[t] if t < len(gp) else (int(self.bounds[j]), 0xFFFFFFFF)
+        return (torch.from_numpy(out.astype(np.uint32).view(np.int32)).reshape(-1, 2),
+                torch.tensor([overflow], dtype=torch.int32))
+
+    def list_size(self):
+        """A_{r+1}: the owned vertices that found a candidate and stayed unmatched."""
+        return torch.tensor([sum(1 for v in self.cand if not self._is_matched(v))], dtype=torch.int32)
 
     def recv_buffer(self, count: int):
         self.recv = torch.zeros((int(count), 2), dtype=torch.int32)
